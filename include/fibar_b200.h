@@ -1,0 +1,123 @@
+/*
+ * fibar_b200.h -- C ABI of the B200-native FIBAR reconstruction hot path.
+ *
+ * A plain C interface (opaque handle, plain pointers and sizes, no torch types)
+ * that replaces the reference's native layer for the event->image path.  Each
+ * entry point names the reference interface it stands in for
+ * (paths relative to /root/reference/pkg/src/fibar):
+ *
+ *   fibar_create / fibar_destroy
+ *       ReconstructionEngine.__init__ state allocation, pipeline.py:381-439
+ *       (p_bar, l, active_count, tile_count, ring qx/qy, qs[10], gain map,
+ *       float32 coefficient casts).
+ *   fibar_process
+ *       ReconstructionEngine.process_array, pipeline.py:511-558, i.e. the OOB
+ *       filter (non-strict) plus the numba kernels _temporal_chunk
+ *       (_kernels.py:62-73) / _full_chunk (_kernels.py:76-216).
+ *   fibar_flush
+ *       (no reference equivalent: the engine coalesces packets on the device
+ *       between read-outs; state is packet-size invariant).
+ *   fibar_render
+ *       ReconstructionEngine.render, pipeline.py:562-584.
+ *   fibar_read_qs / fibar_counters
+ *       the qs[10] slots (_kernels.py:48-59, pipeline.py:451-477) and
+ *       event_count / oob_dropped (pipeline.py:437-439).
+ *   fibar_read_state
+ *       the arrays hashed by state_digest / returned by iap, l_grid,
+ *       p_bar_grid (pipeline.py:443-496).
+ *
+ * Threading: one engine = one CUDA stream; calls on one engine must not race
+ * (same contract as the reference).  Every call returns 0 on
+ * success or one of the FIBAR_E_* codes below; the Python shim maps them to
+ * the reference's exception classes (errors.py).
+ */
+#ifndef FIBAR_B200_H
+#define FIBAR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FIBAR_OK 0
+#define FIBAR_E_CONFIG 1     /* -> ConfigError */
+#define FIBAR_E_DATA 2       /* -> DataError */
+#define FIBAR_E_ORDER 3      /* -> OrderError */
+#define FIBAR_E_INVARIANT 4  /* -> InvariantError (e.g. counter saturation) */
+#define FIBAR_E_CUDA 5       /* -> DeviceError */
+#define FIBAR_E_NODEVICE 6   /* -> DeviceError */
+
+#define FIBAR_MEM_HOST 0
+#define FIBAR_MEM_DEVICE 1
+
+#define FIBAR_RENDER_ROBUST 0
+#define FIBAR_RENDER_FIXED 1
+
+typedef struct fibar_engine fibar_engine;
+
+typedef struct fibar_config {
+  int32_t width;
+  int32_t height;
+  int32_t tile_side;        /* FilterParams.tile_side (core.py:68) */
+  int32_t spatial_enabled;  /* FilterParams.spatial_enabled (core.py:71) */
+  int32_t blur_enabled;     /* ReconstructionEngine(blur_enabled=) */
+  int32_t reserved0;
+  int64_t regulate_every;   /* ReconstructionEngine(regulate_every=) */
+  int64_t fill_num;         /* fill_ratio_target numerator / denominator */
+  int64_t fill_den;
+  int64_t q_min;
+  int64_t q_max;
+  float alpha;              /* float32(params.alpha)            pipeline.py:432 */
+  float one_m_alpha;        /* float32(1 - params.alpha)        pipeline.py:433 */
+  float beta;               /* float32(params.beta)             pipeline.py:434 */
+  float half_1p_beta;       /* float32(params.half_one_plus_beta) pipeline.py:435 */
+  const float *gain;        /* optional host array [height*width] or NULL */
+  int64_t batch_capacity;   /* max in-bounds events per device batch; 0 = default */
+} fibar_config;
+
+/* Allocate device state for one sensor.  stream: a cudaStream_t (NULL = legacy default). */
+int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out);
+int fibar_destroy(fibar_engine *eng);
+int fibar_set_stream(fibar_engine *eng, void *stream);
+/* Return to the freshly constructed state (zero filter state, empty window). */
+int fibar_reset(fibar_engine *eng);
+
+/* Append one packet of n events (SoA columns x, y uint16 and p int8 in {-1,+1}).
+ * mem = FIBAR_MEM_HOST or FIBAR_MEM_DEVICE says where the three columns live.
+ * Out-of-bounds events are dropped and counted (non-strict semantics of
+ * pipeline.py:516-528); strict checks are the caller's.  Work is queued on the
+ * engine stream; packets may be coalesced until the next read. */
+int fibar_process(fibar_engine *eng, const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n,
+                  int32_t mem);
+/* Run any coalesced events now (asynchronous on the engine stream). */
+int fibar_flush(fibar_engine *eng);
+
+/* Render the brightness grid to uint8 [height*width].  out_mem says where
+ * `out` lives.  bounds (host double[2]) and degenerate (host int) are written
+ * after a stream synchronisation; pass NULL to skip them (then nothing blocks
+ * when out is device memory). */
+int fibar_render(fibar_engine *eng, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem,
+                 double *bounds, int32_t *degenerate);
+
+/* Synchronising reads (host pointers). */
+int fibar_read_qs(fibar_engine *eng, int64_t qs[10]);
+int fibar_counters(fibar_engine *eng, int64_t *event_count, int64_t *oob_dropped);
+/* Any pointer may be NULL.  Sizes: p_bar, l: n_pix float; active: n_pix uint16;
+ * tiles: tiles_x*tiles_y uint8; qx, qy: n_pix+1 uint16. */
+int fibar_read_state(fibar_engine *eng, float *p_bar, float *l, uint16_t *active, uint8_t *tiles,
+                     uint16_t *qx, uint16_t *qy);
+
+/* Diagnostics: stats[0] = device kernel launches so far, [1] = device batches,
+ * [2] = speculative window chunks, [3] = chunks re-run by the verifier,
+ * [4] = pops (window evictions) processed, [5] = counter-saturation flag. */
+int fibar_stats(fibar_engine *eng, int64_t stats[8]);
+/* Device pointer of the float32 brightness grid (valid until destroy). */
+int fibar_brightness_ptr(fibar_engine *eng, float **out);
+
+const char *fibar_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FIBAR_B200_H */

@@ -1,0 +1,95 @@
+"""ctypes binding of the C ABI in include/fibar_b200.h.
+
+The shared library is built in-tree (``python -m paper_2510_20071_b200.build``
+or ``__graft_entry__.build()``) at ``paper_2510_20071_b200/_lib/libfibar_b200.so``.
+There is no CPU fallback: if the library or a CUDA device is missing, the first
+engine construction raises :class:`~.errors.DeviceError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .errors import DeviceError, raise_for_status
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libfibar_b200.so")
+
+FIBAR_MEM_HOST = 0
+FIBAR_MEM_DEVICE = 1
+FIBAR_RENDER_ROBUST = 0
+FIBAR_RENDER_FIXED = 1
+
+EXPORTED = (
+    "fibar_create", "fibar_destroy", "fibar_set_stream", "fibar_reset", "fibar_process", "fibar_flush",
+    "fibar_render", "fibar_read_qs", "fibar_counters", "fibar_read_state", "fibar_stats",
+    "fibar_brightness_ptr", "fibar_last_error",
+)
+
+
+class FibarConfig(C.Structure):
+    _fields_ = [
+        ("width", C.c_int32),
+        ("height", C.c_int32),
+        ("tile_side", C.c_int32),
+        ("spatial_enabled", C.c_int32),
+        ("blur_enabled", C.c_int32),
+        ("reserved0", C.c_int32),
+        ("regulate_every", C.c_int64),
+        ("fill_num", C.c_int64),
+        ("fill_den", C.c_int64),
+        ("q_min", C.c_int64),
+        ("q_max", C.c_int64),
+        ("alpha", C.c_float),
+        ("one_m_alpha", C.c_float),
+        ("beta", C.c_float),
+        ("half_1p_beta", C.c_float),
+        ("gain", C.c_void_p),
+        ("batch_capacity", C.c_int64),
+    ]
+
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Load (once) and type the native library; raises DeviceError if it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        raise DeviceError(f"native library {path} not built; run __graft_entry__.build()")
+    L = C.CDLL(path)
+    P, i32, i64, f64 = C.c_void_p, C.c_int32, C.c_int64, C.c_double
+    sig = {
+        "fibar_create": ([C.POINTER(FibarConfig), P, C.POINTER(P)], C.c_int),
+        "fibar_destroy": ([P], C.c_int),
+        "fibar_set_stream": ([P, P], C.c_int),
+        "fibar_reset": ([P], C.c_int),
+        "fibar_process": ([P, P, P, P, i64, i32], C.c_int),
+        "fibar_flush": ([P], C.c_int),
+        "fibar_render": ([P, i32, f64, P, i32, P, P], C.c_int),
+        "fibar_read_qs": ([P, P], C.c_int),
+        "fibar_counters": ([P, P, P], C.c_int),
+        "fibar_read_state": ([P, P, P, P, P, P, P], C.c_int),
+        "fibar_stats": ([P, P], C.c_int),
+        "fibar_brightness_ptr": ([P, C.POINTER(P)], C.c_int),
+        "fibar_last_error": ([], C.c_char_p),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+def check(code: int, what: str) -> None:
+    if code:
+        msg = load().fibar_last_error().decode(errors="replace")
+        try:
+            raise_for_status(code, what)
+        except Exception as exc:  # attach the native message
+            raise type(exc)(f"{exc}: {msg}") from None

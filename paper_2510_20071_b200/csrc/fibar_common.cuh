@@ -1,0 +1,65 @@
+// fibar_common.cuh -- shared device types and helpers for the FIBAR sm_100a path.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define FIBAR_INF32 0xFFFFFFFFu
+
+// Per-pixel bookkeeping record (16 B, one random access per pixel touch).
+//   last : global in-bounds index of the pixel's latest event before the
+//          current device batch (-1 = never), i.e. the reference's implicit
+//          "is the pixel still queued" history, kept as a last-touch index.
+//   st/end : [st, end) positions of the pixel's events in the current batch's
+//          pixel-sorted order (st == end: no events this batch).  Reset by the
+//          final pass, so the table is clean at every batch start.
+struct __align__(16) PixRec {
+  long long last;
+  unsigned st;
+  unsigned end;
+};
+
+// Window / counter state living in device memory so no kernel needs a host
+// round trip.  Mirrors the reference's qs[10] slots (_kernels.py:48-59) plus
+// the engine counters (pipeline.py:437-439).
+struct DevState {
+  long long s;        // window start (global in-bounds index); QS_HEAD = s mod (n_pix+1)
+  long long q;        // QS_TARGET
+  long long npix;     // QS_NPIX
+  long long ntiles;   // QS_NTILES
+  long long evctr;    // QS_EVCTR
+  long long qtmin;    // QS_QTMIN
+  long long qtmax;    // QS_QTMAX
+  long long blur;     // QS_BLUR
+  long long stale;    // QS_STALE
+  long long E;        // in-bounds events consumed (event_count)
+  long long oob;      // oob_dropped
+  long long B;        // in-bounds events of the batch being processed
+  long long s_start;  // window start when the batch began
+  long long chunks;   // speculative window chunks launched (stats)
+  long long mismatch; // chunks re-run by the verifier (stats)
+  long long pops;     // total evictions (stats)
+  long long stale_batch;
+  unsigned epoch;     // batch counter (tags blur ready flags)
+  unsigned ticket;    // blur work ticket
+  long long saturated;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// strictly IEEE, separately rounded float32 arithmetic (no FMA contraction),
+// matching the reference's numba kernels bit for bit.
+__device__ __forceinline__ float fmulr(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float faddr(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float fsubr(float a, float b) { return __fsub_rn(a, b); }
+
+__device__ __forceinline__ unsigned dist32(long long later, long long earlier) {
+  long long d = later - earlier;
+  return (earlier < 0 || d >= (long long)FIBAR_INF32) ? FIBAR_INF32 : (unsigned)d;
+}

@@ -1,0 +1,1491 @@
+// fibar_engine.cu -- B200-native FIBAR reconstruction engine (sm_100a) + C ABI.
+//
+// One device batch (coalesced packets) flows through:
+//   ingest     k_count_inb / k_compact      OOB filter + compaction (pipeline.py:516-528),
+//                                            pixel keys, ring of window keys
+//   group      radix_sort_pairs              stable (tile-major key, index) sort
+//   link       k_seg_marks / k_link          per event: distance to previous same-pixel /
+//                                            same-tile event; per ring slot: distance to next
+//   window     k_anchor / k_anchor_scan /    the reference's FIFO window (_kernels.py:132-205)
+//              k_window_run / k_window_fix   reproduced exactly by chunked speculation +
+//                                            verification
+//   stale      k_popj                        eviction event of every popped entry; stale iff
+//                                            the pixel has no later event before its eviction
+//   temporal   k_temporal                    per-pixel in-order replay of the two-stage IIR
+//                                            (_kernels.py:62-73 / 120-130), bit exact
+//   blur       k_blur                        3x3 renormalised blur of stale pixels in eviction
+//                                            order (_kernels.py:173-189), dataflow over a
+//                                            persistent grid with per-item ready flags
+//   final      k_final / k_batch_end         end-of-batch brightness, last-touch tables
+//
+// Float32 arithmetic uses __fmul_rn/__fadd_rn (never contracted to FMA) so the
+// result is bit-identical to the reference's strict-IEEE numba kernels.
+#include <cstdio>
+#include <cstring>
+#include <cmath>
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "fibar_common.cuh"
+#include "fibar_internal.h"
+#include "../../include/fibar_b200.h"
+
+using namespace fibar;
+
+namespace {
+
+constexpr int CHUNK = 64;    // events per speculative window chunk
+constexpr int WARM = 128;    // warm-up events before a chunk's first own event
+constexpr int NCAND = 24;    // candidate window lengths per chunk (fixed-point search)
+constexpr int TPB = 256;
+
+__constant__ long long c_cand_off[NCAND] = {-16384, -8192, -4096, -2048, -1024, -512, -256, -128,
+                                            -64,    -32,   0,     32,    64,    128,   256,  512,
+                                            1024,   2048,  4096,  8192,  16384, 32768, 65536, 131072};
+
+struct ChunkRec {
+  long long st_s, st_q;                          // state after event b_c - 1 (speculative start)
+  long long en_s, en_q, en_np, en_nt, en_ev;     // state after the chunk's last event
+  long long qlo, qhi;                            // extrema of the targets set inside the chunk
+};
+
+struct SelState {
+  unsigned prefix[4];
+  unsigned rank[4];
+  unsigned hist[4][2048];
+  double lo, hi;
+  int degenerate;
+  int pad;
+};
+
+struct Ctx {
+  int W, H, ts, tiles_x, A;
+  long long n_pix;
+  long long num, den, qmin, qmax, every;
+  float alpha, oma, beta, h;
+  int use_gain, blur_on, spatial;
+  DevState *st;
+  float *pbar, *l;
+  const float *gain;
+  PixRec *pt;
+  long long *last_tile;
+  uint2 *ptt;
+  unsigned *rkey;
+  uint2 *rnext;
+  unsigned long long Rm;
+  const uint16_t *raw_x, *raw_y;
+  const int8_t *raw_p;
+  long long n_raw;
+  unsigned *blockcnt;
+  unsigned *ekey;
+  int8_t *epol;
+  unsigned *tkey;                 // unsorted tile-major keys (sort input)
+  const unsigned *skey, *sidx;    // sorted keys / batch-local event index
+  uint2 *dp;
+  unsigned *S, *popj;
+  float *t2, *L0, *bval;
+  unsigned *ready;
+  int2 *anc;
+  ChunkRec *ch;
+};
+
+// ---------------------------------------------------------------- ingest ---
+
+constexpr int IN_ITEMS = 8;
+constexpr int IN_TILE = TPB * IN_ITEMS;
+
+__global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
+  __shared__ unsigned wsum[TPB / 32];
+  const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
+  unsigned cnt = 0;
+#pragma unroll
+  for (int r = 0; r < IN_ITEMS; ++r) {
+    long long i = base + r;
+    if (i < x.n_raw) cnt += (x.raw_x[i] < x.W) & (x.raw_y[i] < x.H);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < TPB / 32; ++w) t += wsum[w];
+    x.blockcnt[blockIdx.x] = t;
+    if (blockIdx.x == 0) x.blockcnt[nblocks] = 0;
+  }
+}
+
+__global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
+  __shared__ unsigned wsum[TPB / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long E0 = x.st->E;
+  const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
+  bool keep[IN_ITEMS];
+  unsigned cnt = 0;
+#pragma unroll
+  for (int r = 0; r < IN_ITEMS; ++r) {
+    long long i = base + r;
+    keep[r] = i < x.n_raw && (x.raw_x[i] < x.W) && (x.raw_y[i] < x.H);
+    cnt += keep[r];
+  }
+  unsigned incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  unsigned wofs = 0;
+  for (int w = 0; w < wid; ++w) wofs += wsum[w];
+  unsigned pos = x.blockcnt[blockIdx.x] + wofs + incl - cnt;
+#pragma unroll
+  for (int r = 0; r < IN_ITEMS; ++r) {
+    if (!keep[r]) continue;
+    long long i = base + r;
+    const unsigned xx = x.raw_x[i], yy = x.raw_y[i];
+    const unsigned key = yy * (unsigned)x.W + xx;
+    const unsigned tile = (yy / x.ts) * (unsigned)x.tiles_x + xx / x.ts;
+    const unsigned sub = (yy % x.ts) * x.ts + xx % x.ts;
+    x.ekey[pos] = key;
+    x.tkey[pos] = tile * (unsigned)x.A + sub;
+    x.epol[pos] = x.raw_p[i];
+    if (x.spatial) x.rkey[(unsigned long long)(E0 + pos) & x.Rm] = key;
+    ++pos;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const long long B = x.blockcnt[nblocks];
+    DevState *s = x.st;
+    s->B = B;
+    s->oob += x.n_raw - B;
+    s->s_start = s->s;
+    s->stale_batch = 0;
+    s->ticket = 0;
+  }
+}
+
+// ------------------------------------------------------------------ link ---
+
+__global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
+  const long long B = x.st->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned k = x.skey[i];
+  const unsigned c = x.ekey[x.sidx[i]];
+  const bool head = i == 0 || x.skey[i - 1] != k;
+  const bool tail = i == B - 1 || x.skey[i + 1] != k;
+  if (head) x.pt[c].st = (unsigned)i;
+  if (tail) x.pt[c].end = (unsigned)(i + 1);
+  const unsigned t = k / x.A;
+  if (i == 0 || x.skey[i - 1] / x.A != t) x.ptt[t].x = (unsigned)i;
+  if (i == B - 1 || x.skey[i + 1] / x.A != t) x.ptt[t].y = (unsigned)(i + 1);
+}
+
+__global__ void __launch_bounds__(TPB) k_link(Ctx x) {
+  const long long B = x.st->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const long long E0 = x.st->E;
+  const unsigned key = x.skey[i];
+  const unsigned jj = x.sidx[i];
+  const long long j = E0 + jj;
+  const unsigned c = x.ekey[jj];
+  const unsigned t = key / x.A;
+  const long long lo_ok = max(0LL, E0 + B - (long long)(x.Rm + 1));   // oldest index whose slot is not reused
+
+  // pixel links: neighbours in the sorted order
+  const bool first_pix = i == 0 || x.skey[i - 1] != key;
+  const bool last_pix = i == B - 1 || x.skey[i + 1] != key;
+  const long long pre_last = x.pt[c].last;
+  const long long prev_p = first_pix ? pre_last : E0 + x.sidx[i - 1];
+  const long long next_p = last_pix ? -1 : E0 + x.sidx[i + 1];
+
+  // tile links: latest earlier / earliest later event in the tile segment
+  const uint2 tr = x.ptt[t];
+  long long prev_t = -1, next_t = -1;
+  if (tr.y - tr.x <= 64) {
+    unsigned best_lo = 0, best_hi = 0xFFFFFFFFu;
+    bool have_lo = false;
+    for (unsigned q = tr.x; q < tr.y; ++q) {
+      unsigned o = x.sidx[q];
+      if (o < jj) {
+        if (!have_lo || o > best_lo) best_lo = o;
+        have_lo = true;
+      } else if (o > jj && o < best_hi) {
+        best_hi = o;
+      }
+    }
+    if (have_lo) prev_t = E0 + best_lo;
+    if (best_hi != 0xFFFFFFFFu) next_t = E0 + best_hi;
+  } else {
+    const int tx = (int)(t % (unsigned)x.tiles_x), ty = (int)(t / (unsigned)x.tiles_x);
+    for (int dy = 0; dy < x.ts; ++dy) {
+      const int yy = ty * x.ts + dy;
+      if (yy >= x.H) break;
+      for (int dx = 0; dx < x.ts; ++dx) {
+        const int xx = tx * x.ts + dx;
+        if (xx >= x.W) break;
+        const PixRec r = x.pt[(unsigned)yy * x.W + xx];
+        if (r.end <= r.st) continue;
+        // first position in [st, end) with sidx >= jj
+        unsigned lo = r.st, hi = r.end;
+        while (lo < hi) {
+          unsigned mid = (lo + hi) >> 1;
+          if (x.sidx[mid] < jj) lo = mid + 1; else hi = mid;
+        }
+        if (lo > r.st) prev_t = max(prev_t, E0 + (long long)x.sidx[lo - 1]);
+        unsigned up = (lo < r.end && x.sidx[lo] == jj) ? lo + 1 : lo;
+        if (up < r.end) {
+          long long cand = E0 + x.sidx[up];
+          next_t = next_t < 0 ? cand : min(next_t, cand);
+        }
+      }
+    }
+  }
+  const bool first_tile = prev_t < 0;
+  if (first_tile) prev_t = x.last_tile[t];
+
+  x.dp[jj] = make_uint2(dist32(j, prev_p), dist32(j, prev_t));
+  x.rnext[(unsigned long long)j & x.Rm] =
+      make_uint2(next_p < 0 ? FIBAR_INF32 : (unsigned)(next_p - j), next_t < 0 ? FIBAR_INF32 : (unsigned)(next_t - j));
+  if (first_pix && pre_last >= lo_ok && pre_last >= 0) {
+    long long d = j - pre_last;
+    x.rnext[(unsigned long long)pre_last & x.Rm].x = d >= FIBAR_INF32 ? FIBAR_INF32 : (unsigned)d;
+  }
+  if (first_tile && prev_t >= lo_ok && prev_t >= 0) {
+    long long d = j - prev_t;
+    x.rnext[(unsigned long long)prev_t & x.Rm].y = d >= FIBAR_INF32 ? FIBAR_INF32 : (unsigned)d;
+  }
+}
+
+// ---------------------------------------------------------------- window ---
+
+struct WState {
+  long long s, q, npix, ntiles, evctr;
+};
+
+__device__ __forceinline__ long long chunk_warm_start(long long E0, int c) {
+  return max(E0, E0 + (long long)c * CHUNK - WARM);
+}
+
+__device__ __forceinline__ long long cand_len(const Ctx &x, long long q0, int i) {
+  long long L = q0 + c_cand_off[i];
+  return L < 1 ? 1 : (L > x.qmax ? x.qmax : L);
+}
+
+// The reference's per-event queue bookkeeping (_kernels.py:132-205) restated on
+// the suffix window [s, j]: the push of event j activates its pixel / tile iff
+// its previous same-pixel / same-tile event lies before s; the trim pops
+// [s, j+1-q) and each popped k deactivates iff its next occurrence lies after j.
+__device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, long long E0, long long s_start,
+                           bool write, long long &qlo, long long &qhi) {
+  for (long long j = jf; j < jt; ++j) {
+    const uint2 d = x.dp[j - E0];
+    const unsigned long long js = (unsigned long long)(j - w.s);
+    w.npix += (unsigned long long)d.x > js;
+    w.ntiles += (unsigned long long)d.y > js;
+    long long len = j - w.s + 1;
+    if (len > w.q) {
+      const long long snew = j + 1 - w.q;
+      long long np = w.npix, nt = w.ntiles;
+      for (long long k = w.s; k < snew; ++k) {
+        const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+        const unsigned long long dd = (unsigned long long)(j - k);
+        np -= (unsigned long long)r.x > dd;
+        nt -= (unsigned long long)r.y > dd;
+      }
+      w.npix = np;
+      w.ntiles = nt;
+      w.s = snew;
+      len = w.q;
+    }
+    if (++w.evctr >= x.every) {
+      w.evctr = 0;
+      if (w.npix >= 1 && w.ntiles >= 1) {
+        long long qn = (len * x.num * w.ntiles * (long long)x.A) / (x.den * w.npix);
+        qn = qn < x.qmin ? x.qmin : (qn > x.qmax ? x.qmax : qn);
+        w.q = qn;
+        qlo = min(qlo, qn);
+        qhi = max(qhi, qn);
+      }
+    }
+    if (write) x.S[j - E0] = (unsigned)(w.s - s_start);
+  }
+}
+
+// Exact distinct-pixel / distinct-tile counts for every chunk's candidate
+// windows [max(s_start, a_c - L_i), a_c - 1], as deltas from the previous
+// chunk's window of the same candidate (one warp per chunk).
+__global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
+  const long long B = x.st->B;
+  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const int lane = threadIdx.x & 31;
+  const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
+  if (c >= T) return;
+  const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
+  const long long a = chunk_warm_start(E0, c);
+  const long long Jc = a - 1;
+  const long long ap = c == 1 ? E0 : chunk_warm_start(E0, c - 1);
+  const long long Jp = ap - 1;
+  int cp[NCAND], ct[NCAND];
+  long long sp[NCAND];
+#pragma unroll
+  for (int i = 0; i < NCAND; ++i) {
+    cp[i] = 0;
+    ct[i] = 0;
+    const long long L = cand_len(x, q0, i);
+    sp[i] = c == 1 ? s0 : max(s0, ap - L);
+  }
+  // grow the right edge (Jp, Jc] with the previous starts
+  for (long long k = Jp + 1 + lane; k <= Jc; k += 32) {
+    const uint2 d = x.dp[k - E0];
+#pragma unroll
+    for (int i = 0; i < NCAND; ++i) {
+      const unsigned long long ks = (unsigned long long)(k - sp[i]);
+      cp[i] += (unsigned long long)d.x > ks;
+      ct[i] += (unsigned long long)d.y > ks;
+    }
+  }
+  // shrink the left edge to the new starts
+#pragma unroll
+  for (int i = 0; i < NCAND; ++i) {
+    const long long L = cand_len(x, q0, i);
+    const long long sn = max(s0, a - L);
+    for (long long k = sp[i] + lane; k < sn; k += 32) {
+      const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+      const unsigned long long dd = (unsigned long long)(Jc - k);
+      cp[i] -= (unsigned long long)r.x > dd;
+      ct[i] -= (unsigned long long)r.y > dd;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NCAND; ++i) {
+    int vp = cp[i], vt = ct[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      vp += __shfl_xor_sync(0xffffffffu, vp, o);
+      vt += __shfl_xor_sync(0xffffffffu, vt, o);
+    }
+    if (lane == 0) x.anc[(long long)c * NCAND + i] = make_int2(vp, vt);
+  }
+}
+
+// inclusive scan of the deltas over chunks, one CTA per candidate
+__global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x) {
+  __shared__ int2 wt[32];
+  __shared__ int2 carry;
+  const long long B = x.st->B;
+  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const int i = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = make_int2((int)x.st->npix, (int)x.st->ntiles);
+  __syncthreads();
+  for (int base = 1; base < T; base += 1024) {
+    const int c = base + threadIdx.x;
+    int2 v = c < T ? x.anc[(long long)c * NCAND + i] : make_int2(0, 0);
+    int2 inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int tx = __shfl_up_sync(0xffffffffu, inc.x, o), ty = __shfl_up_sync(0xffffffffu, inc.y, o);
+      if (lane >= o) {
+        inc.x += tx;
+        inc.y += ty;
+      }
+    }
+    if (lane == 31) wt[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      int2 w = wt[lane], wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int tx = __shfl_up_sync(0xffffffffu, wi.x, o), ty = __shfl_up_sync(0xffffffffu, wi.y, o);
+        if (lane >= o) {
+          wi.x += tx;
+          wi.y += ty;
+        }
+      }
+      wt[lane] = make_int2(wi.x - w.x, wi.y - w.y);
+    }
+    __syncthreads();
+    const int2 cc = carry;
+    const int2 out = make_int2(cc.x + wt[wid].x + inc.x, cc.y + wt[wid].y + inc.y);
+    if (c < T) x.anc[(long long)c * NCAND + i] = out;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = out;
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ long long regulate(const Ctx &x, long long len, long long np, long long nt) {
+  long long qn = (len * x.num * nt * (long long)x.A) / (x.den * np);
+  return qn < x.qmin ? x.qmin : (qn > x.qmax ? x.qmax : qn);
+}
+
+// one thread per chunk: choose a start window (longest candidate just past
+// the regulator's fixed point), warm up, then run the chunk's own events.
+__global__ void __launch_bounds__(128) k_window_run(Ctx x) {
+  const long long B = x.st->B;
+  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const int c = blockIdx.x * 128 + threadIdx.x;
+  if (c >= T) return;
+  const DevState s = *x.st;
+  const long long E0 = s.E;
+  const long long b = E0 + (long long)c * CHUNK;
+  const long long e = min(E0 + B, b + CHUNK);
+  long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
+  WState w;
+  const long long a = chunk_warm_start(E0, c);
+  if (a == E0) {
+    w.s = s.s_start;
+    w.q = s.q;
+    w.npix = s.npix;
+    w.ntiles = s.ntiles;
+    w.evctr = s.evctr;
+  } else {
+    int g = 0, istar = -1;
+#pragma unroll 1
+    for (int i = 0; i < NCAND; ++i) {
+      const long long L = cand_len(x, s.q, i);
+      const long long sc = max(s.s_start, a - L);
+      const int2 cnt = x.anc[(long long)c * NCAND + i];
+      const long long len = a - sc;
+      if (cnt.x >= 1 && cnt.y >= 1 && regulate(x, len, cnt.x, cnt.y) >= len) istar = i;
+    }
+    g = istar + 1 < NCAND ? istar + 1 : NCAND - 1;
+    const long long L = cand_len(x, s.q, g);
+    const int2 cnt = x.anc[(long long)c * NCAND + g];
+    w.s = max(s.s_start, a - L);
+    w.npix = cnt.x;
+    w.ntiles = cnt.y;
+    const long long len = a - w.s;
+    w.q = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) : len;
+    w.evctr = (s.evctr + (a - E0)) % x.every;
+  }
+  long long dlo = qlo, dhi = qhi;
+  run_window(x, w, a, b, E0, s.s_start, false, dlo, dhi);
+  ChunkRec r;
+  r.st_s = w.s;
+  r.st_q = w.q;
+  run_window(x, w, b, e, E0, s.s_start, true, qlo, qhi);
+  r.en_s = w.s;
+  r.en_q = w.q;
+  r.en_np = w.npix;
+  r.en_nt = w.ntiles;
+  r.en_ev = w.evctr;
+  r.qlo = qlo;
+  r.qhi = qhi;
+  x.ch[c] = r;
+}
+
+// verify chunk boundaries in order, re-running any chunk whose speculative
+// start differs from its predecessor's exact end; then publish the state.
+__global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
+  __shared__ int first_bad;
+  __shared__ long long red_lo[32], red_hi[32];
+  const long long B = x.st->B;
+  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const long long E0 = x.st->E, s_start = x.st->s_start;
+  int c0 = 1;
+  int nfix = 0;
+  while (true) {
+    if (threadIdx.x == 0) first_bad = 0x7FFFFFFF;
+    __syncthreads();
+    for (int c = c0 + threadIdx.x; c < T; c += 1024) {
+      const ChunkRec &p = x.ch[c - 1];
+      const ChunkRec &q = x.ch[c];
+      if (q.st_s != p.en_s || q.st_q != p.en_q) atomicMin(&first_bad, c);
+    }
+    __syncthreads();
+    const int m = first_bad;
+    __syncthreads();
+    if (m == 0x7FFFFFFF) break;
+    if (threadIdx.x == 0) {
+      const ChunkRec p = x.ch[m - 1];
+      WState w{p.en_s, p.en_q, p.en_np, p.en_nt, p.en_ev};
+      long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
+      const long long b = E0 + (long long)m * CHUNK;
+      const long long e = min(E0 + B, b + CHUNK);
+      run_window(x, w, b, e, E0, s_start, true, qlo, qhi);
+      ChunkRec r;
+      r.st_s = p.en_s;
+      r.st_q = p.en_q;
+      r.en_s = w.s;
+      r.en_q = w.q;
+      r.en_np = w.npix;
+      r.en_nt = w.ntiles;
+      r.en_ev = w.evctr;
+      r.qlo = qlo;
+      r.qhi = qhi;
+      x.ch[m] = r;
+      __threadfence_block();
+    }
+    ++nfix;
+    c0 = m + 1;
+    __syncthreads();
+  }
+  long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
+  for (int c = threadIdx.x; c < T; c += 1024) {
+    lo = min(lo, x.ch[c].qlo);
+    hi = max(hi, x.ch[c].qhi);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red_lo[threadIdx.x >> 5] = lo;
+    red_hi[threadIdx.x >> 5] = hi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < 32; ++w) {
+      lo = min(lo, red_lo[w]);
+      hi = max(hi, red_hi[w]);
+    }
+    DevState *s = x.st;
+    if (T > 0) {
+      const ChunkRec &r = x.ch[T - 1];
+      s->s = r.en_s;
+      s->q = r.en_q;
+      s->npix = r.en_np;
+      s->ntiles = r.en_nt;
+      s->evctr = r.en_ev;
+      if (hi >= 0) {
+        s->qtmin = min(s->qtmin, lo);
+        s->qtmax = max(s->qtmax, hi);
+      }
+      s->pops += r.en_s - s_start;
+    }
+    s->chunks += T;
+    s->mismatch += nfix;
+  }
+}
+
+// ----------------------------------------------------------------- stale ---
+
+__global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
+  __shared__ unsigned wsum[TPB / 32];
+  const long long B = x.st->B;
+  const long long jj = (long long)blockIdx.x * TPB + threadIdx.x;
+  const long long E0 = x.st->E, s_start = x.st->s_start;
+  unsigned nst = 0;
+  if (jj < B) {
+    const unsigned lo = jj == 0 ? 0u : x.S[jj - 1];
+    const unsigned hi = x.S[jj];
+    const long long j = E0 + jj;
+    for (unsigned p = lo; p < hi; ++p) {
+      x.popj[p] = (unsigned)jj;
+      const long long k = s_start + p;
+      nst += (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) nst += __shfl_xor_sync(0xffffffffu, nst, o);
+  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = nst;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < TPB / 32; ++w) t += wsum[w];
+    if (t) atomicAdd((unsigned long long *)&x.st->stale_batch, (unsigned long long)t);
+  }
+}
+
+// -------------------------------------------------------------- temporal ---
+
+// one thread per pixel segment, replaying its events in stream order with the
+// reference's exact float32 operation order (_kernels.py:67-73).
+__global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
+  const long long B = x.st->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned key = x.skey[i];
+  if (i > 0 && x.skey[i - 1] == key) return;
+  const unsigned c = x.ekey[x.sidx[i]];
+  float pb = x.pbar[c], lv = x.l[c];
+  const float g = x.use_gain ? x.gain[c] : 1.0f;
+  long long pos = i;
+  do {
+    const float p = (float)x.epol[x.sidx[pos]];
+    pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+    float d = fsubr(p, pb);
+    if (x.use_gain) d = fmulr(d, g);
+    const float tt = fmulr(x.h, d);
+    lv = faddr(fmulr(x.beta, lv), tt);
+    if (x.spatial) {
+      x.t2[pos] = tt;
+      x.L0[pos] = lv;
+    }
+    ++pos;
+  } while (pos < B && x.skey[pos] == key);
+  x.pbar[c] = pb;
+  if (!x.spatial) x.l[c] = lv;
+}
+
+// ------------------------------------------------------------------- blur ---
+
+struct BatchScalars {
+  long long E0, B, s_start, s_end;
+  unsigned epoch;
+};
+
+__device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
+  BatchScalars b;
+  b.E0 = x.st->E;
+  b.B = x.st->B;
+  b.s_start = x.st->s_start;
+  b.s_end = b.B > 0 ? b.s_start + x.S[b.B - 1] : b.s_start;
+  b.epoch = x.st->epoch;
+  return b;
+}
+
+// k popped in this batch and stale (no later same-pixel event before its pop)?
+__device__ __forceinline__ bool stale_item(const Ctx &x, const BatchScalars &b, long long k, unsigned &item) {
+  if (k < b.s_start || k >= b.s_end) return false;
+  const unsigned p = (unsigned)(k - b.s_start);
+  const long long J = b.E0 + x.popj[p];
+  if ((unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(J - k)) {
+    item = p;
+    return true;
+  }
+  return false;
+}
+
+__device__ __forceinline__ bool fetch_bval(const Ctx &x, const BatchScalars &b, unsigned q, float &v) {
+  if (ld_acquire_u32(&x.ready[q]) != b.epoch) return false;
+  v = __ldcg(&x.bval[q]);
+  return true;
+}
+
+// brightness of pixel n right after the temporal update at sorted position i
+// (segment starting at st; lp = pixel's last event before the batch)
+__device__ bool value_after(const Ctx &x, const BatchScalars &b, long long st, long long i, long long lp, float &v) {
+  long long pos = i - 1;
+  for (; pos >= st; --pos) {
+    unsigned q;
+    if (stale_item(x, b, b.E0 + x.sidx[pos], q)) {
+      if (!fetch_bval(x, b, q, v)) return false;
+      break;
+    }
+  }
+  if (pos < st) {
+    unsigned q;
+    if (lp >= 0 && stale_item(x, b, lp, q)) {
+      if (!fetch_bval(x, b, q, v)) return false;
+    } else {
+      v = x.L0[i];
+      return true;
+    }
+  }
+  for (long long r = pos + 1; r <= i; ++r) v = faddr(fmulr(x.beta, v), x.t2[r]);
+  return true;
+}
+
+// brightness of pixel n as seen by blur item pb (eviction at event J)
+__device__ bool tap_value(const Ctx &x, const BatchScalars &b, unsigned n, long long J, unsigned pb, float &v) {
+  const PixRec r = x.pt[n];
+  if (r.end <= r.st || b.E0 + (long long)x.sidx[r.st] > J) {
+    unsigned q;
+    if (r.last >= 0 && stale_item(x, b, r.last, q) && q < pb) return fetch_bval(x, b, q, v);
+    v = x.l[n];
+    return true;
+  }
+  unsigned lo = r.st, hi = r.end;
+  while (lo < hi) {
+    const unsigned mid = (lo + hi) >> 1;
+    if (b.E0 + (long long)x.sidx[mid] <= J) lo = mid + 1; else hi = mid;
+  }
+  const long long i = (long long)lo - 1;
+  unsigned q;
+  if (stale_item(x, b, b.E0 + x.sidx[i], q) && q < pb) return fetch_bval(x, b, q, v);
+  return value_after(x, b, r.st, i, r.last, v);
+}
+
+// renormalised 3x3 binomial blur, taps dy-outer / dx-inner (_kernels.py:174-188)
+__device__ bool blur_item(const Ctx &x, const BatchScalars &b, unsigned p, float &out) {
+  const long long k = b.s_start + p;
+  const long long J = b.E0 + x.popj[p];
+  const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
+  const int cx = (int)(c % (unsigned)x.W), cy = (int)(c / (unsigned)x.W);
+  float num = 0.0f, den = 0.0f;
+  for (int dy = -1; dy <= 1; ++dy) {
+    const int yy = cy + dy;
+    if (yy < 0 || yy >= x.H) continue;
+    const int wy = dy == 0 ? 2 : 1;
+    for (int dx = -1; dx <= 1; ++dx) {
+      const int xx = cx + dx;
+      if (xx < 0 || xx >= x.W) continue;
+      const float w = (float)(wy * (dx == 0 ? 2 : 1));
+      float v;
+      if (!tap_value(x, b, (unsigned)yy * x.W + xx, J, p, v)) return false;
+      num = faddr(num, fmulr(w, v));
+      den = faddr(den, w);
+    }
+  }
+  out = __fdiv_rn(num, den);
+  return true;
+}
+
+// Persistent dataflow: warps take 32 consecutive eviction items in order from
+// a global ticket, so every dependency (an earlier item) is held by a warp that
+// is already running; items wait on per-item ready flags (epoch tagged).
+__global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
+  const BatchScalars b = load_bs(x);
+  const unsigned npop = (unsigned)(b.s_end - b.s_start);
+  const int lane = threadIdx.x & 31;
+  while (true) {
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(&x.st->ticket, 32u);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (base >= npop) break;
+    const unsigned p = base + lane;
+    bool done = true;
+    if (p < npop) {
+      unsigned q;
+      done = !stale_item(x, b, b.s_start + p, q);
+    }
+    while (true) {
+      if (!done) {
+        float v;
+        if (blur_item(x, b, p, v)) {
+          __stcg(&x.bval[p], v);
+          st_release_u32(&x.ready[p], b.epoch);
+          done = true;
+        }
+      }
+      if (__all_sync(0xffffffffu, done)) break;
+      if (!done) __nanosleep(20);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ final ---
+
+__global__ void __launch_bounds__(TPB) k_final(Ctx x) {
+  const BatchScalars b = load_bs(x);
+  const long long npop = b.s_end - b.s_start;
+  const long long total = b.B + npop;
+  for (long long idx = (long long)blockIdx.x * TPB + threadIdx.x; idx < total; idx += (long long)gridDim.x * TPB) {
+    if (idx < b.B) {
+      const long long pos = idx;
+      if (pos + 1 < b.B && x.skey[pos + 1] == x.skey[pos]) continue;   // segment tails only
+      const unsigned c = x.ekey[x.sidx[pos]];
+      const PixRec r = x.pt[c];
+      const long long e = b.E0 + x.sidx[pos];
+      float v = x.L0[pos];
+      if (x.blur_on) {
+        unsigned q;
+        if (stale_item(x, b, e, q)) v = x.bval[q];
+        else value_after(x, b, r.st, pos, r.last, v);
+      }
+      x.l[c] = v;
+      PixRec nr;
+      nr.last = e;
+      nr.st = 0;
+      nr.end = 0;
+      x.pt[c] = nr;
+      const unsigned t = x.skey[pos] / x.A;
+      atomicMax(&x.last_tile[t], e);
+    } else if (x.blur_on) {
+      const unsigned p = (unsigned)(idx - b.B);
+      const long long k = b.s_start + p;
+      unsigned q;
+      if (k < b.E0 && stale_item(x, b, k, q)) {
+        // carried-only pixel: no events in this batch after its last pre-batch event
+        const uint2 rn = x.rnext[(unsigned long long)k & x.Rm];
+        if ((unsigned long long)rn.x > (unsigned long long)(b.E0 + b.B - 1 - k)) x.l[x.rkey[(unsigned long long)k & x.Rm]] = x.bval[p];
+      }
+    }
+  }
+}
+
+__global__ void k_batch_end(Ctx x) {
+  DevState *s = x.st;
+  s->E += s->B;
+  if (x.spatial) {
+    s->stale += s->stale_batch;
+    if (x.blur_on) s->blur += s->stale_batch;
+  }
+  s->epoch += 1;
+}
+
+// ---------------------------------------------------------------- read-out ---
+
+__device__ __forceinline__ unsigned order_key(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float order_unkey(unsigned k) {
+  const unsigned u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(u);
+}
+
+// histogram pass of an exact radix select (digits 11/11/10 bits, MSB first)
+__global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, long long n, SelState *sel, int pass) {
+  __shared__ unsigned h[4][2048];
+  const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+  const unsigned dmask = pass == 2 ? 1023u : 2047u;
+  const unsigned hmask = pass == 0 ? 0u : (pass == 1 ? 0xFFE00000u : 0xFFFFFC00u);
+  unsigned pref[4];
+  bool act[4];
+  for (int t = 0; t < 4; ++t) {
+    pref[t] = sel->prefix[t];
+    act[t] = true;
+    for (int u = 0; u < t; ++u)
+      if (pref[u] == pref[t]) act[t] = false;
+  }
+  for (int i = threadIdx.x; i < 4 * 2048; i += TPB) (&h[0][0])[i] = 0;
+  __syncthreads();
+  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
+    const unsigned k = order_key(l[i]);
+    const unsigned d = (k >> shift) & dmask;
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      if (act[t] && (k & hmask) == pref[t]) atomicAdd(&h[t][d], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 2048; i += TPB) {
+    const unsigned v = (&h[0][0])[i];
+    if (v) atomicAdd(&(&sel->hist[0][0])[i], v);
+  }
+}
+
+__global__ void k_sel_pick(SelState *sel, int pass) {
+  // one warp per target
+  const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (t >= 4) return;
+  const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
+  const int nd = pass == 2 ? 1024 : 2048;
+  int src = t;
+  for (int u = 0; u < t; ++u)
+    if (sel->prefix[u] == sel->prefix[t]) {
+      src = u;
+      break;
+    }
+  unsigned rank = sel->rank[t];
+  unsigned run = 0;
+  unsigned found_d = 0, found_before = 0;
+  bool found = false;
+  for (int base = 0; base < nd && !found; base += 32) {
+    const unsigned v = sel->hist[src][base + lane];
+    unsigned inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned tt = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += tt;
+    }
+    const unsigned excl = run + inc - v;
+    const bool hit = rank >= excl && rank < run + inc;
+    const unsigned m = __ballot_sync(0xffffffffu, hit);
+    if (m) {
+      const int L = __ffs(m) - 1;
+      found_d = base + L;
+      found_before = __shfl_sync(0xffffffffu, excl, L);
+      found = true;
+    }
+    run += __shfl_sync(0xffffffffu, inc, 31);
+  }
+  __syncwarp();
+  __syncthreads();
+  if (lane == 0) {
+    sel->prefix[t] |= found_d << shift;
+    sel->rank[t] = rank - found_before;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 4 * 2048; i += blockDim.x) (&sel->hist[0][0])[i] = 0;
+}
+
+// lo/hi from the selected order statistics (numpy 'linear' percentile, _lerp)
+__global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound) {
+  double lo, hi;
+  if (mode == FIBAR_RENDER_ROBUST) {
+    const double a0 = (double)order_unkey(sel->prefix[0]), b0 = (double)order_unkey(sel->prefix[1]);
+    const double a1 = (double)order_unkey(sel->prefix[2]), b1 = (double)order_unkey(sel->prefix[3]);
+    const double d0 = __dsub_rn(b0, a0), d1 = __dsub_rn(b1, a1);
+    lo = g_lo >= 0.5 ? __dsub_rn(b0, __dmul_rn(d0, __dsub_rn(1.0, g_lo))) : __dadd_rn(a0, __dmul_rn(d0, g_lo));
+    hi = g_hi >= 0.5 ? __dsub_rn(b1, __dmul_rn(d1, __dsub_rn(1.0, g_hi))) : __dadd_rn(a1, __dmul_rn(d1, g_hi));
+  } else {
+    lo = -fixed_bound;
+    hi = fixed_bound;
+  }
+  sel->lo = lo;
+  sel->hi = hi;
+  sel->degenerate = !(hi > lo);
+}
+
+// u8 = clip(floor((v - lo) * (255 / (hi - lo)) + 0.5), 0, 255) in float64
+// (pipeline.py:582-583); degenerate grids render mid-gray (pipeline.py:578-581)
+__global__ void __launch_bounds__(TPB) k_render_map(const float *__restrict__ l, long long n,
+                                                     const SelState *__restrict__ sel, uint8_t *__restrict__ out) {
+  const double lo = sel->lo, hi = sel->hi;
+  const bool deg = sel->degenerate;
+  const double scale = deg ? 0.0 : __ddiv_rn(255.0, __dsub_rn(hi, lo));
+  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
+    uint8_t o = 128;
+    if (!deg) {
+      const double s = __dmul_rn(__dsub_rn((double)l[i], lo), scale);
+      double r = floor(__dadd_rn(s, 0.5));
+      r = r < 0.0 ? 0.0 : (r > 255.0 ? 255.0 : r);
+      o = (uint8_t)r;
+    }
+    out[i] = o;
+  }
+}
+
+// --------------------------------------------------------- state export ---
+
+__global__ void k_active_counts(Ctx x, unsigned *cnt) {
+  const long long s = x.st->s, E = x.st->E;
+  for (long long k = s + (long long)blockIdx.x * TPB + threadIdx.x; k < E; k += (long long)gridDim.x * TPB)
+    atomicAdd(&cnt[x.rkey[(unsigned long long)k & x.Rm]], 1u);
+}
+
+__global__ void k_tile_counts(Ctx x, const unsigned *cnt, unsigned *tcnt) {
+  for (long long c = (long long)blockIdx.x * TPB + threadIdx.x; c < x.n_pix; c += (long long)gridDim.x * TPB) {
+    if (cnt[c] == 0) continue;
+    const unsigned xx = (unsigned)(c % x.W), yy = (unsigned)(c / x.W);
+    atomicAdd(&tcnt[(yy / x.ts) * x.tiles_x + xx / x.ts], 1u);
+  }
+}
+
+__global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy) {
+  const long long E = x.st->E;
+  const long long qcap = x.n_pix + 1;
+  for (long long t = (long long)blockIdx.x * TPB + threadIdx.x; t < qcap; t += (long long)gridDim.x * TPB) {
+    uint16_t ox = 0, oy = 0;
+    if (E - 1 >= t) {
+      const long long k = t + ((E - 1 - t) / qcap) * qcap;
+      const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
+      ox = (uint16_t)(c % (unsigned)x.W);
+      oy = (uint16_t)(c / (unsigned)x.W);
+    }
+    qx[t] = ox;
+    qy[t] = oy;
+  }
+}
+
+__global__ void k_init_state(DevState *s, long long q0) {
+  memset(s, 0, sizeof(DevState));
+  s->q = q0;
+  s->qtmin = q0;
+  s->qtmax = q0;
+  s->epoch = 1;
+}
+
+__global__ void k_fill_ll(long long *p, long long n, long long v) {
+  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) p[i] = v;
+}
+__global__ void k_init_pt(PixRec *p, long long n) {
+  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
+    PixRec r;
+    r.last = -1;
+    r.st = 0;
+    r.end = 0;
+    p[i] = r;
+  }
+}
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return FIBAR_E_CUDA;
+}
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+  } while (0)
+
+int ceil_log2(long long v) {
+  int b = 0;
+  while ((1LL << b) < v) ++b;
+  return b;
+}
+
+}  // namespace
+
+struct fibar_engine {
+  fibar_config cfg{};
+  int W = 0, H = 0, ts = 2, A = 4, tiles_x = 0, tiles_y = 0;
+  long long n_pix = 0, n_tiles = 0;
+  long long q0 = 0;
+  Launcher L;
+  long long Bcap = 0;
+  int key_bits = 0;
+  long long R = 0;
+  bool spatial = true, blur_on = true, use_gain = false;
+  DevState *st = nullptr;
+  float *pbar = nullptr, *l = nullptr, *gain = nullptr;
+  PixRec *pt = nullptr;
+  long long *last_tile = nullptr;
+  uint2 *ptt = nullptr;
+  unsigned *rkey = nullptr;
+  uint2 *rnext = nullptr;
+  uint16_t *raw_x = nullptr, *raw_y = nullptr;
+  int8_t *raw_p = nullptr;
+  unsigned *blockcnt = nullptr;
+  unsigned *ekey = nullptr;
+  int8_t *epol = nullptr;
+  unsigned *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr, *hist = nullptr;
+  uint2 *dp = nullptr;
+  unsigned *S = nullptr, *popj = nullptr, *ready = nullptr;
+  float *t2 = nullptr, *L0 = nullptr, *bval = nullptr;
+  int2 *anc = nullptr;
+  ChunkRec *ch = nullptr;
+  SelState *sel = nullptr;
+  uint8_t *frame = nullptr;
+  unsigned *cnt_tmp = nullptr, *tcnt_tmp = nullptr;
+  uint16_t *q_tmp = nullptr;
+  long long fill = 0;
+  long long batches = 0;
+  int nsm = 148;
+
+  Ctx ctx(const unsigned *skey, const unsigned *sidx, long long n_raw) const {
+    Ctx x{};
+    x.W = W;
+    x.H = H;
+    x.ts = ts;
+    x.tiles_x = tiles_x;
+    x.A = A;
+    x.n_pix = n_pix;
+    x.num = cfg.fill_num;
+    x.den = cfg.fill_den;
+    x.qmin = cfg.q_min;
+    x.qmax = cfg.q_max;
+    x.every = cfg.regulate_every;
+    x.alpha = cfg.alpha;
+    x.oma = cfg.one_m_alpha;
+    x.beta = cfg.beta;
+    x.h = cfg.half_1p_beta;
+    x.use_gain = use_gain;
+    x.blur_on = blur_on;
+    x.spatial = spatial;
+    x.st = st;
+    x.pbar = pbar;
+    x.l = l;
+    x.gain = gain;
+    x.pt = pt;
+    x.last_tile = last_tile;
+    x.ptt = ptt;
+    x.rkey = rkey;
+    x.rnext = rnext;
+    x.Rm = (unsigned long long)(R - 1);
+    x.raw_x = raw_x;
+    x.raw_y = raw_y;
+    x.raw_p = raw_p;
+    x.n_raw = n_raw;
+    x.blockcnt = blockcnt;
+    x.ekey = ekey;
+    x.epol = epol;
+    x.tkey = ka;
+    x.skey = skey;
+    x.sidx = sidx;
+    x.dp = dp;
+    x.S = S;
+    x.popj = popj;
+    x.t2 = t2;
+    x.L0 = L0;
+    x.bval = bval;
+    x.ready = ready;
+    x.anc = anc;
+    x.ch = ch;
+    return x;
+  }
+};
+
+namespace {
+
+template <class T>
+int dalloc(T **p, long long count) {
+  if (count <= 0) count = 1;
+  cudaError_t e = cudaMalloc((void **)p, sizeof(T) * (size_t)count);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+  return 0;
+}
+
+int init_state(fibar_engine *g) {
+  cudaStream_t s = g->L.stream;
+  k_init_state<<<1, 1, 0, s>>>(g->st, g->q0);
+  CK(cudaMemsetAsync(g->pbar, 0, sizeof(float) * g->n_pix, s));
+  CK(cudaMemsetAsync(g->l, 0, sizeof(float) * g->n_pix, s));
+  if (g->spatial) {
+    k_init_pt<<<g->nsm * 4, TPB, 0, s>>>(g->pt, g->n_pix);
+    k_fill_ll<<<g->nsm * 4, TPB, 0, s>>>(g->last_tile, g->n_tiles, -1);
+    CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
+    CK(cudaMemsetAsync(g->rnext, 0xFF, sizeof(uint2) * g->R, s));
+    CK(cudaMemsetAsync(g->ready, 0, sizeof(unsigned) * (g->Bcap + g->n_pix + 2), s));
+  }
+  g->L.launches += g->spatial ? 3 : 1;
+  g->fill = 0;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int run_batch(fibar_engine *g) {
+  if (g->fill == 0) return 0;
+  const long long n_raw = g->fill;
+  Launcher &L = g->L;
+  cudaStream_t s = L.stream;
+  const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
+  Ctx x = g->ctx(nullptr, nullptr, n_raw);
+  k_count_inb<<<nb_in, TPB, 0, s>>>(x, nb_in);
+  L.count();
+  scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
+  k_compact<<<nb_in, TPB, 0, s>>>(x, nb_in);
+  L.count();
+  const int where = radix_sort_pairs(L, g->ka, g->va, g->kb, g->vb, g->hist, &g->st->B, n_raw, g->key_bits);
+  const unsigned *skey = where ? g->kb : g->ka;
+  const unsigned *sidx = where ? g->vb : g->va;
+  x = g->ctx(skey, sidx, n_raw);
+  const int nb = (int)((n_raw + TPB - 1) / TPB);
+  if (g->spatial) {
+    const int T = (int)((n_raw + CHUNK - 1) / CHUNK);
+    k_seg_marks<<<nb, TPB, 0, s>>>(x);
+    k_link<<<nb, TPB, 0, s>>>(x);
+    k_anchor<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x);
+    k_anchor_scan<<<NCAND, 1024, 0, s>>>(x);
+    k_window_run<<<(T + 127) / 128, 128, 0, s>>>(x);
+    k_window_fix<<<1, 1024, 0, s>>>(x);
+    k_popj<<<nb, TPB, 0, s>>>(x);
+    k_temporal<<<nb, TPB, 0, s>>>(x);
+    L.launches += 8;
+    if (g->blur_on) {
+      k_blur<<<g->nsm * 8, TPB, 0, s>>>(x);
+      L.count();
+    }
+    k_final<<<g->nsm * 8, TPB, 0, s>>>(x);
+    L.count();
+  } else {
+    k_temporal<<<nb, TPB, 0, s>>>(x);
+    L.count();
+  }
+  k_batch_end<<<1, 1, 0, s>>>(x);
+  L.count();
+  CK(cudaGetLastError());
+  g->fill = 0;
+  g->batches++;
+  return 0;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ C ABI ---
+
+extern "C" {
+
+const char *fibar_last_error(void) { return g_err.c_str(); }
+
+int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
+  if (!cfg || !out) return fail(FIBAR_E_CONFIG, "null argument");
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(FIBAR_E_NODEVICE, "no CUDA device");
+  if (cfg->width < 2 || cfg->height < 2) return fail(FIBAR_E_CONFIG, "geometry must be at least 2x2");
+  if (cfg->tile_side < 2) return fail(FIBAR_E_CONFIG, "tile_side must be >= 2");
+  if (cfg->regulate_every < 1) return fail(FIBAR_E_CONFIG, "regulate_every must be >= 1");
+  const long long n = (long long)cfg->width * cfg->height;
+  if (cfg->q_max > n) return fail(FIBAR_E_CONFIG, "q_max exceeds pixel count");
+  if (cfg->q_min < 1 || cfg->q_min > cfg->q_max) return fail(FIBAR_E_CONFIG, "bad q_min/q_max");
+  if (cfg->fill_num < 1 || cfg->fill_den < 1) return fail(FIBAR_E_CONFIG, "bad fill ratio");
+  if (cfg->width > 65535 || cfg->height > 65535) return fail(FIBAR_E_CONFIG, "coordinates must fit uint16");
+  fibar_engine *g = new fibar_engine();
+  g->cfg = *cfg;
+  g->cfg.gain = nullptr;
+  g->W = cfg->width;
+  g->H = cfg->height;
+  g->ts = cfg->tile_side;
+  g->A = g->ts * g->ts;
+  g->tiles_x = (g->W + g->ts - 1) / g->ts;
+  g->tiles_y = (g->H + g->ts - 1) / g->ts;
+  g->n_pix = n;
+  g->n_tiles = (long long)g->tiles_x * g->tiles_y;
+  g->q0 = std::min(std::max(n / 16, (long long)cfg->q_min), (long long)cfg->q_max);
+  g->L.stream = (cudaStream_t)stream;
+  g->spatial = cfg->spatial_enabled != 0;
+  g->blur_on = cfg->blur_enabled != 0;
+  g->use_gain = cfg->gain != nullptr;
+  g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : (1LL << 20);
+  if (g->Bcap > (1LL << 28)) g->Bcap = 1LL << 28;
+  g->key_bits = ceil_log2(g->n_tiles * g->A);
+  g->R = 1LL << ceil_log2(n + 1 + g->Bcap);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, dev);
+  int rc = 0;
+  const long long Bc = g->Bcap;
+  const int nb_in = (int)((Bc + IN_TILE - 1) / IN_TILE);
+  const int nb_rs = (int)((Bc + 2047) / 2048);
+  const long long T = (Bc + CHUNK - 1) / CHUNK + 1;
+  const long long npop_cap = Bc + n + 2;
+  rc |= dalloc(&g->st, 1);
+  rc |= dalloc(&g->pbar, n);
+  rc |= dalloc(&g->l, n);
+  rc |= dalloc(&g->raw_x, Bc);
+  rc |= dalloc(&g->raw_y, Bc);
+  rc |= dalloc(&g->raw_p, Bc);
+  rc |= dalloc(&g->blockcnt, nb_in + 1);
+  rc |= dalloc(&g->ekey, Bc);
+  rc |= dalloc(&g->epol, Bc);
+  rc |= dalloc(&g->ka, Bc);
+  rc |= dalloc(&g->va, Bc);
+  rc |= dalloc(&g->kb, Bc);
+  rc |= dalloc(&g->vb, Bc);
+  rc |= dalloc(&g->hist, 256LL * nb_rs + 1);
+  rc |= dalloc(&g->sel, 1);
+  rc |= dalloc(&g->frame, n);
+  if (g->use_gain) {
+    rc |= dalloc(&g->gain, n);
+    if (!rc) cudaMemcpy(g->gain, cfg->gain, sizeof(float) * n, cudaMemcpyHostToDevice);
+  }
+  if (g->spatial) {
+    rc |= dalloc(&g->pt, n);
+    rc |= dalloc(&g->last_tile, g->n_tiles);
+    rc |= dalloc(&g->ptt, g->n_tiles);
+    rc |= dalloc(&g->rkey, g->R);
+    rc |= dalloc(&g->rnext, g->R);
+    rc |= dalloc(&g->dp, Bc);
+    rc |= dalloc(&g->S, Bc);
+    rc |= dalloc(&g->popj, npop_cap);
+    rc |= dalloc(&g->ready, npop_cap);
+    rc |= dalloc(&g->bval, npop_cap);
+    rc |= dalloc(&g->t2, Bc);
+    rc |= dalloc(&g->L0, Bc);
+    rc |= dalloc(&g->anc, T * NCAND);
+    rc |= dalloc(&g->ch, T);
+  }
+  if (rc) {
+    fibar_destroy(g);
+    return rc;
+  }
+  rc = init_state(g);
+  if (rc) {
+    fibar_destroy(g);
+    return rc;
+  }
+  *out = g;
+  return 0;
+}
+
+int fibar_destroy(fibar_engine *g) {
+  if (!g) return 0;
+  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->pt, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
+                  g->raw_y, g->raw_p, g->blockcnt, g->ekey, g->epol, g->ka, g->va, g->kb, g->vb, g->hist,
+                  g->dp, g->S, g->popj, g->ready, g->t2, g->L0, g->bval, g->anc, g->ch, g->sel, g->frame,
+                  g->cnt_tmp, g->tcnt_tmp, g->q_tmp};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  delete g;
+  return 0;
+}
+
+int fibar_set_stream(fibar_engine *g, void *stream) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  g->L.stream = (cudaStream_t)stream;
+  return 0;
+}
+
+int fibar_reset(fibar_engine *g) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  return init_state(g);
+}
+
+int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n, int32_t mem) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (n <= 0) return 0;
+  const cudaMemcpyKind kind = mem == FIBAR_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  long long off = 0;
+  while (off < n) {
+    if (g->fill == g->Bcap) {
+      int rc = run_batch(g);
+      if (rc) return rc;
+    }
+    const long long take = std::min((long long)n - off, g->Bcap - g->fill);
+    CK(cudaMemcpyAsync(g->raw_x + g->fill, x + off, sizeof(uint16_t) * take, kind, g->L.stream));
+    CK(cudaMemcpyAsync(g->raw_y + g->fill, y + off, sizeof(uint16_t) * take, kind, g->L.stream));
+    CK(cudaMemcpyAsync(g->raw_p + g->fill, p + off, sizeof(int8_t) * take, kind, g->L.stream));
+    g->fill += take;
+    off += take;
+  }
+  return 0;
+}
+
+int fibar_flush(fibar_engine *g) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  return run_batch(g);
+}
+
+int fibar_render(fibar_engine *g, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem, double *bounds,
+                 int32_t *degenerate) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (mode == FIBAR_RENDER_FIXED && !(fixed_bound > 0)) return fail(FIBAR_E_CONFIG, "fixed scale bound must be positive");
+  if (mode != FIBAR_RENDER_FIXED && mode != FIBAR_RENDER_ROBUST) return fail(FIBAR_E_CONFIG, "unknown scale mode");
+  int rc = run_batch(g);
+  if (rc) return rc;
+  cudaStream_t s = g->L.stream;
+  const long long n = g->n_pix;
+  double g_lo = 0, g_hi = 0;
+  if (mode == FIBAR_RENDER_ROBUST) {
+    // numpy percentile 'linear': virtual index (n-1)*q, neighbours floor/floor+1
+    SelState init;
+    memset(&init, 0, sizeof(init));
+    const double qs[2] = {1.0 / 100.0, 99.0 / 100.0};
+    double gam[2];
+    for (int t = 0; t < 2; ++t) {
+      const double v = (double)(n - 1) * qs[t];
+      long long prev, next;
+      if (v >= (double)(n - 1)) {
+        prev = next = n - 1;
+        gam[t] = v - (double)(-1);   // numpy's gamma uses index -1 here; a == b so the value is unaffected
+      } else if (v < 0) {
+        prev = next = 0;
+        gam[t] = v;
+      } else {
+        prev = (long long)std::floor(v);
+        next = prev + 1;
+        gam[t] = v - (double)prev;
+      }
+      init.rank[2 * t] = (unsigned)prev;
+      init.rank[2 * t + 1] = (unsigned)next;
+    }
+    g_lo = gam[0];
+    g_hi = gam[1];
+    CK(cudaMemcpyAsync(g->sel, &init, sizeof(SelState), cudaMemcpyHostToDevice, s));
+    const int grid = g->nsm * 2;
+    for (int pass = 0; pass < 3; ++pass) {
+      k_sel_hist<<<grid, TPB, 0, s>>>(g->l, n, g->sel, pass);
+      k_sel_pick<<<1, 128, 0, s>>>(g->sel, pass);
+      g->L.launches += 2;
+    }
+    CK(cudaStreamSynchronize(s));   // init lives on the host stack
+  }
+  k_sel_bounds<<<1, 1, 0, s>>>(g->sel, g_lo, g_hi, mode, fixed_bound);
+  uint8_t *dst = out_mem == FIBAR_MEM_DEVICE ? out : g->frame;
+  k_render_map<<<g->nsm * 4, TPB, 0, s>>>(g->l, n, g->sel, dst);
+  g->L.launches += 2;
+  CK(cudaGetLastError());
+  if (out_mem != FIBAR_MEM_DEVICE) CK(cudaMemcpyAsync(out, g->frame, n, cudaMemcpyDeviceToHost, s));
+  if (bounds || degenerate || out_mem != FIBAR_MEM_DEVICE) {
+    SelState h;
+    CK(cudaMemcpyAsync(&h, g->sel, sizeof(SelState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bounds) {
+      bounds[0] = h.lo;
+      bounds[1] = h.hi;
+    }
+    if (degenerate) *degenerate = h.degenerate;
+  }
+  return 0;
+}
+
+int fibar_read_qs(fibar_engine *g, int64_t qs[10]) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  int rc = run_batch(g);
+  if (rc) return rc;
+  DevState h;
+  CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
+  CK(cudaStreamSynchronize(g->L.stream));
+  qs[0] = h.s % (g->n_pix + 1);
+  qs[1] = h.E - h.s;
+  qs[2] = h.q;
+  qs[3] = h.npix;
+  qs[4] = h.ntiles;
+  qs[5] = h.blur;
+  qs[6] = h.stale;
+  qs[7] = h.qtmin;
+  qs[8] = h.qtmax;
+  qs[9] = h.evctr;
+  if (!g->spatial) {
+    qs[0] = 0;
+    qs[1] = 0;
+  }
+  return 0;
+}
+
+int fibar_counters(fibar_engine *g, int64_t *event_count, int64_t *oob_dropped) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  int rc = run_batch(g);
+  if (rc) return rc;
+  DevState h;
+  CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
+  CK(cudaStreamSynchronize(g->L.stream));
+  if (event_count) *event_count = h.E;
+  if (oob_dropped) *oob_dropped = h.oob;
+  return 0;
+}
+
+int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, uint8_t *tiles, uint16_t *qx,
+                     uint16_t *qy) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  int rc = run_batch(g);
+  if (rc) return rc;
+  cudaStream_t s = g->L.stream;
+  const long long n = g->n_pix;
+  if (p_bar) CK(cudaMemcpyAsync(p_bar, g->pbar, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+  if (l) CK(cudaMemcpyAsync(l, g->l, sizeof(float) * n, cudaMemcpyDeviceToHost, s));
+  if (active || tiles || qx || qy) {
+    if (!g->cnt_tmp) {
+      rc |= dalloc(&g->cnt_tmp, n);
+      rc |= dalloc(&g->tcnt_tmp, g->n_tiles);
+      rc |= dalloc(&g->q_tmp, 2 * (n + 1));
+      if (rc) return rc;
+    }
+    CK(cudaMemsetAsync(g->cnt_tmp, 0, sizeof(unsigned) * n, s));
+    CK(cudaMemsetAsync(g->tcnt_tmp, 0, sizeof(unsigned) * g->n_tiles, s));
+    Ctx x = g->ctx(nullptr, nullptr, 0);
+    if (g->spatial) {
+      k_active_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp);
+      k_tile_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp, g->tcnt_tmp);
+      k_ring_xy<<<g->nsm * 4, TPB, 0, s>>>(x, g->q_tmp, g->q_tmp + n + 1);
+      g->L.launches += 3;
+    } else {
+      CK(cudaMemsetAsync(g->q_tmp, 0, sizeof(uint16_t) * 2 * (n + 1), s));
+    }
+    CK(cudaGetLastError());
+    std::vector<unsigned> hc, ht;
+    if (active) hc.resize(n);
+    if (tiles) ht.resize(g->n_tiles);
+    if (active) CK(cudaMemcpyAsync(hc.data(), g->cnt_tmp, sizeof(unsigned) * n, cudaMemcpyDeviceToHost, s));
+    if (tiles) CK(cudaMemcpyAsync(ht.data(), g->tcnt_tmp, sizeof(unsigned) * g->n_tiles, cudaMemcpyDeviceToHost, s));
+    if (qx) CK(cudaMemcpyAsync(qx, g->q_tmp, sizeof(uint16_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    if (qy) CK(cudaMemcpyAsync(qy, g->q_tmp + n + 1, sizeof(uint16_t) * (n + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (active)
+      for (long long i = 0; i < n; ++i) active[i] = (uint16_t)std::min<unsigned>(hc[i], 65535u);
+    if (tiles)
+      for (long long i = 0; i < g->n_tiles; ++i) tiles[i] = (uint8_t)std::min<unsigned>(ht[i], 255u);
+  }
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+int fibar_stats(fibar_engine *g, int64_t stats[8]) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  DevState h;
+  CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
+  CK(cudaStreamSynchronize(g->L.stream));
+  stats[0] = g->L.launches;
+  stats[1] = g->batches;
+  stats[2] = h.chunks;
+  stats[3] = h.mismatch;
+  stats[4] = h.pops;
+  stats[5] = h.saturated;
+  stats[6] = h.E;
+  stats[7] = g->Bcap;
+  return 0;
+}
+
+int fibar_brightness_ptr(fibar_engine *g, float **out) {
+  if (!g || !out) return fail(FIBAR_E_CONFIG, "null argument");
+  *out = g->l;
+  return 0;
+}
+
+}  // extern "C"
