@@ -92,6 +92,10 @@ int fibar_process(fibar_engine *eng, const uint16_t *x, const uint16_t *y, const
                   int32_t mem);
 /* Run any coalesced events now (asynchronous on the engine stream). */
 int fibar_flush(fibar_engine *eng);
+/* Events waiting for the next batch: device_events are read in place from the
+ * caller's device buffers (contiguous device packets are coalesced without a
+ * copy), so those buffers must stay valid until this count drops to 0. */
+int fibar_pending(fibar_engine *eng, int64_t *device_events, int64_t *staged_events);
 
 /* Render the brightness grid to uint8 [height*width].  out_mem says where
  * `out` lives.  bounds (host double[2]) and degenerate (host int) are written
@@ -112,6 +116,13 @@ int fibar_read_state(fibar_engine *eng, float *p_bar, float *l, uint16_t *active
  * [2] = speculative window chunks, [3] = chunks re-run by the verifier,
  * [4] = pops (window evictions) processed, [5] = counter-saturation flag. */
 int fibar_stats(fibar_engine *eng, int64_t stats[8]);
+/* Per-kernel CUDA-event timing (bench.py's roofline leg; adds events around
+ * every launch, so never enable it in a timed region).  fibar_profile
+ * synchronises and clears; fibar_profile_read aggregates by kernel name:
+ * names is max_entries x name_len chars, total_ms / launches per entry. */
+int fibar_profile(fibar_engine *eng, int32_t enable);
+int fibar_profile_read(fibar_engine *eng, int32_t max_entries, char *names, int32_t name_len, double *total_ms,
+                       int64_t *launches, int32_t *n_entries);
 /* Device pointer of the float32 brightness grid (valid until destroy). */
 int fibar_brightness_ptr(fibar_engine *eng, float **out);
 

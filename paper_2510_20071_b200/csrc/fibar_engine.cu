@@ -1044,7 +1044,10 @@ struct fibar_engine {
   uint8_t *frame = nullptr;
   unsigned *cnt_tmp = nullptr, *tcnt_tmp = nullptr;
   uint16_t *q_tmp = nullptr;
-  long long fill = 0;
+  long long fill = 0;                       // events staged in raw_* (host packets, or non-contiguous device packets)
+  const uint16_t *zx = nullptr, *zy = nullptr;  // pending zero-copy device range (contiguous device packets)
+  const int8_t *zp = nullptr;
+  long long zn = 0;
   long long batches = 0;
   int nsm = 148;
 
@@ -1113,64 +1116,69 @@ int dalloc(T **p, long long count) {
 
 int init_state(fibar_engine *g) {
   cudaStream_t s = g->L.stream;
-  k_init_state<<<1, 1, 0, s>>>(g->st, g->q0);
+  FIBAR_LAUNCH(g->L, "init", k_init_state<<<1, 1, 0, s>>>(g->st, g->q0));
   CK(cudaMemsetAsync(g->pbar, 0, sizeof(float) * g->n_pix, s));
   CK(cudaMemsetAsync(g->l, 0, sizeof(float) * g->n_pix, s));
   if (g->spatial) {
-    k_init_pt<<<g->nsm * 4, TPB, 0, s>>>(g->pt, g->n_pix);
-    k_fill_ll<<<g->nsm * 4, TPB, 0, s>>>(g->last_tile, g->n_tiles, -1);
+    FIBAR_LAUNCH(g->L, "init", k_init_pt<<<g->nsm * 4, TPB, 0, s>>>(g->pt, g->n_pix));
+    FIBAR_LAUNCH(g->L, "init", k_fill_ll<<<g->nsm * 4, TPB, 0, s>>>(g->last_tile, g->n_tiles, -1));
     CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
     CK(cudaMemsetAsync(g->rnext, 0xFF, sizeof(uint2) * g->R, s));
     CK(cudaMemsetAsync(g->ready, 0, sizeof(unsigned) * (g->Bcap + g->n_pix + 2), s));
   }
-  g->L.launches += g->spatial ? 3 : 1;
   g->fill = 0;
+  g->zn = 0;
   CK(cudaGetLastError());
   return 0;
 }
 
 int run_batch(fibar_engine *g) {
-  if (g->fill == 0) return 0;
-  const long long n_raw = g->fill;
+  if (g->fill == 0 && g->zn == 0) return 0;
+  const bool zero_copy = g->zn > 0;
+  const long long n_raw = zero_copy ? g->zn : g->fill;
   Launcher &L = g->L;
   cudaStream_t s = L.stream;
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
   Ctx x = g->ctx(nullptr, nullptr, n_raw);
-  k_count_inb<<<nb_in, TPB, 0, s>>>(x, nb_in);
-  L.count();
+  if (zero_copy) {
+    x.raw_x = g->zx;
+    x.raw_y = g->zy;
+    x.raw_p = g->zp;
+  }
+  FIBAR_LAUNCH(L, "count_inb", k_count_inb<<<nb_in, TPB, 0, s>>>(x, nb_in));
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
-  k_compact<<<nb_in, TPB, 0, s>>>(x, nb_in);
-  L.count();
+  FIBAR_LAUNCH(L, "compact", k_compact<<<nb_in, TPB, 0, s>>>(x, nb_in));
   const int where = radix_sort_pairs(L, g->ka, g->va, g->kb, g->vb, g->hist, &g->st->B, n_raw, g->key_bits);
   const unsigned *skey = where ? g->kb : g->ka;
   const unsigned *sidx = where ? g->vb : g->va;
-  x = g->ctx(skey, sidx, n_raw);
+  {
+    const uint16_t *rx = x.raw_x, *ry = x.raw_y;
+    const int8_t *rp = x.raw_p;
+    x = g->ctx(skey, sidx, n_raw);
+    x.raw_x = rx;
+    x.raw_y = ry;
+    x.raw_p = rp;
+  }
   const int nb = (int)((n_raw + TPB - 1) / TPB);
   if (g->spatial) {
     const int T = (int)((n_raw + CHUNK - 1) / CHUNK);
-    k_seg_marks<<<nb, TPB, 0, s>>>(x);
-    k_link<<<nb, TPB, 0, s>>>(x);
-    k_anchor<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x);
-    k_anchor_scan<<<NCAND, 1024, 0, s>>>(x);
-    k_window_run<<<(T + 127) / 128, 128, 0, s>>>(x);
-    k_window_fix<<<1, 1024, 0, s>>>(x);
-    k_popj<<<nb, TPB, 0, s>>>(x);
-    k_temporal<<<nb, TPB, 0, s>>>(x);
-    L.launches += 8;
-    if (g->blur_on) {
-      k_blur<<<g->nsm * 8, TPB, 0, s>>>(x);
-      L.count();
-    }
-    k_final<<<g->nsm * 8, TPB, 0, s>>>(x);
-    L.count();
+    FIBAR_LAUNCH(L, "seg_marks", k_seg_marks<<<nb, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "link", k_link<<<nb, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "anchor", k_anchor<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NCAND, 1024, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "window_run", k_window_run<<<(T + 127) / 128, 128, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "window_fix", k_window_fix<<<1, 1024, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "popj", k_popj<<<nb, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
+    if (g->blur_on) FIBAR_LAUNCH(L, "blur", k_blur<<<g->nsm * 8, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, s>>>(x));
   } else {
-    k_temporal<<<nb, TPB, 0, s>>>(x);
-    L.count();
+    FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
   }
-  k_batch_end<<<1, 1, 0, s>>>(x);
-  L.count();
+  FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
   CK(cudaGetLastError());
   g->fill = 0;
+  g->zn = 0;
   g->batches++;
   return 0;
 }
@@ -1282,6 +1290,7 @@ int fibar_destroy(fibar_engine *g) {
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  for (cudaEvent_t ev : g->L.pool) cudaEventDestroy(ev);
   delete g;
   return 0;
 }
@@ -1302,6 +1311,37 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
   if (n <= 0) return 0;
   const cudaMemcpyKind kind = mem == FIBAR_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   long long off = 0;
+  if (mem == FIBAR_MEM_DEVICE) {
+    // contiguous device packets are coalesced without copies: the batch reads
+    // them in place (the caller keeps them alive until the next flush point)
+    if (g->fill > 0) {
+      int rc = run_batch(g);
+      if (rc) return rc;
+    }
+    while (off < n) {
+      if (g->zn > 0 && !(x + off == g->zx + g->zn && y + off == g->zy + g->zn && p + off == g->zp + g->zn)) {
+        int rc = run_batch(g);
+        if (rc) return rc;
+      }
+      if (g->zn == 0) {
+        g->zx = x + off;
+        g->zy = y + off;
+        g->zp = p + off;
+      }
+      const long long take = std::min((long long)n - off, g->Bcap - g->zn);
+      g->zn += take;
+      off += take;
+      if (g->zn == g->Bcap) {
+        int rc = run_batch(g);
+        if (rc) return rc;
+      }
+    }
+    return 0;
+  }
+  if (g->zn > 0) {
+    int rc = run_batch(g);
+    if (rc) return rc;
+  }
   while (off < n) {
     if (g->fill == g->Bcap) {
       int rc = run_batch(g);
@@ -1320,6 +1360,13 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
 int fibar_flush(fibar_engine *g) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
   return run_batch(g);
+}
+
+int fibar_pending(fibar_engine *g, int64_t *device_events, int64_t *staged_events) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (device_events) *device_events = g->zn;
+  if (staged_events) *staged_events = g->fill;
+  return 0;
 }
 
 int fibar_render(fibar_engine *g, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem, double *bounds,
@@ -1360,16 +1407,14 @@ int fibar_render(fibar_engine *g, int32_t mode, double fixed_bound, uint8_t *out
     CK(cudaMemcpyAsync(g->sel, &init, sizeof(SelState), cudaMemcpyHostToDevice, s));
     const int grid = g->nsm * 2;
     for (int pass = 0; pass < 3; ++pass) {
-      k_sel_hist<<<grid, TPB, 0, s>>>(g->l, n, g->sel, pass);
-      k_sel_pick<<<1, 128, 0, s>>>(g->sel, pass);
-      g->L.launches += 2;
+      FIBAR_LAUNCH(g->L, "sel_hist", k_sel_hist<<<grid, TPB, 0, s>>>(g->l, n, g->sel, pass));
+      FIBAR_LAUNCH(g->L, "sel_pick", k_sel_pick<<<1, 128, 0, s>>>(g->sel, pass));
     }
     CK(cudaStreamSynchronize(s));   // init lives on the host stack
   }
-  k_sel_bounds<<<1, 1, 0, s>>>(g->sel, g_lo, g_hi, mode, fixed_bound);
+  FIBAR_LAUNCH(g->L, "sel_bounds", k_sel_bounds<<<1, 1, 0, s>>>(g->sel, g_lo, g_hi, mode, fixed_bound));
   uint8_t *dst = out_mem == FIBAR_MEM_DEVICE ? out : g->frame;
-  k_render_map<<<g->nsm * 4, TPB, 0, s>>>(g->l, n, g->sel, dst);
-  g->L.launches += 2;
+  FIBAR_LAUNCH(g->L, "render_map", k_render_map<<<g->nsm * 4, TPB, 0, s>>>(g->l, n, g->sel, dst));
   CK(cudaGetLastError());
   if (out_mem != FIBAR_MEM_DEVICE) CK(cudaMemcpyAsync(out, g->frame, n, cudaMemcpyDeviceToHost, s));
   if (bounds || degenerate || out_mem != FIBAR_MEM_DEVICE) {
@@ -1441,10 +1486,9 @@ int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, 
     CK(cudaMemsetAsync(g->tcnt_tmp, 0, sizeof(unsigned) * g->n_tiles, s));
     Ctx x = g->ctx(nullptr, nullptr, 0);
     if (g->spatial) {
-      k_active_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp);
-      k_tile_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp, g->tcnt_tmp);
-      k_ring_xy<<<g->nsm * 4, TPB, 0, s>>>(x, g->q_tmp, g->q_tmp + n + 1);
-      g->L.launches += 3;
+      FIBAR_LAUNCH(g->L, "state_active", k_active_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp));
+      FIBAR_LAUNCH(g->L, "state_tiles", k_tile_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp, g->tcnt_tmp));
+      FIBAR_LAUNCH(g->L, "state_ring", k_ring_xy<<<g->nsm * 4, TPB, 0, s>>>(x, g->q_tmp, g->q_tmp + n + 1));
     } else {
       CK(cudaMemsetAsync(g->q_tmp, 0, sizeof(uint16_t) * 2 * (n + 1), s));
     }
@@ -1479,6 +1523,49 @@ int fibar_stats(fibar_engine *g, int64_t stats[8]) {
   stats[5] = h.saturated;
   stats[6] = h.E;
   stats[7] = g->Bcap;
+  return 0;
+}
+
+int fibar_profile(fibar_engine *g, int32_t enable) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  CK(cudaStreamSynchronize(g->L.stream));
+  g->L.prof = enable != 0;
+  g->L.recs.clear();
+  g->L.used = 0;
+  return 0;
+}
+
+int fibar_profile_read(fibar_engine *g, int32_t max_entries, char *names, int32_t name_len, double *total_ms,
+                       int64_t *launches, int32_t *n_entries) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  CK(cudaStreamSynchronize(g->L.stream));
+  std::vector<std::string> keys;
+  std::vector<double> ms;
+  std::vector<long long> cnt;
+  for (auto &r : g->L.recs) {
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, r.a, r.b));
+    size_t k = 0;
+    for (; k < keys.size(); ++k)
+      if (keys[k] == r.name) break;
+    if (k == keys.size()) {
+      keys.push_back(r.name);
+      ms.push_back(0.0);
+      cnt.push_back(0);
+    }
+    ms[k] += t;
+    cnt[k] += 1;
+  }
+  const int m = (int)std::min<size_t>(keys.size(), (size_t)max_entries);
+  for (int k = 0; k < m; ++k) {
+    strncpy(names + (size_t)k * name_len, keys[k].c_str(), name_len - 1);
+    names[(size_t)k * name_len + name_len - 1] = 0;
+    total_ms[k] = ms[k];
+    launches[k] = cnt[k];
+  }
+  *n_entries = m;
+  g->L.recs.clear();
+  g->L.used = 0;
   return 0;
 }
 

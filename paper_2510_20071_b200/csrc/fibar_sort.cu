@@ -152,19 +152,16 @@ int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, u
     const unsigned *vi = ps == 0 ? nullptr : (a_to_b ? v_a : v_b);
     unsigned *ko = a_to_b ? k_b : k_a;
     unsigned *vo = a_to_b ? v_b : v_a;
-    k_rs_hist<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, n_dev, shift, hist, nblocks);
-    L.count();
-    k_scan_inplace<<<1, 1024, 0, L.stream>>>(hist, 256 * nblocks);
-    L.count();
-    k_rs_scatter<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, vi, ko, vo, n_dev, shift, hist, nblocks);
-    L.count();
+    FIBAR_LAUNCH(L, "rs_hist", k_rs_hist<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, n_dev, shift, hist, nblocks));
+    FIBAR_LAUNCH(L, "rs_scan", k_scan_inplace<<<1, 1024, 0, L.stream>>>(hist, 256 * nblocks));
+    FIBAR_LAUNCH(L, "rs_scatter",
+                 k_rs_scatter<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, vi, ko, vo, n_dev, shift, hist, nblocks));
   }
   return (passes % 2) == 1 ? 1 : 0;
 }
 
 void scan_exclusive_u32(Launcher &L, unsigned *a, int len) {
-  k_scan_inplace<<<1, 1024, 0, L.stream>>>(a, len);
-  L.count();
+  FIBAR_LAUNCH(L, "scan", k_scan_inplace<<<1, 1024, 0, L.stream>>>(a, len));
 }
 
 }  // namespace fibar

@@ -157,6 +157,8 @@ class ReconstructionEngine:
         self._h = handle
         self._stream_ptr = stream
         self.last_t: int | None = None
+        self._held = []          # device packets the native side still reads in place
+        self._held_n = 0
 
     # -- lifecycle -----------------------------------------------------------
     def close(self) -> None:
@@ -182,17 +184,21 @@ class ReconstructionEngine:
         self._sync_stream()
         _native.check(self._lib.fibar_reset(self._h), "fibar_reset")
         self.last_t = None
+        self._held.clear()
+        self._held_n = 0
 
     def flush(self) -> None:
         """Run coalesced packets now (asynchronous on the current stream)."""
         self._sync_stream()
         _native.check(self._lib.fibar_flush(self._h), "fibar_flush")
+        self._release_held()
 
     # -- counters ------------------------------------------------------------
     def _counters(self) -> tuple[int, int]:
         ec, ob = C.c_int64(), C.c_int64()
         self._sync_stream()
         _native.check(self._lib.fibar_counters(self._h, C.byref(ec), C.byref(ob)), "fibar_counters")
+        self._release_held()
         return ec.value, ob.value
 
     @property
@@ -208,6 +214,7 @@ class ReconstructionEngine:
         out = np.zeros(QS_SIZE, np.int64)
         self._sync_stream()
         _native.check(self._lib.fibar_read_qs(self._h, out.ctypes.data), "fibar_read_qs")
+        self._release_held()
         return out
 
     def stats(self) -> dict:
@@ -216,6 +223,24 @@ class ReconstructionEngine:
         _native.check(self._lib.fibar_stats(self._h, st.ctypes.data), "fibar_stats")
         keys = ("launches", "batches", "window_chunks", "window_reruns", "pops", "saturated", "events", "batch_capacity")
         return dict(zip(keys, (int(v) for v in st)))
+
+    def profile(self, enable: bool) -> None:
+        """Per-kernel CUDA-event timing on/off (synchronises; never inside a timed region)."""
+        self._sync_stream()
+        _native.check(self._lib.fibar_profile(self._h, int(enable)), "fibar_profile")
+
+    def profile_read(self) -> dict:
+        """{kernel name: (total_ms, launches)} since profiling was enabled (synchronises, clears)."""
+        m, L = 64, 32
+        names = C.create_string_buffer(m * L)
+        ms = np.zeros(m, np.float64)
+        cnt = np.zeros(m, np.int64)
+        k = C.c_int32(0)
+        self._sync_stream()
+        _native.check(self._lib.fibar_profile_read(self._h, m, names, L, ms.ctypes.data, cnt.ctypes.data, C.byref(k)),
+                      "fibar_profile_read")
+        raw = names.raw
+        return {raw[i * L:(i + 1) * L].split(b"\0")[0].decode(): (float(ms[i]), int(cnt[i])) for i in range(k.value)}
 
     # -- state views (host copies) ---------------------------------------------
     def _read(self, **want) -> dict:
@@ -231,6 +256,7 @@ class ReconstructionEngine:
         ptr = [None if b is None else b.ctypes.data for b in bufs.values()]
         self._sync_stream()
         _native.check(self._lib.fibar_read_state(self._h, *ptr), "fibar_read_state")
+        self._release_held()
         return {k: v for k, v in bufs.items() if v is not None}
 
     @property
@@ -393,6 +419,9 @@ class ReconstructionEngine:
         self._sync_stream()
         _native.check(self._lib.fibar_process(self._h, x.data_ptr(), y.data_ptr(), p.data_ptr(), n,
                                               _native.FIBAR_MEM_DEVICE), "fibar_process")
+        self._held.append((n, x, y, p))
+        self._held_n += n
+        self._release_held()
         if block.t is not None:
             if self.strict:
                 self.last_t = int(block.t[-1])
@@ -401,6 +430,18 @@ class ReconstructionEngine:
                 # common case, resolved lazily on the device copy only when it is out of bounds
                 self._pending_last = (x, y, block.t)
                 self.last_t = self._resolve_last_t()
+
+    def _release_held(self) -> None:
+        """Drop references to device packets the native side no longer reads in place."""
+        if not self._held:
+            return
+        pend = C.c_int64(0)
+        _native.check(self._lib.fibar_pending(self._h, C.byref(pend), None), "fibar_pending")
+        while self._held and self._held_n - self._held[0][0] >= pend.value:
+            self._held_n -= self._held.pop(0)[0]
+        if pend.value == 0:
+            self._held.clear()
+            self._held_n = 0
 
     def _resolve_last_t(self):
         x, y, t = self._pending_last
@@ -425,6 +466,7 @@ class ReconstructionEngine:
         self._sync_stream()
         _native.check(self._lib.fibar_render(self._h, mode, float(fixed_bound), out.ctypes.data, _native.FIBAR_MEM_HOST,
                                              bounds.ctypes.data, C.byref(deg)), "fibar_render")
+        self._release_held()
         return Frame(out.reshape(g.height, g.width), readout_time, scale_mode, (float(bounds[0]), float(bounds[1])),
                      bool(deg.value))
 
@@ -438,6 +480,7 @@ class ReconstructionEngine:
         self._sync_stream()
         _native.check(self._lib.fibar_render(self._h, mode, float(fixed_bound), out.data_ptr(), _native.FIBAR_MEM_DEVICE,
                                              None, None), "fibar_render")
+        self._release_held()
         return out
 
     @staticmethod
