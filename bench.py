@@ -298,7 +298,7 @@ def run_ours(args, rank, world, dist):
         "e2e": e2e, "gpu_launches": int(launches), "roofline": roofline, "path_roofline": path_roofline,
         "clocks": clk.summary(),
         "kernel_ms_per_step": {k: round(v[0], 4) for k, v in sorted(prof.items(), key=lambda kv: -kv[1][0])},
-        "window": {"chunks": st2["window_chunks"], "reruns": st2["window_reruns"]},
+        "window": {k: st2[k] for k in ("window_chunks", "window_reruns", "warm_pops", "coop_iters", "fix_rounds", "pops")},
         "blur_count": int(qs[5]), "event_count": n,
     }
     return result, (geom, params, ev, packet)

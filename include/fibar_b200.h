@@ -114,8 +114,10 @@ int fibar_read_state(fibar_engine *eng, float *p_bar, float *l, uint16_t *active
 
 /* Diagnostics: stats[0] = device kernel launches so far, [1] = device batches,
  * [2] = speculative window chunks, [3] = chunks re-run by the verifier,
- * [4] = pops (window evictions) processed, [5] = counter-saturation flag. */
-int fibar_stats(fibar_engine *eng, int64_t stats[8]);
+ * [4] = pops (window evictions) processed, [5] = counter-saturation flag,
+ * [6] = in-bounds events, [7] = batch capacity, [8] = evictions replayed in
+ * speculative warm-ups, [9] = warp-cooperative eviction-count steps. */
+int fibar_stats(fibar_engine *eng, int64_t stats[16]);
 /* Per-kernel CUDA-event timing (bench.py's roofline leg; adds events around
  * every launch, so never enable it in a timed region).  fibar_profile
  * synchronises and clears; fibar_profile_read aggregates by kernel name:

@@ -5,17 +5,44 @@
 
 #define FIBAR_INF32 0xFFFFFFFFu
 
-// Per-pixel bookkeeping record (16 B, one random access per pixel touch).
+// Per-pixel bookkeeping record (32 B = one sector, one random access per pixel touch).
 //   last : global in-bounds index of the pixel's latest event before the
 //          current device batch (-1 = never), i.e. the reference's implicit
 //          "is the pixel still queued" history, kept as a last-touch index.
 //   st/end : [st, end) positions of the pixel's events in the current batch's
 //          pixel-sorted order (st == end: no events this batch).  Reset by the
 //          final pass, so the table is clean at every batch start.
-struct __align__(16) PixRec {
-  long long last;
+//   carried : blur item of the pixel's `last` event when that event is evicted
+//          stale during the current batch (else FIBAR_NONE); reset by the final pass.
+struct __align__(32) PixRec {
   unsigned st;
   unsigned end;
+  unsigned carried;
+  unsigned pad0;
+  long long last;
+  unsigned pad1, pad2;
+};
+
+#define FIBAR_NONE 0xFFFFFFFFu
+
+// Per sorted position of the current batch (16 B, one load per tap):
+//   jj      : batch-local event index (stream order)
+//   bidx    : blur item of this event if it is evicted stale in this batch, else NONE
+//   runbase : blur item whose value this position's brightness is built on
+//             (latest earlier blur of the same pixel in the batch), else NONE
+//   val     : brightness right after this event's temporal update; written by
+//             the temporal pass when runbase == NONE, else by blur item runbase
+struct __align__(16) PosRec {
+  unsigned jj;
+  unsigned bidx;
+  unsigned runbase;
+  float val;
+};
+
+// Per eviction item (popped window entry) of the current batch.
+struct __align__(8) Item {
+  unsigned jrel;   // batch-local index of the event whose trim popped it
+  unsigned pix;    // pixel (row-major) if the entry went stale, else NONE
 };
 
 // Window / counter state living in device memory so no kernel needs a host
@@ -42,6 +69,9 @@ struct DevState {
   unsigned epoch;     // batch counter (tags blur ready flags)
   unsigned ticket;    // blur work ticket
   long long saturated;
+  long long warm_pops;   // evictions replayed during speculative warm-ups (stats)
+  long long coop_iters;  // warp-cooperative eviction-count steps (stats)
+  long long fix_rounds;  // verifier rounds (stats)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {

@@ -21,6 +21,7 @@
 // Float32 arithmetic uses __fmul_rn/__fadd_rn (never contracted to FMA) so the
 // result is bit-identical to the reference's strict-IEEE numba kernels.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cmath>
 #include <algorithm>
@@ -35,14 +36,17 @@ using namespace fibar;
 
 namespace {
 
-constexpr int CHUNK = 64;    // events per speculative window chunk
-constexpr int WARM = 128;    // warm-up events before a chunk's first own event
-constexpr int NCAND = 24;    // candidate window lengths per chunk (fixed-point search)
+constexpr int NFINE = 10;     // fine candidate windows around the interpolated fixed point
+constexpr int CHUNK_MIN = 32;  // smallest speculative window chunk (sizes the chunk arrays)
+constexpr int NLIN = 7;      // coarse candidates q0 + c_lin_off[i]
+constexpr int NGEO = 12;     // coarse candidates q0 * c_geo_mul[i]
+constexpr int NCAND = NLIN + NGEO;
 constexpr int TPB = 256;
 
-__constant__ long long c_cand_off[NCAND] = {-16384, -8192, -4096, -2048, -1024, -512, -256, -128,
-                                            -64,    -32,   0,     32,    64,    128,   256,  512,
-                                            1024,   2048,  4096,  8192,  16384, 32768, 65536, 131072};
+
+__constant__ long long c_fine_mul[NFINE] = {-8, -4, -2, -1, 0, 1, 2, 4, 8, 16};
+__constant__ long long c_lin_off[NLIN] = {-1024, -256, -64, 0, 64, 256, 1024};
+__constant__ double c_geo_mul[NGEO] = {0.25, 0.5, 0.75, 1.25, 1.5, 2.0, 2.5, 3.0, 4.0, 6.0, 8.0, 12.0};
 
 struct ChunkRec {
   long long st_s, st_q;                          // state after event b_c - 1 (speculative start)
@@ -83,10 +87,15 @@ struct Ctx {
   unsigned *tkey;                 // unsorted tile-major keys (sort input)
   const unsigned *skey, *sidx;    // sorted keys / batch-local event index
   uint2 *dp;
-  unsigned *S, *popj;
-  float *t2, *L0, *bval;
+  unsigned *S;
+  Item *item;
+  PosRec *posrec;
+  unsigned *pos_of;
+  float *t2, *bval;
   unsigned *ready;
-  int2 *anc;
+  int chunk, warm, debug;
+  int2 *anc, *anc2;
+  long long *lc, *lu;
   ChunkRec *ch;
 };
 
@@ -172,7 +181,9 @@ __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
   const unsigned k = x.skey[i];
-  const unsigned c = x.ekey[x.sidx[i]];
+  const unsigned jj = x.sidx[i];
+  const unsigned c = x.ekey[jj];
+  x.pos_of[jj] = (unsigned)i;
   const bool head = i == 0 || x.skey[i - 1] != k;
   const bool tail = i == B - 1 || x.skey[i + 1] != k;
   if (head) x.pt[c].st = (unsigned)i;
@@ -265,19 +276,39 @@ struct WState {
   long long s, q, npix, ntiles, evctr;
 };
 
-__device__ __forceinline__ long long chunk_warm_start(long long E0, int c) {
-  return max(E0, E0 + (long long)c * CHUNK - WARM);
+__device__ __forceinline__ long long chunk_warm_start(const Ctx &x, long long E0, int c) {
+  return max(E0, E0 + (long long)c * x.chunk - x.warm);
 }
 
+// coarse candidate i: a dense linear grid around the batch-start target q0
+// plus a geometric one that reaches windows far from it (cold start, scene change)
 __device__ __forceinline__ long long cand_len(const Ctx &x, long long q0, int i) {
-  long long L = q0 + c_cand_off[i];
+  long long L = i < NLIN ? q0 + c_lin_off[i] : (long long)((double)q0 * c_geo_mul[i - NLIN]);
   return L < 1 ? 1 : (L > x.qmax ? x.qmax : L);
+}
+
+// floor(N / D) for N >= 0, D > 0 via a float64 quotient and an exact integer fix-up
+__device__ __forceinline__ long long floordiv_nn(long long N, long long D) {
+  long long q = (long long)__ddiv_rn((double)N, (double)D);
+  if (q * D > N) {
+    do { --q; } while (q * D > N);
+  } else {
+    while ((q + 1) * D <= N) ++q;
+  }
+  return q;
+}
+
+// integer fill-ratio regulation (_kernels.py:195-201)
+__device__ __forceinline__ long long regulate(const Ctx &x, long long len, long long np, long long nt) {
+  const long long qn = floordiv_nn(len * x.num * nt * (long long)x.A, x.den * np);
+  return qn < x.qmin ? x.qmin : (qn > x.qmax ? x.qmax : qn);
 }
 
 // The reference's per-event queue bookkeeping (_kernels.py:132-205) restated on
 // the suffix window [s, j]: the push of event j activates its pixel / tile iff
 // its previous same-pixel / same-tile event lies before s; the trim pops
 // [s, j+1-q) and each popped k deactivates iff its next occurrence lies after j.
+// Scalar form, used by the verifier's re-runs.
 __device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, long long E0, long long s_start,
                            bool write, long long &qlo, long long &qhi) {
   for (long long j = jf; j < jt; ++j) {
@@ -303,8 +334,7 @@ __device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, 
     if (++w.evctr >= x.every) {
       w.evctr = 0;
       if (w.npix >= 1 && w.ntiles >= 1) {
-        long long qn = (len * x.num * w.ntiles * (long long)x.A) / (x.den * w.npix);
-        qn = qn < x.qmin ? x.qmin : (qn > x.qmax ? x.qmax : qn);
+        const long long qn = regulate(x, len, w.npix, w.ntiles);
         w.q = qn;
         qlo = min(qlo, qn);
         qhi = max(qhi, qn);
@@ -319,14 +349,14 @@ __device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, 
 // chunk's window of the same candidate (one warp per chunk).
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   const long long B = x.st->B;
-  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
   if (c >= T) return;
   const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
-  const long long a = chunk_warm_start(E0, c);
+  const long long a = chunk_warm_start(x, E0, c);
   const long long Jc = a - 1;
-  const long long ap = c == 1 ? E0 : chunk_warm_start(E0, c - 1);
+  const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
   const long long Jp = ap - 1;
   int cp[NCAND], ct[NCAND];
   long long sp[NCAND];
@@ -334,8 +364,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   for (int i = 0; i < NCAND; ++i) {
     cp[i] = 0;
     ct[i] = 0;
-    const long long L = cand_len(x, q0, i);
-    sp[i] = c == 1 ? s0 : max(s0, ap - L);
+    sp[i] = c == 1 ? s0 : max(s0, ap - cand_len(x, q0, i));
   }
   // grow the right edge (Jp, Jc] with the previous starts
   for (long long k = Jp + 1 + lane; k <= Jc; k += 32) {
@@ -350,8 +379,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   // shrink the left edge to the new starts
 #pragma unroll
   for (int i = 0; i < NCAND; ++i) {
-    const long long L = cand_len(x, q0, i);
-    const long long sn = max(s0, a - L);
+    const long long sn = max(s0, a - cand_len(x, q0, i));
     for (long long k = sp[i] + lane; k < sn; k += 32) {
       const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
       const unsigned long long dd = (unsigned long long)(Jc - k);
@@ -361,29 +389,26 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   }
 #pragma unroll
   for (int i = 0; i < NCAND; ++i) {
-    int vp = cp[i], vt = ct[i];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      vp += __shfl_xor_sync(0xffffffffu, vp, o);
-      vt += __shfl_xor_sync(0xffffffffu, vt, o);
-    }
+    const int vp = __reduce_add_sync(0xffffffffu, cp[i]);
+    const int vt = __reduce_add_sync(0xffffffffu, ct[i]);
     if (lane == 0) x.anc[(long long)c * NCAND + i] = make_int2(vp, vt);
   }
 }
 
-// inclusive scan of the deltas over chunks, one CTA per candidate
-__global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x) {
+// inclusive scan of the deltas over chunks, one CTA per candidate chain
+// (chains interleaved with stride `nc` in `anc`)
+__global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) {
   __shared__ int2 wt[32];
   __shared__ int2 carry;
   const long long B = x.st->B;
-  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int i = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (threadIdx.x == 0) carry = make_int2((int)x.st->npix, (int)x.st->ntiles);
   __syncthreads();
   for (int base = 1; base < T; base += 1024) {
     const int c = base + threadIdx.x;
-    int2 v = c < T ? x.anc[(long long)c * NCAND + i] : make_int2(0, 0);
+    int2 v = c < T ? anc[(long long)c * nc + i] : make_int2(0, 0);
     int2 inc = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -410,64 +435,272 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x) {
     __syncthreads();
     const int2 cc = carry;
     const int2 out = make_int2(cc.x + wt[wid].x + inc.x, cc.y + wt[wid].y + inc.y);
-    if (c < T) x.anc[(long long)c * NCAND + i] = out;
+    if (c < T) anc[(long long)c * nc + i] = out;
     __syncthreads();
     if (threadIdx.x == 1023) carry = out;
     __syncthreads();
   }
 }
 
-__device__ __forceinline__ long long regulate(const Ctx &x, long long len, long long np, long long nt) {
-  long long qn = (len * x.num * nt * (long long)x.A) / (x.den * np);
-  return qn < x.qmin ? x.qmin : (qn > x.qmax ? x.qmax : qn);
+// Per chunk: locate the regulator's fixed point between the coarse candidate
+// windows (largest stable candidate, G(L) >= L, and the next, unstable one) by
+// linear interpolation of G(L) - L.  The fine candidates of pass 2 are centred
+// on it.  In steady state the true window sits within a few dozen events of
+// that fixed point and never far beyond it, so the first unstable fine
+// candidate above the largest stable one is a start that collapses onto the
+// true trajectory within a handful of events, with few evictions.
+__global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
+  const long long B = x.st->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int c = blockIdx.x * TPB + threadIdx.x;
+  if (c >= T) return;
+  const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
+  const long long a = chunk_warm_start(x, E0, c);
+  if (c == 0 || a == E0) {
+    x.lc[c] = a - s0;
+    x.lu[c] = 32;
+    return;
+  }
+  long long lens[NCAND], fs[NCAND];
+#pragma unroll 1
+  for (int i = 0; i < NCAND; ++i) {
+    const long long len = a - max(s0, a - cand_len(x, q0, i));
+    const int2 cnt = x.anc[(long long)c * NCAND + i];
+    const long long f = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) - len : -1;
+    int k = i;   // insertion by length
+    while (k > 0 && lens[k - 1] > len) {
+      lens[k] = lens[k - 1];
+      fs[k] = fs[k - 1];
+      --k;
+    }
+    lens[k] = len;
+    fs[k] = f;
+  }
+  long long len_lo = -1, len_hi = -1, f_lo = 0, f_hi = 0;
+#pragma unroll 1
+  for (int i = 0; i < NCAND; ++i) {
+    if (fs[i] >= 0) {
+      len_lo = lens[i];
+      f_lo = fs[i];
+      len_hi = -1;
+    } else if (len_hi < 0 && lens[i] > len_lo) {
+      len_hi = lens[i];
+      f_hi = fs[i];
+    }
+  }
+  long long L, unit = 32;
+  if (len_lo < 0) {
+    L = lens[0];                         // even the shortest candidate is unstable
+  } else if (len_hi < 0) {
+    L = len_lo;                          // longest candidate stable (e.g. growth from s_start)
+  } else {
+    const double root = (double)len_lo + (double)(len_hi - len_lo) * (double)f_lo / (double)(f_lo - f_hi);
+    L = (long long)ceil(root);
+    unit = max(32LL, (len_hi - len_lo) / 64);
+  }
+  x.lc[c] = L;
+  x.lu[c] = unit;
 }
 
-// one thread per chunk: choose a start window (longest candidate just past
-// the regulator's fixed point), warm up, then run the chunk's own events.
+__device__ __forceinline__ long long fine_start(const Ctx &x, long long s0, long long a, long long center,
+                                                long long unit, int j) {
+  long long L = center + c_fine_mul[j] * unit;
+  L = L < 1 ? 1 : (L > x.qmax ? x.qmax : L);
+  return max(s0, a - L);
+}
+
+// exact counts of every chunk's fine candidate windows [s_cj, a_c - 1], as
+// deltas from the previous chunk's window of the same candidate (the start
+// may move either way); one warp per chunk
+__global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
+  const long long B = x.st->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int lane = threadIdx.x & 31;
+  const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
+  if (c >= T) return;
+  const long long E0 = x.st->E, s0 = x.st->s_start;
+  const long long ac = chunk_warm_start(x, E0, c);
+  const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
+  const long long Jc = ac - 1, Jp = ap - 1;
+  const long long lcc = x.lc[c], lcp = c == 1 ? 0 : x.lc[c - 1];
+  const long long luc = x.lu[c], lup = c == 1 ? 32 : x.lu[c - 1];
+  long long sp[NFINE];
+  int cp[NFINE], ct[NFINE];
+#pragma unroll
+  for (int j = 0; j < NFINE; ++j) {
+    sp[j] = c == 1 ? s0 : fine_start(x, s0, ap, lcp, lup, j);
+    cp[j] = 0;
+    ct[j] = 0;
+  }
+  for (long long k = Jp + 1 + lane; k <= Jc; k += 32) {
+    const uint2 d = x.dp[k - E0];
+#pragma unroll
+    for (int j = 0; j < NFINE; ++j) {
+      const unsigned long long ks = (unsigned long long)(k - sp[j]);
+      cp[j] += (unsigned long long)d.x > ks;
+      ct[j] += (unsigned long long)d.y > ks;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NFINE; ++j) {
+    const long long sn = fine_start(x, s0, ac, lcc, luc, j);
+    const int sgn = sn >= sp[j] ? -1 : 1;
+    const long long lo = min(sp[j], sn), hi = max(sp[j], sn);
+    for (long long k = lo + lane; k < hi; k += 32) {
+      const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+      const unsigned long long dd = (unsigned long long)(Jc - k);
+      cp[j] += sgn * (int)((unsigned long long)r.x > dd);
+      ct[j] += sgn * (int)((unsigned long long)r.y > dd);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NFINE; ++j) {
+    const int vp = __reduce_add_sync(0xffffffffu, cp[j]);
+    const int vt = __reduce_add_sync(0xffffffffu, ct[j]);
+    if (lane == 0) x.anc2[(long long)c * NFINE + j] = make_int2(vp, vt);
+  }
+}
+
+// One lane per chunk, the warp stepping its lanes' events in lockstep.  Each
+// lane starts from the longest candidate window just past the regulator's
+// fixed point (a too-long window collapses to the true one within a few
+// events), warms up, then runs its own chunk.  Evictions of more than a few
+// entries (the first trims of a long start window) are counted by the whole
+// warp, 32 ring entries per step.
 __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   const long long B = x.st->B;
-  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int c = blockIdx.x * 128 + threadIdx.x;
-  if (c >= T) return;
+  const int lane = threadIdx.x & 31;
+  if ((blockIdx.x * 128 + (threadIdx.x & ~31)) >= T) return;   // whole warp out of range
+  const bool valid = c < T;
   const DevState s = *x.st;
   const long long E0 = s.E;
-  const long long b = E0 + (long long)c * CHUNK;
-  const long long e = min(E0 + B, b + CHUNK);
-  long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
-  WState w;
-  const long long a = chunk_warm_start(E0, c);
-  if (a == E0) {
-    w.s = s.s_start;
-    w.q = s.q;
-    w.npix = s.npix;
-    w.ntiles = s.ntiles;
-    w.evctr = s.evctr;
-  } else {
-    int g = 0, istar = -1;
+  const long long b = E0 + (long long)c * x.chunk;
+  const long long e = valid ? min(E0 + B, b + x.chunk) : b;
+  const long long a = valid ? chunk_warm_start(x, E0, c) : b;
+  WState w{0, 1, 0, 0, 0};
+  if (valid) {
+    if (a == E0) {
+      w.s = s.s_start;
+      w.q = s.q;
+      w.npix = s.npix;
+      w.ntiles = s.ntiles;
+      w.evctr = s.evctr;
+    } else {
+      const long long center = x.lc[c], unit = x.lu[c];
+      int jstar = -1;
 #pragma unroll 1
-    for (int i = 0; i < NCAND; ++i) {
-      const long long L = cand_len(x, s.q, i);
-      const long long sc = max(s.s_start, a - L);
-      const int2 cnt = x.anc[(long long)c * NCAND + i];
-      const long long len = a - sc;
-      if (cnt.x >= 1 && cnt.y >= 1 && regulate(x, len, cnt.x, cnt.y) >= len) istar = i;
+      for (int j = 0; j < NFINE; ++j) {
+        const long long sc = fine_start(x, s.s_start, a, center, unit, j);
+        const int2 cnt = x.anc2[(long long)c * NFINE + j];
+        const long long len = a - sc;
+        if (cnt.x >= 1 && cnt.y >= 1 && regulate(x, len, cnt.x, cnt.y) >= len) jstar = j;
+      }
+      const int g = jstar + 1 < NFINE ? jstar + 1 : NFINE - 1;
+      const int2 cnt = x.anc2[(long long)c * NFINE + g];
+      w.s = fine_start(x, s.s_start, a, center, unit, g);
+      w.npix = cnt.x;
+      w.ntiles = cnt.y;
+      const long long len = a - w.s;
+      w.q = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) : len;
+      if (x.debug) {
+        long long bn = 0, bt = 0;
+        for (long long k = w.s; k < a; ++k) {
+          const uint2 rr = x.rnext[(unsigned long long)k & x.Rm];
+          bn += (unsigned long long)rr.x > (unsigned long long)(a - 1 - k);
+          bt += (unsigned long long)rr.y > (unsigned long long)(a - 1 - k);
+        }
+        if (bn != w.npix || bt != w.ntiles) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);
+      }
+      w.evctr = (s.evctr + (a - E0)) % x.every;
     }
-    g = istar + 1 < NCAND ? istar + 1 : NCAND - 1;
-    const long long L = cand_len(x, s.q, g);
-    const int2 cnt = x.anc[(long long)c * NCAND + g];
-    w.s = max(s.s_start, a - L);
-    w.npix = cnt.x;
-    w.ntiles = cnt.y;
-    const long long len = a - w.s;
-    w.q = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) : len;
-    w.evctr = (s.evctr + (a - E0)) % x.every;
   }
-  long long dlo = qlo, dhi = qhi;
-  run_window(x, w, a, b, E0, s.s_start, false, dlo, dhi);
   ChunkRec r;
   r.st_s = w.s;
   r.st_q = w.q;
-  run_window(x, w, b, e, E0, s.s_start, true, qlo, qhi);
+  long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
+  long long wpops = 0, coop = 0;
+  const unsigned n_my = (unsigned)(e - a);
+  const unsigned n_max = __reduce_max_sync(0xffffffffu, n_my);
+  for (unsigned t = 0; t < n_max; ++t) {
+    const bool act = t < n_my;
+    const long long j = a + t;
+    if (act && j == b) {
+      r.st_s = w.s;
+      r.st_q = w.q;
+    }
+    long long lo = 0, hi = 0;
+    if (act) {
+      const uint2 d = x.dp[j - E0];
+      const unsigned long long js = (unsigned long long)(j - w.s);
+      w.npix += (unsigned long long)d.x > js;
+      w.ntiles += (unsigned long long)d.y > js;
+      if (j - w.s + 1 > w.q) {
+        lo = w.s;
+        hi = j + 1 - w.q;
+      }
+    }
+    const bool big = hi - lo > 8;
+    if (j < b) wpops += hi - lo;
+    if (!big && hi > lo) {
+      long long np = w.npix, nt = w.ntiles;
+      for (long long k = lo; k < hi; ++k) {
+        const uint2 rr = x.rnext[(unsigned long long)k & x.Rm];
+        const unsigned long long dd = (unsigned long long)(j - k);
+        np -= (unsigned long long)rr.x > dd;
+        nt -= (unsigned long long)rr.y > dd;
+      }
+      w.npix = np;
+      w.ntiles = nt;
+      w.s = hi;
+    }
+    unsigned m = __ballot_sync(0xffffffffu, big);
+    while (m) {
+      const int L = __ffs(m) - 1;
+      const long long l0 = __shfl_sync(0xffffffffu, lo, L);
+      const long long h0 = __shfl_sync(0xffffffffu, hi, L);
+      const long long jL = __shfl_sync(0xffffffffu, j, L);
+      int cp = 0, ct = 0;
+      for (long long k = l0 + lane; k < h0; k += 32) {
+        const uint2 rr = x.rnext[(unsigned long long)k & x.Rm];
+        const unsigned long long dd = (unsigned long long)(jL - k);
+        cp += (unsigned long long)rr.x > dd;
+        ct += (unsigned long long)rr.y > dd;
+      }
+      cp = __reduce_add_sync(0xffffffffu, cp);
+      ct = __reduce_add_sync(0xffffffffu, ct);
+      ++coop;
+      if (lane == L) {
+        w.npix -= cp;
+        w.ntiles -= ct;
+        w.s = h0;
+      }
+      m &= m - 1;
+    }
+    if (act) {
+      if (++w.evctr >= x.every) {
+        w.evctr = 0;
+        if (w.npix >= 1 && w.ntiles >= 1) {
+          const long long qn = regulate(x, j - w.s + 1, w.npix, w.ntiles);
+          w.q = qn;
+          if (j >= b) {
+            qlo = min(qlo, qn);
+            qhi = max(qhi, qn);
+          }
+        }
+      }
+      if (j >= b) x.S[j - E0] = (unsigned)(w.s - s.s_start);
+    }
+  }
+  {
+    const unsigned long long wp = __reduce_add_sync(0xffffffffu, (unsigned)wpops);
+    if (lane == 0) {
+      atomicAdd((unsigned long long *)&x.st->warm_pops, wp);
+      atomicAdd((unsigned long long *)&x.st->coop_iters, (unsigned long long)coop);
+    }
+  }
+  if (!valid) return;
   r.en_s = w.s;
   r.en_q = w.q;
   r.en_np = w.npix;
@@ -478,38 +711,57 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   x.ch[c] = r;
 }
 
-// verify chunk boundaries in order, re-running any chunk whose speculative
-// start differs from its predecessor's exact end; then publish the state.
+// Verify chunk boundaries: a chunk is exact once its speculative start state
+// equals its predecessor's end state and the predecessor is exact.  Rounds
+// re-run, in parallel, every chunk whose start disagrees with its
+// predecessor's current end (read before the round writes anything), until
+// every boundary agrees; each round makes at least the first disagreeing
+// chunk exact.  Then publish the batch's final window state.
 __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
-  __shared__ int first_bad;
+  __shared__ int n_bad;
   __shared__ long long red_lo[32], red_hi[32];
   const long long B = x.st->B;
-  const int T = (int)((B + CHUNK - 1) / CHUNK);
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
   const long long E0 = x.st->E, s_start = x.st->s_start;
-  int c0 = 1;
-  int nfix = 0;
+  int rounds = 0, reruns = 0;
   while (true) {
-    if (threadIdx.x == 0) first_bad = 0x7FFFFFFF;
+    if (threadIdx.x == 0) n_bad = 0;
     __syncthreads();
-    for (int c = c0 + threadIdx.x; c < T; c += 1024) {
+    // each thread owns chunks threadIdx.x + 1024*i; snapshot predecessors first
+    constexpr int MAXC = 64;
+    int mine[MAXC];
+    ChunkRec pre[1];
+    int nm = 0;
+    for (int c = 1 + threadIdx.x; c < T && nm < MAXC; c += 1024) {
       const ChunkRec &p = x.ch[c - 1];
       const ChunkRec &q = x.ch[c];
-      if (q.st_s != p.en_s || q.st_q != p.en_q) atomicMin(&first_bad, c);
+      if (q.st_s != p.en_s || q.st_q != p.en_q) mine[nm++] = c;
+    }
+    if (nm) atomicAdd(&n_bad, nm);
+    __syncthreads();
+    if (n_bad == 0) break;
+    // read every rerun's start state before any write of this round
+    long long ss[MAXC], sq[MAXC], snp[MAXC], snt[MAXC], sev[MAXC];
+    (void)pre;
+    for (int i = 0; i < nm; ++i) {
+      const ChunkRec &p = x.ch[mine[i] - 1];
+      ss[i] = p.en_s;
+      sq[i] = p.en_q;
+      snp[i] = p.en_np;
+      snt[i] = p.en_nt;
+      sev[i] = p.en_ev;
     }
     __syncthreads();
-    const int m = first_bad;
-    __syncthreads();
-    if (m == 0x7FFFFFFF) break;
-    if (threadIdx.x == 0) {
-      const ChunkRec p = x.ch[m - 1];
-      WState w{p.en_s, p.en_q, p.en_np, p.en_nt, p.en_ev};
+    for (int i = 0; i < nm; ++i) {
+      const int m = mine[i];
+      WState w{ss[i], sq[i], snp[i], snt[i], sev[i]};
       long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
-      const long long b = E0 + (long long)m * CHUNK;
-      const long long e = min(E0 + B, b + CHUNK);
+      const long long b = E0 + (long long)m * x.chunk;
+      const long long e = min(E0 + B, b + x.chunk);
       run_window(x, w, b, e, E0, s_start, true, qlo, qhi);
       ChunkRec r;
-      r.st_s = p.en_s;
-      r.st_q = p.en_q;
+      r.st_s = ss[i];
+      r.st_q = sq[i];
       r.en_s = w.s;
       r.en_q = w.q;
       r.en_np = w.npix;
@@ -518,10 +770,10 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
       r.qlo = qlo;
       r.qhi = qhi;
       x.ch[m] = r;
-      __threadfence_block();
     }
-    ++nfix;
-    c0 = m + 1;
+    reruns += nm;
+    ++rounds;
+    __threadfence_block();
     __syncthreads();
   }
   long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
@@ -529,6 +781,7 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
     lo = min(lo, x.ch[c].qlo);
     hi = max(hi, x.ch[c].qhi);
   }
+  int rr = __reduce_add_sync(0xffffffffu, reruns);
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
@@ -537,6 +790,7 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
   if ((threadIdx.x & 31) == 0) {
     red_lo[threadIdx.x >> 5] = lo;
     red_hi[threadIdx.x >> 5] = hi;
+    if (rr) atomicAdd((unsigned long long *)&x.st->mismatch, (unsigned long long)rr);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -559,14 +813,16 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
       s->pops += r.en_s - s_start;
     }
     s->chunks += T;
-    s->mismatch += nfix;
+    s->fix_rounds += rounds;
   }
 }
 
 // ----------------------------------------------------------------- stale ---
 
+// Every window entry popped in this batch becomes an item, in pop order (the
+// order the reference blurs them, _kernels.py:152-189).  An entry is stale iff
+// its pixel has no later event up to the popping event.
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
-  __shared__ unsigned wsum[TPB / 32];
   const long long B = x.st->B;
   const long long jj = (long long)blockIdx.x * TPB + threadIdx.x;
   const long long E0 = x.st->E, s_start = x.st->s_start;
@@ -576,26 +832,29 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
     const unsigned hi = x.S[jj];
     const long long j = E0 + jj;
     for (unsigned p = lo; p < hi; ++p) {
-      x.popj[p] = (unsigned)jj;
       const long long k = s_start + p;
-      nst += (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);
+      const bool stale =
+          (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);
+      Item it;
+      it.jrel = (unsigned)jj;
+      it.pix = FIBAR_NONE;
+      if (stale) {
+        const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
+        it.pix = c;
+        if (k < E0) x.pt[c].carried = p;
+        ++nst;
+      }
+      x.item[p] = it;
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) nst += __shfl_xor_sync(0xffffffffu, nst, o);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = nst;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned t = 0;
-    for (int w = 0; w < TPB / 32; ++w) t += wsum[w];
-    if (t) atomicAdd((unsigned long long *)&x.st->stale_batch, (unsigned long long)t);
-  }
+  nst = __reduce_add_sync(0xffffffffu, nst);
+  if ((threadIdx.x & 31) == 0 && nst) atomicAdd((unsigned long long *)&x.st->stale_batch, (unsigned long long)nst);
 }
 
 // -------------------------------------------------------------- temporal ---
 
-// one thread per pixel segment, replaying its events in stream order with the
-// reference's exact float32 operation order (_kernels.py:67-73).
+// Filter OFF: one thread per pixel segment replays its events in stream order
+// with the reference's float32 operation order (_kernels.py:67-73).
 __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
   const long long B = x.st->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
@@ -611,16 +870,54 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
     pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
     float d = fsubr(p, pb);
     if (x.use_gain) d = fmulr(d, g);
-    const float tt = fmulr(x.h, d);
-    lv = faddr(fmulr(x.beta, lv), tt);
-    if (x.spatial) {
-      x.t2[pos] = tt;
-      x.L0[pos] = lv;
-    }
+    lv = faddr(fmulr(x.beta, lv), fmulr(x.h, d));
     ++pos;
   } while (pos < B && x.skey[pos] == key);
   x.pbar[c] = pb;
-  if (!x.spatial) x.l[c] = lv;
+  x.l[c] = lv;
+}
+
+// Filter ON: same replay (_kernels.py:124-130), recording per position the
+// additive term t2 = h*d, the brightness assuming no blur (valid until the
+// pixel's first blur in the batch), and which blur each position builds on.
+__global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
+  const long long B = x.st->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned key = x.skey[i];
+  if (i > 0 && x.skey[i - 1] == key) return;
+  const long long E0 = x.st->E, s_start = x.st->s_start;
+  const long long s_end = B > 0 ? s_start + x.S[B - 1] : s_start;
+  const unsigned c = x.ekey[x.sidx[i]];
+  unsigned carry = x.pt[c].carried;
+  float pb = x.pbar[c], lv = x.l[c];
+  const float g = x.use_gain ? x.gain[c] : 1.0f;
+  long long pos = i;
+  do {
+    const unsigned jj = x.sidx[pos];
+    const float p = (float)x.epol[jj];
+    pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+    float d = fsubr(p, pb);
+    if (x.use_gain) d = fmulr(d, g);
+    const float tt = fmulr(x.h, d);
+    lv = faddr(fmulr(x.beta, lv), tt);
+    x.t2[pos] = tt;
+    const long long e = E0 + jj;
+    unsigned bidx = FIBAR_NONE;
+    if (e < s_end) {
+      const unsigned q = (unsigned)(e - s_start);
+      if (x.item[q].pix != FIBAR_NONE) bidx = q;
+    }
+    PosRec pr;
+    pr.jj = jj;
+    pr.bidx = bidx;
+    pr.runbase = carry;
+    pr.val = lv;
+    x.posrec[pos] = pr;
+    if (bidx != FIBAR_NONE) carry = bidx;
+    ++pos;
+  } while (pos < B && x.skey[pos] == key);
+  x.pbar[c] = pb;
 }
 
 // ------------------------------------------------------------------- blur ---
@@ -640,123 +937,178 @@ __device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
   return b;
 }
 
-// k popped in this batch and stale (no later same-pixel event before its pop)?
-__device__ __forceinline__ bool stale_item(const Ctx &x, const BatchScalars &b, long long k, unsigned &item) {
-  if (k < b.s_start || k >= b.s_end) return false;
-  const unsigned p = (unsigned)(k - b.s_start);
-  const long long J = b.E0 + x.popj[p];
-  if ((unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(J - k)) {
-    item = p;
-    return true;
+// Per-lane state of one blur item while it waits for earlier items.
+struct BlurTask {
+  unsigned p;        // item index, FIBAR_NONE = lane idle
+  unsigned pend;     // bit t: tap t still waits on flag[t]
+  unsigned okm;      // bit t: tap t in bounds
+  unsigned flag[9];  // item whose ready flag gates tap t
+  unsigned src[9];   // where to read tap t once ready: bval index, or posrec index | 0x80000000
+  float v[9];
+};
+
+// First resolution of item p's 3x3 taps (_kernels.py:174-188 tap order).  A
+// tap's brightness "at item p" is the neighbour's value after every temporal
+// update up to the popping event and every earlier blur.  It comes from the
+// pixel record (batch segment, carried blur) and the position record of the
+// neighbour's latest event at that time: directly (batch-start value or
+// first-run value) or, when a blur produced it, after that blur's ready flag.
+__device__ void blur_resolve(const Ctx &x, const BatchScalars &b, BlurTask &k, const Item it) {
+  const unsigned jrel = it.jrel;
+  const int cx = (int)(it.pix % (unsigned)x.W), cy = (int)(it.pix / (unsigned)x.W);
+  unsigned nidx[9];
+  uint4 pr[9];   // (st, end, carried, -) of each tap's pixel record
+  k.okm = 0;
+  k.pend = 0;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int yy = cy + t / 3 - 1, xx = cx + t % 3 - 1;
+    const bool ok = yy >= 0 && yy < x.H && xx >= 0 && xx < x.W;
+    nidx[t] = ok ? (unsigned)yy * x.W + xx : it.pix;
+    k.okm |= (unsigned)ok << t;
+    pr[t] = __ldcg(reinterpret_cast<const uint4 *>(&x.pt[nidx[t]]));
   }
-  return false;
-}
-
-__device__ __forceinline__ bool fetch_bval(const Ctx &x, const BatchScalars &b, unsigned q, float &v) {
-  if (ld_acquire_u32(&x.ready[q]) != b.epoch) return false;
-  v = __ldcg(&x.bval[q]);
-  return true;
-}
-
-// brightness of pixel n right after the temporal update at sorted position i
-// (segment starting at st; lp = pixel's last event before the batch)
-__device__ bool value_after(const Ctx &x, const BatchScalars &b, long long st, long long i, long long lp, float &v) {
-  long long pos = i - 1;
-  for (; pos >= st; --pos) {
-    unsigned q;
-    if (stale_item(x, b, b.E0 + x.sidx[pos], q)) {
-      if (!fetch_bval(x, b, q, v)) return false;
-      break;
+  // latest event of each tap pixel at the blur's time (sorted batch-local indices)
+  unsigned posi[9], first[9], last[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    first[t] = last[t] = 0xFFFFFFFFu;
+    if (pr[t].y > pr[t].x) {
+      first[t] = __ldg(&x.sidx[pr[t].x]);
+      last[t] = __ldg(&x.sidx[pr[t].y - 1]);
     }
   }
-  if (pos < st) {
-    unsigned q;
-    if (lp >= 0 && stale_item(x, b, lp, q)) {
-      if (!fetch_bval(x, b, q, v)) return false;
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    posi[t] = FIBAR_NONE;
+    if (pr[t].y <= pr[t].x || first[t] > jrel) continue;
+    if (last[t] <= jrel) {
+      posi[t] = pr[t].y - 1;
     } else {
-      v = x.L0[i];
-      return true;
+      unsigned lo = pr[t].x + 1, hi = pr[t].y - 1;   // answer in [st, end-2]
+      while (lo < hi) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (__ldg(&x.sidx[mid]) <= jrel) lo = mid + 1; else hi = mid;
+      }
+      posi[t] = lo - 1;
     }
   }
-  for (long long r = pos + 1; r <= i; ++r) v = faddr(fmulr(x.beta, v), x.t2[r]);
-  return true;
+  PosRec rec[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t)
+    if (posi[t] != FIBAR_NONE) rec[t] = x.posrec[posi[t]];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    k.v[t] = 0.0f;
+    k.flag[t] = FIBAR_NONE;
+    if (!((k.okm >> t) & 1)) continue;
+    if (posi[t] == FIBAR_NONE) {
+      if (pr[t].z < k.p) {                  // blurred (carried) before this item
+        k.flag[t] = pr[t].z;
+        k.src[t] = pr[t].z;
+      } else {
+        k.v[t] = x.l[nidx[t]];
+      }
+    } else if (rec[t].bidx < k.p) {         // its own blur came first
+      k.flag[t] = rec[t].bidx;
+      k.src[t] = rec[t].bidx;
+    } else if (rec[t].runbase == FIBAR_NONE) {
+      k.v[t] = rec[t].val;                  // first run: no blur involved
+    } else {                                // rebuilt from blur runbase
+      k.flag[t] = rec[t].runbase;
+      k.src[t] = posi[t] | 0x80000000u;
+    }
+    if (k.flag[t] != FIBAR_NONE) k.pend |= 1u << t;
+  }
 }
 
-// brightness of pixel n as seen by blur item pb (eviction at event J)
-__device__ bool tap_value(const Ctx &x, const BatchScalars &b, unsigned n, long long J, unsigned pb, float &v) {
-  const PixRec r = x.pt[n];
-  if (r.end <= r.st || b.E0 + (long long)x.sidx[r.st] > J) {
-    unsigned q;
-    if (r.last >= 0 && stale_item(x, b, r.last, q) && q < pb) return fetch_bval(x, b, q, v);
-    v = x.l[n];
-    return true;
+// poll the pending taps' flags; returns true when every tap is resolved
+__device__ __forceinline__ bool blur_poll(const Ctx &x, const BatchScalars &b, BlurTask &k) {
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    if (!((k.pend >> t) & 1)) continue;
+    if (ld_acquire_u32(&x.ready[k.flag[t]]) != b.epoch) continue;
+    const unsigned s = k.src[t];
+    k.v[t] = (s & 0x80000000u) ? __ldcg(&x.posrec[s & 0x7FFFFFFFu].val) : __ldcg(&x.bval[s]);
+    k.pend &= ~(1u << t);
   }
-  unsigned lo = r.st, hi = r.end;
-  while (lo < hi) {
-    const unsigned mid = (lo + hi) >> 1;
-    if (b.E0 + (long long)x.sidx[mid] <= J) lo = mid + 1; else hi = mid;
-  }
-  const long long i = (long long)lo - 1;
-  unsigned q;
-  if (stale_item(x, b, b.E0 + x.sidx[i], q) && q < pb) return fetch_bval(x, b, q, v);
-  return value_after(x, b, r.st, i, r.last, v);
+  return k.pend == 0;
 }
 
-// renormalised 3x3 binomial blur, taps dy-outer / dx-inner (_kernels.py:174-188)
-__device__ bool blur_item(const Ctx &x, const BatchScalars &b, unsigned p, float &out) {
-  const long long k = b.s_start + p;
-  const long long J = b.E0 + x.popj[p];
-  const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
-  const int cx = (int)(c % (unsigned)x.W), cy = (int)(c / (unsigned)x.W);
+__device__ __forceinline__ float blur_value(const BlurTask &k) {
   float num = 0.0f, den = 0.0f;
-  for (int dy = -1; dy <= 1; ++dy) {
-    const int yy = cy + dy;
-    if (yy < 0 || yy >= x.H) continue;
-    const int wy = dy == 0 ? 2 : 1;
-    for (int dx = -1; dx <= 1; ++dx) {
-      const int xx = cx + dx;
-      if (xx < 0 || xx >= x.W) continue;
-      const float w = (float)(wy * (dx == 0 ? 2 : 1));
-      float v;
-      if (!tap_value(x, b, (unsigned)yy * x.W + xx, J, p, v)) return false;
-      num = faddr(num, fmulr(w, v));
-      den = faddr(den, w);
-    }
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    if (!((k.okm >> t) & 1)) continue;
+    const float w = (float)((t / 3 == 1 ? 2 : 1) * (t % 3 == 1 ? 2 : 1));
+    num = faddr(num, fmulr(w, k.v[t]));
+    den = faddr(den, w);
   }
-  out = __fdiv_rn(num, den);
-  return true;
+  return __fdiv_rn(num, den);
 }
 
-// Persistent dataflow: warps take 32 consecutive eviction items in order from
-// a global ticket, so every dependency (an earlier item) is held by a warp that
-// is already running; items wait on per-item ready flags (epoch tagged).
+// after blur p of pixel c: brightness of c's following events (up to and
+// including its next blurred event) is rebuilt from the blurred value
+__device__ void materialise_run(const Ctx &x, const BatchScalars &b, unsigned p, unsigned pix, float v) {
+  const long long k = b.s_start + p;
+  long long r;
+  if (k >= b.E0) {
+    r = (long long)x.pos_of[k - b.E0] + 1;
+  } else {
+    const PixRec pc = x.pt[pix];
+    r = pc.end > pc.st ? (long long)pc.st : b.B;
+  }
+  for (; r < b.B; ++r) {
+    if (x.posrec[r].runbase != p) break;
+    v = faddr(fmulr(x.beta, v), x.t2[r]);
+    x.posrec[r].val = v;
+  }
+}
+
+// Persistent dataflow over the eviction items.  Idle lanes take new items in
+// pop order from a global ticket (one warp-aggregated atomic), so every
+// dependency -- always an earlier item -- is held by a lane that is already
+// running; a waiting lane only re-polls its pending flags while the other
+// lanes of its warp keep taking and finishing items.
 __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   const BatchScalars b = load_bs(x);
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
   const int lane = threadIdx.x & 31;
+  BlurTask k;
+  k.p = FIBAR_NONE;
+  unsigned pix = FIBAR_NONE;
+  bool exhausted = false;
   while (true) {
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(&x.st->ticket, 32u);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (base >= npop) break;
-    const unsigned p = base + lane;
-    bool done = true;
-    if (p < npop) {
-      unsigned q;
-      done = !stale_item(x, b, b.s_start + p, q);
-    }
-    while (true) {
-      if (!done) {
-        float v;
-        if (blur_item(x, b, p, v)) {
-          __stcg(&x.bval[p], v);
-          st_release_u32(&x.ready[p], b.epoch);
-          done = true;
+    const unsigned want = __ballot_sync(0xffffffffu, k.p == FIBAR_NONE && !exhausted);
+    if (want) {
+      unsigned base = 0;
+      const int leader = __ffs(want) - 1;
+      if (lane == leader) base = atomicAdd(&x.st->ticket, (unsigned)__popc(want));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if ((want >> lane) & 1) {
+        const unsigned p = base + __popc(want & ((1u << lane) - 1u));
+        if (p >= npop) {
+          exhausted = true;
+        } else {
+          const Item it = x.item[p];
+          if (it.pix != FIBAR_NONE) {
+            k.p = p;
+            pix = it.pix;
+            blur_resolve(x, b, k, it);
+          }
         }
       }
-      if (__all_sync(0xffffffffu, done)) break;
-      if (!done) __nanosleep(20);
     }
+    if (k.p != FIBAR_NONE) {
+      if (blur_poll(x, b, k)) {
+        const float v = blur_value(k);
+        materialise_run(x, b, k.p, pix, v);
+        __stcg(&x.bval[k.p], v);
+        st_release_u32(&x.ready[k.p], b.epoch);
+        k.p = FIBAR_NONE;
+      }
+    }
+    if (__all_sync(0xffffffffu, exhausted && k.p == FIBAR_NONE)) break;
   }
 }
 
@@ -770,31 +1122,33 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
     if (idx < b.B) {
       const long long pos = idx;
       if (pos + 1 < b.B && x.skey[pos + 1] == x.skey[pos]) continue;   // segment tails only
-      const unsigned c = x.ekey[x.sidx[pos]];
-      const PixRec r = x.pt[c];
-      const long long e = b.E0 + x.sidx[pos];
-      float v = x.L0[pos];
-      if (x.blur_on) {
-        unsigned q;
-        if (stale_item(x, b, e, q)) v = x.bval[q];
-        else value_after(x, b, r.st, pos, r.last, v);
-      }
+      const PosRec f = x.posrec[pos];
+      const unsigned c = x.ekey[f.jj];
+      const long long e = b.E0 + f.jj;
+      float v = f.val;
+      if (x.blur_on && f.bidx != FIBAR_NONE) v = x.bval[f.bidx];
       x.l[c] = v;
       PixRec nr;
-      nr.last = e;
       nr.st = 0;
       nr.end = 0;
+      nr.carried = FIBAR_NONE;
+      nr.pad0 = 0;
+      nr.last = e;
+      nr.pad1 = nr.pad2 = 0;
       x.pt[c] = nr;
-      const unsigned t = x.skey[pos] / x.A;
-      atomicMax(&x.last_tile[t], e);
-    } else if (x.blur_on) {
+      atomicMax(&x.last_tile[x.skey[pos] / x.A], e);
+    } else {
       const unsigned p = (unsigned)(idx - b.B);
       const long long k = b.s_start + p;
-      unsigned q;
-      if (k < b.E0 && stale_item(x, b, k, q)) {
-        // carried-only pixel: no events in this batch after its last pre-batch event
+      const Item it = x.item[p];
+      if (k < b.E0 && it.pix != FIBAR_NONE) {
+        // carried stale entry; if its pixel has no events in this batch, this
+        // is the pixel's only update (segment pixels are finished above)
         const uint2 rn = x.rnext[(unsigned long long)k & x.Rm];
-        if ((unsigned long long)rn.x > (unsigned long long)(b.E0 + b.B - 1 - k)) x.l[x.rkey[(unsigned long long)k & x.Rm]] = x.bval[p];
+        if ((unsigned long long)rn.x > (unsigned long long)(b.E0 + b.B - 1 - k)) {
+          if (x.blur_on) x.l[it.pix] = x.bval[p];
+          x.pt[it.pix].carried = FIBAR_NONE;
+        }
       }
     }
   }
@@ -979,9 +1333,12 @@ __global__ void k_fill_ll(long long *p, long long n, long long v) {
 __global__ void k_init_pt(PixRec *p, long long n) {
   for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
     PixRec r;
-    r.last = -1;
     r.st = 0;
     r.end = 0;
+    r.carried = FIBAR_NONE;
+    r.pad0 = 0;
+    r.last = -1;
+    r.pad1 = r.pad2 = 0;
     p[i] = r;
   }
 }
@@ -1036,9 +1393,12 @@ struct fibar_engine {
   int8_t *epol = nullptr;
   unsigned *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr, *hist = nullptr;
   uint2 *dp = nullptr;
-  unsigned *S = nullptr, *popj = nullptr, *ready = nullptr;
-  float *t2 = nullptr, *L0 = nullptr, *bval = nullptr;
-  int2 *anc = nullptr;
+  unsigned *S = nullptr, *ready = nullptr, *pos_of = nullptr;
+  Item *item = nullptr;
+  PosRec *posrec = nullptr;
+  float *t2 = nullptr, *bval = nullptr;
+  int2 *anc = nullptr, *anc2 = nullptr;
+  long long *lc = nullptr, *lu = nullptr;
   ChunkRec *ch = nullptr;
   SelState *sel = nullptr;
   uint8_t *frame = nullptr;
@@ -1050,6 +1410,8 @@ struct fibar_engine {
   long long zn = 0;
   long long batches = 0;
   int nsm = 148;
+  int blur_grid = 148;
+  int chunk = 64, warm = 128, debug = 0;
 
   Ctx ctx(const unsigned *skey, const unsigned *sidx, long long n_raw) const {
     Ctx x{};
@@ -1093,12 +1455,19 @@ struct fibar_engine {
     x.sidx = sidx;
     x.dp = dp;
     x.S = S;
-    x.popj = popj;
+    x.item = item;
+    x.posrec = posrec;
+    x.pos_of = pos_of;
     x.t2 = t2;
-    x.L0 = L0;
     x.bval = bval;
     x.ready = ready;
+    x.chunk = chunk;
+    x.debug = debug;
+    x.warm = warm;
     x.anc = anc;
+    x.anc2 = anc2;
+    x.lc = lc;
+    x.lu = lu;
     x.ch = ch;
     return x;
   }
@@ -1161,16 +1530,19 @@ int run_batch(fibar_engine *g) {
   }
   const int nb = (int)((n_raw + TPB - 1) / TPB);
   if (g->spatial) {
-    const int T = (int)((n_raw + CHUNK - 1) / CHUNK);
+    const int T = (int)((n_raw + g->chunk - 1) / g->chunk);
     FIBAR_LAUNCH(L, "seg_marks", k_seg_marks<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "link", k_link<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "anchor", k_anchor<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NCAND, 1024, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NCAND, 1024, 0, s>>>(x, g->anc, NCAND));
+    FIBAR_LAUNCH(L, "fp", k_fp<<<(T + TPB - 1) / TPB, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "anchor2", k_anchor2<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NFINE, 1024, 0, s>>>(x, g->anc2, NFINE));
     FIBAR_LAUNCH(L, "window_run", k_window_run<<<(T + 127) / 128, 128, 0, s>>>(x));
     FIBAR_LAUNCH(L, "window_fix", k_window_fix<<<1, 1024, 0, s>>>(x));
     FIBAR_LAUNCH(L, "popj", k_popj<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
-    if (g->blur_on) FIBAR_LAUNCH(L, "blur", k_blur<<<g->nsm * 8, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
+    if (g->blur_on) FIBAR_LAUNCH(L, "blur", k_blur<<<g->blur_grid, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, s>>>(x));
   } else {
     FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
@@ -1223,15 +1595,25 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : (1LL << 20);
   if (g->Bcap > (1LL << 28)) g->Bcap = 1LL << 28;
   g->key_bits = ceil_log2(g->n_tiles * g->A);
+  // window-speculation tuning knobs (results never depend on them; the verifier
+  // re-runs any chunk whose speculative start was wrong)
+  if (const char *v = getenv("FIBAR_CHUNK")) g->chunk = std::max(CHUNK_MIN, atoi(v));
+  if (const char *v = getenv("FIBAR_WARM")) g->warm = std::max(0, atoi(v));
+  if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
   g->R = 1LL << ceil_log2(n + 1 + g->Bcap);
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, dev);
+  {
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blur, TPB, 0);
+    g->blur_grid = g->nsm * std::max(1, per_sm);
+  }
   int rc = 0;
   const long long Bc = g->Bcap;
   const int nb_in = (int)((Bc + IN_TILE - 1) / IN_TILE);
   const int nb_rs = (int)((Bc + 2047) / 2048);
-  const long long T = (Bc + CHUNK - 1) / CHUNK + 1;
+  const long long T = (Bc + CHUNK_MIN - 1) / CHUNK_MIN + 1;
   const long long npop_cap = Bc + n + 2;
   rc |= dalloc(&g->st, 1);
   rc |= dalloc(&g->pbar, n);
@@ -1261,12 +1643,16 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->rnext, g->R);
     rc |= dalloc(&g->dp, Bc);
     rc |= dalloc(&g->S, Bc);
-    rc |= dalloc(&g->popj, npop_cap);
+    rc |= dalloc(&g->item, npop_cap);
     rc |= dalloc(&g->ready, npop_cap);
     rc |= dalloc(&g->bval, npop_cap);
     rc |= dalloc(&g->t2, Bc);
-    rc |= dalloc(&g->L0, Bc);
+    rc |= dalloc(&g->posrec, Bc);
+    rc |= dalloc(&g->pos_of, Bc);
     rc |= dalloc(&g->anc, T * NCAND);
+    rc |= dalloc(&g->anc2, T * NFINE);
+    rc |= dalloc(&g->lc, T);
+    rc |= dalloc(&g->lu, T);
     rc |= dalloc(&g->ch, T);
   }
   if (rc) {
@@ -1286,7 +1672,7 @@ int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->pt, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->ekey, g->epol, g->ka, g->va, g->kb, g->vb, g->hist,
-                  g->dp, g->S, g->popj, g->ready, g->t2, g->L0, g->bval, g->anc, g->ch, g->sel, g->frame,
+                  g->dp, g->S, g->item, g->ready, g->t2, g->posrec, g->pos_of, g->bval, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1510,7 +1896,7 @@ int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, 
   return 0;
 }
 
-int fibar_stats(fibar_engine *g, int64_t stats[8]) {
+int fibar_stats(fibar_engine *g, int64_t stats[16]) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
   DevState h;
   CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
@@ -1523,6 +1909,9 @@ int fibar_stats(fibar_engine *g, int64_t stats[8]) {
   stats[5] = h.saturated;
   stats[6] = h.E;
   stats[7] = g->Bcap;
+  stats[8] = h.warm_pops;
+  stats[9] = h.coop_iters;
+  stats[10] = h.fix_rounds;
   return 0;
 }
 

@@ -34,50 +34,70 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const unsigned *__restri
   for (int d = threadIdx.x; d < 256; d += RS_THREADS) hist[(long long)d * nblocks + blockIdx.x] = h[d];
 }
 
-// exclusive scan of `len` counters in place with one CTA of 1024 threads
+// exclusive scan of `len` counters in place with one CTA of 1024 threads,
+// 16 counters per thread per round (uint4 loads when aligned)
 __global__ void __launch_bounds__(1024) k_scan_inplace(unsigned *__restrict__ a, int len) {
+  constexpr int PER = 16;
   __shared__ unsigned warp_tot[32];
-  __shared__ unsigned carry;
-  if (threadIdx.x == 0) carry = 0;
-  __syncthreads();
+  __shared__ unsigned carry_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (int base = 0; base < len; base += 1024 * 4) {
-    unsigned v[4];
+  unsigned carry = 0;
+  for (int base = 0; base < len; base += 1024 * PER) {
+    unsigned v[PER];
+    const int i0 = base + threadIdx.x * PER;
+    if (i0 + PER <= len && ((reinterpret_cast<uintptr_t>(a + i0) & 15) == 0)) {
+#pragma unroll
+      for (int r = 0; r < PER / 4; ++r) {
+        const uint4 q = reinterpret_cast<const uint4 *>(a + i0)[r];
+        v[4 * r] = q.x;
+        v[4 * r + 1] = q.y;
+        v[4 * r + 2] = q.z;
+        v[4 * r + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < PER; ++r) v[r] = i0 + r < len ? a[i0 + r] : 0u;
+    }
     unsigned tsum = 0;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      int i = base + threadIdx.x * 4 + r;
-      v[r] = i < len ? a[i] : 0u;
-      tsum += v[r];
-    }
+    for (int r = 0; r < PER; ++r) tsum += v[r];
     unsigned incl = tsum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+      const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += t;
     }
     if (lane == 31) warp_tot[wid] = incl;
     __syncthreads();
     if (wid == 0) {
-      unsigned w = warp_tot[lane];
+      const unsigned w = warp_tot[lane];
       unsigned wi = w;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        unsigned t = __shfl_up_sync(0xffffffffu, wi, o);
+        const unsigned t = __shfl_up_sync(0xffffffffu, wi, o);
         if (lane >= o) wi += t;
       }
       warp_tot[lane] = wi - w;
+      if (lane == 31) carry_s = wi;
     }
     __syncthreads();
     unsigned run = carry + warp_tot[wid] + incl - tsum;
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      int i = base + threadIdx.x * 4 + r;
-      if (i < len) a[i] = run;
-      run += v[r];
+    for (int r = 0; r < PER; ++r) {
+      const unsigned t = v[r];
+      v[r] = run;
+      run += t;
     }
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = run;
+    if (i0 + PER <= len && ((reinterpret_cast<uintptr_t>(a + i0) & 15) == 0)) {
+#pragma unroll
+      for (int r = 0; r < PER / 4; ++r)
+        reinterpret_cast<uint4 *>(a + i0)[r] = make_uint4(v[4 * r], v[4 * r + 1], v[4 * r + 2], v[4 * r + 3]);
+    } else {
+#pragma unroll
+      for (int r = 0; r < PER; ++r)
+        if (i0 + r < len) a[i0 + r] = v[r];
+    }
+    carry += carry_s;
     __syncthreads();
   }
 }

@@ -218,10 +218,11 @@ class ReconstructionEngine:
         return out
 
     def stats(self) -> dict:
-        st = np.zeros(8, np.int64)
+        st = np.zeros(16, np.int64)
         self._sync_stream()
         _native.check(self._lib.fibar_stats(self._h, st.ctypes.data), "fibar_stats")
-        keys = ("launches", "batches", "window_chunks", "window_reruns", "pops", "saturated", "events", "batch_capacity")
+        keys = ("launches", "batches", "window_chunks", "window_reruns", "pops", "saturated", "events",
+                "batch_capacity", "warm_pops", "coop_iters", "fix_rounds")
         return dict(zip(keys, (int(v) for v in st)))
 
     def profile(self, enable: bool) -> None:
