@@ -125,6 +125,9 @@ int fibar_stats(fibar_engine *eng, int64_t stats[16]);
 int fibar_profile(fibar_engine *eng, int32_t enable);
 int fibar_profile_read(fibar_engine *eng, int32_t max_entries, char *names, int32_t name_len, double *total_ms,
                        int64_t *launches, int32_t *n_entries);
+/* Debug only (env FIBAR_DEBUG_TIMES at create): blur item completion and
+ * take-up timestamps (ns, %globaltimer) of the last batch, n items. */
+int fibar_debug_times(fibar_engine *eng, uint64_t *done_ns, uint64_t *grab_ns, int64_t n);
 /* Device pointer of the float32 brightness grid (valid until destroy). */
 int fibar_brightness_ptr(fibar_engine *eng, float **out);
 

@@ -40,9 +40,22 @@ struct __align__(16) PosRec {
 };
 
 // Per eviction item (popped window entry) of the current batch.
-struct __align__(8) Item {
-  unsigned jrel;   // batch-local index of the event whose trim popped it
-  unsigned pix;    // pixel (row-major) if the entry went stale, else NONE
+struct __align__(16) Item {
+  unsigned jrel;    // batch-local index of the event whose trim popped it
+  unsigned pix;     // pixel (row-major) if the entry went stale, else NONE
+  unsigned runpos;  // first sorted position whose brightness builds on this blur, else NONE
+  unsigned pad;
+};
+
+// A blur item's taps after the dependency-free part of their resolution:
+// tap t is in bounds iff bit t of okm; pending iff bit t of pend, in which case
+// flag[t] names the ready flag to wait for (bit 31: the run-materialised flag)
+// and val[t] the source (bit 31: position record, else blur value index);
+// otherwise val[t] holds the float bits of the tap's brightness.
+struct __align__(16) BlurPrep {
+  unsigned okm, pend;
+  unsigned flag[9];
+  unsigned val[9];
 };
 
 // Window / counter state living in device memory so no kernel needs a host
@@ -66,8 +79,11 @@ struct DevState {
   long long mismatch; // chunks re-run by the verifier (stats)
   long long pops;     // total evictions (stats)
   long long stale_batch;
+  long long npop;      // evictions of the batch being processed (set by the window verifier)
   unsigned epoch;     // batch counter (tags blur ready flags)
   unsigned ticket;    // blur work ticket
+  unsigned qhead, qtail, qtail_res, qpad;   // blur ready FIFO
+  unsigned long long blur_done;              // blur items finished in this batch
   long long saturated;
   long long warm_pops;   // evictions replayed during speculative warm-ups (stats)
   long long coop_iters;  // warp-cooperative eviction-count steps (stats)
@@ -79,6 +95,17 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned ld_relaxed_u32(const unsigned *p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned *p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }

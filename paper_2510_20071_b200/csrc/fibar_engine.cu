@@ -92,8 +92,11 @@ struct Ctx {
   PosRec *posrec;
   unsigned *pos_of;
   float *t2, *bval;
-  unsigned *ready;
+  unsigned *ready, *mready;
+  BlurPrep *prep;
   int chunk, warm, debug;
+  unsigned blur_sleep;
+  unsigned long long *dbg_t, *dbg_g;
   int2 *anc, *anc2;
   long long *lc, *lu;
   ChunkRec *ch;
@@ -171,6 +174,8 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     s->s_start = s->s;
     s->stale_batch = 0;
     s->ticket = 0;
+    s->qhead = s->qtail = s->qtail_res = 0;
+    s->blur_done = 0;
   }
 }
 
@@ -811,6 +816,9 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
         s->qtmax = max(s->qtmax, hi);
       }
       s->pops += r.en_s - s_start;
+      s->npop = r.en_s - s_start;
+    } else {
+      s->npop = 0;
     }
     s->chunks += T;
     s->fix_rounds += rounds;
@@ -838,6 +846,8 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
       Item it;
       it.jrel = (unsigned)jj;
       it.pix = FIBAR_NONE;
+      it.runpos = FIBAR_NONE;
+      it.pad = 0;
       if (stale) {
         const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
         it.pix = c;
@@ -890,6 +900,7 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
   const long long s_end = B > 0 ? s_start + x.S[B - 1] : s_start;
   const unsigned c = x.ekey[x.sidx[i]];
   unsigned carry = x.pt[c].carried;
+  if (carry != FIBAR_NONE) x.item[carry].runpos = (unsigned)i;
   float pb = x.pbar[c], lv = x.l[c];
   const float g = x.use_gain ? x.gain[c] : 1.0f;
   long long pos = i;
@@ -914,7 +925,10 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
     pr.runbase = carry;
     pr.val = lv;
     x.posrec[pos] = pr;
-    if (bidx != FIBAR_NONE) carry = bidx;
+    if (bidx != FIBAR_NONE) {
+      carry = bidx;
+      if (pos + 1 < B && x.skey[pos + 1] == key) x.item[bidx].runpos = (unsigned)(pos + 1);
+    }
     ++pos;
   } while (pos < B && x.skey[pos] == key);
   x.pbar[c] = pb;
@@ -937,38 +951,38 @@ __device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
   return b;
 }
 
-// Per-lane state of one blur item while it waits for earlier items.
-struct BlurTask {
-  unsigned p;        // item index, FIBAR_NONE = lane idle
-  unsigned pend;     // bit t: tap t still waits on flag[t]
-  unsigned okm;      // bit t: tap t in bounds
-  unsigned flag[9];  // item whose ready flag gates tap t
-  unsigned src[9];   // where to read tap t once ready: bval index, or posrec index | 0x80000000
-  float v[9];
-};
-
 // First resolution of item p's 3x3 taps (_kernels.py:174-188 tap order).  A
 // tap's brightness "at item p" is the neighbour's value after every temporal
 // update up to the popping event and every earlier blur.  It comes from the
 // pixel record (batch segment, carried blur) and the position record of the
 // neighbour's latest event at that time: directly (batch-start value or
-// first-run value) or, when a blur produced it, after that blur's ready flag.
-__device__ void blur_resolve(const Ctx &x, const BatchScalars &b, BlurTask &k, const Item it) {
+// first-run value) or, when a blur produced it, after that blur's flag.
+// Runs for all items in parallel, before any blur (no waiting).
+__global__ void __launch_bounds__(TPB) k_blur_prep(Ctx x) {
+  const BatchScalars b = load_bs(x);
+  const unsigned npop = (unsigned)(b.s_end - b.s_start);
+  const unsigned p = blockIdx.x * TPB + threadIdx.x;
+  if (p >= npop) return;
+  const Item it = x.item[p];
+  BlurPrep out;
+  out.okm = 0;
+  out.pend = 0;
+  if (it.pix == FIBAR_NONE) {
+    x.prep[p].okm = 0;
+    return;
+  }
   const unsigned jrel = it.jrel;
   const int cx = (int)(it.pix % (unsigned)x.W), cy = (int)(it.pix / (unsigned)x.W);
   unsigned nidx[9];
   uint4 pr[9];   // (st, end, carried, -) of each tap's pixel record
-  k.okm = 0;
-  k.pend = 0;
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
     const int yy = cy + t / 3 - 1, xx = cx + t % 3 - 1;
     const bool ok = yy >= 0 && yy < x.H && xx >= 0 && xx < x.W;
     nidx[t] = ok ? (unsigned)yy * x.W + xx : it.pix;
-    k.okm |= (unsigned)ok << t;
+    out.okm |= (unsigned)ok << t;
     pr[t] = __ldcg(reinterpret_cast<const uint4 *>(&x.pt[nidx[t]]));
   }
-  // latest event of each tap pixel at the blur's time (sorted batch-local indices)
   unsigned posi[9], first[9], last[9];
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
@@ -999,65 +1013,37 @@ __device__ void blur_resolve(const Ctx &x, const BatchScalars &b, BlurTask &k, c
     if (posi[t] != FIBAR_NONE) rec[t] = x.posrec[posi[t]];
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
-    k.v[t] = 0.0f;
-    k.flag[t] = FIBAR_NONE;
-    if (!((k.okm >> t) & 1)) continue;
+    out.flag[t] = FIBAR_NONE;
+    out.val[t] = 0u;
+    if (!((out.okm >> t) & 1)) continue;
     if (posi[t] == FIBAR_NONE) {
-      if (pr[t].z < k.p) {                  // blurred (carried) before this item
-        k.flag[t] = pr[t].z;
-        k.src[t] = pr[t].z;
+      if (pr[t].z < p) {                    // blurred (carried) before this item
+        out.flag[t] = pr[t].z;
+        out.val[t] = pr[t].z;
       } else {
-        k.v[t] = x.l[nidx[t]];
+        out.val[t] = __float_as_uint(x.l[nidx[t]]);
       }
-    } else if (rec[t].bidx < k.p) {         // its own blur came first
-      k.flag[t] = rec[t].bidx;
-      k.src[t] = rec[t].bidx;
+    } else if (rec[t].bidx < p) {           // its own blur came first
+      out.flag[t] = rec[t].bidx;
+      out.val[t] = rec[t].bidx;
     } else if (rec[t].runbase == FIBAR_NONE) {
-      k.v[t] = rec[t].val;                  // first run: no blur involved
+      out.val[t] = __float_as_uint(rec[t].val);   // first run: no blur involved
     } else {                                // rebuilt from blur runbase
-      k.flag[t] = rec[t].runbase;
-      k.src[t] = posi[t] | 0x80000000u;
+      out.flag[t] = rec[t].runbase | 0x80000000u;
+      out.val[t] = posi[t] | 0x80000000u;
     }
-    if (k.flag[t] != FIBAR_NONE) k.pend |= 1u << t;
+    if (out.flag[t] != FIBAR_NONE) out.pend |= 1u << t;
   }
-}
-
-// poll the pending taps' flags; returns true when every tap is resolved
-__device__ __forceinline__ bool blur_poll(const Ctx &x, const BatchScalars &b, BlurTask &k) {
-#pragma unroll
-  for (int t = 0; t < 9; ++t) {
-    if (!((k.pend >> t) & 1)) continue;
-    if (ld_acquire_u32(&x.ready[k.flag[t]]) != b.epoch) continue;
-    const unsigned s = k.src[t];
-    k.v[t] = (s & 0x80000000u) ? __ldcg(&x.posrec[s & 0x7FFFFFFFu].val) : __ldcg(&x.bval[s]);
-    k.pend &= ~(1u << t);
-  }
-  return k.pend == 0;
-}
-
-__device__ __forceinline__ float blur_value(const BlurTask &k) {
-  float num = 0.0f, den = 0.0f;
-#pragma unroll
-  for (int t = 0; t < 9; ++t) {
-    if (!((k.okm >> t) & 1)) continue;
-    const float w = (float)((t / 3 == 1 ? 2 : 1) * (t % 3 == 1 ? 2 : 1));
-    num = faddr(num, fmulr(w, k.v[t]));
-    den = faddr(den, w);
-  }
-  return __fdiv_rn(num, den);
+  x.prep[p] = out;
 }
 
 // after blur p of pixel c: brightness of c's following events (up to and
 // including its next blurred event) is rebuilt from the blurred value
-__device__ void materialise_run(const Ctx &x, const BatchScalars &b, unsigned p, unsigned pix, float v) {
-  const long long k = b.s_start + p;
-  long long r;
-  if (k >= b.E0) {
-    r = (long long)x.pos_of[k - b.E0] + 1;
-  } else {
-    const PixRec pc = x.pt[pix];
-    r = pc.end > pc.st ? (long long)pc.st : b.B;
-  }
+
+// after blur p of pixel c: brightness of c's following events (up to and
+// including its next blurred event) is rebuilt from the blurred value
+__device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars &b, unsigned p, unsigned r,
+                                                float v) {
   for (; r < b.B; ++r) {
     if (x.posrec[r].runbase != p) break;
     v = faddr(fmulr(x.beta, v), x.t2[r]);
@@ -1068,47 +1054,81 @@ __device__ void materialise_run(const Ctx &x, const BatchScalars &b, unsigned p,
 // Persistent dataflow over the eviction items.  Idle lanes take new items in
 // pop order from a global ticket (one warp-aggregated atomic), so every
 // dependency -- always an earlier item -- is held by a lane that is already
-// running; a waiting lane only re-polls its pending flags while the other
-// lanes of its warp keep taking and finishing items.
+// running; a waiting lane re-polls the pending flags its prep record left
+// open.  The blurred value is published (ready) before the
+// pixel's following run is rebuilt (mready).
 __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   const BatchScalars b = load_bs(x);
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
   const int lane = threadIdx.x & 31;
-  BlurTask k;
-  k.p = FIBAR_NONE;
-  unsigned pix = FIBAR_NONE;
+  unsigned p = FIBAR_NONE, okm = 0, pend = 0, runpos = FIBAR_NONE;
+  unsigned flag[9], val[9];
   bool exhausted = false;
   while (true) {
-    const unsigned want = __ballot_sync(0xffffffffu, k.p == FIBAR_NONE && !exhausted);
+    const unsigned want = __ballot_sync(0xffffffffu, p == FIBAR_NONE && !exhausted);
     if (want) {
       unsigned base = 0;
       const int leader = __ffs(want) - 1;
       if (lane == leader) base = atomicAdd(&x.st->ticket, (unsigned)__popc(want));
       base = __shfl_sync(0xffffffffu, base, leader);
       if ((want >> lane) & 1) {
-        const unsigned p = base + __popc(want & ((1u << lane) - 1u));
-        if (p >= npop) {
+        const unsigned q = base + __popc(want & ((1u << lane) - 1u));
+        if (q >= npop) {
           exhausted = true;
         } else {
-          const Item it = x.item[p];
-          if (it.pix != FIBAR_NONE) {
-            k.p = p;
-            pix = it.pix;
-            blur_resolve(x, b, k, it);
+          const BlurPrep &bp = x.prep[q];
+          okm = bp.okm;
+          if (okm) {
+            p = q;
+            pend = bp.pend;
+#pragma unroll
+            for (int t = 0; t < 9; ++t) {
+              flag[t] = bp.flag[t];
+              val[t] = bp.val[t];
+            }
+            runpos = x.item[q].runpos;
           }
         }
       }
     }
-    if (k.p != FIBAR_NONE) {
-      if (blur_poll(x, b, k)) {
-        const float v = blur_value(k);
-        materialise_run(x, b, k.p, pix, v);
-        __stcg(&x.bval[k.p], v);
-        st_release_u32(&x.ready[k.p], b.epoch);
-        k.p = FIBAR_NONE;
+    if (p != FIBAR_NONE) {
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        if (!((pend >> t) & 1)) continue;
+        const unsigned f = flag[t];
+        const unsigned *fl = (f & 0x80000000u) ? &x.mready[f & 0x7FFFFFFFu] : &x.ready[f];
+        if (ld_acquire_u32(fl) != b.epoch) continue;
+        const unsigned s = val[t];
+        val[t] = __float_as_uint((s & 0x80000000u) ? __ldcg(&x.posrec[s & 0x7FFFFFFFu].val) : __ldcg(&x.bval[s]));
+        pend &= ~(1u << t);
+      }
+      if (pend == 0) {
+        float num = 0.0f, den = 0.0f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          if (!((okm >> t) & 1)) continue;
+          const float w = (float)((t / 3 == 1 ? 2 : 1) * (t % 3 == 1 ? 2 : 1));
+          num = faddr(num, fmulr(w, __uint_as_float(val[t])));
+          den = faddr(den, w);
+        }
+        const float v = __fdiv_rn(num, den);
+        __stcg(&x.bval[p], v);
+        st_release_u32(&x.ready[p], b.epoch);
+        if (x.dbg_t) {
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          x.dbg_t[p] = tt;
+        }
+        if (runpos != FIBAR_NONE) {
+          materialise_run(x, b, p, runpos, v);
+          st_release_u32(&x.mready[p], b.epoch);
+        }
+        p = FIBAR_NONE;
+      } else if (x.blur_sleep) {
+        __nanosleep(x.blur_sleep);
       }
     }
-    if (__all_sync(0xffffffffu, exhausted && k.p == FIBAR_NONE)) break;
+    if (__all_sync(0xffffffffu, exhausted && p == FIBAR_NONE)) break;
   }
 }
 
@@ -1393,7 +1413,8 @@ struct fibar_engine {
   int8_t *epol = nullptr;
   unsigned *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr, *hist = nullptr;
   uint2 *dp = nullptr;
-  unsigned *S = nullptr, *ready = nullptr, *pos_of = nullptr;
+  unsigned *S = nullptr, *ready = nullptr, *mready = nullptr, *pos_of = nullptr;
+  BlurPrep *prep = nullptr;
   Item *item = nullptr;
   PosRec *posrec = nullptr;
   float *t2 = nullptr, *bval = nullptr;
@@ -1412,6 +1433,8 @@ struct fibar_engine {
   int nsm = 148;
   int blur_grid = 148;
   int chunk = 64, warm = 128, debug = 0;
+  unsigned blur_sleep = 0;
+  unsigned long long *dbg_t = nullptr, *dbg_g = nullptr;
 
   Ctx ctx(const unsigned *skey, const unsigned *sidx, long long n_raw) const {
     Ctx x{};
@@ -1461,8 +1484,13 @@ struct fibar_engine {
     x.t2 = t2;
     x.bval = bval;
     x.ready = ready;
+    x.mready = mready;
+    x.prep = prep;
     x.chunk = chunk;
     x.debug = debug;
+    x.blur_sleep = blur_sleep;
+    x.dbg_t = dbg_t;
+    x.dbg_g = dbg_g;
     x.warm = warm;
     x.anc = anc;
     x.anc2 = anc2;
@@ -1494,6 +1522,7 @@ int init_state(fibar_engine *g) {
     CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
     CK(cudaMemsetAsync(g->rnext, 0xFF, sizeof(uint2) * g->R, s));
     CK(cudaMemsetAsync(g->ready, 0, sizeof(unsigned) * (g->Bcap + g->n_pix + 2), s));
+    CK(cudaMemsetAsync(g->mready, 0, sizeof(unsigned) * (g->Bcap + g->n_pix + 2), s));
   }
   g->fill = 0;
   g->zn = 0;
@@ -1542,7 +1571,12 @@ int run_batch(fibar_engine *g) {
     FIBAR_LAUNCH(L, "window_fix", k_window_fix<<<1, 1024, 0, s>>>(x));
     FIBAR_LAUNCH(L, "popj", k_popj<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
-    if (g->blur_on) FIBAR_LAUNCH(L, "blur", k_blur<<<g->blur_grid, TPB, 0, s>>>(x));
+    if (g->blur_on) {
+      const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
+      FIBAR_LAUNCH(L, "blur_prep", k_blur_prep<<<nbp, TPB, 0, s>>>(x));
+
+      FIBAR_LAUNCH(L, "blur", k_blur<<<g->blur_grid, TPB, 0, s>>>(x));
+    }
     FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, s>>>(x));
   } else {
     FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
@@ -1607,7 +1641,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blur, TPB, 0);
+    if (const char *v = getenv("FIBAR_BLUR_BLOCKS")) per_sm = std::min(per_sm, std::max(1, atoi(v)));
     g->blur_grid = g->nsm * std::max(1, per_sm);
+    if (const char *v = getenv("FIBAR_BLUR_SLEEP")) g->blur_sleep = (unsigned)atoi(v);
   }
   int rc = 0;
   const long long Bc = g->Bcap;
@@ -1645,6 +1681,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->S, Bc);
     rc |= dalloc(&g->item, npop_cap);
     rc |= dalloc(&g->ready, npop_cap);
+    rc |= dalloc(&g->mready, npop_cap);
+    rc |= dalloc(&g->prep, npop_cap);
     rc |= dalloc(&g->bval, npop_cap);
     rc |= dalloc(&g->t2, Bc);
     rc |= dalloc(&g->posrec, Bc);
@@ -1654,6 +1692,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->lc, T);
     rc |= dalloc(&g->lu, T);
     rc |= dalloc(&g->ch, T);
+  }
+  if (g->spatial && getenv("FIBAR_DEBUG_TIMES")) {
+    rc |= dalloc(&g->dbg_t, npop_cap);
+    rc |= dalloc(&g->dbg_g, npop_cap);
   }
   if (rc) {
     fibar_destroy(g);
@@ -1672,8 +1714,8 @@ int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->pt, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->ekey, g->epol, g->ka, g->va, g->kb, g->vb, g->hist,
-                  g->dp, g->S, g->item, g->ready, g->t2, g->posrec, g->pos_of, g->bval, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
-                  g->cnt_tmp, g->tcnt_tmp, g->q_tmp};
+                  g->dp, g->S, g->item, g->ready, g->mready, g->prep, g->t2, g->posrec, g->pos_of, g->bval, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
+                  g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : g->L.pool) cudaEventDestroy(ev);
@@ -1955,6 +1997,15 @@ int fibar_profile_read(fibar_engine *g, int32_t max_entries, char *names, int32_
   *n_entries = m;
   g->L.recs.clear();
   g->L.used = 0;
+  return 0;
+}
+
+// debug: item completion / grab timestamps (ns) of the last batch; FIBAR_DEBUG_TIMES must be set
+int fibar_debug_times(fibar_engine *g, uint64_t *done_ns, uint64_t *grab_ns, int64_t n) {
+  if (!g || !g->dbg_t) return fail(FIBAR_E_CONFIG, "debug timestamps not enabled");
+  CK(cudaStreamSynchronize(g->L.stream));
+  CK(cudaMemcpy(done_ns, g->dbg_t, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(grab_ns, g->dbg_g, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   return 0;
 }
 

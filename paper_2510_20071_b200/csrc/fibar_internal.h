@@ -51,5 +51,7 @@ int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, u
                      const long long *n_dev, long long n_max, int bits);
 
 void scan_exclusive_u32(Launcher &L, unsigned *a, int len);
+void scan_exclusive_large(Launcher &L, const unsigned *in, unsigned *out, const long long *n_dev, long long n_fixed,
+                          long long n_max, unsigned *part);
 
 }  // namespace fibar

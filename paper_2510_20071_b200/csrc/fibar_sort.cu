@@ -180,6 +180,82 @@ int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, u
   return (passes % 2) == 1 ? 1 : 0;
 }
 
+// --- multi-block exclusive scan (reduce / scan partials / scan + offset) ---
+constexpr int SC_THREADS = 256, SC_PER = 16, SC_TILE = SC_THREADS * SC_PER;  // 4096 per block
+
+__device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, unsigned &total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += t;
+  }
+  if (lane == 31) wsum[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const unsigned w = lane < SC_THREADS / 32 ? wsum[lane] : 0u;
+    unsigned wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned t = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= o) wi += t;
+    }
+    if (lane < SC_THREADS / 32) wsum[lane] = wi - w;
+    if (lane == SC_THREADS / 32 - 1) wsum[SC_THREADS / 32] = wi;
+  }
+  __syncthreads();
+  total = wsum[SC_THREADS / 32];
+  return wsum[wid] + inc - v;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_reduce(const unsigned *__restrict__ in, const long long *n_dev,
+                                                            long long n_fixed, unsigned *__restrict__ part) {
+  __shared__ unsigned wsum[SC_THREADS / 32 + 1];
+  const long long n = n_dev ? *n_dev : n_fixed;
+  const long long i0 = (long long)blockIdx.x * SC_TILE + threadIdx.x * SC_PER;
+  unsigned v = 0;
+#pragma unroll
+  for (int r = 0; r < SC_PER; ++r)
+    if (i0 + r < n) v += in[i0 + r];
+  unsigned tot;
+  block_excl_scan(v, wsum, tot);
+  if (threadIdx.x == 0) part[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SC_THREADS) k_scan_apply(const unsigned *__restrict__ in, unsigned *__restrict__ out,
+                                                           const long long *n_dev, long long n_fixed,
+                                                           const unsigned *__restrict__ part) {
+  __shared__ unsigned wsum[SC_THREADS / 32 + 1];
+  const long long n = n_dev ? *n_dev : n_fixed;
+  const long long i0 = (long long)blockIdx.x * SC_TILE + threadIdx.x * SC_PER;
+  unsigned v[SC_PER];
+  unsigned t = 0;
+#pragma unroll
+  for (int r = 0; r < SC_PER; ++r) {
+    v[r] = i0 + r < n ? in[i0 + r] : 0u;
+    t += v[r];
+  }
+  unsigned tot;
+  unsigned run = part[blockIdx.x] + block_excl_scan(t, wsum, tot);
+#pragma unroll
+  for (int r = 0; r < SC_PER; ++r) {
+    if (i0 + r < n) out[i0 + r] = run;
+    run += v[r];
+  }
+}
+
+// exclusive scan of n (device count, or n_fixed when n_dev is null) counters,
+// n <= n_max; part needs n_max / 4096 + 2 entries
+void scan_exclusive_large(Launcher &L, const unsigned *in, unsigned *out, const long long *n_dev, long long n_fixed,
+                          long long n_max, unsigned *part) {
+  const int nb = (int)((n_max + SC_TILE - 1) / SC_TILE);
+  if (nb == 0) return;
+  FIBAR_LAUNCH(L, "scan_reduce", k_scan_reduce<<<nb, SC_THREADS, 0, L.stream>>>(in, n_dev, n_fixed, part));
+  FIBAR_LAUNCH(L, "scan", k_scan_inplace<<<1, 1024, 0, L.stream>>>(part, nb));
+  FIBAR_LAUNCH(L, "scan_apply", k_scan_apply<<<nb, SC_THREADS, 0, L.stream>>>(in, out, n_dev, n_fixed, part));
+}
+
 void scan_exclusive_u32(Launcher &L, unsigned *a, int len) {
   FIBAR_LAUNCH(L, "scan", k_scan_inplace<<<1, 1024, 0, L.stream>>>(a, len));
 }

@@ -33,7 +33,11 @@ pd = torch.from_numpy(ev.p).cuda()
 ref_l = None
 for s in a.settings:
     c, w = s.split(":")[:2]
-    os.environ.update(FIBAR_CHUNK=c, FIBAR_WARM=w)
+    parts = s.split(":")
+    dbg = parts[2] if len(parts) > 2 else "0"
+    os.environ.update(FIBAR_CHUNK=c, FIBAR_WARM=w, FIBAR_DEBUG_WINDOW=dbg,
+                      FIBAR_BLUR_BLOCKS=parts[3] if len(parts) > 3 else "64",
+                      FIBAR_BLUR_SLEEP=parts[4] if len(parts) > 4 else "0")
     eng = ReconstructionEngine(geom, params, batch_capacity=a.cap)
     for rep in range(2):
         eng.reset()
@@ -49,8 +53,9 @@ for s in a.settings:
     ch = st1["window_chunks"] - st0["window_chunks"]
     l = eng.l
     same = ref_l is None or np.array_equal(l, ref_l)
+    tb = prof.get('blur_prep', (0, 0))[0]
     ref_l = l if ref_l is None else ref_l
     print(f"{s:>20}: step {tot:8.2f} ms  window {win:8.2f} ms (run {prof['window_run'][0]:.2f} fix {prof['window_fix'][0]:.2f})"
           f"  warm pops/chunk {(st1['warm_pops'] - st0['warm_pops']) / max(ch, 1):8.1f}  reruns {st1['window_reruns'] - st0['window_reruns']}"
-          f"  rounds {st1['fix_rounds'] - st0['fix_rounds']}  blur {prof['blur'][0]:.2f} ms  same={same}", flush=True)
+          f"  rounds {st1['fix_rounds'] - st0['fix_rounds']}  blur {prof['blur'][0]:.2f} ms prep {tb:.2f}  same={same}", flush=True)
     eng.close()
