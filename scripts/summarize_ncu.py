@@ -1,0 +1,91 @@
+"""Summarise ncu outputs into profiles/ (tracked).
+
+    python scripts/summarize_ncu.py TAG
+reads gpurun_out/launches_TAG.csv (gpu__time_duration.sum launch list) and
+gpurun_out/full_TAG.ncu-rep (--set full capture), writes profiles/TAG_launches.md
+and profiles/TAG_ncu_full.md.
+"""
+import collections
+import csv
+import io
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+tag = sys.argv[1]
+out_dir = os.path.join(ROOT, "profiles")
+os.makedirs(out_dir, exist_ok=True)
+
+# launch list
+path = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
+lines = open(path).read().splitlines()
+start = next(i for i, l in enumerate(lines) if l.startswith('"ID"'))
+rows = list(csv.DictReader(io.StringIO("\n".join(lines[start:]))))
+tot = collections.defaultdict(float)
+cnt = collections.Counter()
+for r in rows:
+    if r["Metric Name"] != "gpu__time_duration.sum":
+        continue
+    name = r["Kernel Name"].split("(")[0].replace("<unnamed>::", "").replace("fibar::", "")
+    v = float(r["Metric Value"].replace(",", ""))
+    unit = r["Metric Unit"]
+    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
+    tot[name] += v * scale
+    cnt[name] += 1
+ours = {k: v for k, v in tot.items() if k.startswith("k_")}
+allsum = sum(ours.values())
+with open(os.path.join(out_dir, f"{tag}_launches.md"), "w") as fh:
+    fh.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n")
+    fh.write("Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv "
+             "python bench.py --profile-only --events 3145728` (one step: 3 device batches of 1M events, "
+             "640x480 moving texture, filter ON, robust render). Per-launch times are cold-cache and "
+             "serialised; compare shares, not absolutes.\n\n")
+    fh.write("| kernel | launches | total us | mean us | share of our kernels |\n|---|---:|---:|---:|---:|\n")
+    for k, v in sorted(ours.items(), key=lambda kv: -kv[1]):
+        fh.write(f"| {k} | {cnt[k]} | {v:.1f} | {v / cnt[k]:.1f} | {v / allsum * 100:.1f}% |\n")
+    fh.write(f"\nTotal of our kernels: {allsum:.1f} us over {sum(cnt[k] for k in ours)} launches.\n")
+print("wrote launches summary;", len(ours), "kernels")
+
+# full capture
+rep = os.path.join(ROOT, "gpurun_out", f"full_{tag}.ncu-rep")
+if os.path.exists(rep):
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    idx = {h: i for i, h in enumerate(hdr)}
+    want = ["Duration", "DRAM Throughput", "Memory Throughput", "L2 Cache Throughput", "L1/TEX Cache Throughput",
+            "Compute (SM) Throughput", "Achieved Occupancy", "Theoretical Occupancy", "Registers Per Thread",
+            "Executed Ipc Active", "Warp Cycles Per Issued Instruction", "Avg. Active Threads Per Warp",
+            "Grid Size", "Block Size"]
+    per = collections.OrderedDict()
+    for r in rows[1:]:
+        k = (r[idx["ID"]], r[idx["Kernel Name"]].split("(")[0].replace("<unnamed>::", "").replace("fibar::", ""))
+        if r[idx["Metric Name"]] in want:
+            per.setdefault(k, {})[r[idx["Metric Name"]]] = f"{r[idx['Metric Value']]} {r[idx['Metric Unit']]}".strip()
+    raw2 = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r2 = list(csv.reader(io.StringIO(raw2)))
+    h2 = {h: i for i, h in enumerate(r2[0])}
+    dram = {}
+    for r in r2[2:]:
+        try:
+            k = r[h2["ID"]]
+            rb = float(r[h2["dram__bytes_read.sum"]].replace(",", ""))
+            wb = float(r[h2["dram__bytes_write.sum"]].replace(",", ""))
+            unit_r = r2[1][h2["dram__bytes_read.sum"]]
+            dram[k] = (rb, wb, unit_r)
+        except (KeyError, ValueError, IndexError):
+            pass
+    with open(os.path.join(out_dir, f"{tag}_ncu_full.md"), "w") as fh:
+        fh.write(f"# {tag}: ncu --set full (--clock-control none), top kernels of one bench step\n\n")
+        fh.write("ncu flushes caches between replays, so DRAM traffic here is cold-cache (upper bound).\n\n")
+        for (kid, name), m in per.items():
+            fh.write(f"## {name} (launch id {kid})\n\n")
+            for w in want:
+                if w in m:
+                    fh.write(f"- {w}: {m[w]}\n")
+            if kid in dram:
+                rb, wb, u = dram[kid]
+                fh.write(f"- dram__bytes_read.sum + dram__bytes_write.sum: {rb:.3f} + {wb:.3f} {u}\n")
+            fh.write("\n")
+    print("wrote full summary;", len(per), "kernels")
