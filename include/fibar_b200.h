@@ -128,6 +128,8 @@ int fibar_profile_read(fibar_engine *eng, int32_t max_entries, char *names, int3
 /* Debug only (env FIBAR_DEBUG_TIMES at create): blur item completion and
  * take-up timestamps (ns, %globaltimer) of the last batch, n items. */
 int fibar_debug_times(fibar_engine *eng, uint64_t *done_ns, uint64_t *grab_ns, int64_t n);
+/* Debug only: the blur items' resolved-tap records of the last batch (80 B each). */
+int fibar_debug_prep(fibar_engine *eng, void *out, int64_t n);
 /* Device pointer of the float32 brightness grid (valid until destroy). */
 int fibar_brightness_ptr(fibar_engine *eng, float **out);
 

@@ -24,7 +24,7 @@ FIBAR_RENDER_FIXED = 1
 EXPORTED = (
     "fibar_create", "fibar_destroy", "fibar_set_stream", "fibar_reset", "fibar_process", "fibar_flush",
     "fibar_render", "fibar_read_qs", "fibar_counters", "fibar_read_state", "fibar_stats",
-    "fibar_brightness_ptr", "fibar_last_error", "fibar_profile", "fibar_profile_read", "fibar_pending", "fibar_debug_times",
+    "fibar_brightness_ptr", "fibar_last_error", "fibar_profile", "fibar_profile_read", "fibar_pending", "fibar_debug_times", "fibar_debug_prep",
 )
 
 
@@ -80,6 +80,7 @@ def load(path: str | None = None):
         "fibar_profile": ([P, i32], C.c_int),
         "fibar_pending": ([P, P, P], C.c_int),
         "fibar_debug_times": ([P, P, P, i64], C.c_int),
+        "fibar_debug_prep": ([P, P, i64], C.c_int),
         "fibar_profile_read": ([P, i32, P, i32, P, P, P], C.c_int),
     }
     for name, (args, res) in sig.items():

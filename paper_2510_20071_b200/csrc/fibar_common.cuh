@@ -49,9 +49,9 @@ struct __align__(16) Item {
 
 // A blur item's taps after the dependency-free part of their resolution:
 // tap t is in bounds iff bit t of okm; pending iff bit t of pend, in which case
-// flag[t] names the ready flag to wait for (bit 31: the run-materialised flag)
-// and val[t] the source (bit 31: position record, else blur value index);
-// otherwise val[t] holds the float bits of the tap's brightness.
+// val[t] names the word to wait for (bit 31: a rebuilt-run position, else a
+// blur item) and flag[t] the blur item it comes from; otherwise val[t] holds
+// the float bits of the tap's brightness.
 struct __align__(16) BlurPrep {
   unsigned okm, pend;
   unsigned flag[9];
@@ -104,6 +104,14 @@ __device__ __forceinline__ unsigned atom_add_acq_rel_u32(unsigned *p, unsigned v
   unsigned old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
 __device__ __forceinline__ void st_release_u32(unsigned *p, unsigned v) {

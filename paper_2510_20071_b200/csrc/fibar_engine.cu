@@ -91,8 +91,8 @@ struct Ctx {
   Item *item;
   PosRec *posrec;
   unsigned *pos_of;
-  float *t2, *bval;
-  unsigned *ready, *mready;
+  float *t2;
+  unsigned long long *bv64, *mv64;   // (epoch << 32 | float bits) per blur item / per sorted position
   BlurPrep *prep;
   int chunk, warm, debug;
   unsigned blur_sleep;
@@ -1048,6 +1048,7 @@ __device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars
     if (x.posrec[r].runbase != p) break;
     v = faddr(fmulr(x.beta, v), x.t2[r]);
     x.posrec[r].val = v;
+    st_relaxed_u64(&x.mv64[r], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
   }
 }
 
@@ -1062,7 +1063,7 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
   const int lane = threadIdx.x & 31;
   unsigned p = FIBAR_NONE, okm = 0, pend = 0, runpos = FIBAR_NONE;
-  unsigned flag[9], val[9];
+  unsigned val[9];
   bool exhausted = false;
   while (true) {
     const unsigned want = __ballot_sync(0xffffffffu, p == FIBAR_NONE && !exhausted);
@@ -1082,24 +1083,23 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
             p = q;
             pend = bp.pend;
 #pragma unroll
-            for (int t = 0; t < 9; ++t) {
-              flag[t] = bp.flag[t];
-              val[t] = bp.val[t];
-            }
+            for (int t = 0; t < 9; ++t) val[t] = bp.val[t];
             runpos = x.item[q].runpos;
           }
         }
       }
     }
     if (p != FIBAR_NONE) {
+      // every open tap polls its value word (epoch | float bits) with an
+      // independent relaxed 64-bit load: a matching epoch means the value is
+      // there, so no flag/value ordering (and no fence) is involved
 #pragma unroll
       for (int t = 0; t < 9; ++t) {
         if (!((pend >> t) & 1)) continue;
-        const unsigned f = flag[t];
-        const unsigned *fl = (f & 0x80000000u) ? &x.mready[f & 0x7FFFFFFFu] : &x.ready[f];
-        if (ld_acquire_u32(fl) != b.epoch) continue;
         const unsigned s = val[t];
-        val[t] = __float_as_uint((s & 0x80000000u) ? __ldcg(&x.posrec[s & 0x7FFFFFFFu].val) : __ldcg(&x.bval[s]));
+        const unsigned long long w = ld_relaxed_u64((s & 0x80000000u) ? &x.mv64[s & 0x7FFFFFFFu] : &x.bv64[s]);
+        if ((unsigned)(w >> 32) != b.epoch) continue;
+        val[t] = (unsigned)w;
         pend &= ~(1u << t);
       }
       if (pend == 0) {
@@ -1112,17 +1112,13 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
           den = faddr(den, w);
         }
         const float v = __fdiv_rn(num, den);
-        __stcg(&x.bval[p], v);
-        st_release_u32(&x.ready[p], b.epoch);
+        st_relaxed_u64(&x.bv64[p], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
         if (x.dbg_t) {
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           x.dbg_t[p] = tt;
         }
-        if (runpos != FIBAR_NONE) {
-          materialise_run(x, b, p, runpos, v);
-          st_release_u32(&x.mready[p], b.epoch);
-        }
+        if (runpos != FIBAR_NONE) materialise_run(x, b, p, runpos, v);
         p = FIBAR_NONE;
       } else if (x.blur_sleep) {
         __nanosleep(x.blur_sleep);
@@ -1146,7 +1142,7 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
       const unsigned c = x.ekey[f.jj];
       const long long e = b.E0 + f.jj;
       float v = f.val;
-      if (x.blur_on && f.bidx != FIBAR_NONE) v = x.bval[f.bidx];
+      if (x.blur_on && f.bidx != FIBAR_NONE) v = __uint_as_float((unsigned)x.bv64[f.bidx]);
       x.l[c] = v;
       PixRec nr;
       nr.st = 0;
@@ -1166,7 +1162,7 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
         // is the pixel's only update (segment pixels are finished above)
         const uint2 rn = x.rnext[(unsigned long long)k & x.Rm];
         if ((unsigned long long)rn.x > (unsigned long long)(b.E0 + b.B - 1 - k)) {
-          if (x.blur_on) x.l[it.pix] = x.bval[p];
+          if (x.blur_on) x.l[it.pix] = __uint_as_float((unsigned)x.bv64[p]);
           x.pt[it.pix].carried = FIBAR_NONE;
         }
       }
@@ -1413,11 +1409,12 @@ struct fibar_engine {
   int8_t *epol = nullptr;
   unsigned *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr, *hist = nullptr;
   uint2 *dp = nullptr;
-  unsigned *S = nullptr, *ready = nullptr, *mready = nullptr, *pos_of = nullptr;
+  unsigned *S = nullptr, *pos_of = nullptr;
+  unsigned long long *bv64 = nullptr, *mv64 = nullptr;
   BlurPrep *prep = nullptr;
   Item *item = nullptr;
   PosRec *posrec = nullptr;
-  float *t2 = nullptr, *bval = nullptr;
+  float *t2 = nullptr;
   int2 *anc = nullptr, *anc2 = nullptr;
   long long *lc = nullptr, *lu = nullptr;
   ChunkRec *ch = nullptr;
@@ -1482,9 +1479,8 @@ struct fibar_engine {
     x.posrec = posrec;
     x.pos_of = pos_of;
     x.t2 = t2;
-    x.bval = bval;
-    x.ready = ready;
-    x.mready = mready;
+    x.bv64 = bv64;
+    x.mv64 = mv64;
     x.prep = prep;
     x.chunk = chunk;
     x.debug = debug;
@@ -1521,8 +1517,8 @@ int init_state(fibar_engine *g) {
     FIBAR_LAUNCH(g->L, "init", k_fill_ll<<<g->nsm * 4, TPB, 0, s>>>(g->last_tile, g->n_tiles, -1));
     CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
     CK(cudaMemsetAsync(g->rnext, 0xFF, sizeof(uint2) * g->R, s));
-    CK(cudaMemsetAsync(g->ready, 0, sizeof(unsigned) * (g->Bcap + g->n_pix + 2), s));
-    CK(cudaMemsetAsync(g->mready, 0, sizeof(unsigned) * (g->Bcap + g->n_pix + 2), s));
+    CK(cudaMemsetAsync(g->bv64, 0, sizeof(unsigned long long) * (g->Bcap + g->n_pix + 2), s));
+    CK(cudaMemsetAsync(g->mv64, 0, sizeof(unsigned long long) * g->Bcap, s));
   }
   g->fill = 0;
   g->zn = 0;
@@ -1574,7 +1570,6 @@ int run_batch(fibar_engine *g) {
     if (g->blur_on) {
       const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
       FIBAR_LAUNCH(L, "blur_prep", k_blur_prep<<<nbp, TPB, 0, s>>>(x));
-
       FIBAR_LAUNCH(L, "blur", k_blur<<<g->blur_grid, TPB, 0, s>>>(x));
     }
     FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, s>>>(x));
@@ -1641,9 +1636,12 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blur, TPB, 0);
+    // fewer polling lanes keep L2 free for the producers (measured best at 4 x 256 per SM)
+    per_sm = std::min(per_sm, 4);
     if (const char *v = getenv("FIBAR_BLUR_BLOCKS")) per_sm = std::min(per_sm, std::max(1, atoi(v)));
     g->blur_grid = g->nsm * std::max(1, per_sm);
     if (const char *v = getenv("FIBAR_BLUR_SLEEP")) g->blur_sleep = (unsigned)atoi(v);
+
   }
   int rc = 0;
   const long long Bc = g->Bcap;
@@ -1680,10 +1678,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->dp, Bc);
     rc |= dalloc(&g->S, Bc);
     rc |= dalloc(&g->item, npop_cap);
-    rc |= dalloc(&g->ready, npop_cap);
-    rc |= dalloc(&g->mready, npop_cap);
+    rc |= dalloc(&g->bv64, npop_cap);
+    rc |= dalloc(&g->mv64, Bc);
     rc |= dalloc(&g->prep, npop_cap);
-    rc |= dalloc(&g->bval, npop_cap);
     rc |= dalloc(&g->t2, Bc);
     rc |= dalloc(&g->posrec, Bc);
     rc |= dalloc(&g->pos_of, Bc);
@@ -1714,7 +1711,7 @@ int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->pt, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->ekey, g->epol, g->ka, g->va, g->kb, g->vb, g->hist,
-                  g->dp, g->S, g->item, g->ready, g->mready, g->prep, g->t2, g->posrec, g->pos_of, g->bval, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
+                  g->dp, g->S, g->item, g->bv64, g->mv64, g->prep, g->t2, g->posrec, g->pos_of, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -2006,6 +2003,14 @@ int fibar_debug_times(fibar_engine *g, uint64_t *done_ns, uint64_t *grab_ns, int
   CK(cudaStreamSynchronize(g->L.stream));
   CK(cudaMemcpy(done_ns, g->dbg_t, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(grab_ns, g->dbg_g, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+// debug: copy the blur prep records (80 B each) of the last batch
+int fibar_debug_prep(fibar_engine *g, void *out, int64_t n) {
+  if (!g || !g->prep) return fail(FIBAR_E_CONFIG, "no prep");
+  CK(cudaStreamSynchronize(g->L.stream));
+  CK(cudaMemcpy(out, g->prep, sizeof(BlurPrep) * n, cudaMemcpyDeviceToHost));
   return 0;
 }
 

@@ -37,3 +37,19 @@ for f in (0.1, 0.5, 0.9, 1.0):
     print(f"item rank {f}: index {idx[k]} done at {d[k]:.1f} us")
 late = idx[d > np.percentile(d, 99.9)]
 print("latest items (index):", late[:20])
+
+prep = np.zeros((npop, 20), np.uint32)
+_native.check(eng._lib.fibar_debug_prep(eng._h, prep.ctypes.data, npop), "prep")
+okm, pend = prep[:, 0], prep[:, 1]
+flags = prep[:, 2:11]
+done_f = done.astype(np.float64)
+hops = []; ndeps = []
+for p_ in np.nonzero(okm)[0][::50]:
+    fs = [int(flags[p_, t]) & 0x7FFFFFFF for t in range(9) if (pend[p_] >> t) & 1]
+    ndeps.append(len(fs))
+    if fs and done[p_] > 0:
+        last = max(done_f[f] for f in fs)
+        hops.append((done_f[p_] - last) / 1e3)
+hops = np.array(hops)
+print("pending taps per item: mean", np.mean(ndeps), "frac items with deps", np.mean(np.array(ndeps) > 0))
+print("hop latency (done - last dep done) us percentiles 10/50/90/99:", np.percentile(hops, [10, 50, 90, 99]))

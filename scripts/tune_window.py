@@ -37,7 +37,8 @@ for s in a.settings:
     dbg = parts[2] if len(parts) > 2 else "0"
     os.environ.update(FIBAR_CHUNK=c, FIBAR_WARM=w, FIBAR_DEBUG_WINDOW=dbg,
                       FIBAR_BLUR_BLOCKS=parts[3] if len(parts) > 3 else "64",
-                      FIBAR_BLUR_SLEEP=parts[4] if len(parts) > 4 else "0")
+                      FIBAR_BLUR_SLEEP=parts[4] if len(parts) > 4 else "0",
+                      FIBAR_BLUR_MODE=parts[5] if len(parts) > 5 else "1")
     eng = ReconstructionEngine(geom, params, batch_capacity=a.cap)
     for rep in range(2):
         eng.reset()
