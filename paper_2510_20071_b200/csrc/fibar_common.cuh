@@ -88,6 +88,7 @@ struct DevState {
   long long warm_pops;   // evictions replayed during speculative warm-ups (stats)
   long long coop_iters;  // warp-cooperative eviction-count steps (stats)
   long long fix_rounds;  // verifier rounds (stats)
+  int geo, geo_next;     // window candidates: geometric set needed (this / next batch)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {

@@ -45,7 +45,7 @@ constexpr int TPB = 256;
 
 
 __constant__ long long c_fine_mul[NFINE] = {-8, -4, -2, -1, 0, 1, 2, 4, 8, 16};
-__constant__ long long c_lin_off[NLIN] = {-1024, -256, -64, 0, 64, 256, 1024};
+__constant__ long long c_lin_off[NLIN] = {-4096, -1024, -256, 0, 256, 1024, 4096};
 __constant__ double c_geo_mul[NGEO] = {0.25, 0.5, 0.75, 1.25, 1.5, 2.0, 2.5, 3.0, 4.0, 6.0, 8.0, 12.0};
 
 struct ChunkRec {
@@ -292,9 +292,10 @@ __device__ __forceinline__ long long cand_len(const Ctx &x, long long q0, int i)
   return L < 1 ? 1 : (L > x.qmax ? x.qmax : L);
 }
 
-// floor(N / D) for N >= 0, D > 0 via a float64 quotient and an exact integer fix-up
+// floor(N / D) for N >= 0, D > 0: a float32 reciprocal estimate (relative
+// error ~1e-7, and the quotients here stay below 2^24) and an exact integer fix-up
 __device__ __forceinline__ long long floordiv_nn(long long N, long long D) {
-  long long q = (long long)__ddiv_rn((double)N, (double)D);
+  long long q = (long long)__fmul_rn((float)N, __frcp_rn((float)D));
   if (q * D > N) {
     do { --q; } while (q * D > N);
   } else {
@@ -403,21 +404,27 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
 // inclusive scan of the deltas over chunks, one CTA per candidate chain
 // (chains interleaved with stride `nc` in `anc`)
 __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) {
-  __shared__ int2 wt[32];
-  __shared__ int2 carry;
+  constexpr int PER = 4;
+  __shared__ int2 wt[33];
   const long long B = x.st->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int i = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (threadIdx.x == 0) carry = make_int2((int)x.st->npix, (int)x.st->ntiles);
-  __syncthreads();
-  for (int base = 1; base < T; base += 1024) {
-    const int c = base + threadIdx.x;
-    int2 v = c < T ? anc[(long long)c * nc + i] : make_int2(0, 0);
-    int2 inc = v;
+  int2 carry = make_int2((int)x.st->npix, (int)x.st->ntiles);
+  for (int base = 1; base < T; base += 1024 * PER) {
+    const int c0 = base + threadIdx.x * PER;
+    int2 v[PER];
+    int2 tsum = make_int2(0, 0);
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      v[r] = c0 + r < T ? anc[(long long)(c0 + r) * nc + i] : make_int2(0, 0);
+      tsum.x += v[r].x;
+      tsum.y += v[r].y;
+    }
+    int2 inc = tsum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      int tx = __shfl_up_sync(0xffffffffu, inc.x, o), ty = __shfl_up_sync(0xffffffffu, inc.y, o);
+      const int tx = __shfl_up_sync(0xffffffffu, inc.x, o), ty = __shfl_up_sync(0xffffffffu, inc.y, o);
       if (lane >= o) {
         inc.x += tx;
         inc.y += ty;
@@ -426,23 +433,29 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
     if (lane == 31) wt[wid] = inc;
     __syncthreads();
     if (wid == 0) {
-      int2 w = wt[lane], wi = w;
+      const int2 w = wt[lane];
+      int2 wi = w;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        int tx = __shfl_up_sync(0xffffffffu, wi.x, o), ty = __shfl_up_sync(0xffffffffu, wi.y, o);
+        const int tx = __shfl_up_sync(0xffffffffu, wi.x, o), ty = __shfl_up_sync(0xffffffffu, wi.y, o);
         if (lane >= o) {
           wi.x += tx;
           wi.y += ty;
         }
       }
       wt[lane] = make_int2(wi.x - w.x, wi.y - w.y);
+      if (lane == 31) wt[32] = wi;
     }
     __syncthreads();
-    const int2 cc = carry;
-    const int2 out = make_int2(cc.x + wt[wid].x + inc.x, cc.y + wt[wid].y + inc.y);
-    if (c < T) anc[(long long)c * nc + i] = out;
-    __syncthreads();
-    if (threadIdx.x == 1023) carry = out;
+    int2 run = make_int2(carry.x + wt[wid].x + inc.x - tsum.x, carry.y + wt[wid].y + inc.y - tsum.y);
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      run.x += v[r].x;
+      run.y += v[r].y;
+      if (c0 + r < T) anc[(long long)(c0 + r) * nc + i] = run;
+    }
+    carry.x += wt[32].x;
+    carry.y += wt[32].y;
     __syncthreads();
   }
 }
@@ -466,9 +479,10 @@ __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
     x.lu[c] = 32;
     return;
   }
+  const int nc = x.st->geo ? NCAND : NLIN;
   long long lens[NCAND], fs[NCAND];
 #pragma unroll 1
-  for (int i = 0; i < NCAND; ++i) {
+  for (int i = 0; i < nc; ++i) {
     const long long len = a - max(s0, a - cand_len(x, q0, i));
     const int2 cnt = x.anc[(long long)c * NCAND + i];
     const long long f = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) - len : -1;
@@ -483,7 +497,7 @@ __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
   }
   long long len_lo = -1, len_hi = -1, f_lo = 0, f_hi = 0;
 #pragma unroll 1
-  for (int i = 0; i < NCAND; ++i) {
+  for (int i = 0; i < nc; ++i) {
     if (fs[i] >= 0) {
       len_lo = lens[i];
       f_lo = fs[i];
@@ -503,6 +517,10 @@ __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
     L = (long long)ceil(root);
     unit = max(32LL, (len_hi - len_lo) / 64);
   }
+  // the next batch keeps the linear candidates only while every fixed point
+  // stays well inside their span (windows clamped at the batch start excepted)
+  const bool clamped = len_lo >= 0 && len_hi < 0 && len_lo == a - s0;
+  if (!clamped && (L < q0 + c_lin_off[0] / 2 || L > q0 + c_lin_off[NLIN - 1] / 2)) x.st->geo_next = 1;
   x.lc[c] = L;
   x.lu[c] = unit;
 }
@@ -628,75 +646,95 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   long long wpops = 0, coop = 0;
   const unsigned n_my = (unsigned)(e - a);
   const unsigned n_max = __reduce_max_sync(0xffffffffu, n_my);
+  // 32-bit state relative to the batch's start window (every index in play is
+  // within B + window of it); ring slots as (slot of s_start + offset) & Rm
+  const long long base = s.s_start;
+  const unsigned bslot = (unsigned)((unsigned long long)base & x.Rm);
+  const unsigned rm = (unsigned)x.Rm;
+  unsigned sr = (unsigned)(w.s - base);
+  const unsigned ar = (unsigned)(a - base), br = (unsigned)(b - base);
+  const unsigned e0r = (unsigned)(E0 - base);
+  unsigned q = (unsigned)w.q;
+  int np = (int)w.npix, nt = (int)w.ntiles;
+  unsigned ev = (unsigned)w.evctr;
+  const unsigned every = (unsigned)x.every;
+  unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0;
+  uint2 dnext = n_my > 0 ? x.dp[ar - e0r] : make_uint2(0, 0);
   for (unsigned t = 0; t < n_max; ++t) {
     const bool act = t < n_my;
-    const long long j = a + t;
-    if (act && j == b) {
-      r.st_s = w.s;
-      r.st_q = w.q;
+    const unsigned jr = ar + t;
+    if (act && jr == br) {
+      r.st_s = base + sr;
+      r.st_q = q;
     }
-    long long lo = 0, hi = 0;
+    unsigned lo = 0, hi = 0;
     if (act) {
-      const uint2 d = x.dp[j - E0];
-      const unsigned long long js = (unsigned long long)(j - w.s);
-      w.npix += (unsigned long long)d.x > js;
-      w.ntiles += (unsigned long long)d.y > js;
-      if (j - w.s + 1 > w.q) {
-        lo = w.s;
-        hi = j + 1 - w.q;
+      const uint2 d = dnext;
+      if (t + 1 < n_my) dnext = x.dp[jr + 1 - e0r];
+      const unsigned js = jr - sr;
+      np += d.x > js;
+      nt += d.y > js;
+      if (js + 1 > q) {
+        lo = sr;
+        hi = jr + 1 - q;
       }
     }
     const bool big = hi - lo > 8;
-    if (j < b) wpops += hi - lo;
+    if (jr < br) wpops += hi - lo;
     if (!big && hi > lo) {
-      long long np = w.npix, nt = w.ntiles;
-      for (long long k = lo; k < hi; ++k) {
-        const uint2 rr = x.rnext[(unsigned long long)k & x.Rm];
-        const unsigned long long dd = (unsigned long long)(j - k);
-        np -= (unsigned long long)rr.x > dd;
-        nt -= (unsigned long long)rr.y > dd;
+      for (unsigned k = lo; k < hi; ++k) {
+        const uint2 rr = x.rnext[(bslot + k) & rm];
+        const unsigned dd = jr - k;
+        np -= rr.x > dd;
+        nt -= rr.y > dd;
       }
-      w.npix = np;
-      w.ntiles = nt;
-      w.s = hi;
+      sr = hi;
     }
     unsigned m = __ballot_sync(0xffffffffu, big);
     while (m) {
       const int L = __ffs(m) - 1;
-      const long long l0 = __shfl_sync(0xffffffffu, lo, L);
-      const long long h0 = __shfl_sync(0xffffffffu, hi, L);
-      const long long jL = __shfl_sync(0xffffffffu, j, L);
+      const unsigned l0 = __shfl_sync(0xffffffffu, lo, L);
+      const unsigned h0 = __shfl_sync(0xffffffffu, hi, L);
+      const unsigned jL = __shfl_sync(0xffffffffu, jr, L);
       int cp = 0, ct = 0;
-      for (long long k = l0 + lane; k < h0; k += 32) {
-        const uint2 rr = x.rnext[(unsigned long long)k & x.Rm];
-        const unsigned long long dd = (unsigned long long)(jL - k);
-        cp += (unsigned long long)rr.x > dd;
-        ct += (unsigned long long)rr.y > dd;
+      for (unsigned k = l0 + lane; k < h0; k += 32) {
+        const uint2 rr = x.rnext[(bslot + k) & rm];
+        const unsigned dd = jL - k;
+        cp += rr.x > dd;
+        ct += rr.y > dd;
       }
       cp = __reduce_add_sync(0xffffffffu, cp);
       ct = __reduce_add_sync(0xffffffffu, ct);
       ++coop;
       if (lane == L) {
-        w.npix -= cp;
-        w.ntiles -= ct;
-        w.s = h0;
+        np -= cp;
+        nt -= ct;
+        sr = h0;
       }
       m &= m - 1;
     }
     if (act) {
-      if (++w.evctr >= x.every) {
-        w.evctr = 0;
-        if (w.npix >= 1 && w.ntiles >= 1) {
-          const long long qn = regulate(x, j - w.s + 1, w.npix, w.ntiles);
-          w.q = qn;
-          if (j >= b) {
-            qlo = min(qlo, qn);
-            qhi = max(qhi, qn);
+      if (++ev >= every) {
+        ev = 0;
+        if (np >= 1 && nt >= 1) {
+          q = (unsigned)regulate(x, (long long)(jr - sr + 1), np, nt);
+          if (jr >= br) {
+            qlo32 = min(qlo32, q);
+            qhi32 = max(qhi32, q);
           }
         }
       }
-      if (j >= b) x.S[j - E0] = (unsigned)(w.s - s.s_start);
+      if (jr >= br) x.S[jr - e0r] = sr;
     }
+  }
+  w.s = base + sr;
+  w.q = q;
+  w.npix = np;
+  w.ntiles = nt;
+  w.evctr = ev;
+  if (qhi32 > 0) {
+    qlo = qlo32;
+    qhi = qhi32;
   }
   {
     const unsigned long long wp = __reduce_add_sync(0xffffffffu, (unsigned)wpops);
@@ -958,7 +996,7 @@ __device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
 // neighbour's latest event at that time: directly (batch-start value or
 // first-run value) or, when a blur produced it, after that blur's flag.
 // Runs for all items in parallel, before any blur (no waiting).
-__global__ void __launch_bounds__(TPB) k_blur_prep(Ctx x) {
+__global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x) {
   const BatchScalars b = load_bs(x);
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
   const unsigned p = blockIdx.x * TPB + threadIdx.x;
@@ -1172,6 +1210,10 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
 
 __global__ void k_batch_end(Ctx x) {
   DevState *s = x.st;
+  if (x.spatial && s->B > 0) {
+    s->geo = s->geo_next;
+    s->geo_next = 0;
+  }
   s->E += s->B;
   if (x.spatial) {
     s->stale += s->stale_batch;
@@ -1337,6 +1379,7 @@ __global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy) {
 
 __global__ void k_init_state(DevState *s, long long q0) {
   memset(s, 0, sizeof(DevState));
+  s->geo = 1;
   s->q = q0;
   s->qtmin = q0;
   s->qtmax = q0;
@@ -1429,7 +1472,7 @@ struct fibar_engine {
   long long batches = 0;
   int nsm = 148;
   int blur_grid = 148;
-  int chunk = 64, warm = 128, debug = 0;
+  int chunk = 64, warm = 64, debug = 0;
   unsigned blur_sleep = 0;
   unsigned long long *dbg_t = nullptr, *dbg_g = nullptr;
 
@@ -1662,7 +1705,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   rc |= dalloc(&g->va, Bc);
   rc |= dalloc(&g->kb, Bc);
   rc |= dalloc(&g->vb, Bc);
-  rc |= dalloc(&g->hist, 256LL * nb_rs + 1);
+  rc |= dalloc(&g->hist, 256LL * nb_rs + 256LL * nb_rs / 4096 + 8);
   rc |= dalloc(&g->sel, 1);
   rc |= dalloc(&g->frame, n);
   if (g->use_gain) {

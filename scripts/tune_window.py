@@ -56,6 +56,8 @@ for s in a.settings:
     same = ref_l is None or np.array_equal(l, ref_l)
     tb = prof.get('blur_prep', (0, 0))[0]
     ref_l = l if ref_l is None else ref_l
+    detail = " ".join(f"{k}={prof[k][0]:.2f}" for k in ("anchor", "anchor_scan", "fp", "anchor2", "rs_scan", "rs_scatter", "blur_prep", "temporal", "link") if k in prof)
+    print(detail)
     print(f"{s:>20}: step {tot:8.2f} ms  window {win:8.2f} ms (run {prof['window_run'][0]:.2f} fix {prof['window_fix'][0]:.2f})"
           f"  warm pops/chunk {(st1['warm_pops'] - st0['warm_pops']) / max(ch, 1):8.1f}  reruns {st1['window_reruns'] - st0['window_reruns']}"
           f"  rounds {st1['fix_rounds'] - st0['fix_rounds']}  blur {prof['blur'][0]:.2f} ms prep {tb:.2f}  same={same}", flush=True)
