@@ -83,7 +83,8 @@ struct Ctx {
   long long n_raw;
   unsigned *blockcnt;
   unsigned *ekey;
-  int8_t *epol;
+  int8_t *epol, *spol;
+  uint2 *longseg;
   unsigned *tkey;                 // unsorted tile-major keys (sort input)
   const unsigned *skey, *sidx;    // sorted keys / batch-local event index
   uint2 *dp;
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     s->stale_batch = 0;
     s->ticket = 0;
     s->qhead = s->qtail = s->qtail_res = 0;
+    s->nlong = 0;
     s->blur_done = 0;
   }
 }
@@ -901,8 +903,35 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
 
 // -------------------------------------------------------------- temporal ---
 
-// Filter OFF: one thread per pixel segment replays its events in stream order
-// with the reference's float32 operation order (_kernels.py:67-73).
+// Per sorted position, fully parallel: the event's polarity gathered into
+// sorted order and (filter ON) whether the event is evicted stale in this
+// batch -- the random loads the serial per-pixel replay would otherwise wait on.
+__global__ void __launch_bounds__(TPB) k_posinfo(Ctx x) {
+  const long long B = x.st->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned jj = x.sidx[i];
+  x.spol[i] = x.epol[jj];
+  if (!x.spatial) return;
+  const long long E0 = x.st->E, s_start = x.st->s_start;
+  const long long s_end = s_start + x.S[B - 1];
+  const long long e = E0 + jj;
+  unsigned bidx = FIBAR_NONE;
+  if (e < s_end) {
+    const unsigned q = (unsigned)(e - s_start);
+    if (x.item[q].pix != FIBAR_NONE) bidx = q;
+  }
+  *reinterpret_cast<uint2 *>(&x.posrec[i]) = make_uint2(jj, bidx);
+}
+
+// One thread per pixel segment replays its events in stream order with the
+// reference's float32 operation order (_kernels.py:67-73 / 124-130).  Inputs
+// are read GROUP positions at a time (all loads issued before the dependent
+// arithmetic), so long segments (hot pixels) run at the arithmetic chain's speed.
+constexpr int GROUP = 8;
+constexpr int LONG_SEG = 512;    // segments longer than this go to k_temporal_long
+constexpr int MAX_LONG = 16384;
+
 __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
   const long long B = x.st->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
@@ -910,66 +939,207 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
   const unsigned key = x.skey[i];
   if (i > 0 && x.skey[i - 1] == key) return;
   const unsigned c = x.ekey[x.sidx[i]];
+  const long long end = x.spatial ? (long long)x.pt[c].end : -1;
+  if (i + LONG_SEG < B && x.skey[i + LONG_SEG] == key) {   // long segment: the warp-parallel kernel
+    const unsigned slot = atomicAdd(&x.st->nlong, 1u);
+    if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
+    return;
+  }
   float pb = x.pbar[c], lv = x.l[c];
   const float g = x.use_gain ? x.gain[c] : 1.0f;
   long long pos = i;
-  do {
-    const float p = (float)x.epol[x.sidx[pos]];
-    pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
-    float d = fsubr(p, pb);
-    if (x.use_gain) d = fmulr(d, g);
-    lv = faddr(fmulr(x.beta, lv), fmulr(x.h, d));
-    ++pos;
-  } while (pos < B && x.skey[pos] == key);
+  bool more = true;
+  while (more) {
+    int8_t pol[GROUP];
+    bool in[GROUP];
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      const long long q = pos + u;
+      in[u] = q < B && (end >= 0 ? q < end : x.skey[q] == key);
+      pol[u] = in[u] ? x.spol[q] : (int8_t)0;
+    }
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      if (!in[u]) {
+        more = false;
+        break;
+      }
+      const float p = (float)pol[u];
+      pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+      float d = fsubr(p, pb);
+      if (x.use_gain) d = fmulr(d, g);
+      lv = faddr(fmulr(x.beta, lv), fmulr(x.h, d));
+    }
+    pos += GROUP;
+  }
   x.pbar[c] = pb;
   x.l[c] = lv;
 }
 
-// Filter ON: same replay (_kernels.py:124-130), recording per position the
-// additive term t2 = h*d, the brightness assuming no blur (valid until the
-// pixel's first blur in the batch), and which blur each position builds on.
+// Filter ON: same replay, recording per position the additive term t2 = h*d,
+// the brightness assuming no blur (valid until the pixel's first blur in the
+// batch), and which blur each position builds on.
 __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
   const long long B = x.st->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
   const unsigned key = x.skey[i];
   if (i > 0 && x.skey[i - 1] == key) return;
-  const long long E0 = x.st->E, s_start = x.st->s_start;
-  const long long s_end = B > 0 ? s_start + x.S[B - 1] : s_start;
   const unsigned c = x.ekey[x.sidx[i]];
-  unsigned carry = x.pt[c].carried;
+  const PixRec prc = x.pt[c];
+  const long long end = prc.end;
+  if (end - i > LONG_SEG) {   // long segment (hot pixel): the warp-parallel kernel
+    const unsigned slot = atomicAdd(&x.st->nlong, 1u);
+    if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
+    return;
+  }
+  unsigned carry = prc.carried;
   if (carry != FIBAR_NONE) x.item[carry].runpos = (unsigned)i;
   float pb = x.pbar[c], lv = x.l[c];
   const float g = x.use_gain ? x.gain[c] : 1.0f;
-  long long pos = i;
-  do {
-    const unsigned jj = x.sidx[pos];
-    const float p = (float)x.epol[jj];
-    pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
-    float d = fsubr(p, pb);
-    if (x.use_gain) d = fmulr(d, g);
-    const float tt = fmulr(x.h, d);
-    lv = faddr(fmulr(x.beta, lv), tt);
-    x.t2[pos] = tt;
-    const long long e = E0 + jj;
-    unsigned bidx = FIBAR_NONE;
-    if (e < s_end) {
-      const unsigned q = (unsigned)(e - s_start);
-      if (x.item[q].pix != FIBAR_NONE) bidx = q;
+  for (long long pos = i; pos < end; pos += GROUP) {
+    int8_t pol[GROUP];
+    unsigned bidx[GROUP];
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      const long long q = pos + u;
+      pol[u] = q < end ? x.spol[q] : (int8_t)0;
+      bidx[u] = q < end ? x.posrec[q].bidx : FIBAR_NONE;
     }
-    PosRec pr;
-    pr.jj = jj;
-    pr.bidx = bidx;
-    pr.runbase = carry;
-    pr.val = lv;
-    x.posrec[pos] = pr;
-    if (bidx != FIBAR_NONE) {
-      carry = bidx;
-      if (pos + 1 < B && x.skey[pos + 1] == key) x.item[bidx].runpos = (unsigned)(pos + 1);
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      const long long q = pos + u;
+      if (q >= end) break;
+      const float p = (float)pol[u];
+      pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+      float d = fsubr(p, pb);
+      if (x.use_gain) d = fmulr(d, g);
+      const float tt = fmulr(x.h, d);
+      lv = faddr(fmulr(x.beta, lv), tt);
+      x.t2[q] = tt;
+      *reinterpret_cast<uint2 *>(&x.posrec[q].runbase) = make_uint2(carry, __float_as_uint(lv));
+      if (bidx[u] != FIBAR_NONE) {
+        carry = bidx[u];
+        if (q + 1 < end) x.item[bidx[u]].runpos = (unsigned)(q + 1);
+      }
     }
-    ++pos;
-  } while (pos < B && x.skey[pos] == key);
+  }
   x.pbar[c] = pb;
+}
+
+// Long pixel segments (hot pixels: thousands of events per batch) replayed by
+// a warp: lane i takes the i-th piece, starting TWARM events early from a
+// zero state.  The two float32 recurrences are contractions (|alpha|, |beta|
+// < 1), so trajectories from different starts become bit-identical within
+// ~170 events; each lane's piece-start state is then checked against the
+// previous lane's piece-end state and any piece whose start differed is
+// replayed serially from the exact state, so the result is exact either way.
+constexpr int TWARM = 256;
+
+__device__ __forceinline__ void iir_step(const Ctx &x, float &pb, float &lv, float p, float g, float &tt) {
+  pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+  float d = fsubr(p, pb);
+  if (x.use_gain) d = fmulr(d, g);
+  tt = fmulr(x.h, d);
+  lv = faddr(fmulr(x.beta, lv), tt);
+}
+
+// replay [q0, q1) from (pb, lv), writing the per-position outputs
+__device__ __forceinline__ void replay_piece(const Ctx &x, long long q0, long long q1, float &pb, float &lv, float g,
+                                             bool write) {
+  for (long long q = q0; q < q1; ++q) {
+    float tt;
+    iir_step(x, pb, lv, (float)x.spol[q], g, tt);
+    if (write && x.spatial) {
+      x.t2[q] = tt;
+      x.posrec[q].val = lv;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32) k_temporal_long(Ctx x) {
+  const unsigned n = min(x.st->nlong, (unsigned)MAX_LONG);
+  const int lane = threadIdx.x;
+  for (unsigned sidx = blockIdx.x; sidx < n; sidx += gridDim.x) {
+    const uint2 ls = x.longseg[sidx];
+    const long long st = ls.x;
+    const unsigned c = ls.y;
+    long long end;
+    if (x.spatial) {
+      end = x.pt[c].end;
+    } else {
+      // segment end by search on the sorted keys (OFF path has no pixel table)
+      const unsigned key = x.skey[st];
+      long long lo = st + 1, hi = x.st->B;
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (x.skey[mid] == key) lo = mid + 1; else hi = mid;
+      }
+      end = lo;
+    }
+    const long long len = end - st;
+    const long long P = (len + 31) / 32;
+    const long long q0 = min(end, st + lane * P), q1 = min(end, q0 + P);
+    const float g = x.use_gain ? x.gain[c] : 1.0f;
+    float pb, lv;
+    if (lane == 0) {
+      pb = x.pbar[c];
+      lv = x.l[c];
+    } else {
+      pb = 0.0f;
+      lv = 0.0f;
+      replay_piece(x, max(st, q0 - TWARM), q0, pb, lv, g, false);
+    }
+    const float spb = pb, slv = lv;   // speculative state at the piece start
+    replay_piece(x, q0, q1, pb, lv, g, true);
+    // verify boundaries in lane order; re-run pieces whose start was wrong
+    float epb = pb, elv = lv;
+    for (int i = 1; i < 32; ++i) {
+      const float ppb = __shfl_sync(0xffffffffu, epb, i - 1), plv = __shfl_sync(0xffffffffu, elv, i - 1);
+      const bool bad = __float_as_uint(__shfl_sync(0xffffffffu, spb, i)) != __float_as_uint(ppb) ||
+                       __float_as_uint(__shfl_sync(0xffffffffu, slv, i)) != __float_as_uint(plv);
+      if (bad && lane == i) {
+        pb = ppb;
+        lv = plv;
+        replay_piece(x, q0, q1, pb, lv, g, true);
+        epb = pb;
+        elv = lv;
+      }
+      __syncwarp();
+    }
+    const float fpb = __shfl_sync(0xffffffffu, epb, 31), flv = __shfl_sync(0xffffffffu, elv, 31);
+    if (!x.spatial) {
+      if (lane == 0) {
+        x.pbar[c] = fpb;
+        x.l[c] = flv;
+      }
+      continue;
+    }
+    if (lane == 0) x.pbar[c] = fpb;
+    // blur bookkeeping: which blur each position builds on (last stale event
+    // before it in the segment, or the pixel's carried blur)
+    unsigned last = FIBAR_NONE;
+    for (long long q = q0; q < q1; ++q) {
+      const unsigned bidx = x.posrec[q].bidx;
+      if (bidx != FIBAR_NONE) {
+        last = bidx;
+        if (q + 1 < end) x.item[bidx].runpos = (unsigned)(q + 1);
+      }
+    }
+    // exclusive "last non-NONE" scan over lanes
+    unsigned carry_in = x.pt[c].carried;
+    if (lane == 0 && carry_in != FIBAR_NONE) x.item[carry_in].runpos = (unsigned)st;
+    for (int i = 0; i < 31; ++i) {
+      const unsigned li = __shfl_sync(0xffffffffu, last, i);
+      if (lane > i && li != FIBAR_NONE) carry_in = li;
+    }
+    unsigned carry = carry_in;
+    for (long long q = q0; q < q1; ++q) {
+      x.posrec[q].runbase = carry;
+      const unsigned bidx = x.posrec[q].bidx;
+      if (bidx != FIBAR_NONE) carry = bidx;
+    }
+  }
 }
 
 // ------------------------------------------------------------------- blur ---
@@ -1449,7 +1619,8 @@ struct fibar_engine {
   int8_t *raw_p = nullptr;
   unsigned *blockcnt = nullptr;
   unsigned *ekey = nullptr;
-  int8_t *epol = nullptr;
+  int8_t *epol = nullptr, *spol = nullptr;
+  uint2 *longseg = nullptr;
   unsigned *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr, *hist = nullptr;
   uint2 *dp = nullptr;
   unsigned *S = nullptr, *pos_of = nullptr;
@@ -1513,6 +1684,8 @@ struct fibar_engine {
     x.blockcnt = blockcnt;
     x.ekey = ekey;
     x.epol = epol;
+    x.spol = spol;
+    x.longseg = longseg;
     x.tkey = ka;
     x.skey = skey;
     x.sidx = sidx;
@@ -1609,7 +1782,9 @@ int run_batch(fibar_engine *g) {
     FIBAR_LAUNCH(L, "window_run", k_window_run<<<(T + 127) / 128, 128, 0, s>>>(x));
     FIBAR_LAUNCH(L, "window_fix", k_window_fix<<<1, 1024, 0, s>>>(x));
     FIBAR_LAUNCH(L, "popj", k_popj<<<nb, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 8, 32, 0, s>>>(x));
     if (g->blur_on) {
       const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
       FIBAR_LAUNCH(L, "blur_prep", k_blur_prep<<<nbp, TPB, 0, s>>>(x));
@@ -1617,7 +1792,9 @@ int run_batch(fibar_engine *g) {
     }
     FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, s>>>(x));
   } else {
+    FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 8, 32, 0, s>>>(x));
   }
   FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
   CK(cudaGetLastError());
@@ -1701,6 +1878,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   rc |= dalloc(&g->blockcnt, nb_in + 1);
   rc |= dalloc(&g->ekey, Bc);
   rc |= dalloc(&g->epol, Bc);
+  rc |= dalloc(&g->spol, Bc);
+  rc |= dalloc(&g->longseg, 16384);
   rc |= dalloc(&g->ka, Bc);
   rc |= dalloc(&g->va, Bc);
   rc |= dalloc(&g->kb, Bc);
@@ -1753,7 +1932,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->pt, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
-                  g->raw_y, g->raw_p, g->blockcnt, g->ekey, g->epol, g->ka, g->va, g->kb, g->vb, g->hist,
+                  g->raw_y, g->raw_p, g->blockcnt, g->ekey, g->epol, g->spol, g->longseg, g->ka, g->va, g->kb, g->vb, g->hist,
                   g->dp, g->S, g->item, g->bv64, g->mv64, g->prep, g->t2, g->posrec, g->pos_of, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g};
   for (void *p : ptrs)

@@ -88,6 +88,14 @@ def _torch():
     return torch
 
 
+def _addr(a: np.ndarray) -> int:
+    """Data pointer of a numpy array (the buffer-protocol route is ~3x cheaper than .ctypes.data)."""
+    try:
+        return C.addressof(C.c_char.from_buffer(a))
+    except (TypeError, ValueError, BufferError):
+        return a.ctypes.data
+
+
 class ReconstructionEngine:
     """Full reconstruction state for one sensor, resident on a CUDA device."""
 
@@ -375,9 +383,11 @@ class ReconstructionEngine:
                 raise OrderError("event timestamps regress across blocks")
             if np.any(ts[1:] < ts[:-1]):
                 raise OrderError("event timestamps regress within a block")
-        self._sync_stream()
-        _native.check(self._lib.fibar_process(self._h, xs.ctypes.data, ys.ctypes.data, ps.ctypes.data, n,
-                                              _native.FIBAR_MEM_HOST), "fibar_process")
+        # host packets are copied on the engine's stream (no cross-stream hazard),
+        # so the per-packet path skips the current-stream check
+        rc = self._lib.fibar_process(self._h, _addr(xs), _addr(ys), _addr(ps), n, _native.FIBAR_MEM_HOST)
+        if rc:
+            _native.check(rc, "fibar_process")
         self._note_last_t(xs, ys, ts)
 
     def _note_last_t(self, xs, ys, ts) -> None:
@@ -385,10 +395,13 @@ class ReconstructionEngine:
         if ts is None:
             return
         W, H = self.geometry.width, self.geometry.height
-        for i in range(len(xs) - 1, -1, -1):
-            if xs[i] < W and ys[i] < H:
-                self.last_t = int(ts[i])
-                return
+        i = len(xs) - 1
+        if int(xs[i]) < W and int(ys[i]) < H:
+            self.last_t = int(ts[i])
+            return
+        keep = np.nonzero((xs < W) & (ys < H))[0]
+        if keep.size:
+            self.last_t = int(ts[keep[-1]])
 
     def _process_device(self, block: DeviceEventArray) -> None:
         torch = _torch()

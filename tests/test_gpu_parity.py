@@ -109,6 +109,7 @@ def _oracle_stream(kind, w, h, n, packet, spatial=True, seed=11, **kw):
     ("texture", 640, 480, 400_000, 10_000, True),
     ("texture_noise_hot", 320, 180, 300_000, 100_000, True),
     ("uniform", 346, 260, 300_000, 50_000, True),
+    ("texture_noise_hot", 320, 180, 300_000, 300_000, False),
 ])
 def test_oracle_streams(kind, w, h, n, packet, spatial):
     from paper_2510_20071_b200.pipeline import ReconstructionEngine
