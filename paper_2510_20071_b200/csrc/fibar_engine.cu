@@ -384,9 +384,11 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
       ct[i] += (unsigned long long)d.y > ks;
     }
   }
-  // shrink the left edge to the new starts
+  // shrink the left edge to the new starts (chunk 1's edges start at the batch's
+  // whole start window and can be long: k_anchor_base counts those grid-wide)
 #pragma unroll
   for (int i = 0; i < NCAND; ++i) {
+    if (c == 1) break;
     const long long sn = max(s0, a - cand_len(x, q0, i));
     for (long long k = sp[i] + lane; k < sn; k += 32) {
       const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
@@ -400,6 +402,42 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
     const int vp = __reduce_add_sync(0xffffffffu, cp[i]);
     const int vt = __reduce_add_sync(0xffffffffu, ct[i]);
     if (lane == 0) x.anc[(long long)c * NCAND + i] = make_int2(vp, vt);
+  }
+}
+
+// chunk 1's left edges [s_start, s_1i) counted by the whole grid (y = candidate)
+__global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
+  __shared__ int red[2][TPB / 32];
+  const long long B = x.st->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  if (T < 2) return;
+  const int i = blockIdx.y;
+  const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
+  const long long a = chunk_warm_start(x, E0, 1);
+  const long long Jc = a - 1;
+  const long long sn = max(s0, a - cand_len(x, q0, i));
+  int cp = 0, ct = 0;
+  for (long long k = s0 + (long long)blockIdx.x * TPB + threadIdx.x; k < sn; k += (long long)gridDim.x * TPB) {
+    const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+    const unsigned long long dd = (unsigned long long)(Jc - k);
+    cp += (unsigned long long)r.x > dd;
+    ct += (unsigned long long)r.y > dd;
+  }
+  cp = __reduce_add_sync(0xffffffffu, cp);
+  ct = __reduce_add_sync(0xffffffffu, ct);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = cp;
+    red[1][threadIdx.x >> 5] = ct;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sp = 0, st = 0;
+    for (int w = 0; w < TPB / 32; ++w) {
+      sp += red[0][w];
+      st += red[1][w];
+    }
+    if (sp) atomicSub(&x.anc[NCAND + i].x, sp);
+    if (st) atomicSub(&x.anc[NCAND + i].y, st);
   }
 }
 
@@ -872,30 +910,32 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
 // its pixel has no later event up to the popping event.
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
   const long long B = x.st->B;
-  const long long jj = (long long)blockIdx.x * TPB + threadIdx.x;
   const long long E0 = x.st->E, s_start = x.st->s_start;
+  const unsigned npop = B > 0 ? x.S[B - 1] : 0u;
+  const unsigned p = blockIdx.x * TPB + threadIdx.x;   // one thread per eviction (balanced)
   unsigned nst = 0;
-  if (jj < B) {
-    const unsigned lo = jj == 0 ? 0u : x.S[jj - 1];
-    const unsigned hi = x.S[jj];
-    const long long j = E0 + jj;
-    for (unsigned p = lo; p < hi; ++p) {
-      const long long k = s_start + p;
-      const bool stale =
-          (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);
-      Item it;
-      it.jrel = (unsigned)jj;
-      it.pix = FIBAR_NONE;
-      it.runpos = FIBAR_NONE;
-      it.pad = 0;
-      if (stale) {
-        const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
-        it.pix = c;
-        if (k < E0) x.pt[c].carried = p;
-        ++nst;
-      }
-      x.item[p] = it;
+  if (p < npop) {
+    // popping event: the first jj with S[jj] > p (S is non-decreasing)
+    unsigned lo = 0, hi = (unsigned)B - 1;
+    while (lo < hi) {
+      const unsigned mid = (lo + hi) >> 1;
+      if (__ldg(&x.S[mid]) > p) hi = mid; else lo = mid + 1;
     }
+    const long long k = s_start + p;
+    const long long j = E0 + lo;
+    const bool stale = (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);
+    Item it;
+    it.jrel = lo;
+    it.pix = FIBAR_NONE;
+    it.runpos = FIBAR_NONE;
+    it.pad = 0;
+    if (stale) {
+      const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
+      it.pix = c;
+      if (k < E0) x.pt[c].carried = p;
+      ++nst;
+    }
+    x.item[p] = it;
   }
   nst = __reduce_add_sync(0xffffffffu, nst);
   if ((threadIdx.x & 31) == 0 && nst) atomicAdd((unsigned long long *)&x.st->stale_batch, (unsigned long long)nst);
@@ -1775,13 +1815,14 @@ int run_batch(fibar_engine *g) {
     FIBAR_LAUNCH(L, "seg_marks", k_seg_marks<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "link", k_link<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "anchor", k_anchor<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "anchor_base", k_anchor_base<<<dim3(g->nsm / 2, NCAND), TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NCAND, 1024, 0, s>>>(x, g->anc, NCAND));
     FIBAR_LAUNCH(L, "fp", k_fp<<<(T + TPB - 1) / TPB, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "anchor2", k_anchor2<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NFINE, 1024, 0, s>>>(x, g->anc2, NFINE));
     FIBAR_LAUNCH(L, "window_run", k_window_run<<<(T + 127) / 128, 128, 0, s>>>(x));
     FIBAR_LAUNCH(L, "window_fix", k_window_fix<<<1, 1024, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "popj", k_popj<<<nb, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "popj", k_popj<<<(int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 8, 32, 0, s>>>(x));
