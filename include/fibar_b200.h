@@ -74,6 +74,11 @@ typedef struct fibar_config {
   float half_1p_beta;       /* float32(params.half_one_plus_beta) pipeline.py:435 */
   const float *gain;        /* optional host array [height*width] or NULL */
   int64_t batch_capacity;   /* max in-bounds events per device batch; 0 = default */
+  /* Row band (multi-GPU row-band partition, filter OFF only): this engine owns
+   * rows [band_y0, band_y0 + height) of a sensor_height-row sensor; events of
+   * other rows are left to their band's owner.  sensor_height = 0: no band. */
+  int32_t band_y0;
+  int32_t sensor_height;
 } fibar_config;
 
 /* Allocate device state for one sensor.  stream: a cudaStream_t (NULL = legacy default). */
@@ -130,8 +135,16 @@ int fibar_profile_read(fibar_engine *eng, int32_t max_entries, char *names, int3
 int fibar_debug_times(fibar_engine *eng, uint64_t *done_ns, uint64_t *grab_ns, int64_t n);
 /* Debug only: the blur items' resolved-tap records of the last batch (80 B each). */
 int fibar_debug_prep(fibar_engine *eng, void *out, int64_t n);
+/* Copy the float32 brightness grid (after running coalesced events) to dst
+ * (dst_mem: FIBAR_MEM_DEVICE, asynchronous; or FIBAR_MEM_HOST, synchronous). */
+int fibar_copy_brightness(fibar_engine *eng, float *dst, int32_t dst_mem);
 /* Device pointer of the float32 brightness grid (valid until destroy). */
 int fibar_brightness_ptr(fibar_engine *eng, float **out);
+
+/* Stateless read-out of any device float32 grid of n pixels (e.g. a full frame
+ * assembled from row bands), same semantics as fibar_render.  stream: cudaStream_t. */
+int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_bound, uint8_t *out,
+                      int32_t out_mem, double *bounds, int32_t *degenerate, void *stream);
 
 const char *fibar_last_error(void);
 

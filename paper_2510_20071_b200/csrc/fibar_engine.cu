@@ -65,6 +65,7 @@ struct SelState {
 
 struct Ctx {
   int W, H, ts, tiles_x, A;
+  unsigned band_y0, full_H;   // row band [band_y0, band_y0 + H) of a full_H-row sensor
   long long n_pix;
   long long num, den, qmin, qmax, every;
   float alpha, oma, beta, h;
@@ -108,24 +109,44 @@ struct Ctx {
 constexpr int IN_ITEMS = 8;
 constexpr int IN_TILE = TPB * IN_ITEMS;
 
+// an event is kept iff it lies on the sensor (else it is out of bounds,
+// counted like pipeline.py:524-525) and in this engine's row band (a band
+// engine silently leaves other bands' events to their owners)
+__device__ __forceinline__ bool on_sensor(const Ctx &x, unsigned xx, unsigned yy) {
+  return xx < (unsigned)x.W && yy < x.full_H;
+}
+__device__ __forceinline__ bool in_band(const Ctx &x, unsigned yy) { return yy - x.band_y0 < (unsigned)x.H; }
+
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
-  __shared__ unsigned wsum[TPB / 32];
+  __shared__ unsigned wsum[TPB / 32], woob[TPB / 32];
   const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
-  unsigned cnt = 0;
+  unsigned cnt = 0, oob = 0;
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
     long long i = base + r;
-    if (i < x.n_raw) cnt += (x.raw_x[i] < x.W) & (x.raw_y[i] < x.H);
+    if (i < x.n_raw) {
+      const unsigned xx = x.raw_x[i], yy = x.raw_y[i];
+      const bool ok = on_sensor(x, xx, yy);
+      oob += !ok;
+      cnt += ok && in_band(x, yy);
+    }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  oob = __reduce_add_sync(0xffffffffu, oob);
+  if ((threadIdx.x & 31) == 0) {
+    wsum[threadIdx.x >> 5] = cnt;
+    woob[threadIdx.x >> 5] = oob;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned t = 0;
-    for (int w = 0; w < TPB / 32; ++w) t += wsum[w];
+    unsigned t = 0, o = 0;
+    for (int w = 0; w < TPB / 32; ++w) {
+      t += wsum[w];
+      o += woob[w];
+    }
     x.blockcnt[blockIdx.x] = t;
     if (blockIdx.x == 0) x.blockcnt[nblocks] = 0;
+    if (o) atomicAdd((unsigned long long *)&x.st->oob, (unsigned long long)o);
   }
 }
 
@@ -139,7 +160,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
     long long i = base + r;
-    keep[r] = i < x.n_raw && (x.raw_x[i] < x.W) && (x.raw_y[i] < x.H);
+    keep[r] = i < x.n_raw && on_sensor(x, x.raw_x[i], x.raw_y[i]) && in_band(x, x.raw_y[i]);
     cnt += keep[r];
   }
   unsigned incl = cnt;
@@ -157,7 +178,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   for (int r = 0; r < IN_ITEMS; ++r) {
     if (!keep[r]) continue;
     long long i = base + r;
-    const unsigned xx = x.raw_x[i], yy = x.raw_y[i];
+    const unsigned xx = x.raw_x[i], yy = x.raw_y[i] - x.band_y0;
     const unsigned key = yy * (unsigned)x.W + xx;
     const unsigned tile = (yy / x.ts) * (unsigned)x.tiles_x + xx / x.ts;
     const unsigned sub = (yy % x.ts) * x.ts + xx % x.ts;
@@ -171,7 +192,6 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     const long long B = x.blockcnt[nblocks];
     DevState *s = x.st;
     s->B = B;
-    s->oob += x.n_raw - B;
     s->s_start = s->s;
     s->stale_batch = 0;
     s->ticket = 0;
@@ -1518,6 +1538,14 @@ __global__ void k_sel_pick(SelState *sel, int pass) {
   for (int i = threadIdx.x; i < 4 * 2048; i += blockDim.x) (&sel->hist[0][0])[i] = 0;
 }
 
+__global__ void k_sel_init(SelState *sel, unsigned r0, unsigned r1, unsigned r2, unsigned r3) {
+  for (int t = 0; t < 4; ++t) sel->prefix[t] = 0;
+  sel->rank[0] = r0;
+  sel->rank[1] = r1;
+  sel->rank[2] = r2;
+  sel->rank[3] = r3;
+}
+
 // lo/hi from the selected order statistics (numpy 'linear' percentile, _lerp)
 __global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound) {
   double lo, hi;
@@ -1641,6 +1669,7 @@ int ceil_log2(long long v) {
 struct fibar_engine {
   fibar_config cfg{};
   int W = 0, H = 0, ts = 2, A = 4, tiles_x = 0, tiles_y = 0;
+  unsigned band_y0 = 0, full_H = 0;
   long long n_pix = 0, n_tiles = 0;
   long long q0 = 0;
   Launcher L;
@@ -1691,6 +1720,8 @@ struct fibar_engine {
     Ctx x{};
     x.W = W;
     x.H = H;
+    x.band_y0 = band_y0;
+    x.full_H = full_H;
     x.ts = ts;
     x.tiles_x = tiles_x;
     x.A = A;
@@ -1845,6 +1876,63 @@ int run_batch(fibar_engine *g) {
   return 0;
 }
 
+// read-out (pipeline.py:562-584) of n float32 values at l: exact order
+// statistics for the robust bounds (numpy 'linear' percentile), float64 map
+int render_core(Launcher &L, const float *l, long long n, int32_t mode, double fixed_bound, uint8_t *out,
+                int32_t out_mem, double *bounds, int32_t *degenerate, SelState *sel, uint8_t *frame, int nsm) {
+  if (mode == FIBAR_RENDER_FIXED && !(fixed_bound > 0)) return fail(FIBAR_E_CONFIG, "fixed scale bound must be positive");
+  if (mode != FIBAR_RENDER_FIXED && mode != FIBAR_RENDER_ROBUST) return fail(FIBAR_E_CONFIG, "unknown scale mode");
+  cudaStream_t s = L.stream;
+  double g_lo = 0, g_hi = 0;
+  if (mode == FIBAR_RENDER_ROBUST) {
+    // virtual index (n-1)*q, neighbours floor / floor+1, clamped at the top
+    const double qs[2] = {1.0 / 100.0, 99.0 / 100.0};
+    double gam[2];
+    unsigned rk[4];
+    for (int t = 0; t < 2; ++t) {
+      const double v = (double)(n - 1) * qs[t];
+      long long prev, next;
+      if (v >= (double)(n - 1)) {
+        prev = next = n - 1;
+        gam[t] = v + 1.0;   // numpy's gamma uses index -1 here; a == b so the value is unaffected
+      } else if (v < 0) {
+        prev = next = 0;
+        gam[t] = v;
+      } else {
+        prev = (long long)std::floor(v);
+        next = prev + 1;
+        gam[t] = v - (double)prev;
+      }
+      rk[2 * t] = (unsigned)prev;
+      rk[2 * t + 1] = (unsigned)next;
+    }
+    g_lo = gam[0];
+    g_hi = gam[1];
+    FIBAR_LAUNCH(L, "sel_init", k_sel_init<<<1, 1, 0, s>>>(sel, rk[0], rk[1], rk[2], rk[3]));
+    const int grid = nsm * 2;
+    for (int pass = 0; pass < 3; ++pass) {
+      FIBAR_LAUNCH(L, "sel_hist", k_sel_hist<<<grid, TPB, 0, s>>>(l, n, sel, pass));
+      FIBAR_LAUNCH(L, "sel_pick", k_sel_pick<<<1, 128, 0, s>>>(sel, pass));
+    }
+  }
+  FIBAR_LAUNCH(L, "sel_bounds", k_sel_bounds<<<1, 1, 0, s>>>(sel, g_lo, g_hi, mode, fixed_bound));
+  uint8_t *dst = out_mem == FIBAR_MEM_DEVICE ? out : frame;
+  FIBAR_LAUNCH(L, "render_map", k_render_map<<<nsm * 4, TPB, 0, s>>>(l, n, sel, dst));
+  CK(cudaGetLastError());
+  if (out_mem != FIBAR_MEM_DEVICE) CK(cudaMemcpyAsync(out, frame, n, cudaMemcpyDeviceToHost, s));
+  if (bounds || degenerate || out_mem != FIBAR_MEM_DEVICE) {
+    SelState h;
+    CK(cudaMemcpyAsync(&h, sel, sizeof(SelState), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (bounds) {
+      bounds[0] = h.lo;
+      bounds[1] = h.hi;
+    }
+    if (degenerate) *degenerate = h.degenerate;
+  }
+  return 0;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ C ABI ---
@@ -1866,11 +1954,19 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   if (cfg->q_min < 1 || cfg->q_min > cfg->q_max) return fail(FIBAR_E_CONFIG, "bad q_min/q_max");
   if (cfg->fill_num < 1 || cfg->fill_den < 1) return fail(FIBAR_E_CONFIG, "bad fill ratio");
   if (cfg->width > 65535 || cfg->height > 65535) return fail(FIBAR_E_CONFIG, "coordinates must fit uint16");
+  if (cfg->sensor_height > 0) {
+    if (cfg->band_y0 < 0 || cfg->band_y0 + cfg->height > cfg->sensor_height)
+      return fail(FIBAR_E_CONFIG, "row band outside the sensor");
+    if (cfg->spatial_enabled && (cfg->band_y0 != 0 || cfg->height != cfg->sensor_height))
+      return fail(FIBAR_E_CONFIG, "row bands need the spatial filter off (the window is one global FIFO)");
+  }
   fibar_engine *g = new fibar_engine();
   g->cfg = *cfg;
   g->cfg.gain = nullptr;
   g->W = cfg->width;
   g->H = cfg->height;
+  g->band_y0 = (unsigned)cfg->band_y0;
+  g->full_H = cfg->sensor_height > 0 ? (unsigned)cfg->sensor_height : (unsigned)cfg->height;
   g->ts = cfg->tile_side;
   g->A = g->ts * g->ts;
   g->tiles_x = (g->W + g->ts - 1) / g->ts;
@@ -1927,6 +2023,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   rc |= dalloc(&g->vb, Bc);
   rc |= dalloc(&g->hist, 256LL * nb_rs + 256LL * nb_rs / 4096 + 8);
   rc |= dalloc(&g->sel, 1);
+  if (!rc) cudaMemset(g->sel, 0, sizeof(SelState));
   rc |= dalloc(&g->frame, n);
   if (g->use_gain) {
     rc |= dalloc(&g->gain, n);
@@ -2060,62 +2157,36 @@ int fibar_pending(fibar_engine *g, int64_t *device_events, int64_t *staged_event
 int fibar_render(fibar_engine *g, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem, double *bounds,
                  int32_t *degenerate) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  if (mode == FIBAR_RENDER_FIXED && !(fixed_bound > 0)) return fail(FIBAR_E_CONFIG, "fixed scale bound must be positive");
-  if (mode != FIBAR_RENDER_FIXED && mode != FIBAR_RENDER_ROBUST) return fail(FIBAR_E_CONFIG, "unknown scale mode");
   int rc = run_batch(g);
   if (rc) return rc;
-  cudaStream_t s = g->L.stream;
-  const long long n = g->n_pix;
-  double g_lo = 0, g_hi = 0;
-  if (mode == FIBAR_RENDER_ROBUST) {
-    // numpy percentile 'linear': virtual index (n-1)*q, neighbours floor/floor+1
-    SelState init;
-    memset(&init, 0, sizeof(init));
-    const double qs[2] = {1.0 / 100.0, 99.0 / 100.0};
-    double gam[2];
-    for (int t = 0; t < 2; ++t) {
-      const double v = (double)(n - 1) * qs[t];
-      long long prev, next;
-      if (v >= (double)(n - 1)) {
-        prev = next = n - 1;
-        gam[t] = v - (double)(-1);   // numpy's gamma uses index -1 here; a == b so the value is unaffected
-      } else if (v < 0) {
-        prev = next = 0;
-        gam[t] = v;
-      } else {
-        prev = (long long)std::floor(v);
-        next = prev + 1;
-        gam[t] = v - (double)prev;
-      }
-      init.rank[2 * t] = (unsigned)prev;
-      init.rank[2 * t + 1] = (unsigned)next;
-    }
-    g_lo = gam[0];
-    g_hi = gam[1];
-    CK(cudaMemcpyAsync(g->sel, &init, sizeof(SelState), cudaMemcpyHostToDevice, s));
-    const int grid = g->nsm * 2;
-    for (int pass = 0; pass < 3; ++pass) {
-      FIBAR_LAUNCH(g->L, "sel_hist", k_sel_hist<<<grid, TPB, 0, s>>>(g->l, n, g->sel, pass));
-      FIBAR_LAUNCH(g->L, "sel_pick", k_sel_pick<<<1, 128, 0, s>>>(g->sel, pass));
-    }
-    CK(cudaStreamSynchronize(s));   // init lives on the host stack
+  return render_core(g->L, g->l, g->n_pix, mode, fixed_bound, out, out_mem, bounds, degenerate, g->sel, g->frame, g->nsm);
+}
+
+int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem,
+                      double *bounds, int32_t *degenerate, void *stream) {
+  static SelState *sel = nullptr;
+  static uint8_t *frame = nullptr;
+  static long long cap = 0;
+  static Launcher L;
+  static int nsm = 0;
+  if (!l_dev || n < 1) return fail(FIBAR_E_CONFIG, "empty grid");
+  if (!sel) {
+    int rc = dalloc(&sel, 1);
+    if (rc) return rc;
+    CK(cudaMemset(sel, 0, sizeof(SelState)));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  FIBAR_LAUNCH(g->L, "sel_bounds", k_sel_bounds<<<1, 1, 0, s>>>(g->sel, g_lo, g_hi, mode, fixed_bound));
-  uint8_t *dst = out_mem == FIBAR_MEM_DEVICE ? out : g->frame;
-  FIBAR_LAUNCH(g->L, "render_map", k_render_map<<<g->nsm * 4, TPB, 0, s>>>(g->l, n, g->sel, dst));
-  CK(cudaGetLastError());
-  if (out_mem != FIBAR_MEM_DEVICE) CK(cudaMemcpyAsync(out, g->frame, n, cudaMemcpyDeviceToHost, s));
-  if (bounds || degenerate || out_mem != FIBAR_MEM_DEVICE) {
-    SelState h;
-    CK(cudaMemcpyAsync(&h, g->sel, sizeof(SelState), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    if (bounds) {
-      bounds[0] = h.lo;
-      bounds[1] = h.hi;
-    }
-    if (degenerate) *degenerate = h.degenerate;
+  if (out_mem != FIBAR_MEM_DEVICE && n > cap) {
+    if (frame) cudaFree(frame);
+    frame = nullptr;
+    int rc = dalloc(&frame, n);
+    if (rc) return rc;
+    cap = n;
   }
-  return 0;
+  L.stream = (cudaStream_t)stream;
+  return render_core(L, l_dev, n, mode, fixed_bound, out, out_mem, bounds, degenerate, sel, frame, nsm);
 }
 
 int fibar_read_qs(fibar_engine *g, int64_t qs[10]) {
@@ -2274,6 +2345,16 @@ int fibar_debug_prep(fibar_engine *g, void *out, int64_t n) {
   if (!g || !g->prep) return fail(FIBAR_E_CONFIG, "no prep");
   CK(cudaStreamSynchronize(g->L.stream));
   CK(cudaMemcpy(out, g->prep, sizeof(BlurPrep) * n, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int fibar_copy_brightness(fibar_engine *g, float *dst, int32_t dst_mem) {
+  if (!g || !dst) return fail(FIBAR_E_CONFIG, "null argument");
+  int rc = run_batch(g);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(dst, g->l, sizeof(float) * g->n_pix,
+                     dst_mem == FIBAR_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, g->L.stream));
+  if (dst_mem != FIBAR_MEM_DEVICE) CK(cudaStreamSynchronize(g->L.stream));
   return 0;
 }
 

@@ -110,6 +110,7 @@ class ReconstructionEngine:
         *,
         batch_capacity: int | None = None,
         device=None,
+        row_band: tuple[int, int] | None = None,
     ):
         if params.q_max > geometry.n_pix:
             raise ConfigError("q_max exceeds pixel count")
@@ -157,6 +158,8 @@ class ReconstructionEngine:
             alpha=float(self._alpha32), one_m_alpha=float(self._one_m_alpha32), beta=float(self._beta32),
             half_1p_beta=float(self._half_1p_beta32), gain=gain_ptr,
             batch_capacity=int(batch_capacity or 0),
+            band_y0=int(row_band[0]) if row_band else 0,
+            sensor_height=int(row_band[1]) if row_band else 0,
         )
         handle = C.c_void_p()
         with torch.cuda.device(self.device):
@@ -484,6 +487,18 @@ class ReconstructionEngine:
         return Frame(out.reshape(g.height, g.width), readout_time, scale_mode, (float(bounds[0]), float(bounds[1])),
                      bool(deg.value))
 
+    def brightness_device(self, out=None):
+        """The brightness grid as a CUDA float32 (H, W) tensor (device copy, no sync)."""
+        torch = _torch()
+        g = self.geometry
+        if out is None:
+            out = torch.empty((g.height, g.width), dtype=torch.float32, device=self.device)
+        self._sync_stream()
+        _native.check(self._lib.fibar_copy_brightness(self._h, out.data_ptr(), _native.FIBAR_MEM_DEVICE),
+                      "fibar_copy_brightness")
+        self._release_held()
+        return out
+
     def render_device(self, scale_mode: str = "robust", fixed_bound: float = 1.0, out=None):
         """Render into a CUDA uint8 tensor (H, W) without synchronising; returns the tensor."""
         torch = _torch()
@@ -506,6 +521,24 @@ class ReconstructionEngine:
                 raise ConfigError("fixed scale bound must be positive")
             return _native.FIBAR_RENDER_FIXED
         raise ConfigError(f"unknown scale mode {scale_mode!r}")
+
+
+def render_grid(l, scale_mode: str = "robust", fixed_bound: float = 1.0, readout_time: int = 0) -> Frame:
+    """Read out any CUDA float32 (H, W) brightness grid (e.g. assembled from row bands)."""
+    torch = _torch()
+    mode = ReconstructionEngine._mode(scale_mode, fixed_bound)
+    lib = _native.load()
+    g = l.contiguous()
+    if g.dtype != torch.float32 or not g.is_cuda:
+        raise ConfigError("render_grid needs a CUDA float32 tensor")
+    out = np.empty(g.numel(), np.uint8)
+    bounds = np.zeros(2, np.float64)
+    deg = C.c_int32(0)
+    stream = torch.cuda.current_stream(g.device).cuda_stream
+    _native.check(lib.fibar_render_grid(g.data_ptr(), g.numel(), mode, float(fixed_bound), out.ctypes.data,
+                                        _native.FIBAR_MEM_HOST, bounds.ctypes.data, C.byref(deg), C.c_void_p(stream)),
+                  "fibar_render_grid")
+    return Frame(out.reshape(g.shape), readout_time, scale_mode, (float(bounds[0]), float(bounds[1])), bool(deg.value))
 
 
 # -- frame output ----------------------------------------------------------------
