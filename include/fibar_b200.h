@@ -146,6 +146,15 @@ int fibar_brightness_ptr(fibar_engine *eng, float **out);
 int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_bound, uint8_t *out,
                       int32_t out_mem, double *bounds, int32_t *degenerate, void *stream);
 
+/* Decode nrec EVF1 records (event_io.py:353-369: dt u32 | xp u16 | y u16,
+ * little endian) already in device memory into device columns x, y (uint16),
+ * p (int8 +-1) and, if t is non-NULL, t = t_base + cumulative dt (uint64).
+ * records must be 16-byte aligned.  *first_bad receives the index of the
+ * first record outside width x height, or -1 (the caller raises DataError as
+ * the reference's decoder does).  Synchronises the stream. */
+int fibar_decode_evf1(const uint8_t *records, int64_t nrec, int32_t width, int32_t height, uint64_t t_base,
+                      uint16_t *x, uint16_t *y, int8_t *p, uint64_t *t, int64_t *first_bad, void *stream);
+
 const char *fibar_last_error(void);
 
 #ifdef __cplusplus

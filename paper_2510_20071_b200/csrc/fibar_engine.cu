@@ -1583,6 +1583,130 @@ __global__ void __launch_bounds__(TPB) k_render_map(const float *__restrict__ l,
   }
 }
 
+// ------------------------------------------------------------ EVF1 decode ---
+
+// EVF1 records (event_io.py:353-369): dt u32 LE | xp u16 (bit 15 polarity,
+// bits 0..14 x) | y u16.  Two records per thread through one 16-byte load;
+// columns out, per-block dt sums for the timestamp scan, first out-of-bounds
+// record index (the container is invalid then: DataError, event_io.py:359-365).
+constexpr int EV_PER_THREAD = 2;
+constexpr int EV_TILE = TPB * EV_PER_THREAD;
+
+__global__ void __launch_bounds__(TPB) k_evf1_decode(const uint4 *__restrict__ rec2, const uint2 *__restrict__ rec1,
+                                                     long long nrec, int W, int H, uint16_t *__restrict__ xo,
+                                                     uint16_t *__restrict__ yo, int8_t *__restrict__ po,
+                                                     unsigned *__restrict__ dto, unsigned long long *__restrict__ bsum,
+                                                     unsigned long long *__restrict__ first_bad) {
+  __shared__ unsigned long long ws[TPB / 32];
+  const long long i0 = ((long long)blockIdx.x * TPB + threadIdx.x) * EV_PER_THREAD;
+  unsigned dt[2] = {0u, 0u};
+  unsigned xp[2] = {0u, 0u}, yy[2] = {0u, 0u};
+  if (i0 + 1 < nrec) {
+    const uint4 v = __ldcs(&rec2[i0 >> 1]);
+    dt[0] = v.x;
+    xp[0] = v.y & 0xFFFFu;
+    yy[0] = v.y >> 16;
+    dt[1] = v.z;
+    xp[1] = v.w & 0xFFFFu;
+    yy[1] = v.w >> 16;
+  } else if (i0 < nrec) {
+    const uint2 v = rec1[i0];
+    dt[0] = v.x;
+    xp[0] = v.y & 0xFFFFu;
+    yy[0] = v.y >> 16;
+  }
+  unsigned long long s = 0;
+#pragma unroll
+  for (int r = 0; r < EV_PER_THREAD; ++r) {
+    const long long i = i0 + r;
+    if (i >= nrec) break;
+    const unsigned xx = xp[r] & 0x7FFFu;
+    if (xx >= (unsigned)W || yy[r] >= (unsigned)H) atomicMin(first_bad, (unsigned long long)i);
+    xo[i] = (uint16_t)xx;
+    yo[i] = (uint16_t)yy[r];
+    po[i] = (xp[r] >> 15) ? (int8_t)1 : (int8_t)-1;
+    dto[i] = dt[r];
+    s += dt[r];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < TPB / 32; ++w) t += ws[w];
+    bsum[blockIdx.x] = t;
+  }
+}
+
+// t = t_base + inclusive prefix sum of dt (numpy cumsum in uint64, then + t_base)
+__global__ void __launch_bounds__(1024) k_evf1_block_scan(unsigned long long *bsum, int nb, unsigned long long t_base) {
+  // one CTA: exclusive scan of the block sums, seeded with t_base
+  __shared__ unsigned long long carry;
+  __shared__ unsigned long long wt[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x == 0) carry = t_base;
+  __syncthreads();
+  for (int base = 0; base < nb; base += 1024) {
+    const int i = base + threadIdx.x;
+    const unsigned long long v = i < nb ? bsum[i] : 0ull;
+    unsigned long long inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    if (lane == 31) wt[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const unsigned long long w = wt[lane];
+      unsigned long long wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+        if (lane >= o) wi += t;
+      }
+      wt[lane] = wi - w;
+    }
+    __syncthreads();
+    const unsigned long long ex = carry + wt[wid] + inc - v;
+    if (i < nb) bsum[i] = ex;
+    __syncthreads();
+    if (threadIdx.x == 1023) carry = ex + v;
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(TPB) k_evf1_times(const unsigned *__restrict__ dt, long long nrec,
+                                                    const unsigned long long *__restrict__ bofs,
+                                                    unsigned long long *__restrict__ t) {
+  __shared__ unsigned long long ws[TPB / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long i0 = ((long long)blockIdx.x * TPB + threadIdx.x) * EV_PER_THREAD;
+  unsigned long long d[EV_PER_THREAD], s = 0;
+#pragma unroll
+  for (int r = 0; r < EV_PER_THREAD; ++r) {
+    d[r] = i0 + r < nrec ? dt[i0 + r] : 0ull;
+    s += d[r];
+  }
+  unsigned long long inc = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long v = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc += v;
+  }
+  if (lane == 31) ws[wid] = inc;
+  __syncthreads();
+  unsigned long long wofs = 0;
+  for (int w = 0; w < wid; ++w) wofs += ws[w];
+  unsigned long long run = bofs[blockIdx.x] + wofs + inc - s;
+#pragma unroll
+  for (int r = 0; r < EV_PER_THREAD; ++r) {
+    run += d[r];
+    if (i0 + r < nrec) t[i0 + r] = run;
+  }
+}
+
 // --------------------------------------------------------- state export ---
 
 __global__ void k_active_counts(Ctx x, unsigned *cnt) {
@@ -2345,6 +2469,34 @@ int fibar_debug_prep(fibar_engine *g, void *out, int64_t n) {
   if (!g || !g->prep) return fail(FIBAR_E_CONFIG, "no prep");
   CK(cudaStreamSynchronize(g->L.stream));
   CK(cudaMemcpy(out, g->prep, sizeof(BlurPrep) * n, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int fibar_decode_evf1(const uint8_t *records, int64_t nrec, int32_t width, int32_t height, uint64_t t_base,
+                      uint16_t *x, uint16_t *y, int8_t *p, uint64_t *t, int64_t *first_bad, void *stream) {
+  if (nrec < 0 || !first_bad) return fail(FIBAR_E_CONFIG, "bad arguments");
+  *first_bad = -1;
+  if (nrec == 0) return 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  const int nb = (int)((nrec + EV_TILE - 1) / EV_TILE);
+  unsigned *dt = nullptr;
+  unsigned long long *bsum = nullptr, *bad = nullptr;
+  CK(cudaMallocAsync((void **)&dt, sizeof(unsigned) * nrec, s));
+  CK(cudaMallocAsync((void **)&bsum, sizeof(unsigned long long) * (nb + 1), s));
+  CK(cudaMallocAsync((void **)&bad, sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(bad, 0xFF, sizeof(unsigned long long), s));
+  k_evf1_decode<<<nb, TPB, 0, s>>>(reinterpret_cast<const uint4 *>(records), reinterpret_cast<const uint2 *>(records),
+                                   nrec, width, height, x, y, p, dt, bsum, bad);
+  k_evf1_block_scan<<<1, 1024, 0, s>>>(bsum, nb, (unsigned long long)t_base);
+  if (t) k_evf1_times<<<nb, TPB, 0, s>>>(dt, nrec, bsum, reinterpret_cast<unsigned long long *>(t));
+  unsigned long long hb = 0;
+  CK(cudaMemcpyAsync(&hb, bad, sizeof(hb), cudaMemcpyDeviceToHost, s));
+  cudaFreeAsync(dt, s);
+  cudaFreeAsync(bsum, s);
+  cudaFreeAsync(bad, s);
+  CK(cudaStreamSynchronize(s));
+  CK(cudaGetLastError());
+  *first_bad = hb == ~0ull ? -1 : (int64_t)hb;
   return 0;
 }
 

@@ -431,7 +431,7 @@ class ReconstructionEngine:
                 ts = block.t
                 if self.last_t is not None and int(ts[0]) < self.last_t:
                     raise OrderError("event timestamps regress across blocks")
-                if np.any(ts[1:] < ts[:-1]):
+                if bool((ts[1:] < ts[:-1]).any()):
                     raise OrderError("event timestamps regress within a block")
         self._sync_stream()
         _native.check(self._lib.fibar_process(self._h, x.data_ptr(), y.data_ptr(), p.data_ptr(), n,
