@@ -45,7 +45,7 @@ constexpr int TPB = 256;
 
 
 __constant__ long long c_fine_mul[NFINE] = {-8, -4, -2, -1, 0, 1, 2, 4, 8, 16};
-__constant__ long long c_lin_off[NLIN] = {-4096, -1024, -256, 0, 256, 1024, 4096};
+__constant__ long long c_lin_off[NLIN] = {-16384, -4096, -1024, 0, 1024, 4096, 16384};
 __constant__ double c_geo_mul[NGEO] = {0.25, 0.5, 0.75, 1.25, 1.5, 2.0, 2.5, 3.0, 4.0, 6.0, 8.0, 12.0};
 
 struct ChunkRec {
@@ -382,6 +382,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
   if (c >= T) return;
   const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
+  const int nc = x.st->geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
   const long long a = chunk_warm_start(x, E0, c);
   const long long Jc = a - 1;
   const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
@@ -399,6 +400,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
     const uint2 d = x.dp[k - E0];
 #pragma unroll
     for (int i = 0; i < NCAND; ++i) {
+      if (i >= nc) break;
       const unsigned long long ks = (unsigned long long)(k - sp[i]);
       cp[i] += (unsigned long long)d.x > ks;
       ct[i] += (unsigned long long)d.y > ks;
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   // whole start window and can be long: k_anchor_base counts those grid-wide)
 #pragma unroll
   for (int i = 0; i < NCAND; ++i) {
-    if (c == 1) break;
+    if (c == 1 || i >= nc) break;
     const long long sn = max(s0, a - cand_len(x, q0, i));
     for (long long k = sp[i] + lane; k < sn; k += 32) {
       const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
@@ -419,6 +421,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   }
 #pragma unroll
   for (int i = 0; i < NCAND; ++i) {
+    if (i >= nc) break;
     const int vp = __reduce_add_sync(0xffffffffu, cp[i]);
     const int vt = __reduce_add_sync(0xffffffffu, ct[i]);
     if (lane == 0) x.anc[(long long)c * NCAND + i] = make_int2(vp, vt);
@@ -432,6 +435,7 @@ __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   if (T < 2) return;
   const int i = blockIdx.y;
+  if (i >= (x.st->geo ? NCAND : NLIN)) return;
   const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
   const long long a = chunk_warm_start(x, E0, 1);
   const long long Jc = a - 1;
