@@ -59,7 +59,7 @@ def parse():
     ap.add_argument("--events", type=int, default=None, help="override the config's event count")
     ap.add_argument("--packet", type=int, default=None)
     ap.add_argument("--filter", default=None, choices=("on", "off"))
-    ap.add_argument("--batch-cap", type=int, default=1 << 20)
+    ap.add_argument("--batch-cap", type=int, default=1 << 21)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one step, for ncu launch lists")

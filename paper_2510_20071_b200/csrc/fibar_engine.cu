@@ -1833,7 +1833,18 @@ struct fibar_engine {
   uint8_t *frame = nullptr;
   unsigned *cnt_tmp = nullptr, *tcnt_tmp = nullptr;
   uint16_t *q_tmp = nullptr;
-  long long fill = 0;                       // events staged in raw_* (host packets, or non-contiguous device packets)
+  long long fill = 0;                       // unused (kept 0); host packets go through the pinned staging below
+  // host packets: CPU copy into pinned staging set `cur`, one H2D per batch on
+  // a copy stream into device staging set `cur`, double buffered so the copy
+  // of batch k+1 overlaps the compute of batch k
+  uint16_t *hx[2] = {nullptr, nullptr}, *hy[2] = {nullptr, nullptr};
+  int8_t *hp[2] = {nullptr, nullptr};
+  uint16_t *sx[2] = {nullptr, nullptr}, *sy[2] = {nullptr, nullptr};
+  int8_t *sp_[2] = {nullptr, nullptr};
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
+  int cur = 0;
+  long long hfill = 0;
   const uint16_t *zx = nullptr, *zy = nullptr;  // pending zero-copy device range (contiguous device packets)
   const int8_t *zp = nullptr;
   long long zn = 0;
@@ -1937,26 +1948,25 @@ int init_state(fibar_engine *g) {
   }
   g->fill = 0;
   g->zn = 0;
+  g->hfill = 0;
   CK(cudaGetLastError());
   return 0;
 }
 
-int run_batch(fibar_engine *g) {
-  if (g->fill == 0 && g->zn == 0) return 0;
-  const bool zero_copy = g->zn > 0;
-  const long long n_raw = zero_copy ? g->zn : g->fill;
+int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                  cudaEvent_t used_ev) {
+  if (n_raw <= 0) return 0;
   Launcher &L = g->L;
   cudaStream_t s = L.stream;
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
   Ctx x = g->ctx(nullptr, nullptr, n_raw);
-  if (zero_copy) {
-    x.raw_x = g->zx;
-    x.raw_y = g->zy;
-    x.raw_p = g->zp;
-  }
+  x.raw_x = rx0;
+  x.raw_y = ry0;
+  x.raw_p = rp0;
   FIBAR_LAUNCH(L, "count_inb", k_count_inb<<<nb_in, TPB, 0, s>>>(x, nb_in));
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
   FIBAR_LAUNCH(L, "compact", k_compact<<<nb_in, TPB, 0, s>>>(x, nb_in));
+  if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
   const int where = radix_sort_pairs(L, g->ka, g->va, g->kb, g->vb, g->hist, &g->st->B, n_raw, g->key_bits);
   const unsigned *skey = where ? g->kb : g->ka;
   const unsigned *sidx = where ? g->vb : g->va;
@@ -1998,10 +2008,35 @@ int run_batch(fibar_engine *g) {
   }
   FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
   CK(cudaGetLastError());
-  g->fill = 0;
-  g->zn = 0;
   g->batches++;
   return 0;
+}
+
+// hand the filled host staging set to the device and run it
+int launch_host_batch(fibar_engine *g) {
+  if (g->hfill == 0) return 0;
+  const int c = g->cur;
+  const long long n = g->hfill;
+  CK(cudaStreamWaitEvent(g->cstream, g->ev_used[c], 0));
+  CK(cudaMemcpyAsync(g->sx[c], g->hx[c], sizeof(uint16_t) * n, cudaMemcpyHostToDevice, g->cstream));
+  CK(cudaMemcpyAsync(g->sy[c], g->hy[c], sizeof(uint16_t) * n, cudaMemcpyHostToDevice, g->cstream));
+  CK(cudaMemcpyAsync(g->sp_[c], g->hp[c], sizeof(int8_t) * n, cudaMemcpyHostToDevice, g->cstream));
+  CK(cudaEventRecord(g->ev_h2d[c], g->cstream));
+  CK(cudaStreamWaitEvent(g->L.stream, g->ev_h2d[c], 0));
+  g->hfill = 0;
+  g->cur ^= 1;
+  return run_batch_raw(g, g->sx[c], g->sy[c], g->sp_[c], n, g->ev_used[c]);
+}
+
+// run everything pending (zero-copy device range, then staged host packets)
+int run_batch(fibar_engine *g) {
+  if (g->zn > 0) {
+    const long long n = g->zn;
+    g->zn = 0;
+    int rc = run_batch_raw(g, g->zx, g->zy, g->zp, n, nullptr);
+    if (rc) return rc;
+  }
+  return launch_host_batch(g);
 }
 
 // read-out (pipeline.py:562-584) of n float32 values at l: exact order
@@ -2106,8 +2141,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   g->spatial = cfg->spatial_enabled != 0;
   g->blur_on = cfg->blur_enabled != 0;
   g->use_gain = cfg->gain != nullptr;
-  g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : (1LL << 20);
+  g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : (1LL << 21);
   if (g->Bcap > (1LL << 28)) g->Bcap = 1LL << 28;
+  if (g->Bcap < 1024) g->Bcap = std::max(g->Bcap, 16LL);
   g->key_bits = ceil_log2(g->n_tiles * g->A);
   // window-speculation tuning knobs (results never depend on them; the verifier
   // re-runs any chunk whose speculative start was wrong)
@@ -2137,9 +2173,18 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   rc |= dalloc(&g->st, 1);
   rc |= dalloc(&g->pbar, n);
   rc |= dalloc(&g->l, n);
-  rc |= dalloc(&g->raw_x, Bc);
-  rc |= dalloc(&g->raw_y, Bc);
-  rc |= dalloc(&g->raw_p, Bc);
+  for (int c = 0; c < 2; ++c) {
+    rc |= dalloc(&g->sx[c], Bc);
+    rc |= dalloc(&g->sy[c], Bc);
+    rc |= dalloc(&g->sp_[c], Bc);
+    if (cudaMallocHost((void **)&g->hx[c], sizeof(uint16_t) * Bc) != cudaSuccess ||
+        cudaMallocHost((void **)&g->hy[c], sizeof(uint16_t) * Bc) != cudaSuccess ||
+        cudaMallocHost((void **)&g->hp[c], sizeof(int8_t) * Bc) != cudaSuccess)
+      rc |= fail(FIBAR_E_CUDA, "cudaMallocHost");
+    cudaEventCreateWithFlags(&g->ev_h2d[c], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->ev_used[c], cudaEventDisableTiming);
+  }
+  cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking);
   rc |= dalloc(&g->blockcnt, nb_in + 1);
   rc |= dalloc(&g->ekey, Bc);
   rc |= dalloc(&g->epol, Bc);
@@ -2204,6 +2249,17 @@ int fibar_destroy(fibar_engine *g) {
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : g->L.pool) cudaEventDestroy(ev);
+  for (int c = 0; c < 2; ++c) {
+    if (g->sx[c]) cudaFree(g->sx[c]);
+    if (g->sy[c]) cudaFree(g->sy[c]);
+    if (g->sp_[c]) cudaFree(g->sp_[c]);
+    if (g->hx[c]) cudaFreeHost(g->hx[c]);
+    if (g->hy[c]) cudaFreeHost(g->hy[c]);
+    if (g->hp[c]) cudaFreeHost(g->hp[c]);
+    if (g->ev_h2d[c]) cudaEventDestroy(g->ev_h2d[c]);
+    if (g->ev_used[c]) cudaEventDestroy(g->ev_used[c]);
+  }
+  if (g->cstream) cudaStreamDestroy(g->cstream);
   delete g;
   return 0;
 }
@@ -2222,18 +2278,19 @@ int fibar_reset(fibar_engine *g) {
 int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n, int32_t mem) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
   if (n <= 0) return 0;
-  const cudaMemcpyKind kind = mem == FIBAR_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
   long long off = 0;
   if (mem == FIBAR_MEM_DEVICE) {
     // contiguous device packets are coalesced without copies: the batch reads
     // them in place (the caller keeps them alive until the next flush point)
-    if (g->fill > 0) {
-      int rc = run_batch(g);
+    if (g->hfill > 0) {
+      int rc = launch_host_batch(g);
       if (rc) return rc;
     }
     while (off < n) {
       if (g->zn > 0 && !(x + off == g->zx + g->zn && y + off == g->zy + g->zn && p + off == g->zp + g->zn)) {
-        int rc = run_batch(g);
+        const long long zn = g->zn;
+        g->zn = 0;
+        int rc = run_batch_raw(g, g->zx, g->zy, g->zp, zn, nullptr);
         if (rc) return rc;
       }
       if (g->zn == 0) {
@@ -2245,7 +2302,9 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
       g->zn += take;
       off += take;
       if (g->zn == g->Bcap) {
-        int rc = run_batch(g);
+        const long long zn = g->zn;
+        g->zn = 0;
+        int rc = run_batch_raw(g, g->zx, g->zy, g->zp, zn, nullptr);
         if (rc) return rc;
       }
     }
@@ -2256,16 +2315,17 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
     if (rc) return rc;
   }
   while (off < n) {
-    if (g->fill == g->Bcap) {
-      int rc = run_batch(g);
+    if (g->hfill == 0) CK(cudaEventSynchronize(g->ev_h2d[g->cur]));   // host set free again
+    const long long take = std::min((long long)n - off, g->Bcap - g->hfill);
+    memcpy(g->hx[g->cur] + g->hfill, x + off, sizeof(uint16_t) * take);
+    memcpy(g->hy[g->cur] + g->hfill, y + off, sizeof(uint16_t) * take);
+    memcpy(g->hp[g->cur] + g->hfill, p + off, sizeof(int8_t) * take);
+    g->hfill += take;
+    off += take;
+    if (g->hfill == g->Bcap) {
+      int rc = launch_host_batch(g);
       if (rc) return rc;
     }
-    const long long take = std::min((long long)n - off, g->Bcap - g->fill);
-    CK(cudaMemcpyAsync(g->raw_x + g->fill, x + off, sizeof(uint16_t) * take, kind, g->L.stream));
-    CK(cudaMemcpyAsync(g->raw_y + g->fill, y + off, sizeof(uint16_t) * take, kind, g->L.stream));
-    CK(cudaMemcpyAsync(g->raw_p + g->fill, p + off, sizeof(int8_t) * take, kind, g->L.stream));
-    g->fill += take;
-    off += take;
   }
   return 0;
 }
@@ -2278,7 +2338,7 @@ int fibar_flush(fibar_engine *g) {
 int fibar_pending(fibar_engine *g, int64_t *device_events, int64_t *staged_events) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
   if (device_events) *device_events = g->zn;
-  if (staged_events) *staged_events = g->fill;
+  if (staged_events) *staged_events = g->hfill;
   return 0;
 }
 
