@@ -5,22 +5,20 @@
 
 #define FIBAR_INF32 0xFFFFFFFFu
 
-// Per-pixel bookkeeping record (32 B = one sector, one random access per pixel touch).
-//   last : global in-bounds index of the pixel's latest event before the
-//          current device batch (-1 = never), i.e. the reference's implicit
-//          "is the pixel still queued" history, kept as a last-touch index.
+// Per-pixel batch record (16 B, one load per pixel touch), one table per batch
+// parity so batch k+1's front end can run while batch k's blur reads its own.
+// (The pixel's last event index before the batch -- the reference's implicit
+// "is the pixel still queued" history -- lives in a separate last-touch array.)
 //   st/end : [st, end) positions of the pixel's events in the current batch's
 //          pixel-sorted order (st == end: no events this batch).  Reset by the
 //          final pass, so the table is clean at every batch start.
 //   carried : blur item of the pixel's `last` event when that event is evicted
 //          stale during the current batch (else FIBAR_NONE); reset by the final pass.
-struct __align__(32) PixRec {
+struct __align__(16) PixRec {
   unsigned st;
   unsigned end;
   unsigned carried;
   unsigned pad0;
-  long long last;
-  unsigned pad1, pad2;
 };
 
 #define FIBAR_NONE 0xFFFFFFFFu
@@ -56,6 +54,19 @@ struct __align__(16) BlurPrep {
   unsigned okm, pend;
   unsigned flag[9];
   unsigned val[9];
+};
+
+// Scalars of one device batch (double buffered by batch parity).
+struct BatchState {
+  long long E0;        // in-bounds events before the batch (global index of its first event)
+  long long B;         // in-bounds events of the batch
+  long long s_start;   // window start when the batch began
+  long long npop;      // evictions of the batch (set by the window verifier)
+  long long stale_batch;
+  unsigned epoch;      // batch counter (tags blur words)
+  unsigned ticket;     // blur work ticket
+  unsigned nlong;      // long pixel segments
+  unsigned pad;
 };
 
 // Window / counter state living in device memory so no kernel needs a host

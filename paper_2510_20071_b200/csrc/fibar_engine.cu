@@ -42,6 +42,7 @@ constexpr int NLIN = 7;      // coarse candidates q0 + c_lin_off[i]
 constexpr int NGEO = 12;     // coarse candidates q0 * c_geo_mul[i]
 constexpr int NCAND = NLIN + NGEO;
 constexpr int TPB = 256;
+constexpr unsigned ITEM_CARRIED_ONLY = 1u;   // Item.pad flag
 
 
 __constant__ long long c_fine_mul[NFINE] = {-8, -4, -2, -1, 0, 1, 2, 4, 8, 16};
@@ -71,6 +72,8 @@ struct Ctx {
   float alpha, oma, beta, h;
   int use_gain, blur_on, spatial;
   DevState *st;
+  BatchState *bs;     // this batch's scalars (parity buffer)
+  long long *plast;   // per pixel: last event index before the batch
   float *pbar, *l;
   const float *gain;
   PixRec *pt;
@@ -92,7 +95,6 @@ struct Ctx {
   unsigned *S;
   Item *item;
   PosRec *posrec;
-  unsigned *pos_of;
   float *t2;
   unsigned long long *bv64, *mv64;   // (epoch << 32 | float bits) per blur item / per sorted position
   BlurPrep *prep;
@@ -189,28 +191,29 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     ++pos;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    const long long B = x.blockcnt[nblocks];
     DevState *s = x.st;
-    s->B = B;
-    s->s_start = s->s;
-    s->stale_batch = 0;
-    s->ticket = 0;
-    s->qhead = s->qtail = s->qtail_res = 0;
-    s->nlong = 0;
-    s->blur_done = 0;
+    BatchState *b = x.bs;
+    b->E0 = s->E;
+    b->B = x.blockcnt[nblocks];
+    b->s_start = s->s;
+    b->npop = 0;
+    b->stale_batch = 0;
+    b->ticket = 0;
+    b->nlong = 0;
+    s->epoch += 1;
+    b->epoch = s->epoch;
   }
 }
 
 // ------------------------------------------------------------------ link ---
 
 __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
   const unsigned k = x.skey[i];
   const unsigned jj = x.sidx[i];
   const unsigned c = x.ekey[jj];
-  x.pos_of[jj] = (unsigned)i;
   const bool head = i == 0 || x.skey[i - 1] != k;
   const bool tail = i == B - 1 || x.skey[i + 1] != k;
   if (head) x.pt[c].st = (unsigned)i;
@@ -221,10 +224,10 @@ __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
 }
 
 __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
-  const long long E0 = x.st->E;
+  const long long E0 = x.bs->E0;
   const unsigned key = x.skey[i];
   const unsigned jj = x.sidx[i];
   const long long j = E0 + jj;
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
   // pixel links: neighbours in the sorted order
   const bool first_pix = i == 0 || x.skey[i - 1] != key;
   const bool last_pix = i == B - 1 || x.skey[i + 1] != key;
-  const long long pre_last = x.pt[c].last;
+  const long long pre_last = x.plast[c];
   const long long prev_p = first_pix ? pre_last : E0 + x.sidx[i - 1];
   const long long next_p = last_pix ? -1 : E0 + x.sidx[i + 1];
 
@@ -376,12 +379,12 @@ __device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, 
 // windows [max(s_start, a_c - L_i), a_c - 1], as deltas from the previous
 // chunk's window of the same candidate (one warp per chunk).
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
   if (c >= T) return;
-  const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
   const int nc = x.st->geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
   const long long a = chunk_warm_start(x, E0, c);
   const long long Jc = a - 1;
@@ -431,12 +434,12 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
 // chunk 1's left edges [s_start, s_1i) counted by the whole grid (y = candidate)
 __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
   __shared__ int red[2][TPB / 32];
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   if (T < 2) return;
   const int i = blockIdx.y;
   if (i >= (x.st->geo ? NCAND : NLIN)) return;
-  const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
   const long long a = chunk_warm_start(x, E0, 1);
   const long long Jc = a - 1;
   const long long sn = max(s0, a - cand_len(x, q0, i));
@@ -470,7 +473,7 @@ __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
 __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) {
   constexpr int PER = 4;
   __shared__ int2 wt[33];
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int i = blockIdx.x;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -532,11 +535,11 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
 // candidate above the largest stable one is a start that collapses onto the
 // true trajectory within a handful of events, with few evictions.
 __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int c = blockIdx.x * TPB + threadIdx.x;
   if (c >= T) return;
-  const long long E0 = x.st->E, s0 = x.st->s_start, q0 = x.st->q;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
   const long long a = chunk_warm_start(x, E0, c);
   if (c == 0 || a == E0) {
     x.lc[c] = a - s0;
@@ -600,12 +603,12 @@ __device__ __forceinline__ long long fine_start(const Ctx &x, long long s0, long
 // deltas from the previous chunk's window of the same candidate (the start
 // may move either way); one warp per chunk
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
   if (c >= T) return;
-  const long long E0 = x.st->E, s0 = x.st->s_start;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start;
   const long long ac = chunk_warm_start(x, E0, c);
   const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
   const long long Jc = ac - 1, Jp = ap - 1;
@@ -655,21 +658,22 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
 // entries (the first trims of a long start window) are counted by the whole
 // warp, 32 ring entries per step.
 __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int c = blockIdx.x * 128 + threadIdx.x;
   const int lane = threadIdx.x & 31;
   if ((blockIdx.x * 128 + (threadIdx.x & ~31)) >= T) return;   // whole warp out of range
   const bool valid = c < T;
   const DevState s = *x.st;
-  const long long E0 = s.E;
+  const long long E0 = x.bs->E0;
+  const long long s_start0 = x.bs->s_start;
   const long long b = E0 + (long long)c * x.chunk;
   const long long e = valid ? min(E0 + B, b + x.chunk) : b;
   const long long a = valid ? chunk_warm_start(x, E0, c) : b;
   WState w{0, 1, 0, 0, 0};
   if (valid) {
     if (a == E0) {
-      w.s = s.s_start;
+      w.s = s_start0;
       w.q = s.q;
       w.npix = s.npix;
       w.ntiles = s.ntiles;
@@ -679,14 +683,14 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
       int jstar = -1;
 #pragma unroll 1
       for (int j = 0; j < NFINE; ++j) {
-        const long long sc = fine_start(x, s.s_start, a, center, unit, j);
+        const long long sc = fine_start(x, s_start0, a, center, unit, j);
         const int2 cnt = x.anc2[(long long)c * NFINE + j];
         const long long len = a - sc;
         if (cnt.x >= 1 && cnt.y >= 1 && regulate(x, len, cnt.x, cnt.y) >= len) jstar = j;
       }
       const int g = jstar + 1 < NFINE ? jstar + 1 : NFINE - 1;
       const int2 cnt = x.anc2[(long long)c * NFINE + g];
-      w.s = fine_start(x, s.s_start, a, center, unit, g);
+      w.s = fine_start(x, s_start0, a, center, unit, g);
       w.npix = cnt.x;
       w.ntiles = cnt.y;
       const long long len = a - w.s;
@@ -712,7 +716,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   const unsigned n_max = __reduce_max_sync(0xffffffffu, n_my);
   // 32-bit state relative to the batch's start window (every index in play is
   // within B + window of it); ring slots as (slot of s_start + offset) & Rm
-  const long long base = s.s_start;
+  const long long base = s_start0;
   const unsigned bslot = (unsigned)((unsigned long long)base & x.Rm);
   const unsigned rm = (unsigned)x.Rm;
   unsigned sr = (unsigned)(w.s - base);
@@ -827,9 +831,9 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
 __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
   __shared__ int n_bad;
   __shared__ long long red_lo[32], red_hi[32];
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
-  const long long E0 = x.st->E, s_start = x.st->s_start;
+  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
   int rounds = 0, reruns = 0;
   while (true) {
     if (threadIdx.x == 0) n_bad = 0;
@@ -918,9 +922,9 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
         s->qtmax = max(s->qtmax, hi);
       }
       s->pops += r.en_s - s_start;
-      s->npop = r.en_s - s_start;
+      x.bs->npop = r.en_s - s_start;
     } else {
-      s->npop = 0;
+      x.bs->npop = 0;
     }
     s->chunks += T;
     s->fix_rounds += rounds;
@@ -933,8 +937,8 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
 // order the reference blurs them, _kernels.py:152-189).  An entry is stale iff
 // its pixel has no later event up to the popping event.
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
-  const long long B = x.st->B;
-  const long long E0 = x.st->E, s_start = x.st->s_start;
+  const long long B = x.bs->B;
+  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
   const unsigned npop = B > 0 ? x.S[B - 1] : 0u;
   const unsigned p = blockIdx.x * TPB + threadIdx.x;   // one thread per eviction (balanced)
   unsigned nst = 0;
@@ -956,13 +960,18 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
     if (stale) {
       const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
       it.pix = c;
-      if (k < E0) x.pt[c].carried = p;
+      if (k < E0) {
+        x.pt[c].carried = p;
+        // no event of the pixel in this batch after its pre-batch last one
+        if ((unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(E0 + B - 1 - k))
+          it.pad |= ITEM_CARRIED_ONLY;
+      }
       ++nst;
     }
     x.item[p] = it;
   }
   nst = __reduce_add_sync(0xffffffffu, nst);
-  if ((threadIdx.x & 31) == 0 && nst) atomicAdd((unsigned long long *)&x.st->stale_batch, (unsigned long long)nst);
+  if ((threadIdx.x & 31) == 0 && nst) atomicAdd((unsigned long long *)&x.bs->stale_batch, (unsigned long long)nst);
 }
 
 // -------------------------------------------------------------- temporal ---
@@ -971,13 +980,13 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
 // sorted order and (filter ON) whether the event is evicted stale in this
 // batch -- the random loads the serial per-pixel replay would otherwise wait on.
 __global__ void __launch_bounds__(TPB) k_posinfo(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
   const unsigned jj = x.sidx[i];
   x.spol[i] = x.epol[jj];
   if (!x.spatial) return;
-  const long long E0 = x.st->E, s_start = x.st->s_start;
+  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
   const long long s_end = s_start + x.S[B - 1];
   const long long e = E0 + jj;
   unsigned bidx = FIBAR_NONE;
@@ -997,7 +1006,7 @@ constexpr int LONG_SEG = 512;    // segments longer than this go to k_temporal_l
 constexpr int MAX_LONG = 16384;
 
 __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
   const unsigned key = x.skey[i];
@@ -1005,7 +1014,7 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
   const unsigned c = x.ekey[x.sidx[i]];
   const long long end = x.spatial ? (long long)x.pt[c].end : -1;
   if (i + LONG_SEG < B && x.skey[i + LONG_SEG] == key) {   // long segment: the warp-parallel kernel
-    const unsigned slot = atomicAdd(&x.st->nlong, 1u);
+    const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
     if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
     return;
   }
@@ -1044,7 +1053,7 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
 // the brightness assuming no blur (valid until the pixel's first blur in the
 // batch), and which blur each position builds on.
 __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
-  const long long B = x.st->B;
+  const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
   const unsigned key = x.skey[i];
@@ -1053,7 +1062,7 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
   const PixRec prc = x.pt[c];
   const long long end = prc.end;
   if (end - i > LONG_SEG) {   // long segment (hot pixel): the warp-parallel kernel
-    const unsigned slot = atomicAdd(&x.st->nlong, 1u);
+    const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
     if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
     return;
   }
@@ -1089,6 +1098,10 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
     }
   }
   x.pbar[c] = pb;
+  // last-touch tables for the next batch's links (the blur stage never reads them)
+  const long long elast = x.bs->E0 + x.sidx[end - 1];
+  x.plast[c] = elast;
+  atomicMax(&x.last_tile[key / x.A], elast);
 }
 
 // Long pixel segments (hot pixels: thousands of events per batch) replayed by
@@ -1122,7 +1135,7 @@ __device__ __forceinline__ void replay_piece(const Ctx &x, long long q0, long lo
 }
 
 __global__ void __launch_bounds__(32) k_temporal_long(Ctx x) {
-  const unsigned n = min(x.st->nlong, (unsigned)MAX_LONG);
+  const unsigned n = min(x.bs->nlong, (unsigned)MAX_LONG);
   const int lane = threadIdx.x;
   for (unsigned sidx = blockIdx.x; sidx < n; sidx += gridDim.x) {
     const uint2 ls = x.longseg[sidx];
@@ -1134,7 +1147,7 @@ __global__ void __launch_bounds__(32) k_temporal_long(Ctx x) {
     } else {
       // segment end by search on the sorted keys (OFF path has no pixel table)
       const unsigned key = x.skey[st];
-      long long lo = st + 1, hi = x.st->B;
+      long long lo = st + 1, hi = x.bs->B;
       while (lo < hi) {
         const long long mid = (lo + hi) >> 1;
         if (x.skey[mid] == key) lo = mid + 1; else hi = mid;
@@ -1179,7 +1192,12 @@ __global__ void __launch_bounds__(32) k_temporal_long(Ctx x) {
       }
       continue;
     }
-    if (lane == 0) x.pbar[c] = fpb;
+    if (lane == 0) {
+      x.pbar[c] = fpb;
+      const long long elast = x.bs->E0 + x.sidx[end - 1];
+      x.plast[c] = elast;
+      atomicMax(&x.last_tile[x.skey[st] / x.A], elast);
+    }
     // blur bookkeeping: which blur each position builds on (last stale event
     // before it in the segment, or the pixel's carried blur)
     unsigned last = FIBAR_NONE;
@@ -1215,11 +1233,11 @@ struct BatchScalars {
 
 __device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
   BatchScalars b;
-  b.E0 = x.st->E;
-  b.B = x.st->B;
-  b.s_start = x.st->s_start;
-  b.s_end = b.B > 0 ? b.s_start + x.S[b.B - 1] : b.s_start;
-  b.epoch = x.st->epoch;
+  b.E0 = x.bs->E0;
+  b.B = x.bs->B;
+  b.s_start = x.bs->s_start;
+  b.s_end = b.s_start + x.bs->npop;
+  b.epoch = x.bs->epoch;
   return b;
 }
 
@@ -1342,7 +1360,7 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
     if (want) {
       unsigned base = 0;
       const int leader = __ffs(want) - 1;
-      if (lane == leader) base = atomicAdd(&x.st->ticket, (unsigned)__popc(want));
+      if (lane == leader) base = atomicAdd(&x.bs->ticket, (unsigned)__popc(want));
       base = __shfl_sync(0xffffffffu, base, leader);
       if ((want >> lane) & 1) {
         const unsigned q = base + __popc(want & ((1u << lane) - 1u));
@@ -1421,22 +1439,16 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
       nr.end = 0;
       nr.carried = FIBAR_NONE;
       nr.pad0 = 0;
-      nr.last = e;
-      nr.pad1 = nr.pad2 = 0;
       x.pt[c] = nr;
-      atomicMax(&x.last_tile[x.skey[pos] / x.A], e);
+      (void)e;
     } else {
       const unsigned p = (unsigned)(idx - b.B);
-      const long long k = b.s_start + p;
       const Item it = x.item[p];
-      if (k < b.E0 && it.pix != FIBAR_NONE) {
-        // carried stale entry; if its pixel has no events in this batch, this
-        // is the pixel's only update (segment pixels are finished above)
-        const uint2 rn = x.rnext[(unsigned long long)k & x.Rm];
-        if ((unsigned long long)rn.x > (unsigned long long)(b.E0 + b.B - 1 - k)) {
-          if (x.blur_on) x.l[it.pix] = __uint_as_float((unsigned)x.bv64[p]);
-          x.pt[it.pix].carried = FIBAR_NONE;
-        }
+      if (it.pad & ITEM_CARRIED_ONLY) {
+        // carried stale entry whose pixel has no events in this batch: the
+        // blur is the pixel's only update (segment pixels are finished above)
+        if (x.blur_on) x.l[it.pix] = __uint_as_float((unsigned)x.bv64[p]);
+        x.pt[it.pix].carried = FIBAR_NONE;
       }
     }
   }
@@ -1444,16 +1456,16 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
 
 __global__ void k_batch_end(Ctx x) {
   DevState *s = x.st;
-  if (x.spatial && s->B > 0) {
+  const BatchState *bsp = x.bs;
+  if (x.spatial && bsp->B > 0) {
     s->geo = s->geo_next;
     s->geo_next = 0;
   }
-  s->E += s->B;
+  s->E += bsp->B;
   if (x.spatial) {
-    s->stale += s->stale_batch;
-    if (x.blur_on) s->blur += s->stale_batch;
+    s->stale += bsp->stale_batch;
+    if (x.blur_on) s->blur += bsp->stale_batch;
   }
-  s->epoch += 1;
 }
 
 // ---------------------------------------------------------------- read-out ---
@@ -1755,16 +1767,16 @@ __global__ void k_init_state(DevState *s, long long q0) {
 __global__ void k_fill_ll(long long *p, long long n, long long v) {
   for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) p[i] = v;
 }
-__global__ void k_init_pt(PixRec *p, long long n) {
+__global__ void k_init_pt(PixRec *p0, PixRec *p1, long long *plast, long long n) {
   for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
     PixRec r;
     r.st = 0;
     r.end = 0;
     r.carried = FIBAR_NONE;
     r.pad0 = 0;
-    r.last = -1;
-    r.pad1 = r.pad2 = 0;
-    p[i] = r;
+    p0[i] = r;
+    p1[i] = r;
+    plast[i] = -1;
   }
 }
 
@@ -1807,7 +1819,9 @@ struct fibar_engine {
   bool spatial = true, blur_on = true, use_gain = false;
   DevState *st = nullptr;
   float *pbar = nullptr, *l = nullptr, *gain = nullptr;
-  PixRec *pt = nullptr;
+  PixRec *pt2[2] = {nullptr, nullptr};
+  long long *plast = nullptr;
+  BatchState *bsd = nullptr;   // [2]
   long long *last_tile = nullptr;
   uint2 *ptt = nullptr;
   unsigned *rkey = nullptr;
@@ -1815,17 +1829,18 @@ struct fibar_engine {
   uint16_t *raw_x = nullptr, *raw_y = nullptr;
   int8_t *raw_p = nullptr;
   unsigned *blockcnt = nullptr;
-  unsigned *ekey = nullptr;
+  unsigned *ekey2[2] = {nullptr, nullptr};
   int8_t *epol = nullptr, *spol = nullptr;
   uint2 *longseg = nullptr;
-  unsigned *ka = nullptr, *va = nullptr, *kb = nullptr, *vb = nullptr, *hist = nullptr;
+  unsigned *ka2[2] = {nullptr, nullptr}, *va2[2] = {nullptr, nullptr}, *kb2[2] = {nullptr, nullptr},
+           *vb2[2] = {nullptr, nullptr}, *hist = nullptr;
   uint2 *dp = nullptr;
-  unsigned *S = nullptr, *pos_of = nullptr;
+  unsigned *S = nullptr;
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
   BlurPrep *prep = nullptr;
-  Item *item = nullptr;
-  PosRec *posrec = nullptr;
-  float *t2 = nullptr;
+  Item *item2[2] = {nullptr, nullptr};
+  PosRec *posrec2[2] = {nullptr, nullptr};
+  float *t2_2[2] = {nullptr, nullptr};
   int2 *anc = nullptr, *anc2 = nullptr;
   long long *lc = nullptr, *lu = nullptr;
   ChunkRec *ch = nullptr;
@@ -1849,13 +1864,21 @@ struct fibar_engine {
   const int8_t *zp = nullptr;
   long long zn = 0;
   long long batches = 0;
+  // filter ON: batch k's blur stage (blur_prep, blur, final) runs on bstream
+  // while batch k+1's front end runs on the engine stream; per-batch buffers
+  // are double buffered by batch parity
+  cudaStream_t bstream = nullptr;
+  cudaEvent_t evF[2] = {nullptr, nullptr}, evB[2] = {nullptr, nullptr};
+  int last_b = -1;   // parity of the newest batch with a blur stage in flight
+  bool b_used[2] = {false, false};
   int nsm = 148;
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
+  bool serial = false;   // FIBAR_SERIAL: blur stage on the engine stream (no overlap; for measurement)
   unsigned blur_sleep = 0;
   unsigned long long *dbg_t = nullptr, *dbg_g = nullptr;
 
-  Ctx ctx(const unsigned *skey, const unsigned *sidx, long long n_raw) const {
+  Ctx ctx(const unsigned *skey, const unsigned *sidx, long long n_raw, int par) const {
     Ctx x{};
     x.W = W;
     x.H = H;
@@ -1881,7 +1904,9 @@ struct fibar_engine {
     x.pbar = pbar;
     x.l = l;
     x.gain = gain;
-    x.pt = pt;
+    x.pt = pt2[par];
+    x.plast = plast;
+    x.bs = bsd ? bsd + par : nullptr;
     x.last_tile = last_tile;
     x.ptt = ptt;
     x.rkey = rkey;
@@ -1892,19 +1917,18 @@ struct fibar_engine {
     x.raw_p = raw_p;
     x.n_raw = n_raw;
     x.blockcnt = blockcnt;
-    x.ekey = ekey;
+    x.ekey = ekey2[par];
     x.epol = epol;
     x.spol = spol;
     x.longseg = longseg;
-    x.tkey = ka;
+    x.tkey = ka2[par];
     x.skey = skey;
     x.sidx = sidx;
     x.dp = dp;
     x.S = S;
-    x.item = item;
-    x.posrec = posrec;
-    x.pos_of = pos_of;
-    x.t2 = t2;
+    x.item = item2[par];
+    x.posrec = posrec2[par];
+    x.t2 = t2_2[par];
     x.bv64 = bv64;
     x.mv64 = mv64;
     x.prep = prep;
@@ -1933,13 +1957,22 @@ int dalloc(T **p, long long count) {
   return 0;
 }
 
+// make the engine stream wait for the newest blur stage (before any read)
+int join_blur(fibar_engine *g) {
+  if (g->last_b >= 0) CK(cudaStreamWaitEvent(g->L.stream, g->evB[g->last_b], 0));
+  return 0;
+}
+
 int init_state(fibar_engine *g) {
   cudaStream_t s = g->L.stream;
+  join_blur(g);
+  g->last_b = -1;
+  g->b_used[0] = g->b_used[1] = false;
   FIBAR_LAUNCH(g->L, "init", k_init_state<<<1, 1, 0, s>>>(g->st, g->q0));
   CK(cudaMemsetAsync(g->pbar, 0, sizeof(float) * g->n_pix, s));
   CK(cudaMemsetAsync(g->l, 0, sizeof(float) * g->n_pix, s));
   if (g->spatial) {
-    FIBAR_LAUNCH(g->L, "init", k_init_pt<<<g->nsm * 4, TPB, 0, s>>>(g->pt, g->n_pix));
+    FIBAR_LAUNCH(g->L, "init", k_init_pt<<<g->nsm * 4, TPB, 0, s>>>(g->pt2[0], g->pt2[1], g->plast, g->n_pix));
     FIBAR_LAUNCH(g->L, "init", k_fill_ll<<<g->nsm * 4, TPB, 0, s>>>(g->last_tile, g->n_tiles, -1));
     CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
     CK(cudaMemsetAsync(g->rnext, 0xFF, sizeof(uint2) * g->R, s));
@@ -1956,10 +1989,13 @@ int init_state(fibar_engine *g) {
 int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
                   cudaEvent_t used_ev) {
   if (n_raw <= 0) return 0;
+  const int par = g->spatial ? (int)(g->batches & 1) : 0;
   Launcher &L = g->L;
   cudaStream_t s = L.stream;
+  // this parity's buffers are free once the batch two back finished its blur stage
+  if (g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
-  Ctx x = g->ctx(nullptr, nullptr, n_raw);
+  Ctx x = g->ctx(nullptr, nullptr, n_raw, par);
   x.raw_x = rx0;
   x.raw_y = ry0;
   x.raw_p = rp0;
@@ -1967,13 +2003,14 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
   FIBAR_LAUNCH(L, "compact", k_compact<<<nb_in, TPB, 0, s>>>(x, nb_in));
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
-  const int where = radix_sort_pairs(L, g->ka, g->va, g->kb, g->vb, g->hist, &g->st->B, n_raw, g->key_bits);
-  const unsigned *skey = where ? g->kb : g->ka;
-  const unsigned *sidx = where ? g->vb : g->va;
+  const int where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B,
+                                     n_raw, g->key_bits);
+  const unsigned *skey = where ? g->kb2[par] : g->ka2[par];
+  const unsigned *sidx = where ? g->vb2[par] : g->va2[par];
   {
     const uint16_t *rx = x.raw_x, *ry = x.raw_y;
     const int8_t *rp = x.raw_p;
-    x = g->ctx(skey, sidx, n_raw);
+    x = g->ctx(skey, sidx, n_raw, par);
     x.raw_x = rx;
     x.raw_y = ry;
     x.raw_p = rp;
@@ -1993,20 +2030,32 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     FIBAR_LAUNCH(L, "window_fix", k_window_fix<<<1, 1024, 0, s>>>(x));
     FIBAR_LAUNCH(L, "popj", k_popj<<<(int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
+    // the replay reads the brightness the previous batch's blur stage finishes
+    if (g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
     FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 8, 32, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
+    CK(cudaEventRecord(g->evF[par], s));
+    // blur stage on its own stream: overlaps the next batch's front end
+    cudaStream_t bs = g->serial ? s : g->bstream;
+    CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
+    L.stream = bs;
     if (g->blur_on) {
       const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
-      FIBAR_LAUNCH(L, "blur_prep", k_blur_prep<<<nbp, TPB, 0, s>>>(x));
-      FIBAR_LAUNCH(L, "blur", k_blur<<<g->blur_grid, TPB, 0, s>>>(x));
+      FIBAR_LAUNCH(L, "blur_prep", k_blur_prep<<<nbp, TPB, 0, bs>>>(x));
+      FIBAR_LAUNCH(L, "blur", k_blur<<<g->blur_grid, TPB, 0, bs>>>(x));
     }
-    FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, bs>>>(x));
+    L.stream = s;
+    CK(cudaEventRecord(g->evB[par], bs));
+    g->b_used[par] = true;
+    g->last_b = par;
   } else {
     FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 8, 32, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
   }
-  FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
   CK(cudaGetLastError());
   g->batches++;
   return 0;
@@ -2037,6 +2086,13 @@ int run_batch(fibar_engine *g) {
     if (rc) return rc;
   }
   return launch_host_batch(g);
+}
+
+// run everything pending and order the engine stream after the blur stage
+int sync_point(fibar_engine *g) {
+  int rc = run_batch(g);
+  if (rc) return rc;
+  return join_blur(g);
 }
 
 // read-out (pipeline.py:562-584) of n float32 values at l: exact order
@@ -2141,7 +2197,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   g->spatial = cfg->spatial_enabled != 0;
   g->blur_on = cfg->blur_enabled != 0;
   g->use_gain = cfg->gain != nullptr;
-  g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : (1LL << 21);
+  g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : (1LL << 20);
   if (g->Bcap > (1LL << 28)) g->Bcap = 1LL << 28;
   if (g->Bcap < 1024) g->Bcap = std::max(g->Bcap, 16LL);
   g->key_bits = ceil_log2(g->n_tiles * g->A);
@@ -2150,6 +2206,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   if (const char *v = getenv("FIBAR_CHUNK")) g->chunk = std::max(CHUNK_MIN, atoi(v));
   if (const char *v = getenv("FIBAR_WARM")) g->warm = std::max(0, atoi(v));
   if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
+  if (const char *v = getenv("FIBAR_SERIAL")) g->serial = atoi(v) != 0;
   g->R = 1LL << ceil_log2(n + 1 + g->Bcap);
   int dev = 0;
   cudaGetDevice(&dev);
@@ -2157,8 +2214,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blur, TPB, 0);
-    // fewer polling lanes keep L2 free for the producers (measured best at 4 x 256 per SM)
-    per_sm = std::min(per_sm, 4);
+    // the blur stage overlaps the next batch's front end: one 256-thread block
+    // per SM leaves the rest of each SM to the front end (measured: 1/SM gives
+    // 10.2 ms per 10M config-2 events vs 11.2 at 2/SM and 12.6 serialised)
+    per_sm = std::min(per_sm, g->serial ? 4 : 1);
     if (const char *v = getenv("FIBAR_BLUR_BLOCKS")) per_sm = std::min(per_sm, std::max(1, atoi(v)));
     g->blur_grid = g->nsm * std::max(1, per_sm);
     if (const char *v = getenv("FIBAR_BLUR_SLEEP")) g->blur_sleep = (unsigned)atoi(v);
@@ -2186,14 +2245,22 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   }
   cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking);
   rc |= dalloc(&g->blockcnt, nb_in + 1);
-  rc |= dalloc(&g->ekey, Bc);
   rc |= dalloc(&g->epol, Bc);
   rc |= dalloc(&g->spol, Bc);
   rc |= dalloc(&g->longseg, 16384);
-  rc |= dalloc(&g->ka, Bc);
-  rc |= dalloc(&g->va, Bc);
-  rc |= dalloc(&g->kb, Bc);
-  rc |= dalloc(&g->vb, Bc);
+  rc |= dalloc(&g->bsd, 2);
+  if (!rc) cudaMemset(g->bsd, 0, 2 * sizeof(BatchState));
+  for (int c = 0; c < 2; ++c) {
+    // the filter-off path runs every batch on one stream: one set suffices
+    const bool own = c == 0 || g->spatial;
+    if (own) {
+      rc |= dalloc(&g->ekey2[c], Bc);
+      rc |= dalloc(&g->ka2[c], Bc);
+      rc |= dalloc(&g->va2[c], Bc);
+      rc |= dalloc(&g->kb2[c], Bc);
+      rc |= dalloc(&g->vb2[c], Bc);
+    }
+  }
   rc |= dalloc(&g->hist, 256LL * nb_rs + 256LL * nb_rs / 4096 + 8);
   rc |= dalloc(&g->sel, 1);
   if (!rc) cudaMemset(g->sel, 0, sizeof(SelState));
@@ -2203,20 +2270,34 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     if (!rc) cudaMemcpy(g->gain, cfg->gain, sizeof(float) * n, cudaMemcpyHostToDevice);
   }
   if (g->spatial) {
-    rc |= dalloc(&g->pt, n);
+    for (int c = 0; c < 2; ++c) {
+      rc |= dalloc(&g->pt2[c], n);
+      rc |= dalloc(&g->item2[c], npop_cap);
+      rc |= dalloc(&g->t2_2[c], Bc);
+      rc |= dalloc(&g->posrec2[c], Bc);
+    }
+    rc |= dalloc(&g->plast, n);
+    {
+      // the blur stage is the latency-critical chain: its blocks go first when
+      // SM slots free up, the next batch's front end fills the rest
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      if (const char *v = getenv("FIBAR_BLUR_PRIO")) hi = atoi(v) ? hi : lo;
+      cudaStreamCreateWithPriority(&g->bstream, cudaStreamNonBlocking, hi);
+    }
+    for (int c = 0; c < 2; ++c) {
+      cudaEventCreateWithFlags(&g->evF[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evB[c], cudaEventDisableTiming);
+    }
     rc |= dalloc(&g->last_tile, g->n_tiles);
     rc |= dalloc(&g->ptt, g->n_tiles);
     rc |= dalloc(&g->rkey, g->R);
     rc |= dalloc(&g->rnext, g->R);
     rc |= dalloc(&g->dp, Bc);
     rc |= dalloc(&g->S, Bc);
-    rc |= dalloc(&g->item, npop_cap);
     rc |= dalloc(&g->bv64, npop_cap);
     rc |= dalloc(&g->mv64, Bc);
     rc |= dalloc(&g->prep, npop_cap);
-    rc |= dalloc(&g->t2, Bc);
-    rc |= dalloc(&g->posrec, Bc);
-    rc |= dalloc(&g->pos_of, Bc);
     rc |= dalloc(&g->anc, T * NCAND);
     rc |= dalloc(&g->anc2, T * NFINE);
     rc |= dalloc(&g->lc, T);
@@ -2242,9 +2323,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
-  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->pt, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
-                  g->raw_y, g->raw_p, g->blockcnt, g->ekey, g->epol, g->spol, g->longseg, g->ka, g->va, g->kb, g->vb, g->hist,
-                  g->dp, g->S, g->item, g->bv64, g->mv64, g->prep, g->t2, g->posrec, g->pos_of, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
+  if (g->bstream) cudaStreamSynchronize(g->bstream);
+  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
+                  g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
+                  g->dp, g->S, g->bv64, g->mv64, g->prep, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -2258,8 +2340,15 @@ int fibar_destroy(fibar_engine *g) {
     if (g->hp[c]) cudaFreeHost(g->hp[c]);
     if (g->ev_h2d[c]) cudaEventDestroy(g->ev_h2d[c]);
     if (g->ev_used[c]) cudaEventDestroy(g->ev_used[c]);
+    void *per[] = {g->pt2[c], g->ekey2[c], g->ka2[c], g->va2[c], g->kb2[c], g->vb2[c], g->item2[c], g->posrec2[c],
+                   g->t2_2[c]};
+    for (void *p : per)
+      if (p) cudaFree(p);
+    if (g->evF[c]) cudaEventDestroy(g->evF[c]);
+    if (g->evB[c]) cudaEventDestroy(g->evB[c]);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
+  if (g->bstream) cudaStreamDestroy(g->bstream);
   delete g;
   return 0;
 }
@@ -2332,7 +2421,7 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
 
 int fibar_flush(fibar_engine *g) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  return run_batch(g);
+  return sync_point(g);
 }
 
 int fibar_pending(fibar_engine *g, int64_t *device_events, int64_t *staged_events) {
@@ -2345,7 +2434,7 @@ int fibar_pending(fibar_engine *g, int64_t *device_events, int64_t *staged_event
 int fibar_render(fibar_engine *g, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem, double *bounds,
                  int32_t *degenerate) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  int rc = run_batch(g);
+  int rc = sync_point(g);
   if (rc) return rc;
   return render_core(g->L, g->l, g->n_pix, mode, fixed_bound, out, out_mem, bounds, degenerate, g->sel, g->frame, g->nsm);
 }
@@ -2379,7 +2468,7 @@ int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_
 
 int fibar_read_qs(fibar_engine *g, int64_t qs[10]) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  int rc = run_batch(g);
+  int rc = sync_point(g);
   if (rc) return rc;
   DevState h;
   CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
@@ -2403,7 +2492,7 @@ int fibar_read_qs(fibar_engine *g, int64_t qs[10]) {
 
 int fibar_counters(fibar_engine *g, int64_t *event_count, int64_t *oob_dropped) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  int rc = run_batch(g);
+  int rc = sync_point(g);
   if (rc) return rc;
   DevState h;
   CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
@@ -2416,7 +2505,7 @@ int fibar_counters(fibar_engine *g, int64_t *event_count, int64_t *oob_dropped) 
 int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, uint8_t *tiles, uint16_t *qx,
                      uint16_t *qy) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  int rc = run_batch(g);
+  int rc = sync_point(g);
   if (rc) return rc;
   cudaStream_t s = g->L.stream;
   const long long n = g->n_pix;
@@ -2431,7 +2520,7 @@ int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, 
     }
     CK(cudaMemsetAsync(g->cnt_tmp, 0, sizeof(unsigned) * n, s));
     CK(cudaMemsetAsync(g->tcnt_tmp, 0, sizeof(unsigned) * g->n_tiles, s));
-    Ctx x = g->ctx(nullptr, nullptr, 0);
+    Ctx x = g->ctx(nullptr, nullptr, 0, 0);
     if (g->spatial) {
       FIBAR_LAUNCH(g->L, "state_active", k_active_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp));
       FIBAR_LAUNCH(g->L, "state_tiles", k_tile_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp, g->tcnt_tmp));
@@ -2459,6 +2548,7 @@ int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, 
 
 int fibar_stats(fibar_engine *g, int64_t stats[16]) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  join_blur(g);
   DevState h;
   CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
   CK(cudaStreamSynchronize(g->L.stream));
@@ -2478,6 +2568,7 @@ int fibar_stats(fibar_engine *g, int64_t stats[16]) {
 
 int fibar_profile(fibar_engine *g, int32_t enable) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  join_blur(g);
   CK(cudaStreamSynchronize(g->L.stream));
   g->L.prof = enable != 0;
   g->L.recs.clear();
@@ -2488,6 +2579,7 @@ int fibar_profile(fibar_engine *g, int32_t enable) {
 int fibar_profile_read(fibar_engine *g, int32_t max_entries, char *names, int32_t name_len, double *total_ms,
                        int64_t *launches, int32_t *n_entries) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  join_blur(g);
   CK(cudaStreamSynchronize(g->L.stream));
   std::vector<std::string> keys;
   std::vector<double> ms;
@@ -2522,6 +2614,7 @@ int fibar_profile_read(fibar_engine *g, int32_t max_entries, char *names, int32_
 // debug: item completion / grab timestamps (ns) of the last batch; FIBAR_DEBUG_TIMES must be set
 int fibar_debug_times(fibar_engine *g, uint64_t *done_ns, uint64_t *grab_ns, int64_t n) {
   if (!g || !g->dbg_t) return fail(FIBAR_E_CONFIG, "debug timestamps not enabled");
+  join_blur(g);
   CK(cudaStreamSynchronize(g->L.stream));
   CK(cudaMemcpy(done_ns, g->dbg_t, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
   CK(cudaMemcpy(grab_ns, g->dbg_g, sizeof(uint64_t) * n, cudaMemcpyDeviceToHost));
@@ -2531,6 +2624,7 @@ int fibar_debug_times(fibar_engine *g, uint64_t *done_ns, uint64_t *grab_ns, int
 // debug: copy the blur prep records (80 B each) of the last batch
 int fibar_debug_prep(fibar_engine *g, void *out, int64_t n) {
   if (!g || !g->prep) return fail(FIBAR_E_CONFIG, "no prep");
+  join_blur(g);
   CK(cudaStreamSynchronize(g->L.stream));
   CK(cudaMemcpy(out, g->prep, sizeof(BlurPrep) * n, cudaMemcpyDeviceToHost));
   return 0;
@@ -2566,7 +2660,7 @@ int fibar_decode_evf1(const uint8_t *records, int64_t nrec, int32_t width, int32
 
 int fibar_copy_brightness(fibar_engine *g, float *dst, int32_t dst_mem) {
   if (!g || !dst) return fail(FIBAR_E_CONFIG, "null argument");
-  int rc = run_batch(g);
+  int rc = sync_point(g);
   if (rc) return rc;
   CK(cudaMemcpyAsync(dst, g->l, sizeof(float) * g->n_pix,
                      dst_mem == FIBAR_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, g->L.stream));
@@ -2576,6 +2670,8 @@ int fibar_copy_brightness(fibar_engine *g, float *dst, int32_t dst_mem) {
 
 int fibar_brightness_ptr(fibar_engine *g, float **out) {
   if (!g || !out) return fail(FIBAR_E_CONFIG, "null argument");
+  int rc = sync_point(g);
+  if (rc) return rc;
   *out = g->l;
   return 0;
 }

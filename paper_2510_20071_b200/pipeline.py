@@ -24,6 +24,7 @@ validates arguments, moves packets, and maps status codes to exceptions.
 
 from __future__ import annotations
 
+import collections
 import ctypes as C
 import hashlib
 import logging
@@ -168,8 +169,16 @@ class ReconstructionEngine:
         self._h = handle
         self._stream_ptr = stream
         self.last_t: int | None = None
-        self._held = []          # device packets the native side still reads in place
+        self._held = collections.deque()   # device packets the native side still reads in place
         self._held_n = 0
+        st = np.zeros(16, dtype=np.int64)
+        _native.check(self._lib.fibar_stats(self._h, st.ctypes.data), "fibar_stats")
+        self._bcap = int(st[7])
+        self._release_at = self._bcap      # check the native pending count once this many are held
+        self._dev_index = self.device.index if self.device.index is not None else torch.cuda.current_device()
+        self._raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        self._xy_ok = (torch.int16, getattr(torch, "uint16", torch.int16))
+        self._i8 = torch.int8
 
     # -- lifecycle -----------------------------------------------------------
     def close(self) -> None:
@@ -184,8 +193,10 @@ class ReconstructionEngine:
             pass
 
     def _sync_stream(self) -> None:
-        torch = _torch()
-        s = torch.cuda.current_stream(self.device).cuda_stream
+        if self._raw_stream is not None:
+            s = self._raw_stream(self._dev_index)
+        else:
+            s = _torch().cuda.current_stream(self.device).cuda_stream
         if s != self._stream_ptr:
             self._lib.fibar_set_stream(self._h, C.c_void_p(s))
             self._stream_ptr = s
@@ -197,6 +208,7 @@ class ReconstructionEngine:
         self.last_t = None
         self._held.clear()
         self._held_n = 0
+        self._release_at = self._bcap
 
     def flush(self) -> None:
         """Run coalesced packets now (asynchronous on the current stream)."""
@@ -407,38 +419,34 @@ class ReconstructionEngine:
             self.last_t = int(ts[keep[-1]])
 
     def _process_device(self, block: DeviceEventArray) -> None:
-        torch = _torch()
-        n = len(block)
+        x, y, p = block.x, block.y, block.p
+        n = x.shape[0]
         if not n:
             return
-        x = block.x.contiguous()
-        y = block.y.contiguous()
-        p = block.p.contiguous()
-        if x.dtype != torch.int16 and x.dtype != getattr(torch, "uint16", None):
-            x = x.to(torch.int16)
-        if y.dtype != torch.int16 and y.dtype != getattr(torch, "uint16", None):
-            y = y.to(torch.int16)
-        if p.dtype != torch.int8:
-            p = p.to(torch.int8)
+        xy_ok = self._xy_ok
+        if not (x.dtype in xy_ok and y.dtype in xy_ok and p.dtype is self._i8 and x.is_contiguous()
+                and y.is_contiguous() and p.is_contiguous()):
+            torch = _torch()
+            x = x.contiguous()
+            y = y.contiguous()
+            p = p.contiguous()
+            if x.dtype not in xy_ok:
+                x = x.to(torch.int16)
+            if y.dtype not in xy_ok:
+                y = y.to(torch.int16)
+            if p.dtype != torch.int8:
+                p = p.to(torch.int8)
         if self.strict:
-            W, H = self.geometry.width, self.geometry.height
-            xi, yi = x.to(torch.int32) & 0xFFFF, y.to(torch.int32) & 0xFFFF
-            oob = (xi >= W) | (yi >= H)
-            if bool(oob.any()):
-                i = int(torch.nonzero(oob)[0, 0])
-                raise DataError(f"event {self.event_count + i} at ({int(xi[i])},{int(yi[i])}) outside {W}x{H}")
-            if block.t is not None:
-                ts = block.t
-                if self.last_t is not None and int(ts[0]) < self.last_t:
-                    raise OrderError("event timestamps regress across blocks")
-                if bool((ts[1:] < ts[:-1]).any()):
-                    raise OrderError("event timestamps regress within a block")
+            self._check_device_packet(block, x, y)
         self._sync_stream()
-        _native.check(self._lib.fibar_process(self._h, x.data_ptr(), y.data_ptr(), p.data_ptr(), n,
-                                              _native.FIBAR_MEM_DEVICE), "fibar_process")
+        rc = self._lib.fibar_process(self._h, x.data_ptr(), y.data_ptr(), p.data_ptr(), n, _native.FIBAR_MEM_DEVICE)
+        if rc:
+            _native.check(rc, "fibar_process")
         self._held.append((n, x, y, p))
         self._held_n += n
-        self._release_held()
+        if self._held_n >= self._release_at:
+            self._release_held()
+            self._release_at = self._held_n + self._bcap
         if block.t is not None:
             if self.strict:
                 self.last_t = int(block.t[-1])
@@ -448,6 +456,21 @@ class ReconstructionEngine:
                 self._pending_last = (x, y, block.t)
                 self.last_t = self._resolve_last_t()
 
+    def _check_device_packet(self, block, x, y) -> None:
+        torch = _torch()
+        W, H = self.geometry.width, self.geometry.height
+        xi, yi = x.to(torch.int32) & 0xFFFF, y.to(torch.int32) & 0xFFFF
+        oob = (xi >= W) | (yi >= H)
+        if bool(oob.any()):
+            i = int(torch.nonzero(oob)[0, 0])
+            raise DataError(f"event {self.event_count + i} at ({int(xi[i])},{int(yi[i])}) outside {W}x{H}")
+        if block.t is not None:
+            ts = block.t
+            if self.last_t is not None and int(ts[0]) < self.last_t:
+                raise OrderError("event timestamps regress across blocks")
+            if bool((ts[1:] < ts[:-1]).any()):
+                raise OrderError("event timestamps regress within a block")
+
     def _release_held(self) -> None:
         """Drop references to device packets the native side no longer reads in place."""
         if not self._held:
@@ -455,7 +478,7 @@ class ReconstructionEngine:
         pend = C.c_int64(0)
         _native.check(self._lib.fibar_pending(self._h, C.byref(pend), None), "fibar_pending")
         while self._held and self._held_n - self._held[0][0] >= pend.value:
-            self._held_n -= self._held.pop(0)[0]
+            self._held_n -= self._held.popleft()[0]
         if pend.value == 0:
             self._held.clear()
             self._held_n = 0

@@ -9,7 +9,7 @@ from paper_2510_20071_b200.pipeline import ReconstructionEngine
 geom = SensorGeometry(640, 480)
 ev = workloads.moving_texture(640, 480, 4_000_000)
 params = compute_params(40.0, Fraction(1, 2), geom)
-eng = ReconstructionEngine(geom, params, batch_capacity=1 << 21)
+eng = ReconstructionEngine(geom, params, batch_capacity=1 << 20)
 xh = torch.from_numpy(ev.x.view(np.int16)).pin_memory().numpy().view(np.uint16)
 yh = torch.from_numpy(ev.y.view(np.int16)).pin_memory().numpy().view(np.uint16)
 ph = torch.from_numpy(ev.p).pin_memory().numpy()
