@@ -117,11 +117,15 @@ int fibar_counters(fibar_engine *eng, int64_t *event_count, int64_t *oob_dropped
 int fibar_read_state(fibar_engine *eng, float *p_bar, float *l, uint16_t *active, uint8_t *tiles,
                      uint16_t *qx, uint16_t *qy);
 
-/* Diagnostics: stats[0] = device kernel launches so far, [1] = device batches,
- * [2] = speculative window chunks, [3] = chunks re-run by the verifier,
- * [4] = pops (window evictions) processed, [5] = counter-saturation flag,
- * [6] = in-bounds events, [7] = batch capacity, [8] = evictions replayed in
- * speculative warm-ups, [9] = warp-cooperative eviction-count steps. */
+/* Diagnostics (runs pending packets first): stats[0] = device kernel launches
+ * so far, [1] = device batches, [2] = speculative window chunks, [3] = chunks
+ * re-run by the verifier, [4] = pops (window evictions) processed, [5] =
+ * counter-saturation flag (> 0 once the reference's u16
+ * active_count -- or u8 tile_count when a tile has > 255 pixels -- could have
+ * hit its cap; conservative, never missed), [6] = in-bounds events, [7] =
+ * batch capacity, [8] = evictions replayed in speculative warm-ups, [9] =
+ * warp-cooperative eviction-count steps, [10] = window verifier rounds, [11] =
+ * FIBAR_DEBUG_WINDOW anchor recount mismatches. */
 int fibar_stats(fibar_engine *eng, int64_t stats[16]);
 /* Per-kernel CUDA-event timing (bench.py's roofline leg; adds events around
  * every launch, so never enable it in a timed region).  fibar_profile

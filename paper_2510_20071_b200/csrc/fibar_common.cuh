@@ -99,8 +99,9 @@ struct DevState {
   long long warm_pops;   // evictions replayed during speculative warm-ups (stats)
   long long coop_iters;  // warp-cooperative eviction-count steps (stats)
   long long fix_rounds;  // verifier rounds (stats)
-  int geo, geo_next;
-  unsigned nlong, nlong_pad;   // long pixel segments of the batch     // window candidates: geometric set needed (this / next batch)
+  int geo, geo_next;     // window candidates: geometric set needed (this / next batch)
+  unsigned nlong, nlong_pad;   // long pixel segments of the batch
+  long long dbg_bad;           // FIBAR_DEBUG_WINDOW: anchor counts that disagreed with a serial recount
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {

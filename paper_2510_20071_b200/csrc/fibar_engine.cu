@@ -74,6 +74,7 @@ struct Ctx {
   DevState *st;
   BatchState *bs;     // this batch's scalars (parity buffer)
   long long *plast;   // per pixel: last event index before the batch
+  unsigned *wcnt;     // per pixel: exact in-window event count (saturation check)
   float *pbar, *l;
   const float *gain;
   PixRec *pt;
@@ -290,6 +291,17 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
   x.dp[jj] = make_uint2(dist32(j, prev_p), dist32(j, prev_t));
   x.rnext[(unsigned long long)j & x.Rm] =
       make_uint2(next_p < 0 ? FIBAR_INF32 : (unsigned)(next_p - j), next_t < 0 ? FIBAR_INF32 : (unsigned)(next_t - j));
+  if (first_pix) {
+    // the reference's active_count saturates at 65535, after which
+    // its count-based staleness departs from this exact restatement.  wcnt is
+    // the pixel's exact in-window event count at batch start; the count seen
+    // by its t-th event this batch is at most wcnt + t, so a batch can only
+    // reach the cap if wcnt + seglen > 65535 -- flag that (never misses).
+    const unsigned seglen = x.pt[c].end - (unsigned)i;
+    const unsigned wc = x.wcnt[c];
+    if ((unsigned long long)wc + seglen > 65535ull) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);
+    x.wcnt[c] = wc + seglen;
+  }
   if (first_pix && pre_last >= lo_ok && pre_last >= 0) {
     long long d = j - pre_last;
     x.rnext[(unsigned long long)pre_last & x.Rm].x = d >= FIBAR_INF32 ? FIBAR_INF32 : (unsigned)d;
@@ -702,7 +714,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
           bn += (unsigned long long)rr.x > (unsigned long long)(a - 1 - k);
           bt += (unsigned long long)rr.y > (unsigned long long)(a - 1 - k);
         }
-        if (bn != w.npix || bt != w.ntiles) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);
+        if (bn != w.npix || bt != w.ntiles) atomicAdd((unsigned long long *)&x.st->dbg_bad, 1ull);
       }
       w.evctr = (s.evctr + (a - E0)) % x.every;
     }
@@ -952,13 +964,14 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
     const long long k = s_start + p;
     const long long j = E0 + lo;
     const bool stale = (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);
+    const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
+    atomicSub(&x.wcnt[c], 1u);   // the entry leaves the window (H7 bookkeeping)
     Item it;
     it.jrel = lo;
     it.pix = FIBAR_NONE;
     it.runpos = FIBAR_NONE;
     it.pad = 0;
     if (stale) {
-      const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
       it.pix = c;
       if (k < E0) {
         x.pt[c].carried = p;
@@ -1821,6 +1834,7 @@ struct fibar_engine {
   float *pbar = nullptr, *l = nullptr, *gain = nullptr;
   PixRec *pt2[2] = {nullptr, nullptr};
   long long *plast = nullptr;
+  unsigned *wcnt = nullptr;
   BatchState *bsd = nullptr;   // [2]
   long long *last_tile = nullptr;
   uint2 *ptt = nullptr;
@@ -1906,6 +1920,7 @@ struct fibar_engine {
     x.gain = gain;
     x.pt = pt2[par];
     x.plast = plast;
+    x.wcnt = wcnt;
     x.bs = bsd ? bsd + par : nullptr;
     x.last_tile = last_tile;
     x.ptt = ptt;
@@ -1975,6 +1990,7 @@ int init_state(fibar_engine *g) {
     FIBAR_LAUNCH(g->L, "init", k_init_pt<<<g->nsm * 4, TPB, 0, s>>>(g->pt2[0], g->pt2[1], g->plast, g->n_pix));
     FIBAR_LAUNCH(g->L, "init", k_fill_ll<<<g->nsm * 4, TPB, 0, s>>>(g->last_tile, g->n_tiles, -1));
     CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
+    CK(cudaMemsetAsync(g->wcnt, 0, sizeof(unsigned) * g->n_pix, s));
     CK(cudaMemsetAsync(g->rnext, 0xFF, sizeof(uint2) * g->R, s));
     CK(cudaMemsetAsync(g->bv64, 0, sizeof(unsigned long long) * (g->Bcap + g->n_pix + 2), s));
     CK(cudaMemsetAsync(g->mv64, 0, sizeof(unsigned long long) * g->Bcap, s));
@@ -2277,6 +2293,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       rc |= dalloc(&g->posrec2[c], Bc);
     }
     rc |= dalloc(&g->plast, n);
+    rc |= dalloc(&g->wcnt, n);
     {
       // the blur stage is the latency-critical chain: its blocks go first when
       // SM slots free up, the next batch's front end fills the rest
@@ -2324,7 +2341,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
   if (g->bstream) cudaStreamSynchronize(g->bstream);
-  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
+  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
                   g->dp, g->S, g->bv64, g->mv64, g->prep, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g};
@@ -2548,7 +2565,8 @@ int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, 
 
 int fibar_stats(fibar_engine *g, int64_t stats[16]) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  join_blur(g);
+  int rc = sync_point(g);
+  if (rc) return rc;
   DevState h;
   CK(cudaMemcpyAsync(&h, g->st, sizeof(DevState), cudaMemcpyDeviceToHost, g->L.stream));
   CK(cudaStreamSynchronize(g->L.stream));
@@ -2557,12 +2575,14 @@ int fibar_stats(fibar_engine *g, int64_t stats[16]) {
   stats[2] = h.chunks;
   stats[3] = h.mismatch;
   stats[4] = h.pops;
-  stats[5] = h.saturated;
+  // tile_count (u8) can only saturate when a tile has more than 255 pixels
+  stats[5] = h.saturated + ((g->spatial && g->A > 255 && h.E > 0) ? 1 : 0);
   stats[6] = h.E;
   stats[7] = g->Bcap;
   stats[8] = h.warm_pops;
   stats[9] = h.coop_iters;
   stats[10] = h.fix_rounds;
+  stats[11] = h.dbg_bad;
   return 0;
 }
 

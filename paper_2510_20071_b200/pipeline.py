@@ -179,6 +179,7 @@ class ReconstructionEngine:
         self._raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
         self._xy_ok = (torch.int16, getattr(torch, "uint16", torch.int16))
         self._i8 = torch.int8
+        self._sat_warned = False
 
     # -- lifecycle -----------------------------------------------------------
     def close(self) -> None:
@@ -245,8 +246,22 @@ class ReconstructionEngine:
         self._sync_stream()
         _native.check(self._lib.fibar_stats(self._h, st.ctypes.data), "fibar_stats")
         keys = ("launches", "batches", "window_chunks", "window_reruns", "pops", "saturated", "events",
-                "batch_capacity", "warm_pops", "coop_iters", "fix_rounds")
+                "batch_capacity", "warm_pops", "coop_iters", "fix_rounds", "debug_window_bad")
         return dict(zip(keys, (int(v) for v in st)))
+
+    @property
+    def saturation_detected(self) -> bool:
+        """True once the reference's u16 active_count (or u8 tile_count) could have
+        saturated (_kernels.py:146-149).  From then on the reference's
+        count-based staleness may differ from this engine's exact one; the flag is
+        conservative (never missed, may fire up to one device batch early)."""
+        return self.stats()["saturated"] > 0
+
+    def _warn_saturation(self) -> None:
+        if not self._sat_warned and self.params.spatial_enabled and self.saturation_detected:
+            self._sat_warned = True
+            logger.warning("active_count may have reached the reference's 65535 cap: results can differ "
+                           "from the reference from here on (SURVEY H7)")
 
     def profile(self, enable: bool) -> None:
         """Per-kernel CUDA-event timing on/off (synchronises; never inside a timed region)."""
@@ -507,6 +522,7 @@ class ReconstructionEngine:
         _native.check(self._lib.fibar_render(self._h, mode, float(fixed_bound), out.ctypes.data, _native.FIBAR_MEM_HOST,
                                              bounds.ctypes.data, C.byref(deg)), "fibar_render")
         self._release_held()
+        self._warn_saturation()
         return Frame(out.reshape(g.height, g.width), readout_time, scale_mode, (float(bounds[0]), float(bounds[1])),
                      bool(deg.value))
 

@@ -16,4 +16,4 @@ for a in range(0, len(ev), 1 << 20):
     eng.process_array(DeviceEventArray(xd[a:a + (1 << 20)], yd[a:a + (1 << 20)], pd[a:a + (1 << 20)]))
     eng.flush()
     s1 = eng.stats()
-    print("batch", a, {k: s1[k] - s0[k] for k in ("saturated", "window_reruns", "fix_rounds", "warm_pops", "window_chunks")})
+    print("batch", a, {k: s1[k] - s0[k] for k in ("debug_window_bad", "window_reruns", "fix_rounds", "warm_pops", "window_chunks")})

@@ -123,3 +123,46 @@ def test_oracle_streams(kind, w, h, n, packet, spatial):
     fr = eng.render("robust")
     px, bounds, deg = ref.render("robust")
     assert np.array_equal(fr.pixels, px) and fr.bounds == bounds and fr.degenerate == deg
+
+
+@pytest.mark.parametrize("n,flag", [(60_000, False), (70_000, True)])
+def test_saturation_flag(n, flag):
+    """one pixel with more than 65535 events in the window reaches the
+    reference's u16 cap.  The engine flags it (and, while no entry of the pixel
+    has been popped yet, still matches the saturating oracle)."""
+    from paper_2510_20071_b200.core import EventArray, SensorGeometry, compute_params
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    from oracle import oracle as orc
+    geom = SensorGeometry(300, 300)
+    params = compute_params(40.0, Fraction(1, 2), geom)
+    x = np.full(n, 5, np.uint16)
+    y = np.full(n, 7, np.uint16)
+    p = np.where(np.arange(n) % 3 == 0, -1, 1).astype(np.int8)
+    t = np.arange(n, dtype=np.uint64)
+    eng = ReconstructionEngine(geom, params, batch_capacity=1 << 14)
+    ref = orc.OracleEngine(300, 300, params)
+    for a in range(0, n, 20_000):
+        b = min(n, a + 20_000)
+        eng.process_array(EventArray(t[a:b], x[a:b], y[a:b], p[a:b]))
+        ref.process_array(t[a:b], x[a:b], y[a:b], p[a:b])
+    assert eng.saturation_detected == flag
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, f"single pixel n={n}")
+
+
+def test_saturation_flag_after_pops():
+    """Past the cap with pops the reference's counts diverge: the flag must be up."""
+    from paper_2510_20071_b200.core import EventArray, SensorGeometry, compute_params
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    geom = SensorGeometry(300, 300)
+    params = compute_params(40.0, Fraction(1, 2), geom)
+    n = 200_000
+    rng = np.random.default_rng(3)
+    hot = rng.random(n) < 0.9
+    x = np.where(hot, 5, rng.integers(0, 300, n)).astype(np.uint16)
+    y = np.where(hot, 7, rng.integers(0, 300, n)).astype(np.uint16)
+    p = rng.choice(np.array([-1, 1], np.int8), n)
+    eng = ReconstructionEngine(geom, params)
+    eng.process_array(EventArray(np.arange(n, dtype=np.uint64), x, y, p))
+    assert eng.saturation_detected
