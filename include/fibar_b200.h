@@ -159,6 +159,29 @@ int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_
 int fibar_decode_evf1(const uint8_t *records, int64_t nrec, int32_t width, int32_t height, uint64_t t_base,
                       uint16_t *x, uint16_t *y, int8_t *p, uint64_t *t, int64_t *first_bad, void *stream);
 
+/* Per-pixel ON / OFF event counts, calib.count_events (calib.py:26-45): for
+ * each event flat = y*width + x (as the reference forms it); counts are ADDED
+ * into the device int64 arrays n_on / n_off (n_pix each; zero them first).
+ * *first_bad receives the index of the first event with flat >= n_pix, or -1
+ * (the caller raises DataError like the reference).  x, y, p are device
+ * pointers.  Synchronises the stream. */
+int fibar_count_events(const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n, int32_t width, int64_t n_pix,
+                       int64_t *n_on, int64_t *n_off, int64_t *first_bad, void *stream);
+
+/* Single-pixel trajectories, temporal.stream_pixel -> _kernels.temporal_trace
+ * (_kernels.py:219-233): ntraces independent polarity sequences of n int8
+ * values each (trace i at p + i*n), dtype 0 = float32 / 1 = float64 state;
+ * coef = {alpha, 1-alpha, beta, (1+beta)/2} as float64, cast to dtype;
+ * state = 2 values per trace (p_bar, l) read and updated; p_bar / delta / l
+ * receive n values per trace.  All pointers are device pointers; asynchronous. */
+int fibar_pixel_trace(const int8_t *p, int64_t n, int32_t ntraces, int32_t dtype, const double coef[4], void *state,
+                      void *p_bar, void *delta, void *l, void *stream);
+/* The combined recurrence, temporal.stream_pixel_iir -> _kernels.iir_trace
+ * (_kernels.py:236-249): coef = {alpha+beta, alpha*beta, alpha*(1+beta)/2};
+ * state = 3 values per trace (l_prev, l_prev2, p_prev). */
+int fibar_pixel_trace_iir(const int8_t *p, int64_t n, int32_t ntraces, int32_t dtype, const double coef[3],
+                          void *state, void *l, void *stream);
+
 const char *fibar_last_error(void);
 
 #ifdef __cplusplus

@@ -20,6 +20,9 @@
  *   oracle_render          <- pipeline.py:562-584 (render) + numpy 2.3.5
  *                             percentile 'linear' (virtual index (n-1)q, _lerp)
  *   oracle_decode_evf1     <- event_io.py:353-369 (_decode_block)
+ *   oracle_trace_f32/_f64  <- _kernels.py:219-233 (_temporal_trace)
+ *   oracle_trace_iir_f32/_f64 <- _kernels.py:236-249 (_iir_trace)
+ *   oracle_count_events    <- calib.py:26-45 (count_events, flat = y*W + x)
  */
 #include <math.h>
 #include <stdint.h>
@@ -297,6 +300,68 @@ int64_t oracle_decode_evf1(const uint8_t *raw, int64_t nrec, int64_t width,
     x[r] = xx;
     y[r] = yy;
     p[r] = (xp >> 15) ? 1 : -1;
+  }
+  return -1;
+}
+
+/* Single-pixel two-stage trajectory (_kernels.py:219-233), float32 and float64
+ * state; state[0] = p_bar, state[1] = l, updated in place. */
+#define ORACLE_TRACE(NAME, T)                                                    \
+  void NAME(const int8_t *ps, int64_t n, T a, T oma, T b, T h, T *state,        \
+            T *out_pbar, T *out_delta, T *out_l) {                              \
+    T pb = state[0], lv = state[1];                                             \
+    for (int64_t j = 0; j < n; ++j) {                                           \
+      T p = (T)ps[j];                                                           \
+      T t1 = a * pb;                                                            \
+      T t2 = oma * p;                                                           \
+      pb = t1 + t2;                                                             \
+      T d = p - pb;                                                             \
+      T t3 = b * lv;                                                            \
+      T t4 = h * d;                                                             \
+      lv = t3 + t4;                                                             \
+      out_pbar[j] = pb;                                                         \
+      out_delta[j] = d;                                                         \
+      out_l[j] = lv;                                                            \
+    }                                                                           \
+    state[0] = pb;                                                              \
+    state[1] = lv;                                                              \
+  }
+ORACLE_TRACE(oracle_trace_f32, float)
+ORACLE_TRACE(oracle_trace_f64, double)
+
+/* Combined recurrence (_kernels.py:236-249): state = (l_prev, l_prev2, p_prev). */
+#define ORACLE_TRACE_IIR(NAME, T)                                                \
+  void NAME(const int8_t *ps, int64_t n, T apb, T atb, T h, T *state, T *out_l) { \
+    T l1 = state[0], l2 = state[1], pp = state[2];                              \
+    for (int64_t j = 0; j < n; ++j) {                                           \
+      T p = (T)ps[j];                                                           \
+      T t1 = apb * l1;                                                          \
+      T t2 = atb * l2;                                                          \
+      T t3 = t1 - t2;                                                           \
+      T t4 = p - pp;                                                            \
+      T t5 = h * t4;                                                            \
+      T lv = t3 + t5;                                                           \
+      out_l[j] = lv;                                                            \
+      l2 = l1;                                                                  \
+      l1 = lv;                                                                  \
+      pp = p;                                                                   \
+    }                                                                           \
+    state[0] = l1;                                                              \
+    state[1] = l2;                                                              \
+    state[2] = pp;                                                              \
+  }
+ORACLE_TRACE_IIR(oracle_trace_iir_f32, float)
+ORACLE_TRACE_IIR(oracle_trace_iir_f64, double)
+
+/* Per-pixel ON/OFF counts (calib.py:26-45); returns the first event index
+ * whose flat index y*W + x is >= n_pix (counts untouched then), else -1. */
+int64_t oracle_count_events(const uint16_t *xs, const uint16_t *ys, const int8_t *ps, int64_t n, int64_t width,
+                            int64_t n_pix, int64_t *n_on, int64_t *n_off) {
+  for (int64_t e = 0; e < n; ++e)
+    if ((int64_t)ys[e] * width + xs[e] >= n_pix) return e;
+  for (int64_t e = 0; e < n; ++e) {
+    const int64_t f = (int64_t)ys[e] * width + xs[e];
+    if (ps[e] > 0) ++n_on[f]; else ++n_off[f];
   }
   return -1;
 }

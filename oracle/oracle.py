@@ -57,6 +57,12 @@ def lib():
     L.oracle_render.argtypes = [P, i64, i32, f64, P, P, P]
     L.oracle_render.restype = i32
     L.oracle_decode_evf1.argtypes = [P, i64, i64, i64, C.c_uint64, P, P, P, P]
+    L.oracle_trace_f32.argtypes = [P, i64, f32, f32, f32, f32, P, P, P, P]
+    L.oracle_trace_f64.argtypes = [P, i64, f64, f64, f64, f64, P, P, P, P]
+    L.oracle_trace_iir_f32.argtypes = [P, i64, f32, f32, f32, P, P]
+    L.oracle_trace_iir_f64.argtypes = [P, i64, f64, f64, f64, P, P]
+    L.oracle_count_events.argtypes = [P, P, P, i64, i64, i64, P, P]
+    L.oracle_count_events.restype = i64
     L.oracle_decode_evf1.restype = i64
     _lib = L
     return L
@@ -91,6 +97,41 @@ def decode_evf1(raw: bytes, width: int, height: int, t_base: int = 0):
     if bad >= 0:
         raise IndexError(int(bad))
     return t, x, y, p
+
+
+def trace(ps, coef, dtype=np.float32):
+    """Two-stage single-pixel trajectory (_kernels.py:219-233); coef = (a, 1-a, b, (1+b)/2) as float64."""
+    ps = np.ascontiguousarray(ps, np.int8)
+    dt = np.dtype(dtype)
+    out = [np.empty(ps.size, dt) for _ in range(3)]
+    st = np.zeros(2, dt)
+    fn = lib().oracle_trace_f32 if dt == np.float32 else lib().oracle_trace_f64
+    fn(_p(ps), ps.size, *[float(dt.type(c)) for c in coef], _p(st), _p(out[0]), _p(out[1]), _p(out[2]))
+    return tuple(out)
+
+
+def trace_iir(ps, coef, dtype=np.float32):
+    """Combined recurrence (_kernels.py:236-249); coef = (a+b, a*b, a(1+b)/2) as float64."""
+    ps = np.ascontiguousarray(ps, np.int8)
+    dt = np.dtype(dtype)
+    out = np.empty(ps.size, dt)
+    st = np.zeros(3, dt)
+    fn = lib().oracle_trace_iir_f32 if dt == np.float32 else lib().oracle_trace_iir_f64
+    fn(_p(ps), ps.size, *[float(dt.type(c)) for c in coef], _p(st), _p(out))
+    return out
+
+
+def count_events(x, y, p, width: int, n_pix: int):
+    """(n_on, n_off) flat int64 counts (calib.py:26-45) or raises IndexError(first bad event)."""
+    x = np.ascontiguousarray(x, np.uint16)
+    y = np.ascontiguousarray(y, np.uint16)
+    p = np.ascontiguousarray(p, np.int8)
+    on = np.zeros(n_pix, np.int64)
+    off = np.zeros(n_pix, np.int64)
+    bad = lib().oracle_count_events(_p(x), _p(y), _p(p), x.size, width, n_pix, _p(on), _p(off))
+    if bad >= 0:
+        raise IndexError(int(bad))
+    return on, off
 
 
 class OracleEngine:

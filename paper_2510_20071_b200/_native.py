@@ -25,6 +25,7 @@ EXPORTED = (
     "fibar_create", "fibar_destroy", "fibar_set_stream", "fibar_reset", "fibar_process", "fibar_flush",
     "fibar_render", "fibar_read_qs", "fibar_counters", "fibar_read_state", "fibar_stats",
     "fibar_brightness_ptr", "fibar_last_error", "fibar_profile", "fibar_profile_read", "fibar_pending", "fibar_debug_times", "fibar_debug_prep", "fibar_render_grid", "fibar_copy_brightness", "fibar_decode_evf1",
+    "fibar_count_events", "fibar_pixel_trace", "fibar_pixel_trace_iir",
 )
 
 
@@ -87,6 +88,9 @@ def load(path: str | None = None):
         "fibar_copy_brightness": ([P, P, i32], C.c_int),
         "fibar_decode_evf1": ([P, i64, i32, i32, C.c_uint64, P, P, P, P, P, P], C.c_int),
         "fibar_profile_read": ([P, i32, P, i32, P, P, P], C.c_int),
+        "fibar_count_events": ([P, P, P, i64, i32, i64, P, P, P, P], C.c_int),
+        "fibar_pixel_trace": ([P, i64, i32, i32, P, P, P, P, P, P], C.c_int),
+        "fibar_pixel_trace_iir": ([P, i64, i32, i32, P, P, P, P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

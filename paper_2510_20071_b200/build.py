@@ -15,7 +15,7 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("fibar_engine.cu", "fibar_sort.cu")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("fibar_engine.cu", "fibar_sort.cu", "fibar_tools.cu")]
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("fibar_common.cuh", "fibar_internal.h")] + [
     os.path.join(HERE, "..", "include", "fibar_b200.h")]
 OUT = os.path.join(HERE, "_lib", "libfibar_b200.so")

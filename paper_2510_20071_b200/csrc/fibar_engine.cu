@@ -34,6 +34,20 @@
 
 using namespace fibar;
 
+namespace fibar {
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+  g_err = std::string(where) + ": " + cudaGetErrorString(e);
+  return FIBAR_E_CUDA;
+}
+}  // namespace fibar
+
 namespace {
 
 constexpr int NFINE = 10;     // fine candidate windows around the interpolated fixed point
@@ -1792,24 +1806,6 @@ __global__ void k_init_pt(PixRec *p0, PixRec *p1, long long *plast, long long n)
     plast[i] = -1;
   }
 }
-
-thread_local std::string g_err;
-
-int fail(int code, const std::string &msg) {
-  g_err = msg;
-  return code;
-}
-
-int cuda_fail(cudaError_t e, const char *where) {
-  g_err = std::string(where) + ": " + cudaGetErrorString(e);
-  return FIBAR_E_CUDA;
-}
-
-#define CK(call)                                          \
-  do {                                                    \
-    cudaError_t _e = (call);                              \
-    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
-  } while (0)
 
 int ceil_log2(long long v) {
   int b = 0;

@@ -1,9 +1,21 @@
 // fibar_internal.h -- host-side declarations shared by the .cu files.
 #pragma once
 #include <cuda_runtime.h>
+#include <string>
 #include <vector>
 
 namespace fibar {
+
+// error reporting behind fibar_last_error (thread-local message + FIBAR_E_* code)
+extern thread_local std::string g_err;
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *where);
+
+#define CK(call)                                          \
+  do {                                                    \
+    cudaError_t _e = (call);                              \
+    if (_e != cudaSuccess) return cuda_fail(_e, #call);   \
+  } while (0)
 
 // Stream + launch counter (the bench reports how many of our kernels ran) and
 // an optional per-kernel CUDA-event profiler (bench.py's roofline leg).

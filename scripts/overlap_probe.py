@@ -23,6 +23,7 @@ ap.add_argument("--cap", type=int, default=1 << 20)
 ap.add_argument("--packet", type=int, default=10_000)
 ap.add_argument("--kind", default="texture")
 ap.add_argument("--reps", type=int, default=4)
+ap.add_argument("--profile", action="store_true", help="also print per-kernel ms from one profiled pass")
 ap.add_argument("settings", nargs="+")
 a = ap.parse_args()
 geom = SensorGeometry(640, 480)
@@ -66,4 +67,15 @@ for s in a.settings:
     best = min(times[1:]) if len(times) > 1 else times[0]
     print(f"{s:>40}: {best:8.3f} ms  ({a.events / best / 1e3:7.1f} Mev/s)  all={['%.2f' % t for t in times]} host_enqueue={host_ms:.2f} ms same={same}",
           flush=True)
+    if a.profile:
+        eng.reset()
+        eng.profile(True)
+        for p in packets:
+            eng.process_array(p)
+        eng.render_device()
+        prof = eng.profile_read()
+        eng.profile(False)
+        tot = sum(v[0] for v in prof.values())
+        print("    kernels (sum %.2f ms): " % tot + " ".join(f"{k}={v[0]:.3f}" for k, v in
+                                                          sorted(prof.items(), key=lambda kv: -kv[1][0])), flush=True)
     eng.close()

@@ -9,7 +9,11 @@ Every case feeds seeded inputs through the unmodified reference
 (`fibar.pipeline.ReconstructionEngine`, `fibar.spatial.SpatialFilter`,
 `fibar.event_io`, `fibar.core`) and stores inputs + outputs in
 tests/golden/*.npz.  tests/test_oracle_golden.py pins the C oracle against
-these files; tests/test_gpu_parity.py pins the CUDA path against them too.
+these files; tests/test_gpu_parity.py (engine) and tests/test_tools.py
+(calibration counts, pixel traces) pin the CUDA path against them too.
+
+    python tests/golden/make_golden.py            # every case
+    python tests/golden/make_golden.py tools      # only tests/golden/tools.npz
 """
 
 from __future__ import annotations
@@ -31,6 +35,8 @@ from fibar import event_io as rio  # noqa: E402
 from fibar import pipeline as rpipe  # noqa: E402
 from fibar import spatial as rspatial  # noqa: E402
 from fibar import _kernels as rk  # noqa: E402
+from fibar import calib as rcalib  # noqa: E402
+from fibar import temporal as rtemporal  # noqa: E402
 
 from paper_2510_20071_b200 import workloads  # noqa: E402
 
@@ -158,6 +164,62 @@ def misc_cases():
     print("misc: done")
 
 
+def tools_cases():
+    """Calibration feeder + single-pixel traces."""
+    out = {}
+    rng = np.random.default_rng(21)
+    # traces: random polarities with long same-sign runs, two cutoffs, both dtypes
+    ps = np.where(rng.random(6000) < 0.5, -1, 1).astype(np.int8)
+    ps[1000:1600] = 1
+    ps[3000:3300] = -1
+    out["trace_ps"] = ps
+    for tc in (40.0, 10.0):
+        params = rcore.compute_params(tc, Fraction(1, 2), rcore.SensorGeometry(4, 4))
+        for dt in (np.float32, np.float64):
+            tr = rtemporal.stream_pixel(ps, params, dtype=dt)
+            tag = f"{int(tc)}_{np.dtype(dt).name}"
+            out[f"trace_pbar_{tag}"], out[f"trace_delta_{tag}"], out[f"trace_l_{tag}"] = tr.p_bar, tr.delta, tr.l
+            out[f"trace_iir_{tag}"] = rtemporal.stream_pixel_iir(ps, params, dtype=dt)
+        st = rtemporal.PixelState()
+        seq = []
+        for pol in ps[:50]:
+            st, d = rtemporal.update_pixel(st, int(pol), params)
+            seq.append((st.p_bar, st.l, d))
+        out[f"update_{int(tc)}"] = np.array(seq)
+        out[f"update_iir_{int(tc)}"] = np.array([rtemporal.update_pixel_iir(0.3, -0.2, a, b, params)
+                                                 for a in (-1, 1) for b in (-1, 1)])
+    out["thr_delta"] = np.array([0.5, -0.25, 1e-3])
+    out["thr_c"] = np.array([1.5, 0.7, 3.0])
+    out["thr_out"] = np.array([rtemporal.apply_threshold_map(d, c) for d, c in zip(out["thr_delta"], out["thr_c"])])
+    # calibration: counts over several blocks of a hot-pixel stream, thresholds, histogram
+    geom, ev = _stream("noise_hot", 60, 40, 30000, 9)
+    blocks = [ev.slice(a, min(len(ev), a + 7000)) for a in range(0, len(ev), 7000)]
+    n_on, n_off = rcalib.count_events(iter(blocks), geom)
+    out["cal_t"], out["cal_x"], out["cal_y"], out["cal_p"] = ev.t, ev.x, ev.y, ev.p
+    out["cal_w"], out["cal_h"] = np.int64(geom.width), np.int64(geom.height)
+    out["cal_n_on"], out["cal_n_off"] = n_on, n_off
+    for qtag, q in (("q01", 0.01), ("q0", 0.0), ("q20", 0.2)):
+        tm = rcalib.estimate_thresholds(n_on, n_off, exclusion_quantile=q)
+        out[f"cal_{qtag}_c"], out[f"cal_{qtag}_con"], out[f"cal_{qtag}_coff"] = tm.c_prime, tm.c_on_prime, tm.c_off_prime
+        out[f"cal_{qtag}_excl"], out[f"cal_{qtag}_nbar"] = tm.excluded, np.float64(tm.n_bar_tot)
+        out[f"cal_{qtag}_gain"] = tm.gain_grid()
+        out[f"cal_{qtag}_hmean"] = np.float64(tm.harmonic_mean())
+        edges, counts = rcalib.histogram(tm, "c_prime", bins=20)
+        out[f"cal_{qtag}_hist_edges"], out[f"cal_{qtag}_hist_counts"] = edges, counts
+        if qtag == "q01":
+            path = "/tmp/_golden_map.csv"
+            tm.save_csv(path)
+            out[f"cal_{qtag}_csv"] = np.frombuffer(open(path, "rb").read(), np.uint8)
+    # an event whose flat index y*W + x wraps into the next row still counts (x is not checked alone)
+    wx = np.array([65, 3], np.uint16)
+    wy = np.array([2, 39], np.uint16)
+    w_on, w_off = rcalib.count_events(rcore.EventArray(np.arange(2, dtype=np.uint64), wx, wy,
+                                                       np.array([1, -1], np.int8)), geom)
+    out["wrap_x"], out["wrap_y"], out["wrap_on"], out["wrap_off"] = wx, wy, w_on, w_off
+    np.savez_compressed(os.path.join(HERE, "tools.npz"), **out)
+    print("tools: done")
+
+
 def main():
     rk.warmup()
     engine_case("uniform_off", "uniform", 64, 48, 30000, 0, spatial=False, packet=7000)
@@ -172,7 +234,12 @@ def main():
     engine_case("tiny_on", "uniform", 3, 2, 500, 7, packet=37, q_min=2, stale_log=True)
     engine_case("odd_on", "uniform", 17, 13, 8000, 8, packet=999, q_min=20, q_max=150, stale_log=True)
     misc_cases()
+    tools_cases()
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["tools"]:
+        rk.warmup()
+        tools_cases()
+    else:
+        main()
