@@ -23,6 +23,7 @@ ap.add_argument("--cap", type=int, default=1 << 20)
 ap.add_argument("--packet", type=int, default=10_000)
 ap.add_argument("--kind", default="texture")
 ap.add_argument("--reps", type=int, default=4)
+ap.add_argument("--noblur", action="store_true", help="blur_enabled=False (front-end cost alone)")
 ap.add_argument("--profile", action="store_true", help="also print per-kernel ms from one profiled pass")
 ap.add_argument("settings", nargs="+")
 a = ap.parse_args()
@@ -40,7 +41,7 @@ for s in a.settings:
     env = dict(kv.split("=", 1) for kv in s.split())
     saved = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
-    eng = ReconstructionEngine(geom, params, batch_capacity=a.cap)
+    eng = ReconstructionEngine(geom, params, batch_capacity=a.cap, blur_enabled=not a.noblur)
     for k, v in saved.items():
         if v is None:
             os.environ.pop(k, None)
