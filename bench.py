@@ -165,6 +165,27 @@ def kernel_bytes(name, B, P, D, n_pix):
     return table.get(name)
 
 
+def committed_traffic(kernel: str, batch_cap: int):
+    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
+    capture (profiles/*_traffic.json, written by scripts/summarize_ncu.py from a
+    run with the same 1M-event device batches); None when absent or the batch
+    size differs."""
+    import glob
+    import json
+    if batch_cap != 1 << 20:
+        return None
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")),
+                   key=os.path.getmtime)
+    for f in reversed(files):
+        try:
+            v = json.load(open(f))["bytes_per_launch"].get(kernel)
+        except (OSError, ValueError, KeyError):
+            continue
+        if v:
+            return v
+    return None
+
+
 def run_ours(args, rank, world, dist):
     import torch
     from paper_2510_20071_b200.core import EventArray
@@ -271,7 +292,8 @@ def run_ours(args, rank, world, dist):
     achieved = bytes_launch / launch_s / 1e9 if bytes_launch else None
     roofline = {
         "bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "peak_source": peak_kind,
-        "unit": "GB/s", "frac": (achieved / peak) if achieved else None, "traffic": None,
+        "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
+        "traffic": committed_traffic(dname, args.batch_cap),
         "share_of_step": dms / tot_ms if tot_ms else None, "mean_launch_us": launch_s * 1e6,
         "bytes_per_launch": bytes_launch,
     }

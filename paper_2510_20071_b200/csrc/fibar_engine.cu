@@ -114,6 +114,7 @@ struct Ctx {
   unsigned long long *bv64, *mv64;   // (epoch << 32 | float bits) per blur item / per sorted position
   BlurPrep *prep;
   int chunk, warm, debug;
+  int twarm;                  // warm-up events of a speculative long-segment piece
   unsigned blur_sleep;
   unsigned long long *dbg_t, *dbg_g;
   int2 *anc, *anc2;
@@ -1132,13 +1133,14 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
 }
 
 // Long pixel segments (hot pixels: thousands of events per batch) replayed by
-// a warp: lane i takes the i-th piece, starting TWARM events early from a
-// zero state.  The two float32 recurrences are contractions (|alpha|, |beta|
-// < 1), so trajectories from different starts become bit-identical within
-// ~170 events; each lane's piece-start state is then checked against the
-// previous lane's piece-end state and any piece whose start differed is
-// replayed serially from the exact state, so the result is exact either way.
-constexpr int TWARM = 256;
+// a block: lane i takes the i-th piece (at least LONG_PIECE events), starting
+// `twarm` events early from a zero state.  The two float32 recurrences are
+// contractions (|alpha|, |beta| < 1), so trajectories from different starts
+// become bit-identical after ~24*ln2/-ln(max(alpha, beta)) events (~110 at
+// t_cut = 40; twarm is 1.6x that); each lane's piece-start state is checked
+// against the previous lane's piece-end state and any piece whose start
+// differed is replayed serially from the exact state, so the result is exact
+// either way.
 
 __device__ __forceinline__ void iir_step(const Ctx &x, float &pb, float &lv, float p, float g, float &tt) {
   pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
@@ -1148,22 +1150,36 @@ __device__ __forceinline__ void iir_step(const Ctx &x, float &pb, float &lv, flo
   lv = faddr(fmulr(x.beta, lv), tt);
 }
 
-// replay [q0, q1) from (pb, lv), writing the per-position outputs
+// replay [q0, q1) from (pb, lv), writing the per-position outputs; inputs are
+// loaded GROUP at a time so the chain waits on one load per group
 __device__ __forceinline__ void replay_piece(const Ctx &x, long long q0, long long q1, float &pb, float &lv, float g,
                                              bool write) {
-  for (long long q = q0; q < q1; ++q) {
-    float tt;
-    iir_step(x, pb, lv, (float)x.spol[q], g, tt);
-    if (write && x.spatial) {
-      x.t2[q] = tt;
-      x.posrec[q].val = lv;
+  for (long long q = q0; q < q1; q += GROUP) {
+    int8_t pol[GROUP];
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) pol[u] = q + u < q1 ? x.spol[q + u] : (int8_t)0;
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      if (q + u >= q1) break;
+      float tt;
+      iir_step(x, pb, lv, (float)pol[u], g, tt);
+      if (write && x.spatial) {
+        x.t2[q + u] = tt;
+        x.posrec[q + u].val = lv;
+      }
     }
   }
 }
 
-__global__ void __launch_bounds__(32) k_temporal_long(Ctx x) {
+constexpr int LONG_TPB = 256;      // lanes per long segment (one block)
+constexpr int LONG_PIECE = 64;     // minimum events per lane before more lanes join
+
+__global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
+  __shared__ float s_spb[LONG_TPB], s_slv[LONG_TPB], s_epb[LONG_TPB], s_elv[LONG_TPB];
+  __shared__ unsigned s_last[LONG_TPB];
+  __shared__ int s_bad;
   const unsigned n = min(x.bs->nlong, (unsigned)MAX_LONG);
-  const int lane = threadIdx.x;
+  const int tid = threadIdx.x;
   for (unsigned sidx = blockIdx.x; sidx < n; sidx += gridDim.x) {
     const uint2 ls = x.longseg[sidx];
     const long long st = ls.x;
@@ -1182,44 +1198,56 @@ __global__ void __launch_bounds__(32) k_temporal_long(Ctx x) {
       end = lo;
     }
     const long long len = end - st;
-    const long long P = (len + 31) / 32;
-    const long long q0 = min(end, st + lane * P), q1 = min(end, q0 + P);
+    const int lanes = (int)min((long long)LONG_TPB, max(32LL, len / LONG_PIECE));
+    const long long P = (len + lanes - 1) / lanes;
+    const bool on = tid < lanes;
+    const long long q0 = on ? min(end, st + tid * P) : end, q1 = on ? min(end, q0 + P) : end;
     const float g = x.use_gain ? x.gain[c] : 1.0f;
-    float pb, lv;
-    if (lane == 0) {
+    float pb = 0.0f, lv = 0.0f;
+    if (tid == 0) {
       pb = x.pbar[c];
       lv = x.l[c];
-    } else {
-      pb = 0.0f;
-      lv = 0.0f;
-      replay_piece(x, max(st, q0 - TWARM), q0, pb, lv, g, false);
+    } else if (on) {
+      replay_piece(x, max(st, q0 - (long long)x.twarm), q0, pb, lv, g, false);
     }
-    const float spb = pb, slv = lv;   // speculative state at the piece start
+    s_spb[tid] = pb;   // speculative state at the piece start
+    s_slv[tid] = lv;
     replay_piece(x, q0, q1, pb, lv, g, true);
-    // verify boundaries in lane order; re-run pieces whose start was wrong
-    float epb = pb, elv = lv;
-    for (int i = 1; i < 32; ++i) {
-      const float ppb = __shfl_sync(0xffffffffu, epb, i - 1), plv = __shfl_sync(0xffffffffu, elv, i - 1);
-      const bool bad = __float_as_uint(__shfl_sync(0xffffffffu, spb, i)) != __float_as_uint(ppb) ||
-                       __float_as_uint(__shfl_sync(0xffffffffu, slv, i)) != __float_as_uint(plv);
-      if (bad && lane == i) {
-        pb = ppb;
-        lv = plv;
-        replay_piece(x, q0, q1, pb, lv, g, true);
-        epb = pb;
-        elv = lv;
+    s_epb[tid] = pb;
+    s_elv[tid] = lv;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    // verify every boundary; in the rare case a start was wrong, re-run the
+    // pieces from there on serially in lane order from the exact states
+    if (on && tid > 0 && (__float_as_uint(s_spb[tid]) != __float_as_uint(s_epb[tid - 1]) ||
+                          __float_as_uint(s_slv[tid]) != __float_as_uint(s_elv[tid - 1])))
+      atomicMax(&s_bad, 1);
+    __syncthreads();
+    if (s_bad) {
+      for (int i = 1; i < lanes; ++i) {
+        if (tid == i && (__float_as_uint(s_spb[i]) != __float_as_uint(s_epb[i - 1]) ||
+                         __float_as_uint(s_slv[i]) != __float_as_uint(s_elv[i - 1]))) {
+          pb = s_epb[i - 1];
+          lv = s_elv[i - 1];
+          s_spb[i] = pb;
+          s_slv[i] = lv;
+          replay_piece(x, q0, q1, pb, lv, g, true);
+          s_epb[i] = pb;
+          s_elv[i] = lv;
+        }
+        __syncthreads();
       }
-      __syncwarp();
     }
-    const float fpb = __shfl_sync(0xffffffffu, epb, 31), flv = __shfl_sync(0xffffffffu, elv, 31);
+    const float fpb = s_epb[lanes - 1], flv = s_elv[lanes - 1];
     if (!x.spatial) {
-      if (lane == 0) {
+      if (tid == 0) {
         x.pbar[c] = fpb;
         x.l[c] = flv;
       }
+      __syncthreads();
       continue;
     }
-    if (lane == 0) {
+    if (tid == 0) {
       x.pbar[c] = fpb;
       const long long elast = x.bs->E0 + x.sidx[end - 1];
       x.plast[c] = elast;
@@ -1228,26 +1256,42 @@ __global__ void __launch_bounds__(32) k_temporal_long(Ctx x) {
     // blur bookkeeping: which blur each position builds on (last stale event
     // before it in the segment, or the pixel's carried blur)
     unsigned last = FIBAR_NONE;
-    for (long long q = q0; q < q1; ++q) {
-      const unsigned bidx = x.posrec[q].bidx;
-      if (bidx != FIBAR_NONE) {
-        last = bidx;
-        if (q + 1 < end) x.item[bidx].runpos = (unsigned)(q + 1);
+    for (long long q = q0; q < q1; q += GROUP) {
+      unsigned bidx[GROUP];
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) bidx[u] = q + u < q1 ? x.posrec[q + u].bidx : FIBAR_NONE;
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) {
+        if (bidx[u] != FIBAR_NONE) {
+          last = bidx[u];
+          if (q + u + 1 < end) x.item[bidx[u]].runpos = (unsigned)(q + u + 1);
+        }
       }
     }
-    // exclusive "last non-NONE" scan over lanes
-    unsigned carry_in = x.pt[c].carried;
-    if (lane == 0 && carry_in != FIBAR_NONE) x.item[carry_in].runpos = (unsigned)st;
-    for (int i = 0; i < 31; ++i) {
-      const unsigned li = __shfl_sync(0xffffffffu, last, i);
-      if (lane > i && li != FIBAR_NONE) carry_in = li;
+    s_last[tid] = last;
+    const unsigned carried = x.pt[c].carried;
+    if (tid == 0 && carried != FIBAR_NONE) x.item[carried].runpos = (unsigned)st;
+    __syncthreads();
+    // exclusive "last non-NONE before me" over the lanes: a short backwards scan
+    unsigned carry = carried;
+    for (int i = tid - 1; i >= 0; --i) {
+      if (s_last[i] != FIBAR_NONE) {
+        carry = s_last[i];
+        break;
+      }
     }
-    unsigned carry = carry_in;
-    for (long long q = q0; q < q1; ++q) {
-      x.posrec[q].runbase = carry;
-      const unsigned bidx = x.posrec[q].bidx;
-      if (bidx != FIBAR_NONE) carry = bidx;
+    for (long long q = q0; q < q1; q += GROUP) {
+      unsigned bidx[GROUP];
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) bidx[u] = q + u < q1 ? x.posrec[q + u].bidx : FIBAR_NONE;
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) {
+        if (q + u >= q1) break;
+        x.posrec[q + u].runbase = carry;
+        if (bidx[u] != FIBAR_NONE) carry = bidx[u];
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -1884,6 +1928,7 @@ struct fibar_engine {
   int nsm = 148;
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
+  int twarm = 256;
   bool serial = false;   // FIBAR_SERIAL: blur stage on the engine stream (no overlap; for measurement)
   unsigned blur_sleep = 0;
   unsigned long long *dbg_t = nullptr, *dbg_g = nullptr;
@@ -1944,6 +1989,7 @@ struct fibar_engine {
     x.mv64 = mv64;
     x.prep = prep;
     x.chunk = chunk;
+    x.twarm = twarm;
     x.debug = debug;
     x.blur_sleep = blur_sleep;
     x.dbg_t = dbg_t;
@@ -2045,7 +2091,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     // the replay reads the brightness the previous batch's blur stage finishes
     if (g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
     FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 8, 32, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 2, LONG_TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
     CK(cudaEventRecord(g->evF[par], s));
     // blur stage on its own stream: overlaps the next batch's front end
@@ -2065,7 +2111,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   } else {
     FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 8, 32, 0, s>>>(x));
+    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 2, LONG_TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
   }
   CK(cudaGetLastError());
@@ -2074,6 +2120,17 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
 }
 
 // hand the filled host staging set to the device and run it
+constexpr long long DIRECT_MIN = 1LL << 16;   // host packets at least this large and pinned skip the CPU copy
+
+bool is_pinned(const void *ptr) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 int launch_host_batch(fibar_engine *g) {
   if (g->hfill == 0) return 0;
   const int c = g->cur;
@@ -2219,6 +2276,13 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   if (const char *v = getenv("FIBAR_WARM")) g->warm = std::max(0, atoi(v));
   if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
   if (const char *v = getenv("FIBAR_SERIAL")) g->serial = atoi(v) != 0;
+  {
+    // contraction of the slower recurrence: events until any two float32
+    // trajectories agree to the last bit, with a 1.6x margin
+    const double r = std::max((double)cfg->alpha, (double)cfg->beta);
+    const double steps = (r > 0.0 && r < 1.0) ? 24.0 * std::log(2.0) / -std::log(r) : 1024.0;
+    g->twarm = (int)std::min(2048.0, std::max(64.0, std::ceil(1.6 * steps)));
+  }
   g->R = 1LL << ceil_log2(n + 1 + g->Bcap);
   int dev = 0;
   cudaGetDevice(&dev);
@@ -2416,6 +2480,31 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
     int rc = run_batch(g);
     if (rc) return rc;
   }
+  // large packets already in pinned memory are DMA'd straight into the device
+  // staging set (no CPU copy); the call returns once those copies are done,
+  // so the caller may reuse its buffers as with any host packet
+  const bool direct = n - off >= DIRECT_MIN && is_pinned(x) && is_pinned(y) && is_pinned(p);
+  cudaEvent_t last_direct = nullptr;
+  if (direct && g->hfill > 0) {   // earlier staged packets go first
+    int rc = launch_host_batch(g);
+    if (rc) return rc;
+  }
+  while (direct && n - off >= DIRECT_MIN) {
+    const int c = g->cur;
+    const long long take = std::min((long long)n - off, g->Bcap);
+    CK(cudaStreamWaitEvent(g->cstream, g->ev_used[c], 0));
+    CK(cudaMemcpyAsync(g->sx[c], x + off, sizeof(uint16_t) * take, cudaMemcpyHostToDevice, g->cstream));
+    CK(cudaMemcpyAsync(g->sy[c], y + off, sizeof(uint16_t) * take, cudaMemcpyHostToDevice, g->cstream));
+    CK(cudaMemcpyAsync(g->sp_[c], p + off, sizeof(int8_t) * take, cudaMemcpyHostToDevice, g->cstream));
+    CK(cudaEventRecord(g->ev_h2d[c], g->cstream));
+    CK(cudaStreamWaitEvent(g->L.stream, g->ev_h2d[c], 0));
+    last_direct = g->ev_h2d[c];
+    g->cur ^= 1;
+    off += take;
+    int rc = run_batch_raw(g, g->sx[c], g->sy[c], g->sp_[c], take, g->ev_used[c]);
+    if (rc) return rc;
+  }
+  if (last_direct) CK(cudaEventSynchronize(last_direct));
   while (off < n) {
     if (g->hfill == 0) CK(cudaEventSynchronize(g->ev_h2d[g->cur]));   // host set free again
     const long long take = std::min((long long)n - off, g->Bcap - g->hfill);

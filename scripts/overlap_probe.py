@@ -22,12 +22,14 @@ ap.add_argument("--events", type=int, default=10_000_000)
 ap.add_argument("--cap", type=int, default=1 << 20)
 ap.add_argument("--packet", type=int, default=10_000)
 ap.add_argument("--kind", default="texture")
+ap.add_argument("--w", type=int, default=640)
+ap.add_argument("--h", type=int, default=480)
 ap.add_argument("--reps", type=int, default=4)
 ap.add_argument("--noblur", action="store_true", help="blur_enabled=False (front-end cost alone)")
 ap.add_argument("--profile", action="store_true", help="also print per-kernel ms from one profiled pass")
 ap.add_argument("settings", nargs="+")
 a = ap.parse_args()
-geom = SensorGeometry(640, 480)
+geom = SensorGeometry(a.w, a.h)
 ev = workloads.make(a.kind, geom, a.events, seed=0)
 params = compute_params(40.0, Fraction(1, 2), geom)
 xd = torch.from_numpy(ev.x.view(np.int16)).cuda()

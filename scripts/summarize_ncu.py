@@ -88,4 +88,16 @@ if os.path.exists(rep):
                 rb, wb, u = dram[kid]
                 fh.write(f"- dram__bytes_read.sum + dram__bytes_write.sum: {rb:.3f} + {wb:.3f} {u}\n")
             fh.write("\n")
+    # per-launch DRAM bytes by kernel (bench.py fills roofline.traffic from this)
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    traffic = {}
+    for (kid, name), m in per.items():
+        if kid in dram:
+            rb, wb, u = dram[kid]
+            short = name.replace("k_", "", 1)
+            traffic.setdefault(short, []).append((rb + wb) * scale.get(u, 1.0))
+    import json
+    with open(os.path.join(out_dir, f"{tag}_traffic.json"), "w") as fh:
+        json.dump({"source": f"ncu --set full capture full_{tag}.ncu-rep (cold cache, one launch each)",
+                   "bytes_per_launch": {k: sum(v) / len(v) for k, v in traffic.items()}}, fh, indent=1)
     print("wrote full summary;", len(per), "kernels")

@@ -166,3 +166,26 @@ def test_saturation_flag_after_pops():
     eng = ReconstructionEngine(geom, params)
     eng.process_array(EventArray(np.arange(n, dtype=np.uint64), x, y, p))
     assert eng.saturation_detected
+
+
+def test_pinned_host_packets_direct_copy():
+    """Large packets in pinned host memory are DMA'd without the CPU staging copy;
+    mixing them with small (staged) packets and device packets changes nothing."""
+    import torch
+    from paper_2510_20071_b200.core import EventArray
+    from paper_2510_20071_b200.pipeline import DeviceEventArray, ReconstructionEngine
+    geom, params, ev, ref = _oracle_stream("texture", 320, 240, 600_000, 600_000, True, seed=5)
+    pin = lambda a: torch.from_numpy(a.view(np.int16) if a.dtype == np.uint16 else a).pin_memory().numpy()
+    xs, ys, ps = pin(ev.x).view(np.uint16), pin(ev.y).view(np.uint16), pin(ev.p)
+    eng = ReconstructionEngine(geom, params, batch_capacity=1 << 17)
+    cuts = [0, 1000, 201_000, 205_000, 405_000, 600_000]   # small, large, small, large(device), large
+    for i, (a, b) in enumerate(zip(cuts[:-1], cuts[1:])):
+        if i == 3:
+            eng.process_array(DeviceEventArray(torch.from_numpy(ev.x[a:b].view(np.int16)).cuda(),
+                                               torch.from_numpy(ev.y[a:b].view(np.int16)).cuda(),
+                                               torch.from_numpy(ev.p[a:b]).cuda()))
+        else:
+            eng.process_array(EventArray(ev.t[a:b], xs[a:b], ys[a:b], ps[a:b]))
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, "pinned direct")
