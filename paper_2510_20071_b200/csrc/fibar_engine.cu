@@ -2120,7 +2120,9 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
 }
 
 // hand the filled host staging set to the device and run it
-constexpr long long DIRECT_MIN = 1LL << 16;   // host packets at least this large and pinned skip the CPU copy
+// pinned host packets of at least half a device batch skip the CPU staging
+// copy (smaller ones are coalesced through the staging buffers as before)
+long long direct_min(const fibar_engine *g) { return std::max(1LL << 16, g->Bcap / 2); }
 
 bool is_pinned(const void *ptr) {
   cudaPointerAttributes a;
@@ -2483,13 +2485,14 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
   // large packets already in pinned memory are DMA'd straight into the device
   // staging set (no CPU copy); the call returns once those copies are done,
   // so the caller may reuse its buffers as with any host packet
-  const bool direct = n - off >= DIRECT_MIN && is_pinned(x) && is_pinned(y) && is_pinned(p);
+  const long long dmin = direct_min(g);
+  const bool direct = n - off >= dmin && is_pinned(x) && is_pinned(y) && is_pinned(p);
   cudaEvent_t last_direct = nullptr;
   if (direct && g->hfill > 0) {   // earlier staged packets go first
     int rc = launch_host_batch(g);
     if (rc) return rc;
   }
-  while (direct && n - off >= DIRECT_MIN) {
+  while (direct && n - off >= dmin) {
     const int c = g->cur;
     const long long take = std::min((long long)n - off, g->Bcap);
     CK(cudaStreamWaitEvent(g->cstream, g->ev_used[c], 0));
