@@ -165,14 +165,14 @@ def kernel_bytes(name, B, P, D, n_pix):
     return table.get(name)
 
 
-def committed_traffic(kernel: str, batch_cap: int):
+def committed_traffic(kernel: str, batch_cap: int, config: int):
     """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
-    capture (profiles/*_traffic.json, written by scripts/summarize_ncu.py from a
-    run with the same 1M-event device batches); None when absent or the batch
-    size differs."""
+    capture (profiles/*_traffic.json, written by scripts/summarize_ncu.py from
+    `bench.py --profile-only`: config 2, 1M-event device batches); None for any
+    other workload or batch size, or when no capture is committed."""
     import glob
     import json
-    if batch_cap != 1 << 20:
+    if batch_cap != 1 << 20 or config != 2:
         return None
     files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")),
                    key=os.path.getmtime)
@@ -293,7 +293,7 @@ def run_ours(args, rank, world, dist):
     roofline = {
         "bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "peak_source": peak_kind,
         "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-        "traffic": committed_traffic(dname, args.batch_cap),
+        "traffic": committed_traffic(dname, args.batch_cap, args.config),
         "share_of_step": dms / tot_ms if tot_ms else None, "mean_launch_us": launch_s * 1e6,
         "bytes_per_launch": bytes_launch,
     }
