@@ -45,15 +45,15 @@ struct __align__(16) Item {
   unsigned pad;
 };
 
-// A blur item's taps after the dependency-free part of their resolution:
-// tap t is in bounds iff bit t of okm; pending iff bit t of pend, in which case
-// val[t] names the word to wait for (bit 31: a rebuilt-run position, else a
-// blur item) and flag[t] the blur item it comes from; otherwise val[t] holds
-// the float bits of the tap's brightness.
+// A blur item's taps after the dependency-free part of their resolution
+// (48 B, three 16-byte loads): tap t is in bounds iff bit t of okm; pending
+// iff bit t of pend, in which case val[t] names the word to wait for (bit 31:
+// a rebuilt-run position, else a blur item); otherwise val[t] holds the float
+// bits of the tap's brightness.  runpos: the item's first rebuilt position.
 struct __align__(16) BlurPrep {
   unsigned okm, pend;
-  unsigned flag[9];
   unsigned val[9];
+  unsigned runpos;
 };
 
 // Scalars of one device batch (double buffered by batch parity).

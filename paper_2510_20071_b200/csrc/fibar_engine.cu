@@ -1374,27 +1374,27 @@ __global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x) {
     if (posi[t] != FIBAR_NONE) rec[t] = x.posrec[posi[t]];
 #pragma unroll
   for (int t = 0; t < 9; ++t) {
-    out.flag[t] = FIBAR_NONE;
     out.val[t] = 0u;
     if (!((out.okm >> t) & 1)) continue;
+    bool wait = true;
     if (posi[t] == FIBAR_NONE) {
       if (pr[t].z < p) {                    // blurred (carried) before this item
-        out.flag[t] = pr[t].z;
         out.val[t] = pr[t].z;
       } else {
         out.val[t] = __float_as_uint(x.l[nidx[t]]);
+        wait = false;
       }
     } else if (rec[t].bidx < p) {           // its own blur came first
-      out.flag[t] = rec[t].bidx;
       out.val[t] = rec[t].bidx;
     } else if (rec[t].runbase == FIBAR_NONE) {
       out.val[t] = __float_as_uint(rec[t].val);   // first run: no blur involved
+      wait = false;
     } else {                                // rebuilt from blur runbase
-      out.flag[t] = rec[t].runbase | 0x80000000u;
       out.val[t] = posi[t] | 0x80000000u;
     }
-    if (out.flag[t] != FIBAR_NONE) out.pend |= 1u << t;
+    if (wait) out.pend |= 1u << t;
   }
+  out.runpos = it.runpos;
   x.prep[p] = out;
 }
 
@@ -1438,14 +1438,23 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
         if (q >= npop) {
           exhausted = true;
         } else {
-          const BlurPrep &bp = x.prep[q];
-          okm = bp.okm;
+          const uint4 *rec = reinterpret_cast<const uint4 *>(&x.prep[q]);
+          const uint4 n0 = __ldcg(rec);
+          okm = n0.x;
           if (okm) {
+            const uint4 n1 = __ldcg(rec + 1), n2 = __ldcg(rec + 2);
             p = q;
-            pend = bp.pend;
-#pragma unroll
-            for (int t = 0; t < 9; ++t) val[t] = bp.val[t];
-            runpos = x.item[q].runpos;
+            pend = n0.y;
+            val[0] = n0.z;
+            val[1] = n0.w;
+            val[2] = n1.x;
+            val[3] = n1.y;
+            val[4] = n1.z;
+            val[5] = n1.w;
+            val[6] = n2.x;
+            val[7] = n2.y;
+            val[8] = n2.z;
+            runpos = n2.w;
           }
         }
       }
