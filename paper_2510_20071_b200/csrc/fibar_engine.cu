@@ -1868,6 +1868,12 @@ int ceil_log2(long long v) {
 
 }  // namespace
 
+struct GraphEntry {
+  long long n;               // batch size the graph was captured for
+  long long kernels;         // kernels per replay (the launch counter)
+  cudaGraphExec_t exec;
+};
+
 struct fibar_engine {
   fibar_config cfg{};
   int W = 0, H = 0, ts = 2, A = 4, tiles_x = 0, tiles_y = 0;
@@ -1931,6 +1937,14 @@ struct fibar_engine {
   // while batch k+1's front end runs on the engine stream; per-batch buffers
   // are double buffered by batch parity
   cudaStream_t bstream = nullptr;
+  // small batches: one CUDA graph per batch size, fed from fixed input buffers
+  bool graphs_on = true;
+  cudaStream_t capstream = nullptr;
+  long long graph_max = 1LL << 17;
+  std::vector<GraphEntry> graphs;
+  uint16_t *gx = nullptr, *gy = nullptr;
+  int8_t *gp = nullptr;
+  int blur_grid_serial = 148;
   cudaEvent_t evF[2] = {nullptr, nullptr}, evB[2] = {nullptr, nullptr};
   int last_b = -1;   // parity of the newest batch with a blur stage in flight
   bool b_used[2] = {false, false};
@@ -2053,14 +2067,16 @@ int init_state(fibar_engine *g) {
   return 0;
 }
 
-int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
-                  cudaEvent_t used_ev) {
-  if (n_raw <= 0) return 0;
-  const int par = g->spatial ? (int)(g->batches & 1) : 0;
+// Enqueue one device batch.  graph == false: the streamed form (blur stage on
+// the second stream, cross-batch events).  graph == true: everything on the
+// engine stream with parity-0 buffers and no events, the form captured into a
+// CUDA graph for small batches (see run_batch_raw).
+int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                  cudaEvent_t used_ev, int par, bool graph) {
   Launcher &L = g->L;
   cudaStream_t s = L.stream;
   // this parity's buffers are free once the batch two back finished its blur stage
-  if (g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
+  if (!graph && g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
   Ctx x = g->ctx(nullptr, nullptr, n_raw, par);
   x.raw_x = rx0;
@@ -2098,25 +2114,29 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     FIBAR_LAUNCH(L, "popj", k_popj<<<(int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
     // the replay reads the brightness the previous batch's blur stage finishes
-    if (g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
+    if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
     FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 2, LONG_TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
-    CK(cudaEventRecord(g->evF[par], s));
     // blur stage on its own stream: overlaps the next batch's front end
-    cudaStream_t bs = g->serial ? s : g->bstream;
-    CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
+    cudaStream_t bs = (g->serial || graph) ? s : g->bstream;
+    if (!graph) {
+      CK(cudaEventRecord(g->evF[par], s));
+      CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
+    }
     L.stream = bs;
     if (g->blur_on) {
       const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
       FIBAR_LAUNCH(L, "blur_prep", k_blur_prep<<<nbp, TPB, 0, bs>>>(x));
-      FIBAR_LAUNCH(L, "blur", k_blur<<<g->blur_grid, TPB, 0, bs>>>(x));
+      FIBAR_LAUNCH(L, "blur", k_blur<<<graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs>>>(x));
     }
     FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, bs>>>(x));
     L.stream = s;
-    CK(cudaEventRecord(g->evB[par], bs));
-    g->b_used[par] = true;
-    g->last_b = par;
+    if (!graph) {
+      CK(cudaEventRecord(g->evB[par], bs));
+      g->b_used[par] = true;
+      g->last_b = par;
+    }
   } else {
     FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
     FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
@@ -2124,6 +2144,68 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
   }
   CK(cudaGetLastError());
+  return 0;
+}
+
+// A small batch is launch-bound (~45 dependent kernels doing a few us of work
+// each), so it runs as one CUDA graph per batch size: its inputs are copied
+// into fixed graph buffers, the kernel sequence is captured once per size and
+// replayed with a single launch.  Large batches stream (two-stream overlap).
+int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                  cudaEvent_t used_ev) {
+  if (n_raw <= 0) return 0;
+  Launcher &L = g->L;
+  cudaStream_t s = L.stream;
+  if (!g->graphs_on || L.prof || n_raw > g->graph_max) {
+    const int par = g->spatial ? (int)(g->batches & 1) : 0;
+    int rc = enqueue_batch(g, rx0, ry0, rp0, n_raw, used_ev, par, false);
+    if (rc) return rc;
+    g->batches++;
+    return 0;
+  }
+  // graph form: after every earlier blur stage (it reuses parity-0 buffers)
+  join_blur(g);
+  g->last_b = -1;
+  g->b_used[0] = g->b_used[1] = false;
+  CK(cudaMemcpyAsync(g->gx, rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(g->gy, ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(g->gp, rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+  if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
+  GraphEntry *hit = nullptr;
+  for (auto &ge : g->graphs)
+    if (ge.n == n_raw) hit = &ge;
+  if (!hit) {
+    if (g->graphs.size() >= 8) {   // small cache: drop the oldest size
+      cudaGraphExecDestroy(g->graphs.front().exec);
+      g->graphs.erase(g->graphs.begin());
+    }
+    // captured on a private stream (the caller's may be the legacy default
+    // stream, which cannot be captured); replayed on the caller's
+    cudaGraph_t graph = nullptr;
+    const long long l0 = L.launches;
+    if (!g->capstream) CK(cudaStreamCreateWithFlags(&g->capstream, cudaStreamNonBlocking));
+    CK(cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal));
+    L.stream = g->capstream;
+    int rc = enqueue_batch(g, g->gx, g->gy, g->gp, n_raw, nullptr, 0, true);
+    L.stream = s;
+    cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
+    if (rc) {
+      if (graph) cudaGraphDestroy(graph);
+      return rc;
+    }
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
+    GraphEntry ge;
+    ge.n = n_raw;
+    ge.kernels = L.launches - l0;
+    L.launches = l0;
+    ce = cudaGraphInstantiate(&ge.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+    g->graphs.push_back(ge);
+    hit = &g->graphs.back();
+  }
+  CK(cudaGraphLaunch(hit->exec, s));
+  L.launches += hit->kernels;
   g->batches++;
   return 0;
 }
@@ -2301,6 +2383,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   {
     int per_sm = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blur, TPB, 0);
+    g->blur_grid_serial = g->nsm * std::max(1, std::min(per_sm, 4));   // graph form: nothing to overlap with
     // the blur stage overlaps the next batch's front end: one 256-thread block
     // per SM leaves the rest of each SM to the front end (measured: 1/SM gives
     // 10.2 ms per 10M config-2 events vs 11.2 at 2/SM and 12.6 serialised)
@@ -2308,7 +2391,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     if (const char *v = getenv("FIBAR_BLUR_BLOCKS")) per_sm = std::min(per_sm, std::max(1, atoi(v)));
     g->blur_grid = g->nsm * std::max(1, per_sm);
     if (const char *v = getenv("FIBAR_BLUR_SLEEP")) g->blur_sleep = (unsigned)atoi(v);
-
+    if (const char *v = getenv("FIBAR_GRAPHS")) g->graphs_on = atoi(v) != 0;
+    if (const char *v = getenv("FIBAR_GRAPH_MAX")) g->graph_max = atoll(v);
+    g->graph_max = std::min(g->graph_max, g->Bcap);
   }
   int rc = 0;
   const long long Bc = g->Bcap;
@@ -2332,6 +2417,11 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   }
   cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking);
   rc |= dalloc(&g->blockcnt, nb_in + 1);
+  if (g->graphs_on && g->graph_max > 0) {
+    rc |= dalloc(&g->gx, g->graph_max);
+    rc |= dalloc(&g->gy, g->graph_max);
+    rc |= dalloc(&g->gp, g->graph_max);
+  }
   rc |= dalloc(&g->epol, Bc);
   rc |= dalloc(&g->spol, Bc);
   rc |= dalloc(&g->longseg, 16384);
@@ -2436,6 +2526,10 @@ int fibar_destroy(fibar_engine *g) {
     if (g->evB[c]) cudaEventDestroy(g->evB[c]);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
+  for (auto &ge : g->graphs) cudaGraphExecDestroy(ge.exec);
+  if (g->capstream) cudaStreamDestroy(g->capstream);
+  for (void *q : {(void *)g->gx, (void *)g->gy, (void *)g->gp})
+    if (q) cudaFree(q);
   if (g->bstream) cudaStreamDestroy(g->bstream);
   delete g;
   return 0;

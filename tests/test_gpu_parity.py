@@ -189,3 +189,20 @@ def test_pinned_host_packets_direct_copy():
     want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
                 qx=ref.qx, qy=ref.qy, qs=ref.qs)
     assert_state(eng, want, "pinned direct")
+
+
+def test_graph_and_streamed_batches_agree(monkeypatch):
+    """Small batches replay a captured CUDA graph, large ones stream on two
+    streams; forcing either form gives the same (oracle-exact) state."""
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    geom, params, ev, ref = _oracle_stream("texture_noise_hot", 320, 240, 300_000, 30_000, True, seed=9)
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    for graphs in ("1", "0"):
+        monkeypatch.setenv("FIBAR_GRAPHS", graphs)
+        eng = ReconstructionEngine(geom, params)
+        for a in range(0, len(ev), 30_000):
+            eng.process_array(ev.slice(a, min(len(ev), a + 30_000)))
+            eng.render("robust")          # a read-out per packet: one batch per packet
+        assert_state(eng, want, f"graphs={graphs}")
+        eng.close()
