@@ -75,7 +75,7 @@ struct SelState {
   unsigned hist[4][2048];
   double lo, hi;
   int degenerate;
-  int pad;
+  unsigned done;   // blocks finished with the current histogram pass
 };
 
 struct Ctx {
@@ -1559,8 +1559,13 @@ __device__ __forceinline__ float order_unkey(unsigned k) {
   return __uint_as_float(u);
 }
 
-// histogram pass of an exact radix select (digits 11/11/10 bits, MSB first)
-__global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, long long n, SelState *sel, int pass) {
+__device__ void sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound);
+
+// One pass of an exact radix select (digits 11/11/10 bits, MSB first): each
+// block histograms the candidates' next digit, and the last block to finish
+// picks the digits from the totals (and after the last pass, the bounds).
+__global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, long long n, SelState *sel, int pass,
+                                                  double g_lo, double g_hi) {
   __shared__ unsigned h[4][2048];
   const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
   const unsigned dmask = pass == 2 ? 1023u : 2047u;
@@ -1575,63 +1580,84 @@ __global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, l
   }
   for (int i = threadIdx.x; i < 4 * 2048; i += TPB) (&h[0][0])[i] = 0;
   __syncthreads();
-  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
-    const unsigned k = order_key(l[i]);
+  // brightness values cluster in a few top digits, so equal digits within a
+  // warp are combined first (one shared atomic per distinct digit and target)
+  const long long stride = (long long)gridDim.x * TPB;
+  const long long n_round = (n + 31) & ~31LL;
+  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n_round; i += stride) {
+    const bool in = i < n;
+    const unsigned k = in ? order_key(l[i]) : 0u;
     const unsigned d = (k >> shift) & dmask;
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
-      if (act[t] && (k & hmask) == pref[t]) atomicAdd(&h[t][d], 1u);
+    for (int t = 0; t < 4; ++t) {
+      if (!act[t]) continue;   // warp-uniform
+      const bool mine = in && (k & hmask) == pref[t];
+      const unsigned key = mine ? d : 0xFFFFFFFFu;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (mine && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&h[t][d], (unsigned)__popc(peers));
+    }
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 4 * 2048; i += TPB) {
     const unsigned v = (&h[0][0])[i];
     if (v) atomicAdd(&(&sel->hist[0][0])[i], v);
   }
-}
-
-__global__ void k_sel_pick(SelState *sel, int pass) {
-  // one warp per target
-  const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (t >= 4) return;
-  const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
-  const int nd = pass == 2 ? 1024 : 2048;
-  int src = t;
-  for (int u = 0; u < t; ++u)
-    if (sel->prefix[u] == sel->prefix[t]) {
-      src = u;
-      break;
-    }
-  unsigned rank = sel->rank[t];
-  unsigned run = 0;
-  unsigned found_d = 0, found_before = 0;
-  bool found = false;
-  for (int base = 0; base < nd && !found; base += 32) {
-    const unsigned v = sel->hist[src][base + lane];
-    unsigned inc = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      unsigned tt = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc += tt;
-    }
-    const unsigned excl = run + inc - v;
-    const bool hit = rank >= excl && rank < run + inc;
-    const unsigned m = __ballot_sync(0xffffffffu, hit);
-    if (m) {
-      const int L = __ffs(m) - 1;
-      found_d = base + L;
-      found_before = __shfl_sync(0xffffffffu, excl, L);
-      found = true;
-    }
-    run += __shfl_sync(0xffffffffu, inc, 31);
-  }
-  __syncwarp();
+  __threadfence();
+  __shared__ bool last;
+  if (threadIdx.x == 0) last = atomicAdd(&sel->done, 1u) == gridDim.x - 1;
   __syncthreads();
-  if (lane == 0) {
-    sel->prefix[t] |= found_d << shift;
+  if (!last) return;
+  __threadfence();
+  // totals into shared memory (and the global table cleared for the next pass)
+  for (int i = threadIdx.x; i < 4 * 2048; i += TPB) {
+    (&h[0][0])[i] = __ldcg(&(&sel->hist[0][0])[i]);
+    (&sel->hist[0][0])[i] = 0u;
+  }
+  __syncthreads();
+  // one warp per target: the digit holding its remaining rank
+  const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nd = pass == 2 ? 1024 : 2048;
+  unsigned found_d = 0, found_before = 0, rank = 0;
+  if (t < 4) {
+    int src = t;
+    for (int u = 0; u < t; ++u)
+      if (pref[u] == pref[t]) {
+        src = u;
+        break;
+      }
+    rank = sel->rank[t];
+    unsigned run = 0;
+    for (int base = 0; base < nd; base += 32) {
+      const unsigned v = h[src][base + lane];
+      unsigned inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned tt = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += tt;
+      }
+      const unsigned excl = run + inc - v;
+      const unsigned m = __ballot_sync(0xffffffffu, rank >= excl && rank < run + inc);
+      if (m) {
+        const int L = __ffs(m) - 1;
+        found_d = base + L;
+        found_before = __shfl_sync(0xffffffffu, excl, L);
+        break;
+      }
+      run += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  if (t < 4 && lane == 0) {
+    sel->prefix[t] = pref[t] | (found_d << shift);
     sel->rank[t] = rank - found_before;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 4 * 2048; i += blockDim.x) (&sel->hist[0][0])[i] = 0;
+  if (threadIdx.x == 0) {
+    sel->done = 0;
+    if (pass == 2) {
+      __threadfence_block();
+      sel_bounds(sel, g_lo, g_hi, FIBAR_RENDER_ROBUST, 0.0);
+    }
+  }
 }
 
 __global__ void k_sel_init(SelState *sel, unsigned r0, unsigned r1, unsigned r2, unsigned r3) {
@@ -1643,7 +1669,7 @@ __global__ void k_sel_init(SelState *sel, unsigned r0, unsigned r1, unsigned r2,
 }
 
 // lo/hi from the selected order statistics (numpy 'linear' percentile, _lerp)
-__global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound) {
+__device__ void sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound) {
   double lo, hi;
   if (mode == FIBAR_RENDER_ROBUST) {
     const double a0 = (double)order_unkey(sel->prefix[0]), b0 = (double)order_unkey(sel->prefix[1]);
@@ -1658,6 +1684,10 @@ __global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, 
   sel->lo = lo;
   sel->hi = hi;
   sel->degenerate = !(hi > lo);
+}
+
+__global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound) {
+  sel_bounds(sel, g_lo, g_hi, mode, fixed_bound);
 }
 
 // u8 = clip(floor((v - lo) * (255 / (hi - lo)) + 0.5), 0, 255) in float64
@@ -2291,19 +2321,21 @@ int render_core(Launcher &L, const float *l, long long n, int32_t mode, double f
     g_hi = gam[1];
     FIBAR_LAUNCH(L, "sel_init", k_sel_init<<<1, 1, 0, s>>>(sel, rk[0], rk[1], rk[2], rk[3]));
     const int grid = nsm * 2;
-    for (int pass = 0; pass < 3; ++pass) {
-      FIBAR_LAUNCH(L, "sel_hist", k_sel_hist<<<grid, TPB, 0, s>>>(l, n, sel, pass));
-      FIBAR_LAUNCH(L, "sel_pick", k_sel_pick<<<1, 128, 0, s>>>(sel, pass));
-    }
+    for (int pass = 0; pass < 3; ++pass)
+      FIBAR_LAUNCH(L, "sel_hist", k_sel_hist<<<grid, TPB, 0, s>>>(l, n, sel, pass, g_lo, g_hi));
+  } else {
+    FIBAR_LAUNCH(L, "sel_bounds", k_sel_bounds<<<1, 1, 0, s>>>(sel, g_lo, g_hi, mode, fixed_bound));
   }
-  FIBAR_LAUNCH(L, "sel_bounds", k_sel_bounds<<<1, 1, 0, s>>>(sel, g_lo, g_hi, mode, fixed_bound));
   uint8_t *dst = out_mem == FIBAR_MEM_DEVICE ? out : frame;
   FIBAR_LAUNCH(L, "render_map", k_render_map<<<nsm * 4, TPB, 0, s>>>(l, n, sel, dst));
   CK(cudaGetLastError());
   if (out_mem != FIBAR_MEM_DEVICE) CK(cudaMemcpyAsync(out, frame, n, cudaMemcpyDeviceToHost, s));
   if (bounds || degenerate || out_mem != FIBAR_MEM_DEVICE) {
-    SelState h;
-    CK(cudaMemcpyAsync(&h, sel, sizeof(SelState), cudaMemcpyDeviceToHost, s));
+    struct {
+      double lo, hi;
+      int degenerate;
+    } h;
+    CK(cudaMemcpyAsync(&h, &sel->lo, sizeof(h), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (bounds) {
       bounds[0] = h.lo;
