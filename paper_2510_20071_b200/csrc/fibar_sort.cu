@@ -173,7 +173,10 @@ int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, u
     unsigned *ko = a_to_b ? k_b : k_a;
     unsigned *vo = a_to_b ? v_b : v_a;
     FIBAR_LAUNCH(L, "rs_hist", k_rs_hist<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, n_dev, shift, hist, nblocks));
-    scan_exclusive_large(L, hist, hist, nullptr, 256LL * nblocks, 256LL * nblocks, hist + 256LL * nblocks);
+    if (256LL * nblocks <= 1024 * 16)   // small sorts: one single-pass scan kernel instead of three
+      scan_exclusive_u32(L, hist, 256 * nblocks);
+    else
+      scan_exclusive_large(L, hist, hist, nullptr, 256LL * nblocks, 256LL * nblocks, hist + 256LL * nblocks);
     FIBAR_LAUNCH(L, "rs_scatter",
                  k_rs_scatter<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, vi, ko, vo, n_dev, shift, hist, nblocks));
   }
