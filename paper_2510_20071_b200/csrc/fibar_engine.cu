@@ -1426,15 +1426,26 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   unsigned p = FIBAR_NONE, okm = 0, pend = 0, runpos = FIBAR_NONE;
   unsigned val[9];
   bool exhausted = false;
+  // the warp draws 32 items at a time from the global ticket and hands them
+  // to its free lanes in order (one contended atomic per 32 items); every
+  // item below a lane's is taken, so the deadlock-freedom argument holds
+  unsigned wbase = 0, wused = 32;
   while (true) {
-    const unsigned want = __ballot_sync(0xffffffffu, p == FIBAR_NONE && !exhausted);
-    if (want) {
-      unsigned base = 0;
-      const int leader = __ffs(want) - 1;
-      if (lane == leader) base = atomicAdd(&x.bs->ticket, (unsigned)__popc(want));
-      base = __shfl_sync(0xffffffffu, base, leader);
-      if ((want >> lane) & 1) {
-        const unsigned q = base + __popc(want & ((1u << lane) - 1u));
+    unsigned want = __ballot_sync(0xffffffffu, p == FIBAR_NONE && !exhausted);
+    while (want) {
+      if (wused == 32) {
+        unsigned nb = 0;
+        if (lane == 0) nb = atomicAdd(&x.bs->ticket, 32u);
+        wbase = __shfl_sync(0xffffffffu, nb, 0);
+        wused = 0;
+      }
+      const unsigned take = min((unsigned)__popc(want), 32u - wused);
+      const unsigned rank = __popc(want & ((1u << lane) - 1u));
+      const bool mine = ((want >> lane) & 1) && rank < take;
+      const unsigned q = wbase + wused + rank;
+      wused += take;
+      want &= ~__ballot_sync(0xffffffffu, mine);
+      if (mine) {
         if (q >= npop) {
           exhausted = true;
         } else {
