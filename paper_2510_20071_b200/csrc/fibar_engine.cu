@@ -2430,8 +2430,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     // the blur stage overlaps the next batch's front end: one 256-thread block
     // per SM leaves the rest of each SM to the front end (measured: 1/SM gives
     // 10.2 ms per 10M config-2 events vs 11.2 at 2/SM and 12.6 serialised)
+    const int occ = per_sm;
     per_sm = std::min(per_sm, g->serial ? 4 : 1);
-    if (const char *v = getenv("FIBAR_BLUR_BLOCKS")) per_sm = std::min(per_sm, std::max(1, atoi(v)));
+    if (const char *v = getenv("FIBAR_BLUR_BLOCKS")) per_sm = std::min(occ, std::max(1, atoi(v)));
     g->blur_grid = g->nsm * std::max(1, per_sm);
     if (const char *v = getenv("FIBAR_BLUR_SLEEP")) g->blur_sleep = (unsigned)atoi(v);
     if (const char *v = getenv("FIBAR_GRAPHS")) g->graphs_on = atoi(v) != 0;
