@@ -136,6 +136,7 @@ __device__ __forceinline__ bool on_sensor(const Ctx &x, unsigned xx, unsigned yy
 __device__ __forceinline__ bool in_band(const Ctx &x, unsigned yy) { return yy - x.band_y0 < (unsigned)x.H; }
 
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
+  pdl_wait();
   __shared__ unsigned wsum[TPB / 32], woob[TPB / 32];
   const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
   unsigned cnt = 0, oob = 0;
@@ -169,6 +170,7 @@ __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
 }
 
 __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
+  pdl_wait();
   __shared__ unsigned wsum[TPB / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long E0 = x.st->E;
@@ -224,6 +226,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
 // ------------------------------------------------------------------ link ---
 
 __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
@@ -240,6 +243,7 @@ __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
 }
 
 __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
@@ -406,6 +410,7 @@ __device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, 
 // windows [max(s_start, a_c - L_i), a_c - 1], as deltas from the previous
 // chunk's window of the same candidate (one warp per chunk).
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
@@ -460,6 +465,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
 
 // chunk 1's left edges [s_start, s_1i) counted by the whole grid (y = candidate)
 __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
+  pdl_wait();
   __shared__ int red[2][TPB / 32];
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
@@ -498,6 +504,7 @@ __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
 // inclusive scan of the deltas over chunks, one CTA per candidate chain
 // (chains interleaved with stride `nc` in `anc`)
 __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) {
+  pdl_wait();
   constexpr int PER = 4;
   __shared__ int2 wt[33];
   const long long B = x.bs->B;
@@ -562,6 +569,7 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
 // candidate above the largest stable one is a start that collapses onto the
 // true trajectory within a handful of events, with few evictions.
 __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int c = blockIdx.x * TPB + threadIdx.x;
@@ -630,6 +638,7 @@ __device__ __forceinline__ long long fine_start(const Ctx &x, long long s0, long
 // deltas from the previous chunk's window of the same candidate (the start
 // may move either way); one warp per chunk
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
@@ -685,6 +694,7 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
 // entries (the first trims of a long start window) are counted by the whole
 // warp, 32 ring entries per step.
 __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int c = blockIdx.x * 128 + threadIdx.x;
@@ -856,6 +866,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
 // every boundary agrees; each round makes at least the first disagreeing
 // chunk exact.  Then publish the batch's final window state.
 __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
+  pdl_wait();
   __shared__ int n_bad;
   __shared__ long long red_lo[32], red_hi[32];
   const long long B = x.bs->B;
@@ -964,6 +975,7 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
 // order the reference blurs them, _kernels.py:152-189).  An entry is stale iff
 // its pixel has no later event up to the popping event.
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const long long E0 = x.bs->E0, s_start = x.bs->s_start;
   const unsigned npop = B > 0 ? x.S[B - 1] : 0u;
@@ -1008,6 +1020,7 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
 // sorted order and (filter ON) whether the event is evicted stale in this
 // batch -- the random loads the serial per-pixel replay would otherwise wait on.
 __global__ void __launch_bounds__(TPB) k_posinfo(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
@@ -1034,6 +1047,7 @@ constexpr int LONG_SEG = 512;    // segments longer than this go to k_temporal_l
 constexpr int MAX_LONG = 16384;
 
 __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
@@ -1081,6 +1095,7 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
 // the brightness assuming no blur (valid until the pixel's first blur in the
 // batch), and which blur each position builds on.
 __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
+  pdl_wait();
   const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
   if (i >= B) return;
@@ -1175,6 +1190,7 @@ constexpr int LONG_TPB = 256;      // lanes per long segment (one block)
 constexpr int LONG_PIECE = 64;     // minimum events per lane before more lanes join
 
 __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
+  pdl_wait();
   __shared__ float s_spb[LONG_TPB], s_slv[LONG_TPB], s_epb[LONG_TPB], s_elv[LONG_TPB];
   __shared__ unsigned s_last[LONG_TPB];
   __shared__ int s_bad;
@@ -1320,6 +1336,7 @@ __device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
 // first-run value) or, when a blur produced it, after that blur's flag.
 // Runs for all items in parallel, before any blur (no waiting).
 __global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x) {
+  pdl_wait();
   const BatchScalars b = load_bs(x);
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
   const unsigned p = blockIdx.x * TPB + threadIdx.x;
@@ -1420,6 +1437,7 @@ __device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars
 // open.  The blurred value is published (ready) before the
 // pixel's following run is rebuilt (mready).
 __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
+  pdl_wait();
   const BatchScalars b = load_bs(x);
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
   const int lane = threadIdx.x & 31;
@@ -1512,6 +1530,7 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
 // ------------------------------------------------------------------ final ---
 
 __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
+  pdl_wait();
   const BatchScalars b = load_bs(x);
   const long long npop = b.s_end - b.s_start;
   const long long total = b.B + npop;
@@ -1546,6 +1565,7 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
 }
 
 __global__ void k_batch_end(Ctx x) {
+  pdl_wait();
   DevState *s = x.st;
   const BatchState *bsp = x.bs;
   if (x.spatial && bsp->B > 0) {
@@ -1577,6 +1597,7 @@ __device__ void sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, do
 // picks the digits from the totals (and after the last pass, the bounds).
 __global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, long long n, SelState *sel, int pass,
                                                   double g_lo, double g_hi) {
+  pdl_wait();
   __shared__ unsigned h[4][2048];
   const int shift = pass == 0 ? 21 : (pass == 1 ? 10 : 0);
   const unsigned dmask = pass == 2 ? 1023u : 2047u;
@@ -1672,6 +1693,7 @@ __global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, l
 }
 
 __global__ void k_sel_init(SelState *sel, unsigned r0, unsigned r1, unsigned r2, unsigned r3) {
+  pdl_wait();
   for (int t = 0; t < 4; ++t) sel->prefix[t] = 0;
   sel->rank[0] = r0;
   sel->rank[1] = r1;
@@ -1698,6 +1720,7 @@ __device__ void sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, do
 }
 
 __global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound) {
+  pdl_wait();
   sel_bounds(sel, g_lo, g_hi, mode, fixed_bound);
 }
 
@@ -1705,6 +1728,7 @@ __global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, 
 // (pipeline.py:582-583); degenerate grids render mid-gray (pipeline.py:578-581)
 __global__ void __launch_bounds__(TPB) k_render_map(const float *__restrict__ l, long long n,
                                                      const SelState *__restrict__ sel, uint8_t *__restrict__ out) {
+  pdl_wait();
   const double lo = sel->lo, hi = sel->hi;
   const bool deg = sel->degenerate;
   const double scale = deg ? 0.0 : __ddiv_rn(255.0, __dsub_rn(hi, lo));
@@ -1734,6 +1758,7 @@ __global__ void __launch_bounds__(TPB) k_evf1_decode(const uint4 *__restrict__ r
                                                      uint16_t *__restrict__ yo, int8_t *__restrict__ po,
                                                      unsigned *__restrict__ dto, unsigned long long *__restrict__ bsum,
                                                      unsigned long long *__restrict__ first_bad) {
+  pdl_wait();
   __shared__ unsigned long long ws[TPB / 32];
   const long long i0 = ((long long)blockIdx.x * TPB + threadIdx.x) * EV_PER_THREAD;
   unsigned dt[2] = {0u, 0u};
@@ -1778,6 +1803,7 @@ __global__ void __launch_bounds__(TPB) k_evf1_decode(const uint4 *__restrict__ r
 
 // t = t_base + inclusive prefix sum of dt (numpy cumsum in uint64, then + t_base)
 __global__ void __launch_bounds__(1024) k_evf1_block_scan(unsigned long long *bsum, int nb, unsigned long long t_base) {
+  pdl_wait();
   // one CTA: exclusive scan of the block sums, seeded with t_base
   __shared__ unsigned long long carry;
   __shared__ unsigned long long wt[32];
@@ -1817,6 +1843,7 @@ __global__ void __launch_bounds__(1024) k_evf1_block_scan(unsigned long long *bs
 __global__ void __launch_bounds__(TPB) k_evf1_times(const unsigned *__restrict__ dt, long long nrec,
                                                     const unsigned long long *__restrict__ bofs,
                                                     unsigned long long *__restrict__ t) {
+  pdl_wait();
   __shared__ unsigned long long ws[TPB / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long i0 = ((long long)blockIdx.x * TPB + threadIdx.x) * EV_PER_THREAD;
@@ -1847,12 +1874,14 @@ __global__ void __launch_bounds__(TPB) k_evf1_times(const unsigned *__restrict__
 // --------------------------------------------------------- state export ---
 
 __global__ void k_active_counts(Ctx x, unsigned *cnt) {
+  pdl_wait();
   const long long s = x.st->s, E = x.st->E;
   for (long long k = s + (long long)blockIdx.x * TPB + threadIdx.x; k < E; k += (long long)gridDim.x * TPB)
     atomicAdd(&cnt[x.rkey[(unsigned long long)k & x.Rm]], 1u);
 }
 
 __global__ void k_tile_counts(Ctx x, const unsigned *cnt, unsigned *tcnt) {
+  pdl_wait();
   for (long long c = (long long)blockIdx.x * TPB + threadIdx.x; c < x.n_pix; c += (long long)gridDim.x * TPB) {
     if (cnt[c] == 0) continue;
     const unsigned xx = (unsigned)(c % x.W), yy = (unsigned)(c / x.W);
@@ -1861,6 +1890,7 @@ __global__ void k_tile_counts(Ctx x, const unsigned *cnt, unsigned *tcnt) {
 }
 
 __global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy) {
+  pdl_wait();
   const long long E = x.st->E;
   const long long qcap = x.n_pix + 1;
   for (long long t = (long long)blockIdx.x * TPB + threadIdx.x; t < qcap; t += (long long)gridDim.x * TPB) {
@@ -1877,6 +1907,7 @@ __global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy) {
 }
 
 __global__ void k_init_state(DevState *s, long long q0) {
+  pdl_wait();
   memset(s, 0, sizeof(DevState));
   s->geo = 1;
   s->q = q0;
@@ -1886,9 +1917,11 @@ __global__ void k_init_state(DevState *s, long long q0) {
 }
 
 __global__ void k_fill_ll(long long *p, long long n, long long v) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) p[i] = v;
 }
 __global__ void k_init_pt(PixRec *p0, PixRec *p1, long long *plast, long long n) {
+  pdl_wait();
   for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
     PixRec r;
     r.st = 0;
@@ -2089,12 +2122,12 @@ int init_state(fibar_engine *g) {
   join_blur(g);
   g->last_b = -1;
   g->b_used[0] = g->b_used[1] = false;
-  FIBAR_LAUNCH(g->L, "init", k_init_state<<<1, 1, 0, s>>>(g->st, g->q0));
+  fibar_launch(g->L, "init", k_init_state, 1, 1, 0, s, g->st, g->q0);
   CK(cudaMemsetAsync(g->pbar, 0, sizeof(float) * g->n_pix, s));
   CK(cudaMemsetAsync(g->l, 0, sizeof(float) * g->n_pix, s));
   if (g->spatial) {
-    FIBAR_LAUNCH(g->L, "init", k_init_pt<<<g->nsm * 4, TPB, 0, s>>>(g->pt2[0], g->pt2[1], g->plast, g->n_pix));
-    FIBAR_LAUNCH(g->L, "init", k_fill_ll<<<g->nsm * 4, TPB, 0, s>>>(g->last_tile, g->n_tiles, -1));
+    fibar_launch(g->L, "init", k_init_pt, g->nsm * 4, TPB, 0, s, g->pt2[0], g->pt2[1], g->plast, g->n_pix);
+    fibar_launch(g->L, "init", k_fill_ll, g->nsm * 4, TPB, 0, s, g->last_tile, g->n_tiles, -1);
     CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
     CK(cudaMemsetAsync(g->wcnt, 0, sizeof(unsigned) * g->n_pix, s));
     CK(cudaMemsetAsync(g->rnext, 0xFF, sizeof(uint2) * g->R, s));
@@ -2123,9 +2156,9 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   x.raw_x = rx0;
   x.raw_y = ry0;
   x.raw_p = rp0;
-  FIBAR_LAUNCH(L, "count_inb", k_count_inb<<<nb_in, TPB, 0, s>>>(x, nb_in));
+  fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
-  FIBAR_LAUNCH(L, "compact", k_compact<<<nb_in, TPB, 0, s>>>(x, nb_in));
+  fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
   const int where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B,
                                      n_raw, g->key_bits);
@@ -2142,23 +2175,23 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   const int nb = (int)((n_raw + TPB - 1) / TPB);
   if (g->spatial) {
     const int T = (int)((n_raw + g->chunk - 1) / g->chunk);
-    FIBAR_LAUNCH(L, "seg_marks", k_seg_marks<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "link", k_link<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "anchor", k_anchor<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "anchor_base", k_anchor_base<<<dim3(g->nsm / 2, NCAND), TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NCAND, 1024, 0, s>>>(x, g->anc, NCAND));
-    FIBAR_LAUNCH(L, "fp", k_fp<<<(T + TPB - 1) / TPB, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "anchor2", k_anchor2<<<(int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "anchor_scan", k_anchor_scan<<<NFINE, 1024, 0, s>>>(x, g->anc2, NFINE));
-    FIBAR_LAUNCH(L, "window_run", k_window_run<<<(T + 127) / 128, 128, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "window_fix", k_window_fix<<<1, 1024, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "popj", k_popj<<<(int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
+    fibar_launch(L, "seg_marks", k_seg_marks, nb, TPB, 0, s, x);
+    fibar_launch(L, "link", k_link, nb, TPB, 0, s, x);
+    fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
+    fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
+    fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND, 1024, 0, s, x, g->anc, NCAND);
+    fibar_launch(L, "fp", k_fp, (T + TPB - 1) / TPB, TPB, 0, s, x);
+    fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
+    fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
+    fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
+    fibar_launch(L, "window_fix", k_window_fix, 1, 1024, 0, s, x);
+    fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
+    fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
     // the replay reads the brightness the previous batch's blur stage finishes
     if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
-    FIBAR_LAUNCH(L, "temporal", k_temporal_runs<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 2, LONG_TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
+    fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
+    fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
+    fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
     // blur stage on its own stream: overlaps the next batch's front end
     cudaStream_t bs = (g->serial || graph) ? s : g->bstream;
     if (!graph) {
@@ -2168,10 +2201,10 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     L.stream = bs;
     if (g->blur_on) {
       const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
-      FIBAR_LAUNCH(L, "blur_prep", k_blur_prep<<<nbp, TPB, 0, bs>>>(x));
-      FIBAR_LAUNCH(L, "blur", k_blur<<<graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs>>>(x));
+      fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, bs, x);
+      fibar_launch(L, "blur", k_blur, graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs, x);
     }
-    FIBAR_LAUNCH(L, "final", k_final<<<g->nsm * 8, TPB, 0, bs>>>(x));
+    fibar_launch(L, "final", k_final, g->nsm * 8, TPB, 0, bs, x);
     L.stream = s;
     if (!graph) {
       CK(cudaEventRecord(g->evB[par], bs));
@@ -2179,10 +2212,10 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       g->last_b = par;
     }
   } else {
-    FIBAR_LAUNCH(L, "posinfo", k_posinfo<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "temporal", k_temporal<<<nb, TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "temporal_long", k_temporal_long<<<g->nsm * 2, LONG_TPB, 0, s>>>(x));
-    FIBAR_LAUNCH(L, "batch_end", k_batch_end<<<1, 1, 0, s>>>(x));
+    fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
+    fibar_launch(L, "temporal", k_temporal, nb, TPB, 0, s, x);
+    fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
+    fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
   }
   CK(cudaGetLastError());
   return 0;
@@ -2330,15 +2363,15 @@ int render_core(Launcher &L, const float *l, long long n, int32_t mode, double f
     }
     g_lo = gam[0];
     g_hi = gam[1];
-    FIBAR_LAUNCH(L, "sel_init", k_sel_init<<<1, 1, 0, s>>>(sel, rk[0], rk[1], rk[2], rk[3]));
+    fibar_launch(L, "sel_init", k_sel_init, 1, 1, 0, s, sel, rk[0], rk[1], rk[2], rk[3]);
     const int grid = nsm * 2;
     for (int pass = 0; pass < 3; ++pass)
-      FIBAR_LAUNCH(L, "sel_hist", k_sel_hist<<<grid, TPB, 0, s>>>(l, n, sel, pass, g_lo, g_hi));
+      fibar_launch(L, "sel_hist", k_sel_hist, grid, TPB, 0, s, l, n, sel, pass, g_lo, g_hi);
   } else {
-    FIBAR_LAUNCH(L, "sel_bounds", k_sel_bounds<<<1, 1, 0, s>>>(sel, g_lo, g_hi, mode, fixed_bound));
+    fibar_launch(L, "sel_bounds", k_sel_bounds, 1, 1, 0, s, sel, g_lo, g_hi, mode, fixed_bound);
   }
   uint8_t *dst = out_mem == FIBAR_MEM_DEVICE ? out : frame;
-  FIBAR_LAUNCH(L, "render_map", k_render_map<<<nsm * 4, TPB, 0, s>>>(l, n, sel, dst));
+  fibar_launch(L, "render_map", k_render_map, nsm * 4, TPB, 0, s, l, n, sel, dst);
   CK(cudaGetLastError());
   if (out_mem != FIBAR_MEM_DEVICE) CK(cudaMemcpyAsync(out, frame, n, cudaMemcpyDeviceToHost, s));
   if (bounds || degenerate || out_mem != FIBAR_MEM_DEVICE) {
@@ -2412,6 +2445,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   if (const char *v = getenv("FIBAR_WARM")) g->warm = std::max(0, atoi(v));
   if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
   if (const char *v = getenv("FIBAR_SERIAL")) g->serial = atoi(v) != 0;
+  if (const char *v = getenv("FIBAR_PDL")) g->L.pdl = atoi(v) != 0;
   {
     // contraction of the slower recurrence: events until any two float32
     // trajectories agree to the last bit, with a 1.6x margin
@@ -2774,9 +2808,9 @@ int fibar_read_state(fibar_engine *g, float *p_bar, float *l, uint16_t *active, 
     CK(cudaMemsetAsync(g->tcnt_tmp, 0, sizeof(unsigned) * g->n_tiles, s));
     Ctx x = g->ctx(nullptr, nullptr, 0, 0);
     if (g->spatial) {
-      FIBAR_LAUNCH(g->L, "state_active", k_active_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp));
-      FIBAR_LAUNCH(g->L, "state_tiles", k_tile_counts<<<g->nsm * 4, TPB, 0, s>>>(x, g->cnt_tmp, g->tcnt_tmp));
-      FIBAR_LAUNCH(g->L, "state_ring", k_ring_xy<<<g->nsm * 4, TPB, 0, s>>>(x, g->q_tmp, g->q_tmp + n + 1));
+      fibar_launch(g->L, "state_active", k_active_counts, g->nsm * 4, TPB, 0, s, x, g->cnt_tmp);
+      fibar_launch(g->L, "state_tiles", k_tile_counts, g->nsm * 4, TPB, 0, s, x, g->cnt_tmp, g->tcnt_tmp);
+      fibar_launch(g->L, "state_ring", k_ring_xy, g->nsm * 4, TPB, 0, s, x, g->q_tmp, g->q_tmp + n + 1);
     } else {
       CK(cudaMemsetAsync(g->q_tmp, 0, sizeof(uint16_t) * 2 * (n + 1), s));
     }

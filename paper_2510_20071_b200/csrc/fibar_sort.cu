@@ -20,6 +20,7 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const unsigned *__restrict__ keys,
                                                          const long long *__restrict__ n_dev, int shift,
                                                          unsigned *__restrict__ hist, int nblocks) {
+  pdl_wait();
   __shared__ unsigned h[256];
   const long long n = *n_dev;
   for (int i = threadIdx.x; i < 256; i += RS_THREADS) h[i] = 0;
@@ -37,6 +38,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_hist(const unsigned *__restri
 // exclusive scan of `len` counters in place with one CTA of 1024 threads,
 // 16 counters per thread per round (uint4 loads when aligned)
 __global__ void __launch_bounds__(1024) k_scan_inplace(unsigned *__restrict__ a, int len) {
+  pdl_wait();
   constexpr int PER = 16;
   __shared__ unsigned warp_tot[32];
   __shared__ unsigned carry_s;
@@ -107,6 +109,7 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const unsigned *__res
                                                             unsigned *__restrict__ kout, unsigned *__restrict__ vout,
                                                             const long long *__restrict__ n_dev, int shift,
                                                             const unsigned *__restrict__ hist, int nblocks) {
+  pdl_wait();
   __shared__ unsigned wcnt[RS_WARPS][256];
   const long long n = *n_dev;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -172,13 +175,12 @@ int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, u
     const unsigned *vi = ps == 0 ? nullptr : (a_to_b ? v_a : v_b);
     unsigned *ko = a_to_b ? k_b : k_a;
     unsigned *vo = a_to_b ? v_b : v_a;
-    FIBAR_LAUNCH(L, "rs_hist", k_rs_hist<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, n_dev, shift, hist, nblocks));
+    fibar_launch(L, "rs_hist", k_rs_hist, nblocks, RS_THREADS, 0, L.stream, ki, n_dev, shift, hist, nblocks);
     if (256LL * nblocks <= 1024 * 16)   // small sorts: one single-pass scan kernel instead of three
       scan_exclusive_u32(L, hist, 256 * nblocks);
     else
       scan_exclusive_large(L, hist, hist, nullptr, 256LL * nblocks, 256LL * nblocks, hist + 256LL * nblocks);
-    FIBAR_LAUNCH(L, "rs_scatter",
-                 k_rs_scatter<<<nblocks, RS_THREADS, 0, L.stream>>>(ki, vi, ko, vo, n_dev, shift, hist, nblocks));
+    fibar_launch(L, "rs_scatter", k_rs_scatter, nblocks, RS_THREADS, 0, L.stream, ki, vi, ko, vo, n_dev, shift, hist, nblocks);
   }
   return (passes % 2) == 1 ? 1 : 0;
 }
@@ -214,6 +216,7 @@ __device__ __forceinline__ unsigned block_excl_scan(unsigned v, unsigned *wsum, 
 
 __global__ void __launch_bounds__(SC_THREADS) k_scan_reduce(const unsigned *__restrict__ in, const long long *n_dev,
                                                             long long n_fixed, unsigned *__restrict__ part) {
+  pdl_wait();
   __shared__ unsigned wsum[SC_THREADS / 32 + 1];
   const long long n = n_dev ? *n_dev : n_fixed;
   const long long i0 = (long long)blockIdx.x * SC_TILE + threadIdx.x * SC_PER;
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(SC_THREADS) k_scan_reduce(const unsigned *__re
 __global__ void __launch_bounds__(SC_THREADS) k_scan_apply(const unsigned *__restrict__ in, unsigned *__restrict__ out,
                                                            const long long *n_dev, long long n_fixed,
                                                            const unsigned *__restrict__ part) {
+  pdl_wait();
   __shared__ unsigned wsum[SC_THREADS / 32 + 1];
   const long long n = n_dev ? *n_dev : n_fixed;
   const long long i0 = (long long)blockIdx.x * SC_TILE + threadIdx.x * SC_PER;
@@ -254,13 +258,13 @@ void scan_exclusive_large(Launcher &L, const unsigned *in, unsigned *out, const 
                           long long n_max, unsigned *part) {
   const int nb = (int)((n_max + SC_TILE - 1) / SC_TILE);
   if (nb == 0) return;
-  FIBAR_LAUNCH(L, "scan_reduce", k_scan_reduce<<<nb, SC_THREADS, 0, L.stream>>>(in, n_dev, n_fixed, part));
-  FIBAR_LAUNCH(L, "scan", k_scan_inplace<<<1, 1024, 0, L.stream>>>(part, nb));
-  FIBAR_LAUNCH(L, "scan_apply", k_scan_apply<<<nb, SC_THREADS, 0, L.stream>>>(in, out, n_dev, n_fixed, part));
+  fibar_launch(L, "scan_reduce", k_scan_reduce, nb, SC_THREADS, 0, L.stream, in, n_dev, n_fixed, part);
+  fibar_launch(L, "scan", k_scan_inplace, 1, 1024, 0, L.stream, part, nb);
+  fibar_launch(L, "scan_apply", k_scan_apply, nb, SC_THREADS, 0, L.stream, in, out, n_dev, n_fixed, part);
 }
 
 void scan_exclusive_u32(Launcher &L, unsigned *a, int len) {
-  FIBAR_LAUNCH(L, "scan", k_scan_inplace<<<1, 1024, 0, L.stream>>>(a, len));
+  fibar_launch(L, "scan", k_scan_inplace, 1, 1024, 0, L.stream, a, len);
 }
 
 }  // namespace fibar
