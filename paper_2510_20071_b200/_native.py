@@ -61,7 +61,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB_PATH
+    path = path or os.environ.get("FIBAR_LIB") or LIB_PATH   # FIBAR_LIB: an alternative build (experiments)
     if not os.path.exists(path):
         raise DeviceError(f"native library {path} not built; run __graft_entry__.build()")
     L = C.CDLL(path)

@@ -20,6 +20,7 @@ DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("fibar_common.cuh", "fibar
     os.path.join(HERE, "..", "include", "fibar_b200.h")]
 OUT = os.path.join(HERE, "_lib", "libfibar_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+EXTRA = [f"-D{d}" for d in os.environ.get("FIBAR_DEFINES", "").split(",") if d]
 
 
 def nvcc() -> str:
@@ -40,7 +41,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", *EXTRA, "-Xcompiler", "-fPIC", "-shared",
            "-I", os.path.join(HERE, "..", "include"), "-o", OUT + ".tmp", *SRC]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")

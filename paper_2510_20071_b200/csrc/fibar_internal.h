@@ -79,7 +79,12 @@ inline void fibar_launch(Launcher &L, const char *name, void (*kern)(KArgs...), 
 // first statement of every kernel launched by fibar_launch: wait until the
 // previous kernel on the stream has completed and its writes are visible
 // (a no-op for launches without the PDL attribute)
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef FIBAR_PDL_EARLY
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
 
 int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, unsigned *v_b, unsigned *hist,
                      const long long *n_dev, long long n_max, int bits);
