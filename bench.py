@@ -166,16 +166,15 @@ def kernel_bytes(name, B, P, D, n_pix):
 
 
 def committed_traffic(kernel: str, batch_cap: int, config: int):
-    """DRAM bytes per launch of `kernel` from the newest committed ncu --set full
-    capture (profiles/*_traffic.json, written by scripts/summarize_ncu.py from
+    """DRAM bytes per launch of `kernel` from the latest committed ncu --set full
+    capture (profiles/rNN*_traffic.json, latest round tag, written by scripts/summarize_ncu.py from
     `bench.py --profile-only`: config 2, 1M-event device batches); None for any
     other workload or batch size, or when no capture is committed."""
     import glob
     import json
     if batch_cap != 1 << 20 or config != 2:
         return None
-    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")),
-                   key=os.path.getmtime)
+    files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")))
     for f in reversed(files):
         try:
             v = json.load(open(f))["bytes_per_launch"].get(kernel)
