@@ -7,17 +7,23 @@
 //   link       k_seg_marks / k_link          per event: distance to previous same-pixel /
 //                                            same-tile event; per ring slot: distance to next
 //   window     k_anchor / k_anchor_scan /    the reference's FIFO window (_kernels.py:132-205)
-//              k_window_run / k_window_fix   reproduced exactly by chunked speculation +
-//                                            verification
+//              k_fp / k_anchor2 /            reproduced exactly by chunked speculation +
+//              k_window_run / k_window_fix   verification
 //   stale      k_popj                        eviction event of every popped entry; stale iff
 //                                            the pixel has no later event before its eviction
-//   temporal   k_temporal                    per-pixel in-order replay of the two-stage IIR
-//                                            (_kernels.py:62-73 / 120-130), bit exact
-//   blur       k_blur                        3x3 renormalised blur of stale pixels in eviction
+//   temporal   k_posinfo / k_temporal_runs / per-pixel in-order replay of the two-stage IIR
+//              k_temporal_long               (_kernels.py:62-73 / 120-130), bit exact;
+//                                            last-touch tables for the next batch
+//   blur       k_blur_prep / k_blur          3x3 renormalised blur of stale pixels in eviction
 //                                            order (_kernels.py:173-189), dataflow over a
-//                                            persistent grid with per-item ready flags
-//   final      k_final / k_batch_end         end-of-batch brightness, last-touch tables
+//                                            persistent grid polling (epoch | value) words
+//   final      k_final / k_batch_end         end-of-batch brightness, counters
+//   read-out   k_sel_init / k_sel_hist /     exact percentile select + float64 map
+//              k_render_map                  (pipeline.py:562-584)
 //
+// Filter ON, the blur stage of batch k runs on a second stream while batch k+1's
+// front end runs; small batches replay a captured CUDA graph
+// (4.6); consecutive kernels use programmatic dependent launch (pdl_wait()).
 // Float32 arithmetic uses __fmul_rn/__fadd_rn (never contracted to FMA) so the
 // result is bit-identical to the reference's strict-IEEE numba kernels.
 #include <cstdio>
