@@ -2264,23 +2264,36 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     cudaGraph_t graph = nullptr;
     const long long l0 = L.launches;
     if (!g->capstream) CK(cudaStreamCreateWithFlags(&g->capstream, cudaStreamNonBlocking));
-    CK(cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal));
-    L.stream = g->capstream;
-    int rc = enqueue_batch(g, g->gx, g->gy, g->gp, n_raw, nullptr, 0, true);
-    L.stream = s;
-    cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
+    cudaError_t ce = cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal);
+    int rc = 0;
+    if (ce == cudaSuccess) {
+      L.stream = g->capstream;
+      rc = enqueue_batch(g, g->gx, g->gy, g->gp, n_raw, nullptr, 0, true);
+      L.stream = s;
+      ce = cudaStreamEndCapture(g->capstream, &graph);
+    }
     if (rc) {
       if (graph) cudaGraphDestroy(graph);
       return rc;
     }
-    if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamEndCapture");
     GraphEntry ge;
     ge.n = n_raw;
     ge.kernels = L.launches - l0;
     L.launches = l0;
-    ce = cudaGraphInstantiate(&ge.exec, graph, 0);
-    cudaGraphDestroy(graph);
-    if (ce != cudaSuccess) return cuda_fail(ce, "cudaGraphInstantiate");
+    if (ce == cudaSuccess) {
+      ce = cudaGraphInstantiate(&ge.exec, graph, 0);
+      cudaGraphDestroy(graph);
+    }
+    if (ce != cudaSuccess) {
+      // capture not possible here (e.g. the calling thread is itself capturing
+      // in global mode): run the same serial schedule without a graph from now on
+      cudaGetLastError();
+      g->graphs_on = false;
+      rc = enqueue_batch(g, g->gx, g->gy, g->gp, n_raw, nullptr, 0, true);
+      if (rc) return rc;
+      g->batches++;
+      return 0;
+    }
     g->graphs.push_back(ge);
     hit = &g->graphs.back();
   }
