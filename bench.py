@@ -431,6 +431,30 @@ def cpu_reference(geom, params, ev, packet, steps=1):
     return times
 
 
+def host_info() -> dict:
+    """CPU model and host core count for the CPU-baseline lines."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_cores": os.cpu_count()}
+
+
+def pinned_one_core():
+    """Pin this process to one core for the single-threaded CPU baseline (as the
+    survey's taskset -c recipe); returns the previous affinity to restore."""
+    try:
+        prev = os.sched_getaffinity(0)
+        os.sched_setaffinity(0, {min(prev)})
+        return prev
+    except (AttributeError, OSError):
+        return None
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -440,9 +464,12 @@ def main():
         if rank != 0:
             return
         geom, params, ev, packet, name = workload(args, 0)
+        prev = pinned_one_core()
         for _ in range(args.warmup):
             cpu_reference(geom, params, ev.slice(0, min(len(ev), 1_000_000)), packet)
         times = cpu_reference(geom, params, ev, packet, steps=args.steps)
+        if prev:
+            os.sched_setaffinity(0, prev)
         v = len(ev) * args.steps / sum(times) / 1e6
         out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": sum(times) / len(times) * 1e3,
@@ -451,7 +478,8 @@ def main():
                "config": {"workload": name, "events_per_step": len(ev), "packet": packet},
                "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
                                 "sample": f"full workload ({len(ev)} events) x {args.steps} steps; C oracle "
-                                          "(oracle/fibar_oracle.c), single thread as the reference"},
+                                          "(oracle/fibar_oracle.c), single thread pinned to one core, as the "
+                                          "single-threaded reference", **host_info()},
                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(out))
         return
@@ -475,11 +503,15 @@ def main():
         return
     result, (geom, params, ev, packet) = res
     if rank == 0 and world == 1 and not args.no_cpu:
+        prev = pinned_one_core()
         times = cpu_reference(geom, params, ev, packet, steps=1)
+        if prev:
+            os.sched_setaffinity(0, prev)
         v = len(ev) / times[0] / 1e6
         result["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port",
-                                  "sample": f"full workload ({len(ev)} events, one pass) on one host core; "
-                                            "C oracle restating the reference's numba kernels"}
+                                  "sample": f"full workload ({len(ev)} events, one pass) pinned to one host "
+                                            "core; C oracle restating the reference's numba kernels",
+                                  **host_info()}
     if rank == 0:
         print(json.dumps(result))
     if dist:
