@@ -89,6 +89,7 @@ struct Ctx {
   unsigned band_y0, full_H;   // row band [band_y0, band_y0 + H) of a full_H-row sensor
   long long n_pix;
   long long num, den, qmin, qmax, every;
+  long long numA;   // num * A (tile area)
   float alpha, oma, beta, h;
   int use_gain, blur_on, spatial;
   DevState *st;
@@ -370,6 +371,20 @@ __device__ __forceinline__ long long floordiv_nn(long long N, long long D) {
 __device__ __forceinline__ long long regulate(const Ctx &x, long long len, long long np, long long nt) {
   const long long qn = floordiv_nn(len * x.num * nt * (long long)x.A, x.den * np);
   return qn < x.qmin ? x.qmin : (qn > x.qmax ? x.qmax : qn);
+}
+
+// the same for the serial window run's 32-bit state: (len * nt) as one wide
+// multiply, num * A folded on the host, an approximate float quotient (a few
+// units off at most below 2^24) fixed up exactly in integers
+__device__ __forceinline__ unsigned regulate32(const Ctx &x, unsigned len, unsigned np, unsigned nt) {
+  const unsigned long long N = (unsigned long long)len * nt * (unsigned long long)x.numA;
+  const unsigned long long D = (unsigned long long)x.den * np;
+  if ((unsigned long long)(x.qmax + 1) * D <= N) return (unsigned)x.qmax;   // clamps high anyway
+  long long q = (long long)__fdividef((float)N, (float)D);
+  q = q < 0 ? 0 : (q > x.qmax + 1 ? x.qmax + 1 : q);
+  while ((unsigned long long)q * D > N) --q;
+  while ((unsigned long long)(q + 1) * D <= N) ++q;
+  return (unsigned)(q < x.qmin ? x.qmin : (q > x.qmax ? x.qmax : q));
 }
 
 // The reference's per-event queue bookkeeping (_kernels.py:132-205) restated on
@@ -828,7 +843,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
       if (++ev >= every) {
         ev = 0;
         if (np >= 1 && nt >= 1) {
-          q = (unsigned)regulate(x, (long long)(jr - sr + 1), np, nt);
+          q = regulate32(x, jr - sr + 1, (unsigned)np, (unsigned)nt);
           if (jr >= br) {
             qlo32 = min(qlo32, q);
             qhi32 = max(qhi32, q);
@@ -2047,6 +2062,7 @@ struct fibar_engine {
     x.A = A;
     x.n_pix = n_pix;
     x.num = cfg.fill_num;
+    x.numA = cfg.fill_num * (long long)A;
     x.den = cfg.fill_den;
     x.qmin = cfg.q_min;
     x.qmax = cfg.q_max;

@@ -1,2 +1,2 @@
-# scratch runner for schedule experiments (edit freely): env knobs are read at engine creation
-timeout 600 python scripts/overlap_probe.py --reps 6 "FIBAR_SERIAL=0" "FIBAR_SERIAL=1" 2>&1
+timeout 300 python -m pytest tests -x -q -m gpu 2>&1 | tail -1
+timeout 600 python scripts/overlap_probe.py --reps 5 --profile "FIBAR_SERIAL=0" "FIBAR_SERIAL=1" 2>&1 | cut -c1-250
