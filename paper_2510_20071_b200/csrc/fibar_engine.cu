@@ -714,6 +714,8 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
 // events), warms up, then runs its own chunk.  Evictions of more than a few
 // entries (the first trims of a long start window) are counted by the whole
 // warp, 32 ring entries per step.
+constexpr unsigned WIN_SOLO = 384;   // evictions a lane counts alone (longer: the whole warp)
+
 __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   pdl_wait();
   const long long B = x.bs->B;
@@ -816,7 +818,12 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
       }
       sr = hi;
     }
-    unsigned m = __ballot_sync(0xffffffffu, big);
+    // a long eviction (the collapse of a too-long speculative start): up to
+    // WIN_SOLO entries each lane streams its own range with 8 loads in flight
+    // (all lanes at once); longer ones are counted by the whole warp, 32
+    // entries per step, one lane after another
+    const bool huge = hi - lo > WIN_SOLO;
+    unsigned m = __ballot_sync(0xffffffffu, huge);
     while (m) {
       const int L = __ffs(m) - 1;
       const unsigned l0 = __shfl_sync(0xffffffffu, lo, L);
@@ -838,6 +845,25 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
         sr = h0;
       }
       m &= m - 1;
+    }
+    if (big && !huge) {
+      int cp = 0, ct = 0;
+      for (unsigned k = lo; k < hi; k += 8) {
+        uint2 rr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rr[u] = k + u < hi ? x.rnext[(bslot + k + u) & rm] : make_uint2(0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (k + u >= hi) break;
+          const unsigned dd = jr - (k + u);
+          cp += rr[u].x > dd;
+          ct += rr[u].y > dd;
+        }
+      }
+      np -= cp;
+      nt -= ct;
+      sr = hi;
+      ++coop;
     }
     if (act) {
       if (++ev >= every) {
