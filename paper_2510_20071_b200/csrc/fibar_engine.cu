@@ -1469,11 +1469,25 @@ __global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x) {
 // including its next blurred event) is rebuilt from the blurred value
 __device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars &b, unsigned p, unsigned r,
                                                 float v) {
-  for (; r < b.B; ++r) {
-    if (x.posrec[r].runbase != p) break;
-    v = faddr(fmulr(x.beta, v), x.t2[r]);
-    x.posrec[r].val = v;
-    st_relaxed_u64(&x.mv64[r], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
+  // run positions and their terms are fetched four at a time, so a run costs
+  // one round trip per four positions instead of one per position
+  while (r < b.B) {
+    unsigned rb[4];
+    float tt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = r + u < b.B;
+      rb[u] = in ? x.posrec[r + u].runbase : FIBAR_NONE;
+      tt[u] = in ? x.t2[r + u] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (rb[u] != p) return;
+      v = faddr(fmulr(x.beta, v), tt[u]);
+      x.posrec[r + u].val = v;
+      st_relaxed_u64(&x.mv64[r + u], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
+    }
+    r += 4;
   }
 }
 
