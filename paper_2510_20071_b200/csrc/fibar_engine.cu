@@ -2052,7 +2052,6 @@ struct fibar_engine {
   uint8_t *frame = nullptr;
   unsigned *cnt_tmp = nullptr, *tcnt_tmp = nullptr;
   uint16_t *q_tmp = nullptr;
-  long long fill = 0;                       // unused (kept 0); host packets go through the pinned staging below
   // host packets: CPU copy into pinned staging set `cur`, one H2D per batch on
   // a copy stream into device staging set `cur`, double buffered so the copy
   // of batch k+1 overlaps the compute of batch k
@@ -2196,7 +2195,6 @@ int init_state(fibar_engine *g) {
     CK(cudaMemsetAsync(g->bv64, 0, sizeof(unsigned long long) * (g->Bcap + g->n_pix + 2), s));
     CK(cudaMemsetAsync(g->mv64, 0, sizeof(unsigned long long) * g->Bcap, s));
   }
-  g->fill = 0;
   g->zn = 0;
   g->hfill = 0;
   CK(cudaGetLastError());
