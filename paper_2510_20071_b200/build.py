@@ -15,8 +15,9 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("fibar_engine.cu", "fibar_sort.cu", "fibar_tools.cu")]
-DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("fibar_common.cuh", "fibar_internal.h")] + [
+SRC = [os.path.join(HERE, "csrc", f) for f in ("fibar_engine.cu", "fibar_front.cu", "fibar_stage.cu", "fibar_readout.cu", "fibar_sort.cu",
+                                                  "fibar_tools.cu")]
+DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("fibar_common.cuh", "fibar_internal.h", "fibar_kernels.cuh")] + [
     os.path.join(HERE, "..", "include", "fibar_b200.h")]
 OUT = os.path.join(HERE, "_lib", "libfibar_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -1,0 +1,942 @@
+// fibar_front.cu -- the front end of a device batch: ingest (OOB filter, compaction),
+// pixel/tile links, the exact window pass (speculation + verification) and the
+// eviction pass (stale items).  See fibar_engine.cu for the batch flow.
+#include "fibar_kernels.cuh"
+
+namespace fibar {
+
+static __constant__ long long c_fine_mul[NFINE] = {-8, -4, -2, -1, 0, 1, 2, 4, 8, 16};
+static __constant__ long long c_lin_off[NLIN] = {-16384, -4096, -1024, 0, 1024, 4096, 16384};
+static __constant__ double c_geo_mul[NGEO] = {0.25, 0.5, 0.75, 1.25, 1.5, 2.0, 2.5, 3.0, 4.0, 6.0, 8.0, 12.0};
+
+// ---------------------------------------------------------------- ingest ---
+
+
+// an event is kept iff it lies on the sensor (else it is out of bounds,
+// counted like pipeline.py:524-525) and in this engine's row band (a band
+// engine silently leaves other bands' events to their owners)
+__device__ __forceinline__ bool on_sensor(const Ctx &x, unsigned xx, unsigned yy) {
+  return xx < (unsigned)x.W && yy < x.full_H;
+}
+__device__ __forceinline__ bool in_band(const Ctx &x, unsigned yy) { return yy - x.band_y0 < (unsigned)x.H; }
+
+__global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
+  pdl_wait();
+  __shared__ unsigned wsum[TPB / 32], woob[TPB / 32];
+  const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
+  unsigned cnt = 0, oob = 0;
+#pragma unroll
+  for (int r = 0; r < IN_ITEMS; ++r) {
+    long long i = base + r;
+    if (i < x.n_raw) {
+      const unsigned xx = x.raw_x[i], yy = x.raw_y[i];
+      const bool ok = on_sensor(x, xx, yy);
+      oob += !ok;
+      cnt += ok && in_band(x, yy);
+    }
+  }
+  cnt = __reduce_add_sync(0xffffffffu, cnt);
+  oob = __reduce_add_sync(0xffffffffu, oob);
+  if ((threadIdx.x & 31) == 0) {
+    wsum[threadIdx.x >> 5] = cnt;
+    woob[threadIdx.x >> 5] = oob;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0, o = 0;
+    for (int w = 0; w < TPB / 32; ++w) {
+      t += wsum[w];
+      o += woob[w];
+    }
+    x.blockcnt[blockIdx.x] = t;
+    if (blockIdx.x == 0) x.blockcnt[nblocks] = 0;
+    if (o) atomicAdd((unsigned long long *)&x.st->oob, (unsigned long long)o);
+  }
+}
+
+__global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
+  pdl_wait();
+  __shared__ unsigned wsum[TPB / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long E0 = x.st->E;
+  const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
+  bool keep[IN_ITEMS];
+  unsigned cnt = 0;
+#pragma unroll
+  for (int r = 0; r < IN_ITEMS; ++r) {
+    long long i = base + r;
+    keep[r] = i < x.n_raw && on_sensor(x, x.raw_x[i], x.raw_y[i]) && in_band(x, x.raw_y[i]);
+    cnt += keep[r];
+  }
+  unsigned incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  unsigned wofs = 0;
+  for (int w = 0; w < wid; ++w) wofs += wsum[w];
+  unsigned pos = x.blockcnt[blockIdx.x] + wofs + incl - cnt;
+#pragma unroll
+  for (int r = 0; r < IN_ITEMS; ++r) {
+    if (!keep[r]) continue;
+    long long i = base + r;
+    const unsigned xx = x.raw_x[i], yy = x.raw_y[i] - x.band_y0;
+    const unsigned key = yy * (unsigned)x.W + xx;
+    const unsigned tile = (yy / x.ts) * (unsigned)x.tiles_x + xx / x.ts;
+    const unsigned sub = (yy % x.ts) * x.ts + xx % x.ts;
+    x.ekey[pos] = key;
+    x.tkey[pos] = tile * (unsigned)x.A + sub;
+    x.epol[pos] = x.raw_p[i];
+    if (x.spatial) x.rkey[(unsigned long long)(E0 + pos) & x.Rm] = key;
+    ++pos;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    DevState *s = x.st;
+    BatchState *b = x.bs;
+    b->E0 = s->E;
+    b->B = x.blockcnt[nblocks];
+    b->s_start = s->s;
+    b->npop = 0;
+    b->stale_batch = 0;
+    b->ticket = 0;
+    b->nlong = 0;
+    s->epoch += 1;
+    b->epoch = s->epoch;
+  }
+}
+
+// ------------------------------------------------------------------ link ---
+
+__global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned k = x.skey[i];
+  const unsigned jj = x.sidx[i];
+  const unsigned c = x.ekey[jj];
+  const bool head = i == 0 || x.skey[i - 1] != k;
+  const bool tail = i == B - 1 || x.skey[i + 1] != k;
+  if (head) x.pt[c].st = (unsigned)i;
+  if (tail) x.pt[c].end = (unsigned)(i + 1);
+  const unsigned t = k / x.A;
+  if (i == 0 || x.skey[i - 1] / x.A != t) x.ptt[t].x = (unsigned)i;
+  if (i == B - 1 || x.skey[i + 1] / x.A != t) x.ptt[t].y = (unsigned)(i + 1);
+}
+
+__global__ void __launch_bounds__(TPB) k_link(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const long long E0 = x.bs->E0;
+  const unsigned key = x.skey[i];
+  const unsigned jj = x.sidx[i];
+  const long long j = E0 + jj;
+  const unsigned c = x.ekey[jj];
+  const unsigned t = key / x.A;
+  const long long lo_ok = max(0LL, E0 + B - (long long)(x.Rm + 1));   // oldest index whose slot is not reused
+
+  // pixel links: neighbours in the sorted order
+  const bool first_pix = i == 0 || x.skey[i - 1] != key;
+  const bool last_pix = i == B - 1 || x.skey[i + 1] != key;
+  const long long pre_last = x.plast[c];
+  const long long prev_p = first_pix ? pre_last : E0 + x.sidx[i - 1];
+  const long long next_p = last_pix ? -1 : E0 + x.sidx[i + 1];
+
+  // tile links: latest earlier / earliest later event in the tile segment
+  const uint2 tr = x.ptt[t];
+  long long prev_t = -1, next_t = -1;
+  if (tr.y - tr.x <= 64) {
+    unsigned best_lo = 0, best_hi = 0xFFFFFFFFu;
+    bool have_lo = false;
+    for (unsigned q = tr.x; q < tr.y; ++q) {
+      unsigned o = x.sidx[q];
+      if (o < jj) {
+        if (!have_lo || o > best_lo) best_lo = o;
+        have_lo = true;
+      } else if (o > jj && o < best_hi) {
+        best_hi = o;
+      }
+    }
+    if (have_lo) prev_t = E0 + best_lo;
+    if (best_hi != 0xFFFFFFFFu) next_t = E0 + best_hi;
+  } else {
+    const int tx = (int)(t % (unsigned)x.tiles_x), ty = (int)(t / (unsigned)x.tiles_x);
+    for (int dy = 0; dy < x.ts; ++dy) {
+      const int yy = ty * x.ts + dy;
+      if (yy >= x.H) break;
+      for (int dx = 0; dx < x.ts; ++dx) {
+        const int xx = tx * x.ts + dx;
+        if (xx >= x.W) break;
+        const PixRec r = x.pt[(unsigned)yy * x.W + xx];
+        if (r.end <= r.st) continue;
+        // first position in [st, end) with sidx >= jj
+        unsigned lo = r.st, hi = r.end;
+        while (lo < hi) {
+          unsigned mid = (lo + hi) >> 1;
+          if (x.sidx[mid] < jj) lo = mid + 1; else hi = mid;
+        }
+        if (lo > r.st) prev_t = max(prev_t, E0 + (long long)x.sidx[lo - 1]);
+        unsigned up = (lo < r.end && x.sidx[lo] == jj) ? lo + 1 : lo;
+        if (up < r.end) {
+          long long cand = E0 + x.sidx[up];
+          next_t = next_t < 0 ? cand : min(next_t, cand);
+        }
+      }
+    }
+  }
+  const bool first_tile = prev_t < 0;
+  if (first_tile) prev_t = x.last_tile[t];
+
+  x.dp[jj] = make_uint2(dist32(j, prev_p), dist32(j, prev_t));
+  x.rnext[(unsigned long long)j & x.Rm] =
+      make_uint2(next_p < 0 ? FIBAR_INF32 : (unsigned)(next_p - j), next_t < 0 ? FIBAR_INF32 : (unsigned)(next_t - j));
+  if (first_pix) {
+    // the reference's active_count saturates at 65535, after which
+    // its count-based staleness departs from this exact restatement.  wcnt is
+    // the pixel's exact in-window event count at batch start; the count seen
+    // by its t-th event this batch is at most wcnt + t, so a batch can only
+    // reach the cap if wcnt + seglen > 65535 -- flag that (never misses).
+    const unsigned seglen = x.pt[c].end - (unsigned)i;
+    const unsigned wc = x.wcnt[c];
+    if ((unsigned long long)wc + seglen > 65535ull) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);
+    x.wcnt[c] = wc + seglen;
+  }
+  if (first_pix && pre_last >= lo_ok && pre_last >= 0) {
+    long long d = j - pre_last;
+    x.rnext[(unsigned long long)pre_last & x.Rm].x = d >= FIBAR_INF32 ? FIBAR_INF32 : (unsigned)d;
+  }
+  if (first_tile && prev_t >= lo_ok && prev_t >= 0) {
+    long long d = j - prev_t;
+    x.rnext[(unsigned long long)prev_t & x.Rm].y = d >= FIBAR_INF32 ? FIBAR_INF32 : (unsigned)d;
+  }
+}
+
+// ---------------------------------------------------------------- window ---
+
+struct WState {
+  long long s, q, npix, ntiles, evctr;
+};
+
+__device__ __forceinline__ long long chunk_warm_start(const Ctx &x, long long E0, int c) {
+  return max(E0, E0 + (long long)c * x.chunk - x.warm);
+}
+
+// coarse candidate i: a dense linear grid around the batch-start target q0
+// plus a geometric one that reaches windows far from it (cold start, scene change)
+__device__ __forceinline__ long long cand_len(const Ctx &x, long long q0, int i) {
+  long long L = i < NLIN ? q0 + c_lin_off[i] : (long long)((double)q0 * c_geo_mul[i - NLIN]);
+  return L < 1 ? 1 : (L > x.qmax ? x.qmax : L);
+}
+
+// floor(N / D) for N >= 0, D > 0: a float32 reciprocal estimate (relative
+// error ~1e-7, and the quotients here stay below 2^24) and an exact integer fix-up
+__device__ __forceinline__ long long floordiv_nn(long long N, long long D) {
+  long long q = (long long)__fmul_rn((float)N, __frcp_rn((float)D));
+  if (q * D > N) {
+    do { --q; } while (q * D > N);
+  } else {
+    while ((q + 1) * D <= N) ++q;
+  }
+  return q;
+}
+
+// integer fill-ratio regulation (_kernels.py:195-201)
+__device__ __forceinline__ long long regulate(const Ctx &x, long long len, long long np, long long nt) {
+  const long long qn = floordiv_nn(len * x.num * nt * (long long)x.A, x.den * np);
+  return qn < x.qmin ? x.qmin : (qn > x.qmax ? x.qmax : qn);
+}
+
+// the same for the serial window run's 32-bit state: (len * nt) as one wide
+// multiply, num * A folded on the host, an approximate float quotient (a few
+// units off at most below 2^24) fixed up exactly in integers
+__device__ __forceinline__ unsigned regulate32(const Ctx &x, unsigned len, unsigned np, unsigned nt) {
+  const unsigned long long N = (unsigned long long)len * nt * (unsigned long long)x.numA;
+  const unsigned long long D = (unsigned long long)x.den * np;
+  if ((unsigned long long)(x.qmax + 1) * D <= N) return (unsigned)x.qmax;   // clamps high anyway
+  long long q = (long long)__fdividef((float)N, (float)D);
+  q = q < 0 ? 0 : (q > x.qmax + 1 ? x.qmax + 1 : q);
+  while ((unsigned long long)q * D > N) --q;
+  while ((unsigned long long)(q + 1) * D <= N) ++q;
+  return (unsigned)(q < x.qmin ? x.qmin : (q > x.qmax ? x.qmax : q));
+}
+
+// The reference's per-event queue bookkeeping (_kernels.py:132-205) restated on
+// the suffix window [s, j]: the push of event j activates its pixel / tile iff
+// its previous same-pixel / same-tile event lies before s; the trim pops
+// [s, j+1-q) and each popped k deactivates iff its next occurrence lies after j.
+// Scalar form, used by the verifier's re-runs.
+__device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, long long E0, long long s_start,
+                           bool write, long long &qlo, long long &qhi) {
+  for (long long j = jf; j < jt; ++j) {
+    const uint2 d = x.dp[j - E0];
+    const unsigned long long js = (unsigned long long)(j - w.s);
+    w.npix += (unsigned long long)d.x > js;
+    w.ntiles += (unsigned long long)d.y > js;
+    long long len = j - w.s + 1;
+    if (len > w.q) {
+      const long long snew = j + 1 - w.q;
+      long long np = w.npix, nt = w.ntiles;
+      for (long long k = w.s; k < snew; ++k) {
+        const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+        const unsigned long long dd = (unsigned long long)(j - k);
+        np -= (unsigned long long)r.x > dd;
+        nt -= (unsigned long long)r.y > dd;
+      }
+      w.npix = np;
+      w.ntiles = nt;
+      w.s = snew;
+      len = w.q;
+    }
+    if (++w.evctr >= x.every) {
+      w.evctr = 0;
+      if (w.npix >= 1 && w.ntiles >= 1) {
+        const long long qn = regulate(x, len, w.npix, w.ntiles);
+        w.q = qn;
+        qlo = min(qlo, qn);
+        qhi = max(qhi, qn);
+      }
+    }
+    if (write) x.S[j - E0] = (unsigned)(w.s - s_start);
+  }
+}
+
+// Exact distinct-pixel / distinct-tile counts for every chunk's candidate
+// windows [max(s_start, a_c - L_i), a_c - 1], as deltas from the previous
+// chunk's window of the same candidate (one warp per chunk).
+__global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int lane = threadIdx.x & 31;
+  const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
+  if (c >= T) return;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
+  const int nc = x.st->geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
+  const long long a = chunk_warm_start(x, E0, c);
+  const long long Jc = a - 1;
+  const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
+  const long long Jp = ap - 1;
+  int cp[NCAND], ct[NCAND];
+  long long sp[NCAND];
+#pragma unroll
+  for (int i = 0; i < NCAND; ++i) {
+    cp[i] = 0;
+    ct[i] = 0;
+    sp[i] = c == 1 ? s0 : max(s0, ap - cand_len(x, q0, i));
+  }
+  // grow the right edge (Jp, Jc] with the previous starts
+  for (long long k = Jp + 1 + lane; k <= Jc; k += 32) {
+    const uint2 d = x.dp[k - E0];
+#pragma unroll
+    for (int i = 0; i < NCAND; ++i) {
+      if (i >= nc) break;
+      const unsigned long long ks = (unsigned long long)(k - sp[i]);
+      cp[i] += (unsigned long long)d.x > ks;
+      ct[i] += (unsigned long long)d.y > ks;
+    }
+  }
+  // shrink the left edge to the new starts (chunk 1's edges start at the batch's
+  // whole start window and can be long: k_anchor_base counts those grid-wide)
+#pragma unroll
+  for (int i = 0; i < NCAND; ++i) {
+    if (c == 1 || i >= nc) break;
+    const long long sn = max(s0, a - cand_len(x, q0, i));
+    for (long long k = sp[i] + lane; k < sn; k += 32) {
+      const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+      const unsigned long long dd = (unsigned long long)(Jc - k);
+      cp[i] -= (unsigned long long)r.x > dd;
+      ct[i] -= (unsigned long long)r.y > dd;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < NCAND; ++i) {
+    if (i >= nc) break;
+    const int vp = __reduce_add_sync(0xffffffffu, cp[i]);
+    const int vt = __reduce_add_sync(0xffffffffu, ct[i]);
+    if (lane == 0) x.anc[(long long)c * NCAND + i] = make_int2(vp, vt);
+  }
+}
+
+// chunk 1's left edges [s_start, s_1i) counted by the whole grid (y = candidate)
+__global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
+  pdl_wait();
+  __shared__ int red[2][TPB / 32];
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  if (T < 2) return;
+  const int i = blockIdx.y;
+  if (i >= (x.st->geo ? NCAND : NLIN)) return;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
+  const long long a = chunk_warm_start(x, E0, 1);
+  const long long Jc = a - 1;
+  const long long sn = max(s0, a - cand_len(x, q0, i));
+  int cp = 0, ct = 0;
+  for (long long k = s0 + (long long)blockIdx.x * TPB + threadIdx.x; k < sn; k += (long long)gridDim.x * TPB) {
+    const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+    const unsigned long long dd = (unsigned long long)(Jc - k);
+    cp += (unsigned long long)r.x > dd;
+    ct += (unsigned long long)r.y > dd;
+  }
+  cp = __reduce_add_sync(0xffffffffu, cp);
+  ct = __reduce_add_sync(0xffffffffu, ct);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = cp;
+    red[1][threadIdx.x >> 5] = ct;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int sp = 0, st = 0;
+    for (int w = 0; w < TPB / 32; ++w) {
+      sp += red[0][w];
+      st += red[1][w];
+    }
+    if (sp) atomicSub(&x.anc[NCAND + i].x, sp);
+    if (st) atomicSub(&x.anc[NCAND + i].y, st);
+  }
+}
+
+// inclusive scan of the deltas over chunks, one CTA per candidate chain
+// (chains interleaved with stride `nc` in `anc`)
+__global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) {
+  pdl_wait();
+  constexpr int PER = 4;
+  __shared__ int2 wt[33];
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int i = blockIdx.x;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int2 carry = make_int2((int)x.st->npix, (int)x.st->ntiles);
+  for (int base = 1; base < T; base += 1024 * PER) {
+    const int c0 = base + threadIdx.x * PER;
+    int2 v[PER];
+    int2 tsum = make_int2(0, 0);
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      v[r] = c0 + r < T ? anc[(long long)(c0 + r) * nc + i] : make_int2(0, 0);
+      tsum.x += v[r].x;
+      tsum.y += v[r].y;
+    }
+    int2 inc = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int tx = __shfl_up_sync(0xffffffffu, inc.x, o), ty = __shfl_up_sync(0xffffffffu, inc.y, o);
+      if (lane >= o) {
+        inc.x += tx;
+        inc.y += ty;
+      }
+    }
+    if (lane == 31) wt[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+      const int2 w = wt[lane];
+      int2 wi = w;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int tx = __shfl_up_sync(0xffffffffu, wi.x, o), ty = __shfl_up_sync(0xffffffffu, wi.y, o);
+        if (lane >= o) {
+          wi.x += tx;
+          wi.y += ty;
+        }
+      }
+      wt[lane] = make_int2(wi.x - w.x, wi.y - w.y);
+      if (lane == 31) wt[32] = wi;
+    }
+    __syncthreads();
+    int2 run = make_int2(carry.x + wt[wid].x + inc.x - tsum.x, carry.y + wt[wid].y + inc.y - tsum.y);
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      run.x += v[r].x;
+      run.y += v[r].y;
+      if (c0 + r < T) anc[(long long)(c0 + r) * nc + i] = run;
+    }
+    carry.x += wt[32].x;
+    carry.y += wt[32].y;
+    __syncthreads();
+  }
+}
+
+// Per chunk: locate the regulator's fixed point between the coarse candidate
+// windows (largest stable candidate, G(L) >= L, and the next, unstable one) by
+// linear interpolation of G(L) - L.  The fine candidates of pass 2 are centred
+// on it.  In steady state the true window sits within a few dozen events of
+// that fixed point and never far beyond it, so the first unstable fine
+// candidate above the largest stable one is a start that collapses onto the
+// true trajectory within a handful of events, with few evictions.
+__global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int c = blockIdx.x * TPB + threadIdx.x;
+  if (c >= T) return;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
+  const long long a = chunk_warm_start(x, E0, c);
+  if (c == 0 || a == E0) {
+    x.lc[c] = a - s0;
+    x.lu[c] = 32;
+    return;
+  }
+  const int nc = x.st->geo ? NCAND : NLIN;
+  long long lens[NCAND], fs[NCAND];
+#pragma unroll 1
+  for (int i = 0; i < nc; ++i) {
+    const long long len = a - max(s0, a - cand_len(x, q0, i));
+    const int2 cnt = x.anc[(long long)c * NCAND + i];
+    const long long f = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) - len : -1;
+    int k = i;   // insertion by length
+    while (k > 0 && lens[k - 1] > len) {
+      lens[k] = lens[k - 1];
+      fs[k] = fs[k - 1];
+      --k;
+    }
+    lens[k] = len;
+    fs[k] = f;
+  }
+  long long len_lo = -1, len_hi = -1, f_lo = 0, f_hi = 0;
+#pragma unroll 1
+  for (int i = 0; i < nc; ++i) {
+    if (fs[i] >= 0) {
+      len_lo = lens[i];
+      f_lo = fs[i];
+      len_hi = -1;
+    } else if (len_hi < 0 && lens[i] > len_lo) {
+      len_hi = lens[i];
+      f_hi = fs[i];
+    }
+  }
+  long long L, unit = 32;
+  if (len_lo < 0) {
+    L = lens[0];                         // even the shortest candidate is unstable
+  } else if (len_hi < 0) {
+    L = len_lo;                          // longest candidate stable (e.g. growth from s_start)
+  } else {
+    const double root = (double)len_lo + (double)(len_hi - len_lo) * (double)f_lo / (double)(f_lo - f_hi);
+    L = (long long)ceil(root);
+    unit = max(32LL, (len_hi - len_lo) / 64);
+  }
+  // the next batch keeps the linear candidates only while every fixed point
+  // stays well inside their span (windows clamped at the batch start excepted)
+  const bool clamped = len_lo >= 0 && len_hi < 0 && len_lo == a - s0;
+  if (!clamped && (L < q0 + c_lin_off[0] / 2 || L > q0 + c_lin_off[NLIN - 1] / 2)) x.st->geo_next = 1;
+  x.lc[c] = L;
+  x.lu[c] = unit;
+}
+
+__device__ __forceinline__ long long fine_start(const Ctx &x, long long s0, long long a, long long center,
+                                                long long unit, int j) {
+  long long L = center + c_fine_mul[j] * unit;
+  L = L < 1 ? 1 : (L > x.qmax ? x.qmax : L);
+  return max(s0, a - L);
+}
+
+// exact counts of every chunk's fine candidate windows [s_cj, a_c - 1], as
+// deltas from the previous chunk's window of the same candidate (the start
+// may move either way); one warp per chunk
+__global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int lane = threadIdx.x & 31;
+  const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
+  if (c >= T) return;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_start;
+  const long long ac = chunk_warm_start(x, E0, c);
+  const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
+  const long long Jc = ac - 1, Jp = ap - 1;
+  const long long lcc = x.lc[c], lcp = c == 1 ? 0 : x.lc[c - 1];
+  const long long luc = x.lu[c], lup = c == 1 ? 32 : x.lu[c - 1];
+  long long sp[NFINE];
+  int cp[NFINE], ct[NFINE];
+#pragma unroll
+  for (int j = 0; j < NFINE; ++j) {
+    sp[j] = c == 1 ? s0 : fine_start(x, s0, ap, lcp, lup, j);
+    cp[j] = 0;
+    ct[j] = 0;
+  }
+  for (long long k = Jp + 1 + lane; k <= Jc; k += 32) {
+    const uint2 d = x.dp[k - E0];
+#pragma unroll
+    for (int j = 0; j < NFINE; ++j) {
+      const unsigned long long ks = (unsigned long long)(k - sp[j]);
+      cp[j] += (unsigned long long)d.x > ks;
+      ct[j] += (unsigned long long)d.y > ks;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NFINE; ++j) {
+    const long long sn = fine_start(x, s0, ac, lcc, luc, j);
+    const int sgn = sn >= sp[j] ? -1 : 1;
+    const long long lo = min(sp[j], sn), hi = max(sp[j], sn);
+    for (long long k = lo + lane; k < hi; k += 32) {
+      const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
+      const unsigned long long dd = (unsigned long long)(Jc - k);
+      cp[j] += sgn * (int)((unsigned long long)r.x > dd);
+      ct[j] += sgn * (int)((unsigned long long)r.y > dd);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NFINE; ++j) {
+    const int vp = __reduce_add_sync(0xffffffffu, cp[j]);
+    const int vt = __reduce_add_sync(0xffffffffu, ct[j]);
+    if (lane == 0) x.anc2[(long long)c * NFINE + j] = make_int2(vp, vt);
+  }
+}
+
+// One lane per chunk, the warp stepping its lanes' events in lockstep.  Each
+// lane starts from the longest candidate window just past the regulator's
+// fixed point (a too-long window collapses to the true one within a few
+// events), warms up, then runs its own chunk.  Evictions of more than a few
+// entries (the first trims of a long start window) are counted by the whole
+// warp, 32 ring entries per step.
+
+__global__ void __launch_bounds__(128) k_window_run(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int c = blockIdx.x * 128 + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  if ((blockIdx.x * 128 + (threadIdx.x & ~31)) >= T) return;   // whole warp out of range
+  const bool valid = c < T;
+  const DevState s = *x.st;
+  const long long E0 = x.bs->E0;
+  const long long s_start0 = x.bs->s_start;
+  const long long b = E0 + (long long)c * x.chunk;
+  const long long e = valid ? min(E0 + B, b + x.chunk) : b;
+  const long long a = valid ? chunk_warm_start(x, E0, c) : b;
+  WState w{0, 1, 0, 0, 0};
+  if (valid) {
+    if (a == E0) {
+      w.s = s_start0;
+      w.q = s.q;
+      w.npix = s.npix;
+      w.ntiles = s.ntiles;
+      w.evctr = s.evctr;
+    } else {
+      const long long center = x.lc[c], unit = x.lu[c];
+      int jstar = -1;
+#pragma unroll 1
+      for (int j = 0; j < NFINE; ++j) {
+        const long long sc = fine_start(x, s_start0, a, center, unit, j);
+        const int2 cnt = x.anc2[(long long)c * NFINE + j];
+        const long long len = a - sc;
+        if (cnt.x >= 1 && cnt.y >= 1 && regulate(x, len, cnt.x, cnt.y) >= len) jstar = j;
+      }
+      const int g = jstar + 1 < NFINE ? jstar + 1 : NFINE - 1;
+      const int2 cnt = x.anc2[(long long)c * NFINE + g];
+      w.s = fine_start(x, s_start0, a, center, unit, g);
+      w.npix = cnt.x;
+      w.ntiles = cnt.y;
+      const long long len = a - w.s;
+      w.q = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) : len;
+      if (x.debug) {
+        long long bn = 0, bt = 0;
+        for (long long k = w.s; k < a; ++k) {
+          const uint2 rr = x.rnext[(unsigned long long)k & x.Rm];
+          bn += (unsigned long long)rr.x > (unsigned long long)(a - 1 - k);
+          bt += (unsigned long long)rr.y > (unsigned long long)(a - 1 - k);
+        }
+        if (bn != w.npix || bt != w.ntiles) atomicAdd((unsigned long long *)&x.st->dbg_bad, 1ull);
+      }
+      w.evctr = (s.evctr + (a - E0)) % x.every;
+    }
+  }
+  ChunkRec r;
+  r.st_s = w.s;
+  r.st_q = w.q;
+  long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
+  long long wpops = 0, coop = 0;
+  const unsigned n_my = (unsigned)(e - a);
+  const unsigned n_max = __reduce_max_sync(0xffffffffu, n_my);
+  // 32-bit state relative to the batch's start window (every index in play is
+  // within B + window of it); ring slots as (slot of s_start + offset) & Rm
+  const long long base = s_start0;
+  const unsigned bslot = (unsigned)((unsigned long long)base & x.Rm);
+  const unsigned rm = (unsigned)x.Rm;
+  unsigned sr = (unsigned)(w.s - base);
+  const unsigned ar = (unsigned)(a - base), br = (unsigned)(b - base);
+  const unsigned e0r = (unsigned)(E0 - base);
+  unsigned q = (unsigned)w.q;
+  int np = (int)w.npix, nt = (int)w.ntiles;
+  unsigned ev = (unsigned)w.evctr;
+  const unsigned every = (unsigned)x.every;
+  unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0;
+  uint2 dnext = n_my > 0 ? x.dp[ar - e0r] : make_uint2(0, 0);
+  for (unsigned t = 0; t < n_max; ++t) {
+    const bool act = t < n_my;
+    const unsigned jr = ar + t;
+    if (act && jr == br) {
+      r.st_s = base + sr;
+      r.st_q = q;
+    }
+    unsigned lo = 0, hi = 0;
+    if (act) {
+      const uint2 d = dnext;
+      if (t + 1 < n_my) dnext = x.dp[jr + 1 - e0r];
+      const unsigned js = jr - sr;
+      np += d.x > js;
+      nt += d.y > js;
+      if (js + 1 > q) {
+        lo = sr;
+        hi = jr + 1 - q;
+      }
+    }
+    const bool big = hi - lo > 8;
+    if (jr < br) wpops += hi - lo;
+    if (!big && hi > lo) {
+      for (unsigned k = lo; k < hi; ++k) {
+        const uint2 rr = x.rnext[(bslot + k) & rm];
+        const unsigned dd = jr - k;
+        np -= rr.x > dd;
+        nt -= rr.y > dd;
+      }
+      sr = hi;
+    }
+    // a long eviction (the collapse of a too-long speculative start): up to
+    // WIN_SOLO entries each lane streams its own range with 8 loads in flight
+    // (all lanes at once); longer ones are counted by the whole warp, 32
+    // entries per step, one lane after another
+    const bool huge = hi - lo > WIN_SOLO;
+    unsigned m = __ballot_sync(0xffffffffu, huge);
+    while (m) {
+      const int L = __ffs(m) - 1;
+      const unsigned l0 = __shfl_sync(0xffffffffu, lo, L);
+      const unsigned h0 = __shfl_sync(0xffffffffu, hi, L);
+      const unsigned jL = __shfl_sync(0xffffffffu, jr, L);
+      int cp = 0, ct = 0;
+      for (unsigned k = l0 + lane; k < h0; k += 32) {
+        const uint2 rr = x.rnext[(bslot + k) & rm];
+        const unsigned dd = jL - k;
+        cp += rr.x > dd;
+        ct += rr.y > dd;
+      }
+      cp = __reduce_add_sync(0xffffffffu, cp);
+      ct = __reduce_add_sync(0xffffffffu, ct);
+      ++coop;
+      if (lane == L) {
+        np -= cp;
+        nt -= ct;
+        sr = h0;
+      }
+      m &= m - 1;
+    }
+    if (big && !huge) {
+      int cp = 0, ct = 0;
+      for (unsigned k = lo; k < hi; k += 8) {
+        uint2 rr[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) rr[u] = k + u < hi ? x.rnext[(bslot + k + u) & rm] : make_uint2(0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (k + u >= hi) break;
+          const unsigned dd = jr - (k + u);
+          cp += rr[u].x > dd;
+          ct += rr[u].y > dd;
+        }
+      }
+      np -= cp;
+      nt -= ct;
+      sr = hi;
+      ++coop;
+    }
+    if (act) {
+      if (++ev >= every) {
+        ev = 0;
+        if (np >= 1 && nt >= 1) {
+          q = regulate32(x, jr - sr + 1, (unsigned)np, (unsigned)nt);
+          if (jr >= br) {
+            qlo32 = min(qlo32, q);
+            qhi32 = max(qhi32, q);
+          }
+        }
+      }
+      if (jr >= br) x.S[jr - e0r] = sr;
+    }
+  }
+  w.s = base + sr;
+  w.q = q;
+  w.npix = np;
+  w.ntiles = nt;
+  w.evctr = ev;
+  if (qhi32 > 0) {
+    qlo = qlo32;
+    qhi = qhi32;
+  }
+  {
+    const unsigned long long wp = __reduce_add_sync(0xffffffffu, (unsigned)wpops);
+    if (lane == 0) {
+      atomicAdd((unsigned long long *)&x.st->warm_pops, wp);
+      atomicAdd((unsigned long long *)&x.st->coop_iters, (unsigned long long)coop);
+    }
+  }
+  if (!valid) return;
+  r.en_s = w.s;
+  r.en_q = w.q;
+  r.en_np = w.npix;
+  r.en_nt = w.ntiles;
+  r.en_ev = w.evctr;
+  r.qlo = qlo;
+  r.qhi = qhi;
+  x.ch[c] = r;
+}
+
+// Verify chunk boundaries: a chunk is exact once its speculative start state
+// equals its predecessor's end state and the predecessor is exact.  Rounds
+// re-run, in parallel, every chunk whose start disagrees with its
+// predecessor's current end (read before the round writes anything), until
+// every boundary agrees; each round makes at least the first disagreeing
+// chunk exact.  Then publish the batch's final window state.
+__global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
+  pdl_wait();
+  __shared__ int n_bad;
+  __shared__ long long red_lo[32], red_hi[32];
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
+  int rounds = 0, reruns = 0;
+  while (true) {
+    if (threadIdx.x == 0) n_bad = 0;
+    __syncthreads();
+    // each thread owns chunks threadIdx.x + 1024*i; snapshot predecessors first
+    constexpr int MAXC = 64;
+    int mine[MAXC];
+    ChunkRec pre[1];
+    int nm = 0;
+    for (int c = 1 + threadIdx.x; c < T && nm < MAXC; c += 1024) {
+      const ChunkRec &p = x.ch[c - 1];
+      const ChunkRec &q = x.ch[c];
+      if (q.st_s != p.en_s || q.st_q != p.en_q) mine[nm++] = c;
+    }
+    if (nm) atomicAdd(&n_bad, nm);
+    __syncthreads();
+    if (n_bad == 0) break;
+    // read every rerun's start state before any write of this round
+    long long ss[MAXC], sq[MAXC], snp[MAXC], snt[MAXC], sev[MAXC];
+    (void)pre;
+    for (int i = 0; i < nm; ++i) {
+      const ChunkRec &p = x.ch[mine[i] - 1];
+      ss[i] = p.en_s;
+      sq[i] = p.en_q;
+      snp[i] = p.en_np;
+      snt[i] = p.en_nt;
+      sev[i] = p.en_ev;
+    }
+    __syncthreads();
+    for (int i = 0; i < nm; ++i) {
+      const int m = mine[i];
+      WState w{ss[i], sq[i], snp[i], snt[i], sev[i]};
+      long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
+      const long long b = E0 + (long long)m * x.chunk;
+      const long long e = min(E0 + B, b + x.chunk);
+      run_window(x, w, b, e, E0, s_start, true, qlo, qhi);
+      ChunkRec r;
+      r.st_s = ss[i];
+      r.st_q = sq[i];
+      r.en_s = w.s;
+      r.en_q = w.q;
+      r.en_np = w.npix;
+      r.en_nt = w.ntiles;
+      r.en_ev = w.evctr;
+      r.qlo = qlo;
+      r.qhi = qhi;
+      x.ch[m] = r;
+    }
+    reruns += nm;
+    ++rounds;
+    __threadfence_block();
+    __syncthreads();
+  }
+  long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
+  for (int c = threadIdx.x; c < T; c += 1024) {
+    lo = min(lo, x.ch[c].qlo);
+    hi = max(hi, x.ch[c].qhi);
+  }
+  int rr = __reduce_add_sync(0xffffffffu, reruns);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red_lo[threadIdx.x >> 5] = lo;
+    red_hi[threadIdx.x >> 5] = hi;
+    if (rr) atomicAdd((unsigned long long *)&x.st->mismatch, (unsigned long long)rr);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < 32; ++w) {
+      lo = min(lo, red_lo[w]);
+      hi = max(hi, red_hi[w]);
+    }
+    DevState *s = x.st;
+    if (T > 0) {
+      const ChunkRec &r = x.ch[T - 1];
+      s->s = r.en_s;
+      s->q = r.en_q;
+      s->npix = r.en_np;
+      s->ntiles = r.en_nt;
+      s->evctr = r.en_ev;
+      if (hi >= 0) {
+        s->qtmin = min(s->qtmin, lo);
+        s->qtmax = max(s->qtmax, hi);
+      }
+      s->pops += r.en_s - s_start;
+      x.bs->npop = r.en_s - s_start;
+    } else {
+      x.bs->npop = 0;
+    }
+    s->chunks += T;
+    s->fix_rounds += rounds;
+  }
+}
+
+// ----------------------------------------------------------------- stale ---
+
+// Every window entry popped in this batch becomes an item, in pop order (the
+// order the reference blurs them, _kernels.py:152-189).  An entry is stale iff
+// its pixel has no later event up to the popping event.
+__global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
+  const unsigned npop = B > 0 ? x.S[B - 1] : 0u;
+  const unsigned p = blockIdx.x * TPB + threadIdx.x;   // one thread per eviction (balanced)
+  unsigned nst = 0;
+  if (p < npop) {
+    // popping event: the first jj with S[jj] > p (S is non-decreasing)
+    unsigned lo = 0, hi = (unsigned)B - 1;
+    while (lo < hi) {
+      const unsigned mid = (lo + hi) >> 1;
+      if (__ldg(&x.S[mid]) > p) hi = mid; else lo = mid + 1;
+    }
+    const long long k = s_start + p;
+    const long long j = E0 + lo;
+    const bool stale = (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);
+    const unsigned c = x.rkey[(unsigned long long)k & x.Rm];
+    atomicSub(&x.wcnt[c], 1u);   // the entry leaves the window (H7 bookkeeping)
+    Item it;
+    it.jrel = lo;
+    it.pix = FIBAR_NONE;
+    it.runpos = FIBAR_NONE;
+    it.pad = 0;
+    if (stale) {
+      it.pix = c;
+      if (k < E0) {
+        x.pt[c].carried = p;
+        // no event of the pixel in this batch after its pre-batch last one
+        if ((unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(E0 + B - 1 - k))
+          it.pad |= ITEM_CARRIED_ONLY;
+      }
+      ++nst;
+    }
+    x.item[p] = it;
+  }
+  nst = __reduce_add_sync(0xffffffffu, nst);
+  if ((threadIdx.x & 31) == 0 && nst) atomicAdd((unsigned long long *)&x.bs->stale_batch, (unsigned long long)nst);
+}
+
+
+}  // namespace fibar

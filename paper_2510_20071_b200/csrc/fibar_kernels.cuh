@@ -1,0 +1,149 @@
+// fibar_kernels.cuh -- what the engine's translation units share: constants,
+// the per-launch context (Ctx), small device helpers and the kernel
+// declarations (definitions: fibar_front.cu, fibar_stage.cu, fibar_readout.cu).
+#pragma once
+#include <cstdint>
+#include "fibar_common.cuh"
+#include "fibar_internal.h"
+#include "../../include/fibar_b200.h"
+
+namespace fibar {
+
+constexpr int NFINE = 10;     // fine candidate windows around the interpolated fixed point
+constexpr int CHUNK_MIN = 32;  // smallest speculative window chunk (sizes the chunk arrays)
+constexpr int NLIN = 7;      // coarse candidates q0 + c_lin_off[i]
+constexpr int NGEO = 12;     // coarse candidates q0 * c_geo_mul[i]
+constexpr int NCAND = NLIN + NGEO;
+constexpr int TPB = 256;
+constexpr unsigned ITEM_CARRIED_ONLY = 1u;   // Item.pad flag
+constexpr int IN_ITEMS = 8;
+constexpr int IN_TILE = TPB * IN_ITEMS;
+constexpr unsigned WIN_SOLO = 384;   // evictions a lane counts alone (longer: the whole warp)
+constexpr int GROUP = 8;
+constexpr int LONG_SEG = 512;    // segments longer than this go to k_temporal_long
+constexpr int MAX_LONG = 16384;
+constexpr int LONG_TPB = 256;      // lanes per long segment (one block)
+constexpr int LONG_PIECE = 64;     // minimum events per lane before more lanes join
+constexpr int EV_PER_THREAD = 2;
+constexpr int EV_TILE = TPB * EV_PER_THREAD;
+
+struct ChunkRec {
+  long long st_s, st_q;                          // state after event b_c - 1 (speculative start)
+  long long en_s, en_q, en_np, en_nt, en_ev;     // state after the chunk's last event
+  long long qlo, qhi;                            // extrema of the targets set inside the chunk
+};
+
+struct SelState {
+  unsigned prefix[4];
+  unsigned rank[4];
+  unsigned hist[4][2048];
+  double lo, hi;
+  int degenerate;
+  unsigned done;   // blocks finished with the current histogram pass
+};
+
+struct Ctx {
+  int W, H, ts, tiles_x, A;
+  unsigned band_y0, full_H;   // row band [band_y0, band_y0 + H) of a full_H-row sensor
+  long long n_pix;
+  long long num, den, qmin, qmax, every;
+  long long numA;   // num * A (tile area)
+  float alpha, oma, beta, h;
+  int use_gain, blur_on, spatial;
+  DevState *st;
+  BatchState *bs;     // this batch's scalars (parity buffer)
+  long long *plast;   // per pixel: last event index before the batch
+  unsigned *wcnt;     // per pixel: exact in-window event count (saturation check)
+  float *pbar, *l;
+  const float *gain;
+  PixRec *pt;
+  long long *last_tile;
+  uint2 *ptt;
+  unsigned *rkey;
+  uint2 *rnext;
+  unsigned long long Rm;
+  const uint16_t *raw_x, *raw_y;
+  const int8_t *raw_p;
+  long long n_raw;
+  unsigned *blockcnt;
+  unsigned *ekey;
+  int8_t *epol, *spol;
+  uint2 *longseg;
+  unsigned *tkey;                 // unsorted tile-major keys (sort input)
+  const unsigned *skey, *sidx;    // sorted keys / batch-local event index
+  uint2 *dp;
+  unsigned *S;
+  Item *item;
+  PosRec *posrec;
+  float *t2;
+  unsigned long long *bv64, *mv64;   // (epoch << 32 | float bits) per blur item / per sorted position
+  BlurPrep *prep;
+  int chunk, warm, debug;
+  int twarm;                  // warm-up events of a speculative long-segment piece
+  unsigned blur_sleep;
+  unsigned long long *dbg_t, *dbg_g;
+  int2 *anc, *anc2;
+  long long *lc, *lu;
+  ChunkRec *ch;
+};
+
+struct BatchScalars {
+  long long E0, B, s_start, s_end;
+  unsigned epoch;
+};
+
+__device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
+  BatchScalars b;
+  b.E0 = x.bs->E0;
+  b.B = x.bs->B;
+  b.s_start = x.bs->s_start;
+  b.s_end = b.s_start + x.bs->npop;
+  b.epoch = x.bs->epoch;
+  return b;
+}
+
+__device__ __forceinline__ unsigned order_key(float f) {
+  const unsigned u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float order_unkey(unsigned k) {
+  const unsigned u = (k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k;
+  return __uint_as_float(u);
+}
+
+// kernels (launched by fibar_engine.cu)
+__global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks);
+__global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
+__global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x);
+__global__ void __launch_bounds__(TPB) k_link(Ctx x);
+__global__ void __launch_bounds__(TPB) k_anchor(Ctx x);
+__global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x);
+__global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc);
+__global__ void __launch_bounds__(TPB) k_fp(Ctx x);
+__global__ void __launch_bounds__(TPB) k_anchor2(Ctx x);
+__global__ void __launch_bounds__(128) k_window_run(Ctx x);
+__global__ void __launch_bounds__(1024) k_window_fix(Ctx x);
+__global__ void __launch_bounds__(TPB) k_popj(Ctx x);
+__global__ void __launch_bounds__(TPB) k_posinfo(Ctx x);
+__global__ void __launch_bounds__(TPB) k_temporal(Ctx x);
+__global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x);
+__global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x);
+__global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x);
+__global__ void __launch_bounds__(TPB) k_blur(Ctx x);
+__global__ void __launch_bounds__(TPB) k_final(Ctx x);
+__global__ void k_batch_end(Ctx x);
+__global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, long long n, SelState *sel, int pass, double g_lo, double g_hi);
+__global__ void k_sel_init(SelState *sel, unsigned r0, unsigned r1, unsigned r2, unsigned r3);
+__global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound);
+__global__ void __launch_bounds__(TPB) k_render_map(const float *__restrict__ l, long long n, const SelState *__restrict__ sel, uint8_t *__restrict__ out);
+__global__ void __launch_bounds__(TPB) k_evf1_decode(const uint4 *__restrict__ rec2, const uint2 *__restrict__ rec1, long long nrec, int W, int H, uint16_t *__restrict__ xo, uint16_t *__restrict__ yo, int8_t *__restrict__ po, unsigned *__restrict__ dto, unsigned long long *__restrict__ bsum, unsigned long long *__restrict__ first_bad);
+__global__ void __launch_bounds__(1024) k_evf1_block_scan(unsigned long long *bsum, int nb, unsigned long long t_base);
+__global__ void __launch_bounds__(TPB) k_evf1_times(const unsigned *__restrict__ dt, long long nrec, const unsigned long long *__restrict__ bofs, unsigned long long *__restrict__ t);
+__global__ void k_active_counts(Ctx x, unsigned *cnt);
+__global__ void k_tile_counts(Ctx x, const unsigned *cnt, unsigned *tcnt);
+__global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy);
+__global__ void k_init_state(DevState *s, long long q0);
+__global__ void k_fill_ll(long long *p, long long n, long long v);
+__global__ void k_init_pt(PixRec *p0, PixRec *p1, long long *plast, long long n);
+
+}  // namespace fibar

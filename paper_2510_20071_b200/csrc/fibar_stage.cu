@@ -1,0 +1,569 @@
+// fibar_stage.cu -- per-pixel temporal replay (short and long segments), the blur
+// dataflow (tap resolution + persistent polling grid) and the end-of-batch pass.
+#include "fibar_kernels.cuh"
+
+namespace fibar {
+
+// -------------------------------------------------------------- temporal ---
+
+// Per sorted position, fully parallel: the event's polarity gathered into
+// sorted order and (filter ON) whether the event is evicted stale in this
+// batch -- the random loads the serial per-pixel replay would otherwise wait on.
+__global__ void __launch_bounds__(TPB) k_posinfo(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned jj = x.sidx[i];
+  x.spol[i] = x.epol[jj];
+  if (!x.spatial) return;
+  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
+  const long long s_end = s_start + x.S[B - 1];
+  const long long e = E0 + jj;
+  unsigned bidx = FIBAR_NONE;
+  if (e < s_end) {
+    const unsigned q = (unsigned)(e - s_start);
+    if (x.item[q].pix != FIBAR_NONE) bidx = q;
+  }
+  *reinterpret_cast<uint2 *>(&x.posrec[i]) = make_uint2(jj, bidx);
+}
+
+// One thread per pixel segment replays its events in stream order with the
+// reference's float32 operation order (_kernels.py:67-73 / 124-130).  Inputs
+// are read GROUP positions at a time (all loads issued before the dependent
+// arithmetic), so long segments (hot pixels) run at the arithmetic chain's speed.
+
+__global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned key = x.skey[i];
+  if (i > 0 && x.skey[i - 1] == key) return;
+  const unsigned c = x.ekey[x.sidx[i]];
+  const long long end = x.spatial ? (long long)x.pt[c].end : -1;
+  if (i + LONG_SEG < B && x.skey[i + LONG_SEG] == key) {   // long segment: the warp-parallel kernel
+    const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
+    if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
+    return;
+  }
+  float pb = x.pbar[c], lv = x.l[c];
+  const float g = x.use_gain ? x.gain[c] : 1.0f;
+  long long pos = i;
+  bool more = true;
+  while (more) {
+    int8_t pol[GROUP];
+    bool in[GROUP];
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      const long long q = pos + u;
+      in[u] = q < B && (end >= 0 ? q < end : x.skey[q] == key);
+      pol[u] = in[u] ? x.spol[q] : (int8_t)0;
+    }
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      if (!in[u]) {
+        more = false;
+        break;
+      }
+      const float p = (float)pol[u];
+      pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+      float d = fsubr(p, pb);
+      if (x.use_gain) d = fmulr(d, g);
+      lv = faddr(fmulr(x.beta, lv), fmulr(x.h, d));
+    }
+    pos += GROUP;
+  }
+  x.pbar[c] = pb;
+  x.l[c] = lv;
+}
+
+// Filter ON: same replay, recording per position the additive term t2 = h*d,
+// the brightness assuming no blur (valid until the pixel's first blur in the
+// batch), and which blur each position builds on.
+__global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= B) return;
+  const unsigned key = x.skey[i];
+  if (i > 0 && x.skey[i - 1] == key) return;
+  const unsigned c = x.ekey[x.sidx[i]];
+  const PixRec prc = x.pt[c];
+  const long long end = prc.end;
+  if (end - i > LONG_SEG) {   // long segment (hot pixel): the warp-parallel kernel
+    const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
+    if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
+    return;
+  }
+  unsigned carry = prc.carried;
+  if (carry != FIBAR_NONE) x.item[carry].runpos = (unsigned)i;
+  float pb = x.pbar[c], lv = x.l[c];
+  const float g = x.use_gain ? x.gain[c] : 1.0f;
+  for (long long pos = i; pos < end; pos += GROUP) {
+    int8_t pol[GROUP];
+    unsigned bidx[GROUP];
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      const long long q = pos + u;
+      pol[u] = q < end ? x.spol[q] : (int8_t)0;
+      bidx[u] = q < end ? x.posrec[q].bidx : FIBAR_NONE;
+    }
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      const long long q = pos + u;
+      if (q >= end) break;
+      const float p = (float)pol[u];
+      pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+      float d = fsubr(p, pb);
+      if (x.use_gain) d = fmulr(d, g);
+      const float tt = fmulr(x.h, d);
+      lv = faddr(fmulr(x.beta, lv), tt);
+      x.t2[q] = tt;
+      *reinterpret_cast<uint2 *>(&x.posrec[q].runbase) = make_uint2(carry, __float_as_uint(lv));
+      if (bidx[u] != FIBAR_NONE) {
+        carry = bidx[u];
+        if (q + 1 < end) x.item[bidx[u]].runpos = (unsigned)(q + 1);
+      }
+    }
+  }
+  x.pbar[c] = pb;
+  // last-touch tables for the next batch's links (the blur stage never reads them)
+  const long long elast = x.bs->E0 + x.sidx[end - 1];
+  x.plast[c] = elast;
+  atomicMax(&x.last_tile[key / x.A], elast);
+}
+
+// Long pixel segments (hot pixels: thousands of events per batch) replayed by
+// a block: lane i takes the i-th piece (at least LONG_PIECE events), starting
+// `twarm` events early from a zero state.  The two float32 recurrences are
+// contractions (|alpha|, |beta| < 1), so trajectories from different starts
+// become bit-identical after ~24*ln2/-ln(max(alpha, beta)) events (~110 at
+// t_cut = 40; twarm is 1.6x that); each lane's piece-start state is checked
+// against the previous lane's piece-end state and any piece whose start
+// differed is replayed serially from the exact state, so the result is exact
+// either way.
+
+__device__ __forceinline__ void iir_step(const Ctx &x, float &pb, float &lv, float p, float g, float &tt) {
+  pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+  float d = fsubr(p, pb);
+  if (x.use_gain) d = fmulr(d, g);
+  tt = fmulr(x.h, d);
+  lv = faddr(fmulr(x.beta, lv), tt);
+}
+
+// replay [q0, q1) from (pb, lv), writing the per-position outputs; inputs are
+// loaded GROUP at a time so the chain waits on one load per group
+__device__ __forceinline__ void replay_piece(const Ctx &x, long long q0, long long q1, float &pb, float &lv, float g,
+                                             bool write) {
+  for (long long q = q0; q < q1; q += GROUP) {
+    int8_t pol[GROUP];
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) pol[u] = q + u < q1 ? x.spol[q + u] : (int8_t)0;
+#pragma unroll
+    for (int u = 0; u < GROUP; ++u) {
+      if (q + u >= q1) break;
+      float tt;
+      iir_step(x, pb, lv, (float)pol[u], g, tt);
+      if (write && x.spatial) {
+        x.t2[q + u] = tt;
+        x.posrec[q + u].val = lv;
+      }
+    }
+  }
+}
+
+
+__global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
+  pdl_wait();
+  __shared__ float s_spb[LONG_TPB], s_slv[LONG_TPB], s_epb[LONG_TPB], s_elv[LONG_TPB];
+  __shared__ unsigned s_last[LONG_TPB];
+  __shared__ int s_bad;
+  const unsigned n = min(x.bs->nlong, (unsigned)MAX_LONG);
+  const int tid = threadIdx.x;
+  for (unsigned sidx = blockIdx.x; sidx < n; sidx += gridDim.x) {
+    const uint2 ls = x.longseg[sidx];
+    const long long st = ls.x;
+    const unsigned c = ls.y;
+    long long end;
+    if (x.spatial) {
+      end = x.pt[c].end;
+    } else {
+      // segment end by search on the sorted keys (OFF path has no pixel table)
+      const unsigned key = x.skey[st];
+      long long lo = st + 1, hi = x.bs->B;
+      while (lo < hi) {
+        const long long mid = (lo + hi) >> 1;
+        if (x.skey[mid] == key) lo = mid + 1; else hi = mid;
+      }
+      end = lo;
+    }
+    const long long len = end - st;
+    const int lanes = (int)min((long long)LONG_TPB, max(32LL, len / LONG_PIECE));
+    const long long P = (len + lanes - 1) / lanes;
+    const bool on = tid < lanes;
+    const long long q0 = on ? min(end, st + tid * P) : end, q1 = on ? min(end, q0 + P) : end;
+    const float g = x.use_gain ? x.gain[c] : 1.0f;
+    float pb = 0.0f, lv = 0.0f;
+    if (tid == 0) {
+      pb = x.pbar[c];
+      lv = x.l[c];
+    } else if (on) {
+      replay_piece(x, max(st, q0 - (long long)x.twarm), q0, pb, lv, g, false);
+    }
+    s_spb[tid] = pb;   // speculative state at the piece start
+    s_slv[tid] = lv;
+    replay_piece(x, q0, q1, pb, lv, g, true);
+    s_epb[tid] = pb;
+    s_elv[tid] = lv;
+    if (tid == 0) s_bad = 0;
+    __syncthreads();
+    // verify every boundary; in the rare case a start was wrong, re-run the
+    // pieces from there on serially in lane order from the exact states
+    if (on && tid > 0 && (__float_as_uint(s_spb[tid]) != __float_as_uint(s_epb[tid - 1]) ||
+                          __float_as_uint(s_slv[tid]) != __float_as_uint(s_elv[tid - 1])))
+      atomicMax(&s_bad, 1);
+    __syncthreads();
+    if (s_bad) {
+      for (int i = 1; i < lanes; ++i) {
+        if (tid == i && (__float_as_uint(s_spb[i]) != __float_as_uint(s_epb[i - 1]) ||
+                         __float_as_uint(s_slv[i]) != __float_as_uint(s_elv[i - 1]))) {
+          pb = s_epb[i - 1];
+          lv = s_elv[i - 1];
+          s_spb[i] = pb;
+          s_slv[i] = lv;
+          replay_piece(x, q0, q1, pb, lv, g, true);
+          s_epb[i] = pb;
+          s_elv[i] = lv;
+        }
+        __syncthreads();
+      }
+    }
+    const float fpb = s_epb[lanes - 1], flv = s_elv[lanes - 1];
+    if (!x.spatial) {
+      if (tid == 0) {
+        x.pbar[c] = fpb;
+        x.l[c] = flv;
+      }
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) {
+      x.pbar[c] = fpb;
+      const long long elast = x.bs->E0 + x.sidx[end - 1];
+      x.plast[c] = elast;
+      atomicMax(&x.last_tile[x.skey[st] / x.A], elast);
+    }
+    // blur bookkeeping: which blur each position builds on (last stale event
+    // before it in the segment, or the pixel's carried blur)
+    unsigned last = FIBAR_NONE;
+    for (long long q = q0; q < q1; q += GROUP) {
+      unsigned bidx[GROUP];
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) bidx[u] = q + u < q1 ? x.posrec[q + u].bidx : FIBAR_NONE;
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) {
+        if (bidx[u] != FIBAR_NONE) {
+          last = bidx[u];
+          if (q + u + 1 < end) x.item[bidx[u]].runpos = (unsigned)(q + u + 1);
+        }
+      }
+    }
+    s_last[tid] = last;
+    const unsigned carried = x.pt[c].carried;
+    if (tid == 0 && carried != FIBAR_NONE) x.item[carried].runpos = (unsigned)st;
+    __syncthreads();
+    // exclusive "last non-NONE before me" over the lanes: a short backwards scan
+    unsigned carry = carried;
+    for (int i = tid - 1; i >= 0; --i) {
+      if (s_last[i] != FIBAR_NONE) {
+        carry = s_last[i];
+        break;
+      }
+    }
+    for (long long q = q0; q < q1; q += GROUP) {
+      unsigned bidx[GROUP];
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) bidx[u] = q + u < q1 ? x.posrec[q + u].bidx : FIBAR_NONE;
+#pragma unroll
+      for (int u = 0; u < GROUP; ++u) {
+        if (q + u >= q1) break;
+        x.posrec[q + u].runbase = carry;
+        if (bidx[u] != FIBAR_NONE) carry = bidx[u];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------- blur ---
+
+
+
+// First resolution of item p's 3x3 taps (_kernels.py:174-188 tap order).  A
+// tap's brightness "at item p" is the neighbour's value after every temporal
+// update up to the popping event and every earlier blur.  It comes from the
+// pixel record (batch segment, carried blur) and the position record of the
+// neighbour's latest event at that time: directly (batch-start value or
+// first-run value) or, when a blur produced it, after that blur's flag.
+// Runs for all items in parallel, before any blur (no waiting).
+__global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x) {
+  pdl_wait();
+  const BatchScalars b = load_bs(x);
+  const unsigned npop = (unsigned)(b.s_end - b.s_start);
+  const unsigned p = blockIdx.x * TPB + threadIdx.x;
+  if (p >= npop) return;
+  const Item it = x.item[p];
+  BlurPrep out;
+  out.okm = 0;
+  out.pend = 0;
+  if (it.pix == FIBAR_NONE) {
+    x.prep[p].okm = 0;
+    return;
+  }
+  const unsigned jrel = it.jrel;
+  const int cx = (int)(it.pix % (unsigned)x.W), cy = (int)(it.pix / (unsigned)x.W);
+  unsigned nidx[9];
+  uint4 pr[9];   // (st, end, carried, -) of each tap's pixel record
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    const int yy = cy + t / 3 - 1, xx = cx + t % 3 - 1;
+    const bool ok = yy >= 0 && yy < x.H && xx >= 0 && xx < x.W;
+    nidx[t] = ok ? (unsigned)yy * x.W + xx : it.pix;
+    out.okm |= (unsigned)ok << t;
+    pr[t] = __ldcg(reinterpret_cast<const uint4 *>(&x.pt[nidx[t]]));
+  }
+  unsigned posi[9], first[9], last[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    first[t] = last[t] = 0xFFFFFFFFu;
+    if (pr[t].y > pr[t].x) {
+      first[t] = __ldg(&x.sidx[pr[t].x]);
+      last[t] = __ldg(&x.sidx[pr[t].y - 1]);
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    posi[t] = FIBAR_NONE;
+    if (pr[t].y <= pr[t].x || first[t] > jrel) continue;
+    if (last[t] <= jrel) {
+      posi[t] = pr[t].y - 1;
+    } else {
+      unsigned lo = pr[t].x + 1, hi = pr[t].y - 1;   // answer in [st, end-2]
+      while (lo < hi) {
+        const unsigned mid = (lo + hi) >> 1;
+        if (__ldg(&x.sidx[mid]) <= jrel) lo = mid + 1; else hi = mid;
+      }
+      posi[t] = lo - 1;
+    }
+  }
+  PosRec rec[9];
+#pragma unroll
+  for (int t = 0; t < 9; ++t)
+    if (posi[t] != FIBAR_NONE) rec[t] = x.posrec[posi[t]];
+#pragma unroll
+  for (int t = 0; t < 9; ++t) {
+    out.val[t] = 0u;
+    if (!((out.okm >> t) & 1)) continue;
+    bool wait = true;
+    if (posi[t] == FIBAR_NONE) {
+      if (pr[t].z < p) {                    // blurred (carried) before this item
+        out.val[t] = pr[t].z;
+      } else {
+        out.val[t] = __float_as_uint(x.l[nidx[t]]);
+        wait = false;
+      }
+    } else if (rec[t].bidx < p) {           // its own blur came first
+      out.val[t] = rec[t].bidx;
+    } else if (rec[t].runbase == FIBAR_NONE) {
+      out.val[t] = __float_as_uint(rec[t].val);   // first run: no blur involved
+      wait = false;
+    } else {                                // rebuilt from blur runbase
+      out.val[t] = posi[t] | 0x80000000u;
+    }
+    if (wait) out.pend |= 1u << t;
+  }
+  out.runpos = it.runpos;
+  x.prep[p] = out;
+}
+
+// after blur p of pixel c: brightness of c's following events (up to and
+// including its next blurred event) is rebuilt from the blurred value
+
+// after blur p of pixel c: brightness of c's following events (up to and
+// including its next blurred event) is rebuilt from the blurred value
+__device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars &b, unsigned p, unsigned r,
+                                                float v) {
+  // run positions and their terms are fetched four at a time, so a run costs
+  // one round trip per four positions instead of one per position
+  while (r < b.B) {
+    unsigned rb[4];
+    float tt[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = r + u < b.B;
+      rb[u] = in ? x.posrec[r + u].runbase : FIBAR_NONE;
+      tt[u] = in ? x.t2[r + u] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (rb[u] != p) return;
+      v = faddr(fmulr(x.beta, v), tt[u]);
+      x.posrec[r + u].val = v;
+      st_relaxed_u64(&x.mv64[r + u], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
+    }
+    r += 4;
+  }
+}
+
+// Persistent dataflow over the eviction items.  Idle lanes take new items in
+// pop order from a global ticket (one warp-aggregated atomic), so every
+// dependency -- always an earlier item -- is held by a lane that is already
+// running; a waiting lane re-polls the pending flags its prep record left
+// open.  The blurred value is published (ready) before the
+// pixel's following run is rebuilt (mready).
+__global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
+  pdl_wait();
+  const BatchScalars b = load_bs(x);
+  const unsigned npop = (unsigned)(b.s_end - b.s_start);
+  const int lane = threadIdx.x & 31;
+  unsigned p = FIBAR_NONE, okm = 0, pend = 0, runpos = FIBAR_NONE;
+  unsigned val[9];
+  bool exhausted = false;
+  // the warp draws 32 items at a time from the global ticket and hands them
+  // to its free lanes in order (one contended atomic per 32 items); every
+  // item below a lane's is taken, so the deadlock-freedom argument holds
+  unsigned wbase = 0, wused = 32;
+  while (true) {
+    unsigned want = __ballot_sync(0xffffffffu, p == FIBAR_NONE && !exhausted);
+    while (want) {
+      if (wused == 32) {
+        unsigned nb = 0;
+        if (lane == 0) nb = atomicAdd(&x.bs->ticket, 32u);
+        wbase = __shfl_sync(0xffffffffu, nb, 0);
+        wused = 0;
+      }
+      const unsigned take = min((unsigned)__popc(want), 32u - wused);
+      const unsigned rank = __popc(want & ((1u << lane) - 1u));
+      const bool mine = ((want >> lane) & 1) && rank < take;
+      const unsigned q = wbase + wused + rank;
+      wused += take;
+      want &= ~__ballot_sync(0xffffffffu, mine);
+      if (mine) {
+        if (q >= npop) {
+          exhausted = true;
+        } else {
+          const uint4 *rec = reinterpret_cast<const uint4 *>(&x.prep[q]);
+          const uint4 n0 = __ldcg(rec);
+          okm = n0.x;
+          if (okm) {
+            const uint4 n1 = __ldcg(rec + 1), n2 = __ldcg(rec + 2);
+            p = q;
+            pend = n0.y;
+            val[0] = n0.z;
+            val[1] = n0.w;
+            val[2] = n1.x;
+            val[3] = n1.y;
+            val[4] = n1.z;
+            val[5] = n1.w;
+            val[6] = n2.x;
+            val[7] = n2.y;
+            val[8] = n2.z;
+            runpos = n2.w;
+          }
+        }
+      }
+    }
+    if (p != FIBAR_NONE) {
+      // every open tap polls its value word (epoch | float bits) with an
+      // independent relaxed 64-bit load: a matching epoch means the value is
+      // there, so no flag/value ordering (and no fence) is involved
+#pragma unroll
+      for (int t = 0; t < 9; ++t) {
+        if (!((pend >> t) & 1)) continue;
+        const unsigned s = val[t];
+        const unsigned long long w = ld_relaxed_u64((s & 0x80000000u) ? &x.mv64[s & 0x7FFFFFFFu] : &x.bv64[s]);
+        if ((unsigned)(w >> 32) != b.epoch) continue;
+        val[t] = (unsigned)w;
+        pend &= ~(1u << t);
+      }
+      if (pend == 0) {
+        float num = 0.0f, den = 0.0f;
+#pragma unroll
+        for (int t = 0; t < 9; ++t) {
+          if (!((okm >> t) & 1)) continue;
+          const float w = (float)((t / 3 == 1 ? 2 : 1) * (t % 3 == 1 ? 2 : 1));
+          num = faddr(num, fmulr(w, __uint_as_float(val[t])));
+          den = faddr(den, w);
+        }
+        const float v = __fdiv_rn(num, den);
+        st_relaxed_u64(&x.bv64[p], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
+        if (x.dbg_t) {
+          unsigned long long tt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+          x.dbg_t[p] = tt;
+        }
+        if (runpos != FIBAR_NONE) materialise_run(x, b, p, runpos, v);
+        p = FIBAR_NONE;
+      } else if (x.blur_sleep) {
+        __nanosleep(x.blur_sleep);
+      }
+    }
+    if (__all_sync(0xffffffffu, exhausted && p == FIBAR_NONE)) break;
+  }
+}
+
+// ------------------------------------------------------------------ final ---
+
+__global__ void __launch_bounds__(TPB) k_final(Ctx x) {
+  pdl_wait();
+  const BatchScalars b = load_bs(x);
+  const long long npop = b.s_end - b.s_start;
+  const long long total = b.B + npop;
+  for (long long idx = (long long)blockIdx.x * TPB + threadIdx.x; idx < total; idx += (long long)gridDim.x * TPB) {
+    if (idx < b.B) {
+      const long long pos = idx;
+      if (pos + 1 < b.B && x.skey[pos + 1] == x.skey[pos]) continue;   // segment tails only
+      const PosRec f = x.posrec[pos];
+      const unsigned c = x.ekey[f.jj];
+      const long long e = b.E0 + f.jj;
+      float v = f.val;
+      if (x.blur_on && f.bidx != FIBAR_NONE) v = __uint_as_float((unsigned)x.bv64[f.bidx]);
+      x.l[c] = v;
+      PixRec nr;
+      nr.st = 0;
+      nr.end = 0;
+      nr.carried = FIBAR_NONE;
+      nr.pad0 = 0;
+      x.pt[c] = nr;
+      (void)e;
+    } else {
+      const unsigned p = (unsigned)(idx - b.B);
+      const Item it = x.item[p];
+      if (it.pad & ITEM_CARRIED_ONLY) {
+        // carried stale entry whose pixel has no events in this batch: the
+        // blur is the pixel's only update (segment pixels are finished above)
+        if (x.blur_on) x.l[it.pix] = __uint_as_float((unsigned)x.bv64[p]);
+        x.pt[it.pix].carried = FIBAR_NONE;
+      }
+    }
+  }
+}
+
+__global__ void k_batch_end(Ctx x) {
+  pdl_wait();
+  DevState *s = x.st;
+  const BatchState *bsp = x.bs;
+  if (x.spatial && bsp->B > 0) {
+    s->geo = s->geo_next;
+    s->geo_next = 0;
+  }
+  s->E += bsp->B;
+  if (x.spatial) {
+    s->stale += bsp->stale_batch;
+    if (x.blur_on) s->blur += bsp->stale_batch;
+  }
+}
+
+
+}  // namespace fibar
