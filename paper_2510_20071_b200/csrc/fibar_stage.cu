@@ -470,6 +470,11 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
             val[7] = n2.y;
             val[8] = n2.z;
             runpos = n2.w;
+            if (x.dbg_g) {
+              unsigned long long tt;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+              x.dbg_g[q] = tt;
+            }
           }
         }
       }
