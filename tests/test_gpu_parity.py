@@ -223,3 +223,36 @@ def test_launch_modes_agree(monkeypatch):
             eng.process_array(ev.slice(a, min(len(ev), a + 50_000)))
         assert_state(eng, want, f"pdl={pdl} serial={serial}")
         eng.close()
+
+
+@pytest.mark.parametrize("kind,w,h,n,packet,kw", [
+    # hot pixels at config-3 geometry: long segments, several 1M-event batches
+    ("texture_noise_hot", 1280, 720, 3_000_000, 100_000, {}),
+    # variants at scale: tile side 3, fill 2/3, regulate_every 2, a gain map, blur off
+    ("texture", 640, 480, 2_500_000, 50_000, dict(tile_side=3, fill=Fraction(2, 3), regulate_every=2, gain=True)),
+    ("texture", 640, 480, 2_500_000, 250_000, dict(blur=False)),
+])
+def test_large_streams_match_oracle(kind, w, h, n, packet, kw):
+    from oracle import oracle as orc
+    from paper_2510_20071_b200 import workloads
+    from paper_2510_20071_b200.core import SensorGeometry, compute_params
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    geom = SensorGeometry(w, h)
+    ev = workloads.make(kind, geom, n, seed=21)
+    params = compute_params(40.0, kw.get("fill", Fraction(1, 2)), geom, tile_side=kw.get("tile_side", 2))
+    gain = None
+    if kw.get("gain"):
+        gain = np.random.default_rng(4).uniform(0.6, 1.6, (h, w)).astype(np.float32)
+    every, blur = kw.get("regulate_every", 1), kw.get("blur", True)
+    eng = ReconstructionEngine(geom, params, threshold_map=gain, regulate_every=every, blur_enabled=blur)
+    ref = orc.OracleEngine(w, h, params, gain=gain, regulate_every=every, blur_enabled=blur)
+    for a in range(0, n, packet):
+        b = min(n, a + packet)
+        eng.process_array(ev.slice(a, b))
+        ref.process_array(ev.t[a:b], ev.x[a:b], ev.y[a:b], ev.p[a:b])
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, f"{kind} {w}x{h} {kw}")
+    fr = eng.render("robust")
+    px, bounds, deg = ref.render("robust")
+    assert np.array_equal(fr.pixels, px) and fr.bounds == bounds
