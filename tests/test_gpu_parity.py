@@ -231,6 +231,8 @@ def test_launch_modes_agree(monkeypatch):
     # variants at scale: tile side 3, fill 2/3, regulate_every 2, a gain map, blur off
     ("texture", 640, 480, 2_500_000, 50_000, dict(tile_side=3, fill=Fraction(2, 3), regulate_every=2, gain=True)),
     ("texture", 640, 480, 2_500_000, 250_000, dict(blur=False)),
+    # config-5 geometry: a window larger than a device batch (warp-counted collapses)
+    ("texture", 2560, 1440, 3_000_000, 1_000_000, {}),
 ])
 def test_large_streams_match_oracle(kind, w, h, n, packet, kw):
     from oracle import oracle as orc
