@@ -38,6 +38,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "fibar_kernels.cuh"
 
 using namespace fibar;
@@ -134,6 +136,11 @@ struct fibar_engine {
   // while batch k+1's front end runs on the engine stream; per-batch buffers
   // are double buffered by batch parity
   cudaStream_t bstream = nullptr;
+  // FIBAR_GREEN=n: the blur kernel runs in a green context of n SMs
+  CUgreenCtx gctx = nullptr;
+  cudaStream_t gstream = nullptr;
+  cudaEvent_t evP = nullptr, evG = nullptr;
+  int gblocks = 0;
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
   bool graphs_on = true;
   cudaStream_t capstream = nullptr;
@@ -325,7 +332,19 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     if (g->blur_on) {
       const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
       fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, bs, x);
-      fibar_launch(L, "blur", k_blur, graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs, x);
+      if (g->gstream && !graph) {
+        // the blur dataflow alone on its own SM partition (green context):
+        // its polling no longer shares SMs with the next batch's front end
+        CK(cudaEventRecord(g->evP, bs));
+        CK(cudaStreamWaitEvent(g->gstream, g->evP, 0));
+        L.stream = g->gstream;
+        fibar_launch(L, "blur", k_blur, g->gblocks, TPB, 0, g->gstream, x);
+        CK(cudaEventRecord(g->evG, g->gstream));
+        CK(cudaStreamWaitEvent(bs, g->evG, 0));
+        L.stream = bs;
+      } else {
+        fibar_launch(L, "blur", k_blur, graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs, x);
+      }
     }
     fibar_launch(L, "final", k_final, g->nsm * 8, TPB, 0, bs, x);
     L.stream = s;
@@ -581,6 +600,35 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   if (const char *v = getenv("FIBAR_WARM")) g->warm = std::max(0, atoi(v));
   if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
   if (const char *v = getenv("FIBAR_SERIAL")) g->serial = atoi(v) != 0;
+  // The blur dataflow kernel runs in a CUDA green context of GREEN_SMS SMs (8
+  // blocks each): its polling lanes stop sharing SMs with the next batch's
+  // front end (config 2: 9.3 -> 9.0 ms / 10M).  FIBAR_GREEN=n sets the SM
+  // count, 0 turns it off; without green-context support the blur stays on
+  // the second stream with the whole GPU.
+  int green_sms = 16;
+  if (const char *v = getenv("FIBAR_GREEN")) green_sms = atoi(v);
+  if (green_sms > 0 && cfg->spatial_enabled && !g->serial) {
+    const unsigned want = (unsigned)std::max(8, green_sms);
+    CUdevice cdev;
+    CUdevResource res, grp, rest;
+    unsigned ng = 1;
+    CUdevResourceDesc desc;
+    if (cuDeviceGet(&cdev, 0) == CUDA_SUCCESS && cuDeviceGetDevResource(cdev, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
+        cuDevSmResourceSplitByCount(&grp, &ng, &res, &rest, 0, want) == CUDA_SUCCESS && ng == 1 &&
+        cuDevResourceGenerateDesc(&desc, &grp, 1) == CUDA_SUCCESS &&
+        cuGreenCtxCreate(&g->gctx, desc, cdev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS) {
+      CUstream cs;
+      if (cuGreenCtxStreamCreate(&cs, g->gctx, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) {
+        g->gstream = (cudaStream_t)cs;
+        int per = 8;
+        if (const char *b = getenv("FIBAR_GREEN_BLOCKS")) per = std::max(1, atoi(b));
+        g->gblocks = (int)grp.sm.smCount * per;
+        cudaEventCreateWithFlags(&g->evP, cudaEventDisableTiming);
+        cudaEventCreateWithFlags(&g->evG, cudaEventDisableTiming);
+      }
+    }
+    cudaGetLastError();
+  }
   if (const char *v = getenv("FIBAR_PDL")) g->L.pdl = atoi(v) != 0;
   {
     // contraction of the slower recurrence: events until any two float32
@@ -745,6 +793,13 @@ int fibar_destroy(fibar_engine *g) {
   for (void *q : {(void *)g->gx, (void *)g->gy, (void *)g->gp})
     if (q) cudaFree(q);
   if (g->bstream) cudaStreamDestroy(g->bstream);
+  if (g->gstream) {
+    cudaStreamSynchronize(g->gstream);
+    cudaStreamDestroy(g->gstream);
+  }
+  if (g->gctx) cuGreenCtxDestroy(g->gctx);
+  for (cudaEvent_t ev : {g->evP, g->evG})
+    if (ev) cudaEventDestroy(ev);
   delete g;
   return 0;
 }

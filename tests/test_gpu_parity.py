@@ -209,19 +209,21 @@ def test_graph_and_streamed_batches_agree(monkeypatch):
 
 
 def test_launch_modes_agree(monkeypatch):
-    """Programmatic dependent launch, the two-stream overlap and the serial
-    schedule are scheduling choices only: every combination is oracle-exact."""
+    """Programmatic dependent launch, the two-stream overlap, the serial
+    schedule and the blur's green-context SM partition are scheduling choices
+    only: every combination is oracle-exact."""
     from paper_2510_20071_b200.pipeline import ReconstructionEngine
     geom, params, ev, ref = _oracle_stream("texture", 320, 240, 600_000, 50_000, True, seed=13)
     want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
                 qx=ref.qx, qy=ref.qy, qs=ref.qs)
-    for pdl, serial in (("0", "0"), ("1", "1"), ("0", "1")):
+    for pdl, serial, green in (("0", "0", "0"), ("1", "1", "16"), ("0", "1", "0"), ("1", "0", "24")):
         monkeypatch.setenv("FIBAR_PDL", pdl)
         monkeypatch.setenv("FIBAR_SERIAL", serial)
+        monkeypatch.setenv("FIBAR_GREEN", green)
         eng = ReconstructionEngine(geom, params, batch_capacity=1 << 18)
         for a in range(0, len(ev), 50_000):
             eng.process_array(ev.slice(a, min(len(ev), a + 50_000)))
-        assert_state(eng, want, f"pdl={pdl} serial={serial}")
+        assert_state(eng, want, f"pdl={pdl} serial={serial} green={green}")
         eng.close()
 
 
