@@ -43,7 +43,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(os.path.dirname(OUT), exist_ok=True)
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", *EXTRA, "-Xcompiler", "-fPIC", "-shared",
-           "-I", os.path.join(HERE, "..", "include"), "-o", OUT + ".tmp", *SRC, "-lcuda"]
+           "-I", os.path.join(HERE, "..", "include"), "-o", OUT + ".tmp", *SRC]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)

@@ -60,6 +60,46 @@ int cuda_fail(cudaError_t e, const char *where) {
 
 namespace {
 
+// CUDA driver entry points for green contexts, resolved at run time through
+// the runtime (cudaGetDriverEntryPoint), so the library does not link libcuda
+// and still loads where no driver is installed (the CPU build/test host).
+struct GreenApi {
+  bool ok = false;
+  CUresult (*deviceGet)(CUdevice *, int) = nullptr;
+  CUresult (*getDevResource)(CUdevice, CUdevResource *, CUdevResourceType) = nullptr;
+  CUresult (*splitByCount)(CUdevResource *, unsigned *, const CUdevResource *, CUdevResource *, unsigned,
+                           unsigned) = nullptr;
+  CUresult (*generateDesc)(CUdevResourceDesc *, CUdevResource *, unsigned) = nullptr;
+  CUresult (*ctxCreate)(CUgreenCtx *, CUdevResourceDesc, CUdevice, unsigned) = nullptr;
+  CUresult (*streamCreate)(CUstream *, CUgreenCtx, unsigned, int) = nullptr;
+  CUresult (*ctxDestroy)(CUgreenCtx) = nullptr;
+};
+
+template <class F>
+bool driver_fn(const char *name, F &fn) {
+  void *p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      !p) {
+    cudaGetLastError();
+    return false;
+  }
+  fn = reinterpret_cast<F>(p);
+  return true;
+}
+
+const GreenApi &green_api() {
+  static GreenApi api = [] {
+    GreenApi a;
+    a.ok = driver_fn("cuDeviceGet", a.deviceGet) && driver_fn("cuDeviceGetDevResource", a.getDevResource) &&
+           driver_fn("cuDevSmResourceSplitByCount", a.splitByCount) &&
+           driver_fn("cuDevResourceGenerateDesc", a.generateDesc) && driver_fn("cuGreenCtxCreate", a.ctxCreate) &&
+           driver_fn("cuGreenCtxStreamCreate", a.streamCreate) && driver_fn("cuGreenCtxDestroy", a.ctxDestroy);
+    return a;
+  }();
+  return api;
+}
+
 int ceil_log2(long long v) {
   int b = 0;
   while ((1LL << b) < v) ++b;
@@ -613,12 +653,16 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     CUdevResource res, grp, rest;
     unsigned ng = 1;
     CUdevResourceDesc desc;
-    if (cuDeviceGet(&cdev, 0) == CUDA_SUCCESS && cuDeviceGetDevResource(cdev, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
-        cuDevSmResourceSplitByCount(&grp, &ng, &res, &rest, 0, want) == CUDA_SUCCESS && ng == 1 &&
-        cuDevResourceGenerateDesc(&desc, &grp, 1) == CUDA_SUCCESS &&
-        cuGreenCtxCreate(&g->gctx, desc, cdev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS) {
+    const GreenApi &api = green_api();
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (api.ok && api.deviceGet(&cdev, cur) == CUDA_SUCCESS &&
+        api.getDevResource(cdev, &res, CU_DEV_RESOURCE_TYPE_SM) == CUDA_SUCCESS &&
+        api.splitByCount(&grp, &ng, &res, &rest, 0, want) == CUDA_SUCCESS && ng == 1 &&
+        api.generateDesc(&desc, &grp, 1) == CUDA_SUCCESS &&
+        api.ctxCreate(&g->gctx, desc, cdev, CU_GREEN_CTX_DEFAULT_STREAM) == CUDA_SUCCESS) {
       CUstream cs;
-      if (cuGreenCtxStreamCreate(&cs, g->gctx, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) {
+      if (api.streamCreate(&cs, g->gctx, CU_STREAM_NON_BLOCKING, 0) == CUDA_SUCCESS) {
         g->gstream = (cudaStream_t)cs;
         int per = 8;
         if (const char *b = getenv("FIBAR_GREEN_BLOCKS")) per = std::max(1, atoi(b));
@@ -797,7 +841,7 @@ int fibar_destroy(fibar_engine *g) {
     cudaStreamSynchronize(g->gstream);
     cudaStreamDestroy(g->gstream);
   }
-  if (g->gctx) cuGreenCtxDestroy(g->gctx);
+  if (g->gctx) green_api().ctxDestroy(g->gctx);
   for (cudaEvent_t ev : {g->evP, g->evG})
     if (ev) cudaEventDestroy(ev);
   delete g;
