@@ -66,7 +66,7 @@ struct BatchState {
   unsigned epoch;      // batch counter (tags blur words)
   unsigned ticket;     // blur work ticket
   unsigned nlong;      // long pixel segments
-  unsigned pad;
+  unsigned nco;        // stale items of pixels with no events in the batch (listed by k_popj)
 };
 
 // Window / counter state living in device memory so no kernel needs a host

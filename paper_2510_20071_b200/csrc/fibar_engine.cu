@@ -146,7 +146,9 @@ struct fibar_engine {
   uint2 *dp = nullptr;
   unsigned *S = nullptr;
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
-  BlurPrep *prep = nullptr;
+  BlurPrep *prep = nullptr;            // = prep2[0] (debug reads)
+  BlurPrep *prep2[2] = {nullptr, nullptr};   // per batch parity: k_popj of batch k+1 writes while batch k blurs
+  unsigned *colist = nullptr;
   Item *item2[2] = {nullptr, nullptr};
   PosRec *posrec2[2] = {nullptr, nullptr};
   float *t2_2[2] = {nullptr, nullptr};
@@ -255,7 +257,8 @@ struct fibar_engine {
     x.t2 = t2_2[par];
     x.bv64 = bv64;
     x.mv64 = mv64;
-    x.prep = prep;
+    x.prep = prep2[par];
+    x.colist = colist;
     x.chunk = chunk;
     x.twarm = twarm;
     x.debug = debug;
@@ -781,7 +784,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->S, Bc);
     rc |= dalloc(&g->bv64, npop_cap);
     rc |= dalloc(&g->mv64, Bc);
-    rc |= dalloc(&g->prep, npop_cap);
+    rc |= dalloc(&g->prep2[0], npop_cap);
+    rc |= dalloc(&g->prep2[1], npop_cap);
+    g->prep = g->prep2[0];
+    rc |= dalloc(&g->colist, n + 1);
     rc |= dalloc(&g->anc, T * NCAND);
     rc |= dalloc(&g->anc2, T * NFINE);
     rc |= dalloc(&g->lc, T);
@@ -810,7 +816,7 @@ int fibar_destroy(fibar_engine *g) {
   if (g->bstream) cudaStreamSynchronize(g->bstream);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
-                  g->dp, g->S, g->bv64, g->mv64, g->prep, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
+                  g->dp, g->S, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g};
   for (void *p : ptrs)
     if (p) cudaFree(p);

@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->stale_batch = 0;
     b->ticket = 0;
     b->nlong = 0;
+    b->nco = 0;
     s->epoch += 1;
     b->epoch = s->epoch;
   }
@@ -927,10 +928,14 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
       if (k < E0) {
         x.pt[c].carried = p;
         // no event of the pixel in this batch after its pre-batch last one
-        if ((unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(E0 + B - 1 - k))
+        if ((unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(E0 + B - 1 - k)) {
           it.pad |= ITEM_CARRIED_ONLY;
+          x.colist[atomicAdd(&x.bs->nco, 1u)] = p;   // resolved by k_blur_prep from this list
+        }
       }
       ++nst;
+    } else {
+      x.prep[p].okm = 0;   // not blurred: the blur lanes skip it
     }
     x.item[p] = it;
   }

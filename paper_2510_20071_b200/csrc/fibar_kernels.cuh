@@ -78,6 +78,7 @@ struct Ctx {
   float *t2;
   unsigned long long *bv64, *mv64;   // (epoch << 32 | float bits) per blur item / per sorted position
   BlurPrep *prep;
+  unsigned *colist;           // carried-only stale items (pixels without events in the batch)
   int chunk, warm, debug;
   int twarm;                  // warm-up events of a speculative long-segment piece
   unsigned blur_sleep;

@@ -307,20 +307,35 @@ __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
 // neighbour's latest event at that time: directly (batch-start value or
 // first-run value) or, when a blur produced it, after that blur's flag.
 // Runs for all items in parallel, before any blur (no waiting).
+__device__ __forceinline__ void prep_item(const Ctx &x, unsigned p);
+
+// Stale items are visited in pixel (tile-major sorted) order, not pop order:
+// a sorted position whose event is evicted stale names its item, a segment
+// head names its pixel's carried item, and k_popj lists the carried items of
+// pixels without events.  Neighbouring threads then resolve neighbouring
+// pixels' 3x3 taps, so the random pixel / position records they read are
+// shared in L1 instead of fetched again from L2.
 __global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x) {
   pdl_wait();
-  const BatchScalars b = load_bs(x);
-  const unsigned npop = (unsigned)(b.s_end - b.s_start);
-  const unsigned p = blockIdx.x * TPB + threadIdx.x;
-  if (p >= npop) return;
+  const long long B = x.bs->B;
+  const long long q = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (q < B) {
+    const unsigned bidx = x.posrec[q].bidx;
+    if (bidx != FIBAR_NONE) prep_item(x, bidx);
+    if (q == 0 || x.skey[q - 1] != x.skey[q]) {
+      const unsigned carried = x.pt[x.ekey[x.sidx[q]]].carried;
+      if (carried != FIBAR_NONE) prep_item(x, carried);
+    }
+  } else if (q - B < (long long)x.bs->nco) {
+    prep_item(x, x.colist[q - B]);
+  }
+}
+
+__device__ __forceinline__ void prep_item(const Ctx &x, unsigned p) {
   const Item it = x.item[p];
   BlurPrep out;
   out.okm = 0;
   out.pend = 0;
-  if (it.pix == FIBAR_NONE) {
-    x.prep[p].okm = 0;
-    return;
-  }
   const unsigned jrel = it.jrel;
   const int cx = (int)(it.pix % (unsigned)x.W), cy = (int)(it.pix / (unsigned)x.W);
   unsigned nidx[9];
