@@ -79,6 +79,16 @@ typedef struct fibar_config {
    * other rows are left to their band's owner.  sensor_height = 0: no band. */
   int32_t band_y0;
   int32_t sensor_height;
+  /* Halo band (multi-GPU row-band partition, filter ON): the
+   * engine keeps the whole sensor's window (every rank sees every event) but
+   * blurs only the items of rows [halo_own_y0 - halo_rows, halo_own_y1 +
+   * halo_rows); the outermost of those rows, when it belongs to a neighbour,
+   * takes its blurred values from that neighbour (fibar_halo_round).
+   * halo_own_y1 = 0: off. */
+  int32_t halo_own_y0;
+  int32_t halo_own_y1;
+  int32_t halo_rows;
+  int32_t reserved1;
 } fibar_config;
 
 /* Allocate device state for one sensor.  stream: a cudaStream_t (NULL = legacy default). */
@@ -181,6 +191,34 @@ int fibar_pixel_trace(const int8_t *p, int64_t n, int32_t ntraces, int32_t dtype
  * state = 3 values per trace (l_prev, l_prev2, p_prev). */
 int fibar_pixel_trace_iir(const int8_t *p, int64_t n, int32_t ntraces, int32_t dtype, const double coef[3],
                           void *state, void *l, void *stream);
+
+/* Halo-band batches (engines created with halo_own_y1 > 0).  The host drives
+ * one batch at a time through rounds of halo exchange:
+ *
+ *   fibar_halo_batch   ingest, window pass, stale items, temporal replay and
+ *                      blur-tap resolution of one batch of n <= batch_capacity
+ *                      events (mem: where x/y/p live); synchronises and returns
+ *                      counts = {in_top, in_bot, out_top, out_bot}: the blur
+ *                      items of the injected rows (values to receive from the
+ *                      neighbours above / below) and of the rows those
+ *                      neighbours inject (values to send).  Both sides derive
+ *                      the same lists from the same global window, in pop order.
+ *   fibar_halo_round   one blur round (asynchronous).  in: in_top + in_bot
+ *                      words from the neighbours' last round, out: out_top +
+ *                      out_bot words.  A word is (bit 63: tainted | float bits
+ *                      in bits 0-31); tainted = the value depends on a halo
+ *                      value that was not yet final.  round 0 must pass all
+ *                      in-words tainted; later rounds recompute only items
+ *                      that were tainted.  When every rank's in-words of a
+ *                      round were untainted, that round was exact everywhere.
+ *   fibar_halo_finish  end-of-batch brightness (after the last round).
+ *
+ * These replace the blur loop of _full_chunk (_kernels.py:173-189) for a row
+ * band; the window pass is the same as fibar_process's. */
+int fibar_halo_batch(fibar_engine *eng, const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n, int32_t mem,
+                     int64_t counts[4]);
+int fibar_halo_round(fibar_engine *eng, int32_t round, const uint64_t *in_words, uint64_t *out_words);
+int fibar_halo_finish(fibar_engine *eng);
 
 const char *fibar_last_error(void);
 

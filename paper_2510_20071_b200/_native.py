@@ -26,6 +26,7 @@ EXPORTED = (
     "fibar_render", "fibar_read_qs", "fibar_counters", "fibar_read_state", "fibar_stats",
     "fibar_brightness_ptr", "fibar_last_error", "fibar_profile", "fibar_profile_read", "fibar_pending", "fibar_debug_times", "fibar_debug_prep", "fibar_render_grid", "fibar_copy_brightness", "fibar_decode_evf1",
     "fibar_count_events", "fibar_pixel_trace", "fibar_pixel_trace_iir",
+    "fibar_halo_batch", "fibar_halo_round", "fibar_halo_finish",
 )
 
 
@@ -50,6 +51,10 @@ class FibarConfig(C.Structure):
         ("batch_capacity", C.c_int64),
         ("band_y0", C.c_int32),
         ("sensor_height", C.c_int32),
+        ("halo_own_y0", C.c_int32),
+        ("halo_own_y1", C.c_int32),
+        ("halo_rows", C.c_int32),
+        ("reserved1", C.c_int32),
     ]
 
 
@@ -91,6 +96,9 @@ def load(path: str | None = None):
         "fibar_count_events": ([P, P, P, i64, i32, i64, P, P, P, P], C.c_int),
         "fibar_pixel_trace": ([P, i64, i32, i32, P, P, P, P, P, P], C.c_int),
         "fibar_pixel_trace_iir": ([P, i64, i32, i32, P, P, P, P], C.c_int),
+        "fibar_halo_batch": ([P, P, P, P, i64, i32, P], C.c_int),
+        "fibar_halo_round": ([P, i32, P, P], C.c_int),
+        "fibar_halo_finish": ([P], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)

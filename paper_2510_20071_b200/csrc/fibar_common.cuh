@@ -67,6 +67,7 @@ struct BatchState {
   unsigned ticket;     // blur work ticket
   unsigned nlong;      // long pixel segments
   unsigned nco;        // stale items of pixels with no events in the batch (listed by k_popj)
+  unsigned epoch0;     // the batch's first epoch (halo bands: one more per exchange round)
 };
 
 // Window / counter state living in device memory so no kernel needs a host

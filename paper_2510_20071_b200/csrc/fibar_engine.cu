@@ -201,6 +201,14 @@ struct fibar_engine {
   bool serial = false;   // FIBAR_SERIAL: blur stage on the engine stream (no overlap; for measurement)
   unsigned blur_sleep = 0;
   unsigned long long *dbg_t = nullptr, *dbg_g = nullptr;
+  // halo band (filter-ON row band): rows, item lists and the batch in flight
+  bool halo = false;
+  int hreg0 = 0, hreg1 = 0, hin_top = -1, hin_bot = -1, hout_top = -1, hout_bot = -1;
+  unsigned *hslot = nullptr, *hlist = nullptr, *hcnt = nullptr;
+  int hnb = 0;
+  long long hcount[4] = {0, 0, 0, 0};
+  bool hopen = false;   // a halo batch awaits its rounds / finish
+  Ctx hctx{};
 
   Ctx ctx(const unsigned *skey, const unsigned *sidx, long long n_raw, int par) const {
     Ctx x{};
@@ -266,6 +274,15 @@ struct fibar_engine {
     x.dbg_t = dbg_t;
     x.dbg_g = dbg_g;
     x.warm = warm;
+    x.halo = halo;
+    x.hreg0 = halo ? hreg0 : 0;
+    x.hreg1 = halo ? hreg1 : H;
+    x.hin_top = hin_top;
+    x.hin_bot = hin_bot;
+    x.hout_top = hout_top;
+    x.hout_bot = hout_bot;
+    x.hslot = hslot;
+    x.hin = nullptr;
     x.anc = anc;
     x.anc2 = anc2;
     x.lc = lc;
@@ -365,6 +382,20 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
     fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
     fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
+    if (g->halo) {
+      // halo band: the item lists of the exchanged rows and the tap
+      // resolution; the host then drives the blur rounds (fibar_halo_round)
+      const int nbh = (int)((n_raw + g->n_pix + 2 + TPB - 1) / TPB);
+      fibar_launch(L, "halo_count", k_halo_count, nbh, TPB, 0, s, x, g->hcnt, nbh);
+      scan_exclusive_u32(L, g->hcnt, 4 * nbh + 1);
+      fibar_launch(L, "halo_write", k_halo_write, nbh, TPB, 0, s, x, (const unsigned *)g->hcnt, nbh, g->hlist);
+      const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
+      fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, s, x);
+      g->hnb = nbh;
+      g->hctx = x;
+      CK(cudaGetLastError());
+      return 0;
+    }
     // blur stage on its own stream: overlaps the next batch's front end
     cudaStream_t bs = (g->serial || graph) ? s : g->bstream;
     if (!graph) {
@@ -615,8 +646,31 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     if (cfg->spatial_enabled && (cfg->band_y0 != 0 || cfg->height != cfg->sensor_height))
       return fail(FIBAR_E_CONFIG, "row bands need the spatial filter off (the window is one global FIFO)");
   }
+  const bool halo = cfg->halo_own_y1 > 0;
+  if (halo) {
+    const int y0 = cfg->halo_own_y0, y1 = cfg->halo_own_y1, G = cfg->halo_rows, Hh = cfg->height;
+    if (!cfg->spatial_enabled || !cfg->blur_enabled)
+      return fail(FIBAR_E_CONFIG, "halo bands are for the spatial filter with blur (filter OFF: row bands)");
+    if (cfg->sensor_height > 0) return fail(FIBAR_E_CONFIG, "halo band and filter-OFF row band are exclusive");
+    if (y0 < 0 || y1 > Hh || y0 >= y1) return fail(FIBAR_E_CONFIG, "halo band rows outside the sensor");
+    if (G < 1 || G > y1 - y0) return fail(FIBAR_E_CONFIG, "halo rows must be in [1, band rows]");
+    if ((y0 > 0 && y0 - G < 0) || (y1 < Hh && y1 + G > Hh))
+      return fail(FIBAR_E_CONFIG, "halo rows exceed the neighbouring band");
+  }
   fibar_engine *g = new fibar_engine();
   g->cfg = *cfg;
+  if (halo) {
+    const int y0 = cfg->halo_own_y0, y1 = cfg->halo_own_y1, G = cfg->halo_rows, Hh = cfg->height;
+    g->halo = true;
+    g->hreg0 = std::max(0, y0 - G);
+    g->hreg1 = std::min(Hh, y1 + G);
+    g->hin_top = y0 > 0 ? y0 - G : -1;
+    g->hin_bot = y1 < Hh ? y1 + G - 1 : -1;
+    g->hout_top = y0 > 0 ? y0 + G - 1 : -1;
+    g->hout_bot = y1 < Hh ? y1 - G : -1;
+    g->serial = true;        // every kernel on the engine stream (rounds are host driven)
+    g->graphs_on = false;
+  }
   g->cfg.gain = nullptr;
   g->W = cfg->width;
   g->H = cfg->height;
@@ -650,6 +704,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // the second stream with the whole GPU.
   int green_sms = 16;
   if (const char *v = getenv("FIBAR_GREEN")) green_sms = atoi(v);
+  if (halo) green_sms = 0;
   if (green_sms > 0 && cfg->spatial_enabled && !g->serial) {
     const unsigned want = (unsigned)std::max(8, green_sms);
     CUdevice cdev;
@@ -794,6 +849,12 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->lu, T);
     rc |= dalloc(&g->ch, T);
   }
+  if (g->halo) {
+    const long long nbh = (Bc + n + 2 + TPB - 1) / TPB;
+    rc |= dalloc(&g->hslot, npop_cap);
+    rc |= dalloc(&g->hlist, 4 * (Bc + n + 2));
+    rc |= dalloc(&g->hcnt, 4 * nbh + 1);
+  }
   if (g->spatial && getenv("FIBAR_DEBUG_TIMES")) {
     rc |= dalloc(&g->dbg_t, npop_cap);
     rc |= dalloc(&g->dbg_g, npop_cap);
@@ -817,7 +878,7 @@ int fibar_destroy(fibar_engine *g) {
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
                   g->dp, g->S, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
-                  g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g};
+                  g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (cudaEvent_t ev : g->L.pool) cudaEventDestroy(ev);
@@ -867,6 +928,7 @@ int fibar_reset(fibar_engine *g) {
 
 int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n, int32_t mem) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (g->halo) return fail(FIBAR_E_CONFIG, "halo-band engines take batches through fibar_halo_batch");
   if (n <= 0) return 0;
   long long off = 0;
   if (mem == FIBAR_MEM_DEVICE) {
@@ -943,6 +1005,68 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
       if (rc) return rc;
     }
   }
+  return 0;
+}
+
+int fibar_halo_batch(fibar_engine *g, const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n, int32_t mem,
+                     int64_t counts[4]) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (!g->halo) return fail(FIBAR_E_CONFIG, "not a halo-band engine");
+  if (g->hopen) return fail(FIBAR_E_CONFIG, "previous halo batch not finished");
+  if (n < 0 || n > g->Bcap) return fail(FIBAR_E_CONFIG, "halo batch larger than the batch capacity");
+  int rc = sync_point(g);   // packets given to fibar_process run first
+  if (rc) return rc;
+  for (int c = 0; c < 4; ++c) g->hcount[c] = 0;
+  if (n > 0) {
+    cudaStream_t s = g->L.stream;
+    if (mem != FIBAR_MEM_DEVICE) {
+      CK(cudaMemcpyAsync(g->sx[0], x, sizeof(uint16_t) * n, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(g->sy[0], y, sizeof(uint16_t) * n, cudaMemcpyHostToDevice, s));
+      CK(cudaMemcpyAsync(g->sp_[0], p, sizeof(int8_t) * n, cudaMemcpyHostToDevice, s));
+      x = g->sx[0];
+      y = g->sy[0];
+      p = g->sp_[0];
+    }
+    const int par = (int)(g->batches & 1);
+    rc = enqueue_batch(g, x, y, p, n, nullptr, par, false);
+    if (rc) return rc;
+    unsigned tot[5];
+    for (int c = 0; c <= 4; ++c)
+      CK(cudaMemcpyAsync(&tot[c], g->hcnt + (long long)c * g->hnb, sizeof(unsigned), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int c = 0; c < 4; ++c) g->hcount[c] = (long long)(tot[c + 1] - tot[c]);
+    g->hopen = true;
+  }
+  for (int c = 0; c < 4; ++c) counts[c] = g->hcount[c];
+  return 0;
+}
+
+int fibar_halo_round(fibar_engine *g, int32_t round, const uint64_t *in_words, uint64_t *out_words) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (!g->halo) return fail(FIBAR_E_CONFIG, "not a halo-band engine");
+  if (!g->hopen) return 0;   // empty batch: nothing to blur
+  Launcher &L = g->L;
+  cudaStream_t s = L.stream;
+  Ctx x = g->hctx;
+  x.hin = (const unsigned long long *)in_words;
+  if (round > 0) fibar_launch(L, "halo_epoch", k_halo_epoch, 1, 1, 0, s, x);
+  fibar_launch(L, "blur", k_blur, g->blur_grid_serial, TPB, 0, s, x);
+  const long long n_in = g->hcount[0] + g->hcount[1], n_out = g->hcount[2] + g->hcount[3];
+  if (n_out > 0)
+    fibar_launch(L, "halo_collect", k_halo_collect, (int)((n_out + TPB - 1) / TPB), TPB, 0, s, x,
+                 (const unsigned *)g->hlist, n_in, n_out, (unsigned long long *)out_words);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int fibar_halo_finish(fibar_engine *g) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (!g->halo) return fail(FIBAR_E_CONFIG, "not a halo-band engine");
+  if (!g->hopen) return 0;
+  fibar_launch(g->L, "final", k_final, g->nsm * 8, TPB, 0, g->L.stream, g->hctx);
+  CK(cudaGetLastError());
+  g->hopen = false;
+  g->batches++;
   return 0;
 }
 

@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->nco = 0;
     s->epoch += 1;
     b->epoch = s->epoch;
+    b->epoch0 = s->epoch;
   }
 }
 

@@ -26,6 +26,9 @@ constexpr int LONG_TPB = 256;      // lanes per long segment (one block)
 constexpr int LONG_PIECE = 64;     // minimum events per lane before more lanes join
 constexpr int EV_PER_THREAD = 2;
 constexpr int EV_TILE = TPB * EV_PER_THREAD;
+// halo bands: a prep record with this okm is an injected item (val[0] = its in-word slot)
+constexpr unsigned HALO_OKM = 1u << 9;
+constexpr unsigned TAINT_HI = 0x80000000u;   // taint bit of a value word's high half (bit 63)
 
 struct ChunkRec {
   long long st_s, st_q;                          // state after event b_c - 1 (speculative start)
@@ -79,6 +82,13 @@ struct Ctx {
   unsigned long long *bv64, *mv64;   // (epoch << 32 | float bits) per blur item / per sorted position
   BlurPrep *prep;
   unsigned *colist;           // carried-only stale items (pixels without events in the batch)
+  // halo band (filter-ON row band); halo == 0: the whole sensor
+  int halo;
+  int hreg0, hreg1;          // rows whose blur items this engine takes
+  int hin_top, hin_bot;      // rows whose items are injected from the neighbours (-1: none)
+  int hout_top, hout_bot;    // rows whose items the neighbours inject (-1: none)
+  unsigned *hslot;           // per injected item: its in-word slot
+  const unsigned long long *hin;   // this round's in-words
   int chunk, warm, debug;
   int twarm;                  // warm-up events of a speculative long-segment piece
   unsigned blur_sleep;
@@ -90,7 +100,7 @@ struct Ctx {
 
 struct BatchScalars {
   long long E0, B, s_start, s_end;
-  unsigned epoch;
+  unsigned epoch, epoch0;
 };
 
 __device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
@@ -100,6 +110,7 @@ __device__ __forceinline__ BatchScalars load_bs(const Ctx &x) {
   b.s_start = x.bs->s_start;
   b.s_end = b.s_start + x.bs->npop;
   b.epoch = x.bs->epoch;
+  b.epoch0 = x.bs->epoch0;
   return b;
 }
 
@@ -133,6 +144,11 @@ __global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x);
 __global__ void __launch_bounds__(TPB) k_blur(Ctx x);
 __global__ void __launch_bounds__(TPB) k_final(Ctx x);
 __global__ void k_batch_end(Ctx x);
+__global__ void __launch_bounds__(TPB) k_halo_count(Ctx x, unsigned *cnt, int nb);
+__global__ void __launch_bounds__(TPB) k_halo_write(Ctx x, const unsigned *cnt, int nb, unsigned *hlist);
+__global__ void k_halo_epoch(Ctx x);
+__global__ void __launch_bounds__(TPB) k_halo_collect(Ctx x, const unsigned *hlist, long long n_in, long long n_out,
+                                                      unsigned long long *out);
 __global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, long long n, SelState *sel, int pass, double g_lo, double g_hi);
 __global__ void k_sel_init(SelState *sel, unsigned r0, unsigned r1, unsigned r2, unsigned r3);
 __global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound);

@@ -338,6 +338,21 @@ __device__ __forceinline__ void prep_item(const Ctx &x, unsigned p) {
   out.pend = 0;
   const unsigned jrel = it.jrel;
   const int cx = (int)(it.pix % (unsigned)x.W), cy = (int)(it.pix / (unsigned)x.W);
+  if (x.halo) {
+    // halo band: items outside the band's rows are not this engine's; the
+    // outermost halo rows take their blurred values from the neighbours
+    if (cy < x.hreg0 || cy >= x.hreg1) {
+      x.prep[p].okm = 0;
+      return;
+    }
+    if (cy == x.hin_top || cy == x.hin_bot) {
+      out.okm = HALO_OKM;
+      out.val[0] = x.hslot[p];
+      out.runpos = it.runpos;
+      x.prep[p] = out;
+      return;
+    }
+  }
   unsigned nidx[9];
   uint4 pr[9];   // (st, end, carried, -) of each tap's pixel record
 #pragma unroll
@@ -408,7 +423,7 @@ __device__ __forceinline__ void prep_item(const Ctx &x, unsigned p) {
 // after blur p of pixel c: brightness of c's following events (up to and
 // including its next blurred event) is rebuilt from the blurred value
 __device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars &b, unsigned p, unsigned r,
-                                                float v) {
+                                                float v, unsigned hi) {
   // run positions and their terms are fetched four at a time, so a run costs
   // one round trip per four positions instead of one per position
   while (r < b.B) {
@@ -425,7 +440,7 @@ __device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars
       if (rb[u] != p) return;
       v = faddr(fmulr(x.beta, v), tt[u]);
       x.posrec[r + u].val = v;
-      st_relaxed_u64(&x.mv64[r + u], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
+      st_relaxed_u64(&x.mv64[r + u], ((unsigned long long)hi << 32) | __float_as_uint(v));
     }
     r += 4;
   }
@@ -443,6 +458,7 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
   const int lane = threadIdx.x & 31;
   unsigned p = FIBAR_NONE, okm = 0, pend = 0, runpos = FIBAR_NONE;
+  unsigned tnt = 0;   // halo bands: the value read a not-yet-final halo value (TAINT_HI or 0)
   unsigned val[9];
   bool exhausted = false;
   // the warp draws 32 items at a time from the global ticket and hands them
@@ -471,7 +487,22 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
           const uint4 *rec = reinterpret_cast<const uint4 *>(&x.prep[q]);
           const uint4 n0 = __ldcg(rec);
           okm = n0.x;
-          if (okm) {
+          tnt = 0;
+          if (okm && x.halo && b.epoch != b.epoch0) {
+            // a later exchange round: an item already final (untainted) in an
+            // earlier round of this batch keeps its value and its rebuilt run
+            const unsigned hw = (unsigned)(ld_relaxed_u64(&x.bv64[q]) >> 32);
+            if (!(hw & TAINT_HI) && hw >= b.epoch0) okm = 0;
+          }
+          if (okm == HALO_OKM) {
+            // injected halo item: its blurred value comes from the neighbour
+            const unsigned long long w = x.hin[n0.z];
+            p = q;
+            pend = 0;
+            val[0] = (unsigned)w;
+            tnt = (unsigned)(w >> 32) & TAINT_HI;
+            runpos = __ldcg(rec + 2).w;
+          } else if (okm) {
             const uint4 n1 = __ldcg(rec + 1), n2 = __ldcg(rec + 2);
             p = q;
             pend = n0.y;
@@ -503,27 +534,40 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
         if (!((pend >> t) & 1)) continue;
         const unsigned s = val[t];
         const unsigned long long w = ld_relaxed_u64((s & 0x80000000u) ? &x.mv64[s & 0x7FFFFFFFu] : &x.bv64[s]);
-        if ((unsigned)(w >> 32) != b.epoch) continue;
+        const unsigned hw = (unsigned)(w >> 32);
+        if (hw != b.epoch) {
+          // halo bands: this round's word (tainted) or a final one from an
+          // earlier round of the batch; otherwise not there yet
+          const unsigned e = hw & ~TAINT_HI;
+          if (!(x.halo && e >= b.epoch0 && (e == b.epoch || !(hw & TAINT_HI)))) continue;
+          tnt |= hw & TAINT_HI;
+        }
         val[t] = (unsigned)w;
         pend &= ~(1u << t);
       }
       if (pend == 0) {
-        float num = 0.0f, den = 0.0f;
+        float v;
+        if (okm == HALO_OKM) {
+          v = __uint_as_float(val[0]);
+        } else {
+          float num = 0.0f, den = 0.0f;
 #pragma unroll
-        for (int t = 0; t < 9; ++t) {
-          if (!((okm >> t) & 1)) continue;
-          const float w = (float)((t / 3 == 1 ? 2 : 1) * (t % 3 == 1 ? 2 : 1));
-          num = faddr(num, fmulr(w, __uint_as_float(val[t])));
-          den = faddr(den, w);
+          for (int t = 0; t < 9; ++t) {
+            if (!((okm >> t) & 1)) continue;
+            const float w = (float)((t / 3 == 1 ? 2 : 1) * (t % 3 == 1 ? 2 : 1));
+            num = faddr(num, fmulr(w, __uint_as_float(val[t])));
+            den = faddr(den, w);
+          }
+          v = __fdiv_rn(num, den);
         }
-        const float v = __fdiv_rn(num, den);
-        st_relaxed_u64(&x.bv64[p], ((unsigned long long)b.epoch << 32) | __float_as_uint(v));
+        const unsigned hi = b.epoch | tnt;
+        st_relaxed_u64(&x.bv64[p], ((unsigned long long)hi << 32) | __float_as_uint(v));
         if (x.dbg_t) {
           unsigned long long tt;
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           x.dbg_t[p] = tt;
         }
-        if (runpos != FIBAR_NONE) materialise_run(x, b, p, runpos, v);
+        if (runpos != FIBAR_NONE) materialise_run(x, b, p, runpos, v, hi);
         p = FIBAR_NONE;
       } else if (x.blur_sleep) {
         __nanosleep(x.blur_sleep);
@@ -568,6 +612,80 @@ __global__ void __launch_bounds__(TPB) k_final(Ctx x) {
       }
     }
   }
+}
+
+// ------------------------------------------------------------ halo band ---
+// Filter-ON row bands.  Each rank blurs the items of its rows
+// plus a halo of G rows; the outermost halo row's items are injected from the
+// neighbour that owns them.  The item lists are built from the global window
+// (identical on every rank) in pop order, so both sides of a boundary agree
+// on the order of the words they exchange without sending indices.
+
+__device__ __forceinline__ unsigned halo_classes(const Ctx &x, unsigned p, unsigned npop) {
+  if (p >= npop) return 0u;
+  const unsigned pix = x.item[p].pix;
+  if (pix == FIBAR_NONE) return 0u;
+  const int row = (int)(pix / (unsigned)x.W);
+  return (unsigned)(row == x.hin_top) | (unsigned)(row == x.hin_bot) << 1 | (unsigned)(row == x.hout_top) << 2 |
+         (unsigned)(row == x.hout_bot) << 3;
+}
+
+// per block and class (in_top, in_bot, out_top, out_bot): item counts, laid
+// out class-major so one exclusive scan gives every item its slot in the
+// concatenated list [in_top | in_bot | out_top | out_bot]
+__global__ void __launch_bounds__(TPB) k_halo_count(Ctx x, unsigned *cnt, int nb) {
+  pdl_wait();
+  const unsigned npop = (unsigned)x.bs->npop;
+  const unsigned p = blockIdx.x * TPB + threadIdx.x;
+  const unsigned cls = halo_classes(x, p, npop);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const int n = __syncthreads_count((cls >> c) & 1u);
+    if (threadIdx.x == 0) cnt[c * nb + blockIdx.x] = (unsigned)n;
+  }
+}
+
+__global__ void __launch_bounds__(TPB) k_halo_write(Ctx x, const unsigned *cnt, int nb, unsigned *hlist) {
+  pdl_wait();
+  __shared__ unsigned wc[4][TPB / 32];
+  const unsigned npop = (unsigned)x.bs->npop;
+  const unsigned p = blockIdx.x * TPB + threadIdx.x;
+  const unsigned cls = halo_classes(x, p, npop);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned below[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const unsigned m = __ballot_sync(0xffffffffu, (cls >> c) & 1u);
+    below[c] = __popc(m & ((1u << lane) - 1u));
+    if (lane == 0) wc[c][wid] = __popc(m);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    if (!((cls >> c) & 1u)) continue;
+    unsigned pos = cnt[c * nb + blockIdx.x] + below[c];
+    for (int w = 0; w < wid; ++w) pos += wc[c][w];
+    hlist[pos] = p;
+    if (c < 2) x.hslot[p] = pos;   // in-words are [in_top | in_bot], the list's first part
+  }
+}
+
+// next exchange round of the batch: a fresh epoch (this round's words) and ticket
+__global__ void k_halo_epoch(Ctx x) {
+  pdl_wait();
+  x.st->epoch += 1;
+  x.bs->epoch = x.st->epoch;
+  x.bs->ticket = 0;
+}
+
+// out-words of the round: taint bit | float bits of the items the neighbours inject
+__global__ void __launch_bounds__(TPB) k_halo_collect(Ctx x, const unsigned *hlist, long long n_in, long long n_out,
+                                                      unsigned long long *out) {
+  pdl_wait();
+  const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (i >= n_out) return;
+  const unsigned long long w = ld_relaxed_u64(&x.bv64[hlist[n_in + i]]);
+  out[i] = (w & (1ull << 63)) | (w & 0xFFFFFFFFull);
 }
 
 __global__ void k_batch_end(Ctx x) {

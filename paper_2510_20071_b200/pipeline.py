@@ -112,6 +112,7 @@ class ReconstructionEngine:
         batch_capacity: int | None = None,
         device=None,
         row_band: tuple[int, int] | None = None,
+        halo_band: tuple[int, int, int] | None = None,
     ):
         if params.q_max > geometry.n_pix:
             raise ConfigError("q_max exceeds pixel count")
@@ -161,6 +162,9 @@ class ReconstructionEngine:
             batch_capacity=int(batch_capacity or 0),
             band_y0=int(row_band[0]) if row_band else 0,
             sensor_height=int(row_band[1]) if row_band else 0,
+            halo_own_y0=int(halo_band[0]) if halo_band else 0,
+            halo_own_y1=int(halo_band[1]) if halo_band else 0,
+            halo_rows=int(halo_band[2]) if halo_band else 0,
         )
         handle = C.c_void_p()
         with torch.cuda.device(self.device):
@@ -419,6 +423,49 @@ class ReconstructionEngine:
         if rc:
             _native.check(rc, "fibar_process")
         self._note_last_t(xs, ys, ts)
+
+    # -- halo-band batches (filter-ON row bands, bands.HaloBandEngine) ----------
+    def halo_batch(self, block) -> tuple[int, int, int, int]:
+        """Front end of one batch (<= batch capacity events) on a halo-band engine:
+        window pass, stale items, temporal replay, blur-tap resolution.  Returns
+        (in_top, in_bot, out_top, out_bot): how many blur values this band
+        receives from / sends to its neighbours per round (fibar_halo_batch)."""
+        counts = np.zeros(4, np.int64)
+        self._sync_stream()
+        if isinstance(block, DeviceEventArray):
+            torch = _torch()
+            x = block.x.to(torch.int16).contiguous() if block.x.dtype not in self._xy_ok else block.x.contiguous()
+            y = block.y.to(torch.int16).contiguous() if block.y.dtype not in self._xy_ok else block.y.contiguous()
+            p = block.p.to(torch.int8).contiguous()
+            if self.strict:
+                self._check_device_packet(block, x, y)
+            rc = self._lib.fibar_halo_batch(self._h, x.data_ptr(), y.data_ptr(), p.data_ptr(), int(x.shape[0]),
+                                            _native.FIBAR_MEM_DEVICE, counts.ctypes.data)
+            _native.check(rc, "fibar_halo_batch")
+            if block.t is not None and len(block.t):
+                self._note_last_t(block.x.cpu().numpy(), block.y.cpu().numpy(), block.t)
+        else:
+            xs = np.ascontiguousarray(block.x, np.uint16)
+            ys = np.ascontiguousarray(block.y, np.uint16)
+            ps = np.ascontiguousarray(block.p, np.int8)
+            rc = self._lib.fibar_halo_batch(self._h, xs.ctypes.data, ys.ctypes.data, ps.ctypes.data, len(xs),
+                                            _native.FIBAR_MEM_HOST, counts.ctypes.data)
+            _native.check(rc, "fibar_halo_batch")
+            if len(xs):
+                self._note_last_t(xs, ys, block.t)
+        return tuple(int(v) for v in counts)
+
+    def halo_round(self, rnd: int, in_words, out_words) -> None:
+        """One blur round: in_words / out_words are int64 CUDA tensors (bit 63 =
+        tainted, bits 0-31 = float32 bits), laid out [top | bottom]."""
+        self._sync_stream()
+        rc = self._lib.fibar_halo_round(self._h, int(rnd), in_words.data_ptr() if in_words.numel() else None,
+                                        out_words.data_ptr() if out_words.numel() else None)
+        _native.check(rc, "fibar_halo_round")
+
+    def halo_finish(self) -> None:
+        self._sync_stream()
+        _native.check(self._lib.fibar_halo_finish(self._h), "fibar_halo_finish")
 
     def _note_last_t(self, xs, ys, ts) -> None:
         # the reference keeps the time of the last *in-bounds* event (pipeline.py:558)
