@@ -22,8 +22,11 @@ push all 1,000 packets through ``ReconstructionEngine.process_array``, render.
 
 ``--impl reference`` times that CPU implementation alone (rank 0; other ranks
 exit) and prints the same JSON shape with ``"impl": "reference"``.
-Multi-GPU: the filter-ON window is one global FIFO, so N GPUs run N
-independent replicas (seeds rank, weak scaling) -- see DESIGN.md.
+Multi-GPU: filter OFF runs row bands (strong scaling).  Filter
+ON runs N independent replicas by default (seeds rank, weak scaling): the
+window is one global FIFO and both of the step's chains are latency-bound, so
+``--bands`` (halo row bands, exact, NCCL halo exchange) is available but not
+faster than one GPU.
 """
 
 from __future__ import annotations
@@ -63,8 +66,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one step, for ncu launch lists")
-    ap.add_argument("--bands", action="store_true", help="row-band partition even on one rank")
-    ap.add_argument("--replicas", action="store_true", help="filter ON, N>1: independent replicas instead of halo bands")
+    ap.add_argument("--bands", action="store_true",
+                    help="row bands (filter OFF: the default at N>1; filter ON: halo bands instead of replicas)")
     ap.add_argument("--halo", type=int, default=8, help="halo rows of the filter-ON row bands")
     ap.add_argument("--halo-batch", type=int, default=1 << 18, help="events per halo-band batch")
     return ap.parse_args()
@@ -593,7 +596,7 @@ def main():
         dist = tdist
         cfg = workloads.CONFIGS[args.config]
         spatial = (args.filter == "on") if args.filter else (cfg["spatial"] if cfg["spatial"] is not None else True)
-        if not spatial or not args.replicas:
+        if not spatial or args.bands:
             line = (run_bands if not spatial else run_halo_bands)(args, rank, world, dist)
             if rank == 0:
                 print(json.dumps(line))

@@ -101,6 +101,8 @@ def load(path: str | None = None):
         "fibar_halo_finish": ([P], C.c_int),
     }
     for name, (args, res) in sig.items():
+        if path != LIB_PATH and not hasattr(L, name):
+            continue   # an older experimental build (FIBAR_LIB) without this entry point
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = res

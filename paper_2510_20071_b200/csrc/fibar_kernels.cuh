@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x);
 __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x);
 __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x);
 __global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x);
+template <bool HALO>
 __global__ void __launch_bounds__(TPB) k_blur(Ctx x);
 __global__ void __launch_bounds__(TPB) k_final(Ctx x);
 __global__ void k_batch_end(Ctx x);

@@ -452,6 +452,7 @@ __device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars
 // running; a waiting lane re-polls the pending flags its prep record left
 // open.  The blurred value is published (ready) before the
 // pixel's following run is rebuilt (mready).
+template <bool HALO>
 __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   pdl_wait();
   const BatchScalars b = load_bs(x);
@@ -460,6 +461,12 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   unsigned p = FIBAR_NONE, okm = 0, pend = 0, runpos = FIBAR_NONE;
   unsigned tnt = 0;   // halo bands: the value read a not-yet-final halo value (TAINT_HI or 0)
   unsigned val[9];
+#ifdef FIBAR_RUN_PREFETCH
+  // the first positions of the run this item rebuilds, loaded while its taps
+  // are still pending: the rebuild then costs no round trip after the blur
+  unsigned prb[FIBAR_RUN_PREFETCH];
+  float ptt[FIBAR_RUN_PREFETCH];
+#endif
   bool exhausted = false;
   // the warp draws 32 items at a time from the global ticket and hands them
   // to its free lanes in order (one contended atomic per 32 items); every
@@ -488,13 +495,13 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
           const uint4 n0 = __ldcg(rec);
           okm = n0.x;
           tnt = 0;
-          if (okm && x.halo && b.epoch != b.epoch0) {
+          if (okm && HALO && b.epoch != b.epoch0) {
             // a later exchange round: an item already final (untainted) in an
             // earlier round of this batch keeps its value and its rebuilt run
             const unsigned hw = (unsigned)(ld_relaxed_u64(&x.bv64[q]) >> 32);
             if (!(hw & TAINT_HI) && hw >= b.epoch0) okm = 0;
           }
-          if (okm == HALO_OKM) {
+          if (HALO && okm == HALO_OKM) {
             // injected halo item: its blurred value comes from the neighbour
             const unsigned long long w = x.hin[n0.z];
             p = q;
@@ -516,6 +523,14 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
             val[7] = n2.y;
             val[8] = n2.z;
             runpos = n2.w;
+#ifdef FIBAR_RUN_PREFETCH
+#pragma unroll
+            for (int u = 0; u < FIBAR_RUN_PREFETCH; ++u) {
+              const bool in = runpos != FIBAR_NONE && runpos + u < b.B;
+              prb[u] = in ? __ldcg(&x.posrec[runpos + u].runbase) : FIBAR_NONE;
+              ptt[u] = in ? __ldcg(&x.t2[runpos + u]) : 0.0f;
+            }
+#endif
             if (x.dbg_g) {
               unsigned long long tt;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
@@ -539,7 +554,7 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
           // halo bands: this round's word (tainted) or a final one from an
           // earlier round of the batch; otherwise not there yet
           const unsigned e = hw & ~TAINT_HI;
-          if (!(x.halo && e >= b.epoch0 && (e == b.epoch || !(hw & TAINT_HI)))) continue;
+          if (!(HALO && e >= b.epoch0 && (e == b.epoch || !(hw & TAINT_HI)))) continue;
           tnt |= hw & TAINT_HI;
         }
         val[t] = (unsigned)w;
@@ -547,7 +562,7 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
       }
       if (pend == 0) {
         float v;
-        if (okm == HALO_OKM) {
+        if (HALO && okm == HALO_OKM) {
           v = __uint_as_float(val[0]);
         } else {
           float num = 0.0f, den = 0.0f;
@@ -567,7 +582,27 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           x.dbg_t[p] = tt;
         }
+#ifdef FIBAR_RUN_PREFETCH
+        if (runpos != FIBAR_NONE && okm != HALO_OKM) {
+          float v2 = v;
+          bool cont = true;
+#pragma unroll
+          for (int u = 0; u < FIBAR_RUN_PREFETCH; ++u) {
+            if (!cont || prb[u] != p) {
+              cont = false;
+              continue;
+            }
+            v2 = faddr(fmulr(x.beta, v2), ptt[u]);
+            x.posrec[runpos + u].val = v2;
+            st_relaxed_u64(&x.mv64[runpos + u], ((unsigned long long)hi << 32) | __float_as_uint(v2));
+          }
+          if (cont) materialise_run(x, b, p, runpos + FIBAR_RUN_PREFETCH, v2, hi);
+        } else if (runpos != FIBAR_NONE) {
+          materialise_run(x, b, p, runpos, v, hi);
+        }
+#else
         if (runpos != FIBAR_NONE) materialise_run(x, b, p, runpos, v, hi);
+#endif
         p = FIBAR_NONE;
       } else if (x.blur_sleep) {
         __nanosleep(x.blur_sleep);
@@ -576,6 +611,9 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
     if (__all_sync(0xffffffffu, exhausted && p == FIBAR_NONE)) break;
   }
 }
+
+template __global__ void k_blur<false>(Ctx x);
+template __global__ void k_blur<true>(Ctx x);
 
 // ------------------------------------------------------------------ final ---
 
