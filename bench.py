@@ -63,6 +63,8 @@ def parse():
     ap.add_argument("--packet", type=int, default=None)
     ap.add_argument("--filter", default=None, choices=("on", "off"))
     ap.add_argument("--batch-cap", type=int, default=1 << 20)
+    ap.add_argument("--readout", default=None, choices=("end", "packet"),
+                    help="robust read-out at the end of the stream or after every packet (config default)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="one step, for ncu launch lists")
@@ -84,8 +86,10 @@ def workload(args, rank):
     kw = {"speed": cfg["speed"]} if "speed" in cfg else {}
     ev = workloads.make(cfg["kind"], geom, n, seed=rank, **kw)
     params = compute_params(40.0, Fraction(1, 2), geom, spatial_enabled=spatial)
+    args.readout = args.readout or cfg.get("readout", "end")
+    ro = "robust read-out after every packet" if args.readout == "packet" else "robust read-out at end"
     name = f"config{args.config}:{geom.width}x{geom.height},{n // 1_000_000}M events,{cfg['kind']}," \
-           f"filter {'on' if spatial else 'off'},{packet}-event packets,robust read-out at end"
+           f"filter {'on' if spatial else 'off'},{packet}-event packets,{ro}"
     return geom, params, ev, packet, name
 
 
@@ -211,11 +215,16 @@ def run_ours(args, rank, world, dist):
     # the step's packets, resident in HBM before timing (views of one buffer)
     dev_packets = [DeviceEventArray(xd[a:b], yd[a:b], pd[a:b]) for a, b in zip(cuts[:-1], cuts[1:])]
 
+    per_packet = args.readout == "packet"
+
     def step_device():
         eng.reset()
         for blk in dev_packets:
             eng.process_array(blk)
-        eng.render_device("robust", out=frame)
+            if per_packet:
+                eng.render_device("robust", out=frame)
+        if not per_packet:
+            eng.render_device("robust", out=frame)
 
     # host arm: pinned host columns, numpy views per packet
     xh = torch.from_numpy(ev.x.view(np.int16)).pin_memory().numpy().view(np.uint16)
@@ -229,7 +238,10 @@ def run_ours(args, rank, world, dist):
         eng.reset()
         for blk in host_packets:
             eng.process_array(blk)
-        last_frame["f"] = eng.render("robust")
+            if per_packet:
+                last_frame["f"] = eng.render("robust")
+        if not per_packet:
+            last_frame["f"] = eng.render("robust")
 
     def timed(step, steps, warmup):
         for _ in range(warmup):
@@ -302,7 +314,7 @@ def run_ours(args, rank, world, dist):
         "share_of_step": dms / tot_ms if tot_ms else None, "mean_launch_us": launch_s * 1e6,
         "bytes_per_launch": bytes_launch,
     }
-    R = 9 * geom.n_pix / n
+    R = 9 * geom.n_pix / (packet if per_packet else n)
     b_on = 21 + 24 * u_packet + 8 * blur_per_ev + R if params.spatial_enabled else 13 + 16 * u_packet + R
     path_achieved = value * 1e6 / world * b_on / 1e9
     path_roofline = {"bytes_per_event": b_on, "u_packet": u_packet, "u_batch": u, "blurs_per_event": blur_per_ev,
@@ -312,7 +324,8 @@ def run_ours(args, rank, world, dist):
     if not args.no_e2e:
         t_h = timed(step_host, max(1, args.steps), 1)
         e2e = {"value": n * world * max(1, args.steps) / t_h / 1e6, "unit": UNIT,
-               "h2d_bytes_per_step": int(5 * n), "d2h_bytes_per_step": int(geom.n_pix + 16),
+               "h2d_bytes_per_step": int(5 * n),
+               "d2h_bytes_per_step": int((geom.n_pix + 16) * (len(host_packets) if per_packet else 1)),
                "ms_per_step": t_h / max(1, args.steps) * 1e3}
         # the two arms must agree
         fd = frame.cpu().numpy()
@@ -519,8 +532,9 @@ def run_halo_bands(args, rank, world, dist):
     }
 
 
-def cpu_reference(geom, params, ev, packet, steps=1):
-    """Time the C oracle (single-threaded restatement of the reference kernels)."""
+def cpu_reference(geom, params, ev, packet, steps=1, per_packet=False):
+    """Time the C oracle (single-threaded restatement of the reference kernels),
+    with the same read-out cadence as our arm."""
     from oracle import oracle as orc
     n = len(ev)
     times = []
@@ -530,7 +544,10 @@ def cpu_reference(geom, params, ev, packet, steps=1):
         for a in range(0, n, packet):
             b = min(n, a + packet)
             eng.process_array(ev.t[a:b], ev.x[a:b], ev.y[a:b], ev.p[a:b])
-        eng.render("robust")
+            if per_packet:
+                eng.render("robust")
+        if not per_packet:
+            eng.render("robust")
         times.append(time.perf_counter() - t0)
     return times
 
@@ -569,9 +586,10 @@ def main():
             return
         geom, params, ev, packet, name = workload(args, 0)
         prev = pinned_one_core()
+        pp = args.readout == "packet"
         for _ in range(args.warmup):
-            cpu_reference(geom, params, ev.slice(0, min(len(ev), 1_000_000)), packet)
-        times = cpu_reference(geom, params, ev, packet, steps=args.steps)
+            cpu_reference(geom, params, ev.slice(0, min(len(ev), 1_000_000)), packet, per_packet=pp)
+        times = cpu_reference(geom, params, ev, packet, steps=args.steps, per_packet=pp)
         if prev:
             os.sched_setaffinity(0, prev)
         v = len(ev) * args.steps / sum(times) / 1e6
@@ -608,7 +626,7 @@ def main():
     result, (geom, params, ev, packet) = res
     if rank == 0 and world == 1 and not args.no_cpu:
         prev = pinned_one_core()
-        times = cpu_reference(geom, params, ev, packet, steps=1)
+        times = cpu_reference(geom, params, ev, packet, steps=1, per_packet=args.readout == "packet")
         if prev:
             os.sched_setaffinity(0, prev)
         v = len(ev) / times[0] / 1e6

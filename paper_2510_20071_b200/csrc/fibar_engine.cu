@@ -412,12 +412,12 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
         CK(cudaEventRecord(g->evP, bs));
         CK(cudaStreamWaitEvent(g->gstream, g->evP, 0));
         L.stream = g->gstream;
-        fibar_launch(L, "blur", k_blur<false>, g->gblocks, TPB, 0, g->gstream, x);
+        fibar_launch(L, "blur", k_blur, g->gblocks, TPB, 0, g->gstream, x);
         CK(cudaEventRecord(g->evG, g->gstream));
         CK(cudaStreamWaitEvent(bs, g->evG, 0));
         L.stream = bs;
       } else {
-        fibar_launch(L, "blur", k_blur<false>, graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs, x);
+        fibar_launch(L, "blur", k_blur, graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs, x);
       }
     }
     fibar_launch(L, "final", k_final, g->nsm * 8, TPB, 0, bs, x);
@@ -746,7 +746,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, dev);
   {
     int per_sm = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blur<false>, TPB, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_blur, TPB, 0);
     g->blur_grid_serial = g->nsm * std::max(1, std::min(per_sm, 4));   // graph form: nothing to overlap with
     // the blur stage overlaps the next batch's front end: one 256-thread block
     // per SM leaves the rest of each SM to the front end (measured: 1/SM gives
@@ -1051,7 +1051,7 @@ int fibar_halo_round(fibar_engine *g, int32_t round, const uint64_t *in_words, u
   Ctx x = g->hctx;
   x.hin = (const unsigned long long *)in_words;
   if (round > 0) fibar_launch(L, "halo_epoch", k_halo_epoch, 1, 1, 0, s, x);
-  fibar_launch(L, "blur", k_blur<true>, g->blur_grid_serial, TPB, 0, s, x);
+  fibar_launch(L, "blur", k_blur_halo, g->blur_grid_serial, TPB, 0, s, x);
   const long long n_in = g->hcount[0] + g->hcount[1], n_out = g->hcount[2] + g->hcount[3];
   if (n_out > 0)
     fibar_launch(L, "halo_collect", k_halo_collect, (int)((n_out + TPB - 1) / TPB), TPB, 0, s, x,

@@ -15,6 +15,10 @@ constexpr int NLIN = 7;      // coarse candidates q0 + c_lin_off[i]
 constexpr int NGEO = 12;     // coarse candidates q0 * c_geo_mul[i]
 constexpr int NCAND = NLIN + NGEO;
 constexpr int TPB = 256;
+#ifndef FIBAR_BLUR_MINB
+#define FIBAR_BLUR_MINB 1
+#endif
+constexpr int BLUR_MINB = FIBAR_BLUR_MINB;   // k_blur: min resident blocks per SM (register cap)
 constexpr unsigned ITEM_CARRIED_ONLY = 1u;   // Item.pad flag
 constexpr int IN_ITEMS = 8;
 constexpr int IN_TILE = TPB * IN_ITEMS;
@@ -141,8 +145,8 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x);
 __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x);
 __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x);
 __global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x);
-template <bool HALO>
-__global__ void __launch_bounds__(TPB) k_blur(Ctx x);
+__global__ void __launch_bounds__(TPB, BLUR_MINB) k_blur(Ctx x);
+__global__ void __launch_bounds__(TPB) k_blur_halo(Ctx x);   // halo-band engines
 __global__ void __launch_bounds__(TPB) k_final(Ctx x);
 __global__ void k_batch_end(Ctx x);
 __global__ void __launch_bounds__(TPB) k_halo_count(Ctx x, unsigned *cnt, int nb);

@@ -453,7 +453,7 @@ __device__ __forceinline__ void materialise_run(const Ctx &x, const BatchScalars
 // open.  The blurred value is published (ready) before the
 // pixel's following run is rebuilt (mready).
 template <bool HALO>
-__global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
+__device__ __forceinline__ void blur_lanes(const Ctx &x) {
   pdl_wait();
   const BatchScalars b = load_bs(x);
   const unsigned npop = (unsigned)(b.s_end - b.s_start);
@@ -612,8 +612,8 @@ __global__ void __launch_bounds__(TPB) k_blur(Ctx x) {
   }
 }
 
-template __global__ void k_blur<false>(Ctx x);
-template __global__ void k_blur<true>(Ctx x);
+__global__ void __launch_bounds__(TPB, BLUR_MINB) k_blur(Ctx x) { blur_lanes<false>(x); }
+__global__ void __launch_bounds__(TPB) k_blur_halo(Ctx x) { blur_lanes<true>(x); }
 
 // ------------------------------------------------------------------ final ---
 

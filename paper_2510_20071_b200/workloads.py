@@ -156,7 +156,8 @@ def packets(events: EventArray, size: int):
 CONFIGS = {
     1: dict(geometry=SensorGeometry(346, 260), n=1_000_000, spatial=False, packet=1_000_000, kind="uniform"),
     2: dict(geometry=SensorGeometry(640, 480), n=10_000_000, spatial=True, packet=10_000, kind="texture"),
-    3: dict(geometry=SensorGeometry(1280, 720), n=100_000_000, spatial=True, packet=100_000, kind="texture_noise_hot"),
+    3: dict(geometry=SensorGeometry(1280, 720), n=100_000_000, spatial=True, packet=100_000, kind="texture_noise_hot",
+            readout="packet"),
     4: dict(geometry=SensorGeometry(1280, 720), n=50_000_000, spatial=None, packet=None, kind="texture"),
     5: dict(geometry=SensorGeometry(2560, 1440), n=1_000_000_000, spatial=True, packet=1_000_000, kind="texture",
             speed=1000.0),
