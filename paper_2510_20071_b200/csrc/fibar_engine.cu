@@ -152,7 +152,7 @@ struct fibar_engine {
   Item *item2[2] = {nullptr, nullptr};
   PosRec *posrec2[2] = {nullptr, nullptr};
   float *t2_2[2] = {nullptr, nullptr};
-  int2 *anc = nullptr, *anc2 = nullptr;
+  int2 *anc = nullptr, *anc2 = nullptr, *anc0 = nullptr;
   long long *lc = nullptr, *lu = nullptr;
   ChunkRec *ch = nullptr;
   SelState *sel = nullptr;
@@ -285,6 +285,7 @@ struct fibar_engine {
     x.hin = nullptr;
     x.anc = anc;
     x.anc2 = anc2;
+    x.anc0 = anc0;
     x.lc = lc;
     x.lu = lu;
     x.ch = ch;
@@ -369,7 +370,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "link", k_link, nb, TPB, 0, s, x);
     fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
-    fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND, 1024, 0, s, x, g->anc, NCAND);
+    fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, g->anc, NCAND);
     fibar_launch(L, "fp", k_fp, (T + TPB - 1) / TPB, TPB, 0, s, x);
     fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
@@ -846,6 +847,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->colist, n + 1);
     rc |= dalloc(&g->anc, T * NCAND);
     rc |= dalloc(&g->anc2, T * NFINE);
+    rc |= dalloc(&g->anc0, T);
     rc |= dalloc(&g->lc, T);
     rc |= dalloc(&g->lu, T);
     rc |= dalloc(&g->ch, T);
@@ -878,7 +880,7 @@ int fibar_destroy(fibar_engine *g) {
   if (g->bstream) cudaStreamSynchronize(g->bstream);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
-                  g->dp, g->S, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist, g->anc, g->anc2, g->lc, g->lu, g->ch, g->sel, g->frame,
+                  g->dp, g->S, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);

@@ -324,6 +324,7 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
   const long long Jp = ap - 1;
   int cp[NCAND], ct[NCAND];
+  int c0p = 0, c0t = 0;   // the no-pop window [s0, Jc] (a growing window: no eviction yet in the batch)
   long long sp[NCAND];
 #pragma unroll
   for (int i = 0; i < NCAND; ++i) {
@@ -334,6 +335,9 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   // grow the right edge (Jp, Jc] with the previous starts
   for (long long k = Jp + 1 + lane; k <= Jc; k += 32) {
     const uint2 d = x.dp[k - E0];
+    const unsigned long long k0 = (unsigned long long)(k - s0);
+    c0p += (unsigned long long)d.x > k0;
+    c0t += (unsigned long long)d.y > k0;
 #pragma unroll
     for (int i = 0; i < NCAND; ++i) {
       if (i >= nc) break;
@@ -362,6 +366,9 @@ __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
     const int vt = __reduce_add_sync(0xffffffffu, ct[i]);
     if (lane == 0) x.anc[(long long)c * NCAND + i] = make_int2(vp, vt);
   }
+  c0p = __reduce_add_sync(0xffffffffu, c0p);
+  c0t = __reduce_add_sync(0xffffffffu, c0t);
+  if (lane == 0) x.anc0[c] = make_int2(c0p, c0t);
 }
 
 // chunk 1's left edges [s_start, s_1i) counted by the whole grid (y = candidate)
@@ -410,7 +417,12 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
   __shared__ int2 wt[33];
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
-  const int i = blockIdx.x;
+  int i = blockIdx.x;
+  if (anc == x.anc && i == NCAND) {   // the extra chain: the no-pop window counts
+    anc = x.anc0;
+    nc = 1;
+    i = 0;
+  }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   int2 carry = make_int2((int)x.st->npix, (int)x.st->ntiles);
   for (int base = 1; base < T; base += 1024 * PER) {
@@ -521,9 +533,10 @@ __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
     unit = max(32LL, (len_hi - len_lo) / 64);
   }
   // the next batch keeps the linear candidates only while every fixed point
-  // stays well inside their span (windows clamped at the batch start excepted)
+  // stays well inside their span; a window still growing from the batch start
+  // (clamped) is unsettled too: its target can run far from q0 next batch
   const bool clamped = len_lo >= 0 && len_hi < 0 && len_lo == a - s0;
-  if (!clamped && (L < q0 + c_lin_off[0] / 2 || L > q0 + c_lin_off[NLIN - 1] / 2)) x.st->geo_next = 1;
+  if (clamped || L < q0 + c_lin_off[0] / 2 || L > q0 + c_lin_off[NLIN - 1] / 2) x.st->geo_next = 1;
   x.lc[c] = L;
   x.lu[c] = unit;
 }
@@ -628,8 +641,17 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
         if (cnt.x >= 1 && cnt.y >= 1 && regulate(x, len, cnt.x, cnt.y) >= len) jstar = j;
       }
       const int g = jstar + 1 < NFINE ? jstar + 1 : NFINE - 1;
-      const int2 cnt = x.anc2[(long long)c * NFINE + g];
+      int2 cnt = x.anc2[(long long)c * NFINE + g];
       w.s = fine_start(x, s_start0, a, center, unit, g);
+      // a window still growing (no eviction yet in this batch: the cold start
+      // or a rising target) has no fixed point near the candidates; its exact
+      // state is the no-pop window [s_start, a - 1] whenever that is stable
+      const int2 c0 = x.anc0[c];
+      const long long len0 = a - s_start0;
+      if (c0.x >= 1 && c0.y >= 1 && regulate(x, len0, c0.x, c0.y) >= len0) {
+        w.s = s_start0;
+        cnt = c0;
+      }
       w.npix = cnt.x;
       w.ntiles = cnt.y;
       const long long len = a - w.s;

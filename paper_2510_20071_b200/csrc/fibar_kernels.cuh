@@ -98,6 +98,7 @@ struct Ctx {
   unsigned blur_sleep;
   unsigned long long *dbg_t, *dbg_g;
   int2 *anc, *anc2;
+  int2 *anc0;   // per chunk: distinct counts of the no-pop window [s_start, a_c - 1]
   long long *lc, *lu;
   ChunkRec *ch;
 };
