@@ -238,6 +238,7 @@ __device__ __forceinline__ long long cand_len(const Ctx &x, long long q0, int i)
 // floor(N / D) for N >= 0, D > 0: a float32 reciprocal estimate (relative
 // error ~1e-7, and the quotients here stay below 2^24) and an exact integer fix-up
 __device__ __forceinline__ long long floordiv_nn(long long N, long long D) {
+  if (N < (1LL << 53)) return (long long)floor(__ddiv_rn((double)N, (double)D));   // exact (see regulate32)
   long long q = (long long)__fmul_rn((float)N, __frcp_rn((float)D));
   if (q * D > N) {
     do { --q; } while (q * D > N);
@@ -259,6 +260,14 @@ __device__ __forceinline__ long long regulate(const Ctx &x, long long len, long 
 __device__ __forceinline__ unsigned regulate32(const Ctx &x, unsigned len, unsigned np, unsigned nt) {
   const unsigned long long N = (unsigned long long)len * nt * (unsigned long long)x.numA;
   const unsigned long long D = (unsigned long long)x.den * np;
+  if (N < (1ull << 53)) {
+    // exact in one double division: N and D convert exactly, and for a
+    // non-integer N/D the distance to the next integer (>= 1/D) exceeds the
+    // rounding error (<= (N/D) 2^-53) because N < 2^53, so the floor is exact
+    const double qd = floor(__ddiv_rn((double)N, (double)D));
+    const double qc = fmin(fmax(qd, (double)x.qmin), (double)x.qmax);
+    return (unsigned)qc;
+  }
   if ((unsigned long long)(x.qmax + 1) * D <= N) return (unsigned)x.qmax;   // clamps high anyway
   long long q = (long long)__fdividef((float)N, (float)D);
   q = q < 0 ? 0 : (q > x.qmax + 1 ? x.qmax + 1 : q);
