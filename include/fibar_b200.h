@@ -25,6 +25,11 @@
  *   fibar_read_state
  *       the arrays hashed by state_digest / returned by iap, l_grid,
  *       p_bar_grid (pipeline.py:443-496).
+ *   fibar_halo_batch / fibar_halo_round / fibar_halo_finish
+ *       _full_chunk (_kernels.py:76-216) for one row band of a filter-ON
+ *       multi-GPU partition: the window pass of the whole stream, the blur loop
+ *       (_kernels.py:173-189) for the band's rows, halo values exchanged by the
+ *       caller between rounds.
  *
  * Threading: one engine = one CUDA stream; calls on one engine must not race
  * (same contract as the reference).  Every call returns 0 on
