@@ -17,8 +17,9 @@
  *   fibar_flush
  *       (no reference equivalent: the engine coalesces packets on the device
  *       between read-outs; state is packet-size invariant).
- *   fibar_render
- *       ReconstructionEngine.render, pipeline.py:562-584.
+ *   fibar_render / fibar_render_async
+ *       ReconstructionEngine.render, pipeline.py:562-584 (async: the frame
+ *       loop of run(), pipeline.py:372-397, without a host wait per frame).
  *   fibar_read_qs / fibar_counters
  *       the qs[10] slots (_kernels.py:48-59, pipeline.py:451-477) and
  *       event_count / oob_dropped (pipeline.py:437-439).
@@ -123,6 +124,16 @@ int fibar_pending(fibar_engine *eng, int64_t *device_events, int64_t *staged_eve
  * when out is device memory). */
 int fibar_render(fibar_engine *eng, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem,
                  double *bounds, int32_t *degenerate);
+
+/* Asynchronous read-out (pipeline.run's frame loop): the same frame as
+ * fibar_render, enqueued after the newest blur stage on the engine's blur
+ * stream so the next batch's front end overlaps it.  Nothing blocks and the
+ * caller's stream does not wait: `ready` (a cudaEvent_t made by the caller) is
+ * recorded when out (uint8 [n_pix], device or pinned host per out_mem) and
+ * meta (same memory kind: double lo, double hi, int32 degenerate) are
+ * written.  Later batches order after the read-out. */
+int fibar_render_async(fibar_engine *eng, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem, void *meta,
+                       void *ready);
 
 /* Synchronising reads (host pointers). */
 int fibar_read_qs(fibar_engine *eng, int64_t qs[10]);

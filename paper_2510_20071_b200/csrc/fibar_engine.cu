@@ -112,6 +112,9 @@ struct GraphEntry {
   long long n;               // batch size the graph was captured for
   long long kernels;         // kernels per replay (the launch counter)
   cudaGraphExec_t exec;
+  int kind = 0;              // 0: whole batch (serial schedule), 1: front end of the streamed schedule
+  int par = 0;               // kind 1: the batch parity whose buffers it uses
+  int where = 0;             // kind 1: which radix-sort buffer holds the sorted keys
 };
 
 struct fibar_engine {
@@ -187,6 +190,10 @@ struct fibar_engine {
   bool graphs_on = true;
   cudaStream_t capstream = nullptr;
   long long graph_max = 1LL << 17;
+  // filter ON: small batches stream (the blur stage overlaps the next batch)
+  // with their front end replayed as a graph; FIBAR_FULL_GRAPHS=1 restores
+  // one whole-batch graph (serial schedule)
+  bool full_graphs = false;
   std::vector<GraphEntry> graphs;
   uint16_t *gx = nullptr, *gy = nullptr;
   int8_t *gp = nullptr;
@@ -332,37 +339,32 @@ int init_state(fibar_engine *g) {
   return 0;
 }
 
-// Enqueue one device batch.  graph == false: the streamed form (blur stage on
-// the second stream, cross-batch events).  graph == true: everything on the
-// engine stream with parity-0 buffers and no events, the form captured into a
-// CUDA graph for small batches (see run_batch_raw).
-int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
-                  cudaEvent_t used_ev, int par, bool graph) {
+// The front end of a batch on stream s: ingest (OOB filter, compaction), the
+// pixel sort and, filter ON, segments, links, the window pass, the stale items
+// and the per-position info.  Returns the batch context (sorted keys) in x.
+int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                  cudaEvent_t used_ev, int par, cudaStream_t s, Ctx &x, int &where) {
   Launcher &L = g->L;
-  cudaStream_t s = L.stream;
-  // this parity's buffers are free once the batch two back finished its blur stage
-  if (!graph && g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
-  Ctx x = g->ctx(nullptr, nullptr, n_raw, par);
+  x = g->ctx(nullptr, nullptr, n_raw, par);
   x.raw_x = rx0;
   x.raw_y = ry0;
   x.raw_p = rp0;
   fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
+  cudaStream_t s_saved = L.stream;
+  L.stream = s;
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
   fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
-  const int where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B,
-                                     n_raw, g->key_bits);
+  where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
+                           g->key_bits);
+  L.stream = s_saved;
   const unsigned *skey = where ? g->kb2[par] : g->ka2[par];
   const unsigned *sidx = where ? g->vb2[par] : g->va2[par];
-  {
-    const uint16_t *rx = x.raw_x, *ry = x.raw_y;
-    const int8_t *rp = x.raw_p;
-    x = g->ctx(skey, sidx, n_raw, par);
-    x.raw_x = rx;
-    x.raw_y = ry;
-    x.raw_p = rp;
-  }
+  x = g->ctx(skey, sidx, n_raw, par);
+  x.raw_x = rx0;
+  x.raw_y = ry0;
+  x.raw_p = rp0;
   const int nb = (int)((n_raw + TPB - 1) / TPB);
   if (g->spatial) {
     const int T = (int)((n_raw + g->chunk - 1) / g->chunk);
@@ -378,6 +380,87 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "window_fix", k_window_fix, 1, 1024, 0, s, x);
     fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
     fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
+  }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// The captured front end for (n_raw, par), reading the fixed input buffers
+// gx/gy/gp; captured on first use (nullptr on failure).
+GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
+  for (auto &ge : g->graphs)
+    if (ge.kind == 1 && ge.n == n_raw && ge.par == par) return &ge;
+  if (g->graphs.size() >= 16) {   // small cache: drop the oldest
+    cudaGraphExecDestroy(g->graphs.front().exec);
+    g->graphs.erase(g->graphs.begin());
+  }
+  if (!g->capstream && cudaStreamCreateWithFlags(&g->capstream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  Launcher &L = g->L;
+  const long long l0 = L.launches;
+  cudaStream_t s0 = L.stream;
+  cudaGraph_t graph = nullptr;
+  GraphEntry ge;
+  Ctx x{};
+  if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  L.stream = g->capstream;
+  const int rc = enqueue_front(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, x, ge.where);
+  L.stream = s0;
+  cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
+  ge.n = n_raw;
+  ge.kind = 1;
+  ge.par = par;
+  ge.kernels = L.launches - l0;
+  L.launches = l0;
+  if (rc == 0 && ce == cudaSuccess) ce = cudaGraphInstantiate(&ge.exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (rc || ce != cudaSuccess) {
+    cudaGetLastError();
+    g->graphs_on = false;   // capture impossible here: stream every kernel from now on
+    return nullptr;
+  }
+  g->graphs.push_back(ge);
+  return &g->graphs.back();
+}
+
+// Enqueue one device batch.  graph == false: the streamed form (blur stage on
+// the second stream, cross-batch events).  graph == true: everything on the
+// engine stream with parity-0 buffers and no events, the form captured into a
+// CUDA graph for small batches (see run_batch_raw).
+int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                  cudaEvent_t used_ev, int par, bool graph) {
+  Launcher &L = g->L;
+  cudaStream_t s = L.stream;
+  // this parity's buffers are free once the batch two back finished its blur stage
+  if (!graph && g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
+  Ctx x{};
+  int where = 0;
+  const int nb = (int)((n_raw + TPB - 1) / TPB);
+  if (g->spatial && !graph && g->graphs_on && !L.prof && n_raw <= g->graph_max) {
+    // a small streamed batch: its front end (ingest .. stale items, ~25
+    // kernels) replays one CUDA graph per (size, parity) from fixed input
+    // buffers, so the host issues a handful of calls per batch while the blur
+    // stage still overlaps the next batch as below
+    CK(cudaMemcpyAsync(g->gx, rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(g->gy, ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(g->gp, rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+    if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
+    GraphEntry *ge = front_graph(g, n_raw, par);
+    if (!ge) return g_err.empty() ? fail(FIBAR_E_CUDA, "front-end graph capture failed") : FIBAR_E_CUDA;
+    CK(cudaGraphLaunch(ge->exec, s));
+    L.launches += ge->kernels;
+    where = ge->where;
+    x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+    x.raw_x = g->gx;
+    x.raw_y = g->gy;
+    x.raw_p = g->gp;
+  } else {
+    int rc = enqueue_front(g, rx0, ry0, rp0, n_raw, used_ev, par, s, x, where);
+    if (rc) return rc;
+  }
+  if (g->spatial) {
     // the replay reads the brightness the previous batch's blur stage finishes
     if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
     fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
@@ -447,7 +530,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   if (n_raw <= 0) return 0;
   Launcher &L = g->L;
   cudaStream_t s = L.stream;
-  if (!g->graphs_on || L.prof || n_raw > g->graph_max) {
+  if (!g->graphs_on || L.prof || n_raw > g->graph_max || !g->full_graphs) {
     const int par = g->spatial ? (int)(g->batches & 1) : 0;
     int rc = enqueue_batch(g, rx0, ry0, rp0, n_raw, used_ev, par, false);
     if (rc) return rc;
@@ -734,6 +817,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     cudaGetLastError();
   }
   if (const char *v = getenv("FIBAR_PDL")) g->L.pdl = atoi(v) != 0;
+  g->full_graphs = !g->spatial;
+  if (const char *v = getenv("FIBAR_FULL_GRAPHS")) g->full_graphs = atoi(v) != 0;
   {
     // contraction of the slower recurrence: events until any two float32
     // trajectories agree to the last bit, with a 1.6x margin
@@ -1091,6 +1176,45 @@ int fibar_render(fibar_engine *g, int32_t mode, double fixed_bound, uint8_t *out
   int rc = sync_point(g);
   if (rc) return rc;
   return render_core(g->L, g->l, g->n_pix, mode, fixed_bound, out, out_mem, bounds, degenerate, g->sel, g->frame, g->nsm);
+}
+
+int fibar_render_async(fibar_engine *g, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem, void *meta,
+                       void *ready) {
+  if (!g) return fail(FIBAR_E_CONFIG, "null engine");
+  if (!meta || !ready) return fail(FIBAR_E_CONFIG, "render_async needs meta and an event");
+  int rc = run_batch(g);
+  if (rc) return rc;
+  Launcher &L = g->L;
+  cudaStream_t s0 = L.stream;
+  const bool on_blur = g->spatial && g->last_b >= 0 && !g->serial;
+  // after the newest blur stage, on its stream: the next batch's front end
+  // (engine stream) does not wait for the read-out, its temporal replay does
+  cudaStream_t rs = on_blur ? g->bstream : s0;
+  L.stream = rs;
+  // rendered into device memory (render_core would wait for a host frame),
+  // copied to a host frame asynchronously here
+  const bool dev_out = out_mem == FIBAR_MEM_DEVICE;
+  rc = render_core(L, g->l, g->n_pix, mode, fixed_bound, dev_out ? out : g->frame, FIBAR_MEM_DEVICE, nullptr, nullptr,
+                   g->sel, g->frame, g->nsm);
+  if (!rc && !dev_out) {
+    cudaError_t e = cudaMemcpyAsync(out, g->frame, g->n_pix, cudaMemcpyDeviceToHost, rs);
+    if (e != cudaSuccess) rc = cuda_fail(e, "render_async frame");
+  }
+  if (!rc) {
+    const cudaMemcpyKind kind = dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    cudaError_t e = cudaMemcpyAsync(meta, &g->sel->lo, 2 * sizeof(double) + sizeof(int), kind, rs);
+    if (e != cudaSuccess) rc = cuda_fail(e, "render_async meta");
+  }
+  if (!rc && on_blur) {
+    cudaError_t e = cudaEventRecord(g->evB[g->last_b], rs);   // later batches order after the read-out
+    if (e != cudaSuccess) rc = cuda_fail(e, "render_async event");
+  }
+  if (!rc) {
+    cudaError_t e = cudaEventRecord((cudaEvent_t)ready, rs);
+    if (e != cudaSuccess) rc = cuda_fail(e, "render_async ready");
+  }
+  L.stream = s0;
+  return rc;
 }
 
 int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem,

@@ -67,6 +67,26 @@ class Frame:
         return self.pixels.shape[0]
 
 
+class AsyncFrame:
+    """A read-out in flight (ReconstructionEngine.render_async)."""
+
+    def __init__(self, out, meta, event, readout_time, scale_mode):
+        self.out, self.meta, self.event = out, meta, event
+        self.readout_time, self.scale_mode = readout_time, scale_mode
+
+    def ready(self) -> bool:
+        return self.event.query()
+
+    def frame(self, copy: bool = True) -> Frame:
+        """Wait for the read-out and return it as a Frame (a fresh array unless copy=False)."""
+        self.event.synchronize()
+        m = self.meta.cpu().numpy() if self.meta.is_cuda else self.meta.numpy()
+        deg = int(np.array([m[2]], np.float64).view(np.int64)[0] & 0xFFFFFFFF)
+        px = self.out.cpu().numpy() if self.out.is_cuda else self.out.numpy()
+        return Frame(px.copy() if copy else px, self.readout_time, self.scale_mode, (float(m[0]), float(m[1])),
+                     bool(deg))
+
+
 @dataclass
 class DeviceEventArray:
     """A packet whose columns are CUDA tensors (x, y: uint16/int16/int32; p: int8).
@@ -573,6 +593,30 @@ class ReconstructionEngine:
         return Frame(out.reshape(g.height, g.width), readout_time, scale_mode, (float(bounds[0]), float(bounds[1])),
                      bool(deg.value))
 
+    def render_async(self, scale_mode: str = "robust", fixed_bound: float = 1.0, readout_time: int = 0,
+                     out=None, meta=None) -> "AsyncFrame":
+        """Enqueue a read-out without waiting (fibar_render_async): the frame of
+        the current state, written into ``out`` (a pinned host or CUDA uint8
+        (H, W) tensor; pinned host by default) once ``AsyncFrame.event`` fires.
+        The next packets' front end overlaps it on the GPU."""
+        torch = _torch()
+        mode = self._mode(scale_mode, fixed_bound)
+        g = self.geometry
+        if out is None:
+            out = torch.empty((g.height, g.width), dtype=torch.uint8, pin_memory=True)
+        dev = out.is_cuda
+        if meta is None:
+            meta = torch.empty(4, dtype=torch.float64, device=self.device) if dev else \
+                torch.empty(4, dtype=torch.float64, pin_memory=True)
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()   # creates the CUDA event (torch makes it lazily); the engine re-records it
+        self._sync_stream()
+        mem = _native.FIBAR_MEM_DEVICE if dev else _native.FIBAR_MEM_HOST
+        _native.check(self._lib.fibar_render_async(self._h, mode, float(fixed_bound), out.data_ptr(), mem,
+                                                   meta.data_ptr(), C.c_void_p(ev.cuda_event)), "fibar_render_async")
+        self._release_held()
+        return AsyncFrame(out, meta, ev, readout_time, scale_mode)
+
     def brightness_device(self, out=None):
         """The brightness grid as a CUDA float32 (H, W) tensor (device copy, no sync)."""
         torch = _torch()
@@ -678,6 +722,20 @@ def _readout_times(fps: float | None, explicit) -> tuple[Iterator[float], bool]:
     return grid(), False
 
 
+_RUN_DEPTH = 4   # read-outs in flight in run()
+
+
+def _time_key(r, dtype):
+    """A read-out time as a scalar of the timestamp dtype with the same 'left'
+    split: for integer timestamps t < r <=> t < ceil(r).  (A Python int or
+    float against a uint64 array would make numpy convert the whole array.)"""
+    if np.issubdtype(dtype, np.integer):
+        c = math.ceil(r)
+        info = np.iinfo(dtype)
+        return dtype.type(min(max(c, info.min), info.max))
+    return r
+
+
 def run(
     engine: ReconstructionEngine,
     blocks: Iterable[EventArray],
@@ -709,9 +767,31 @@ def run(
     times, explicit = _readout_times(fps, readout_times)
     next_r = next(times, None)
     frame_index = 0
+    # Without diagnostics (which read the state at each frame), frames are read
+    # out asynchronously (render_async into a small ring of pinned buffers) and
+    # handed to the sink in order as they land, so the GPU runs the next
+    # packets while earlier frames are copied back.
+    pipelined = diag is None and hasattr(engine, "render_async")
+    pending = collections.deque()
+    ring = []
+
+    def deliver(af) -> None:
+        frame = af.frame()
+        if frame_sink is not None:
+            frame_sink(af.index, frame)
+        ring.append((af.out, af.meta))
 
     def emit(readout) -> None:
         nonlocal frame_index
+        if pipelined:
+            while pending and (len(pending) >= _RUN_DEPTH or pending[0].ready()):
+                deliver(pending.popleft())
+            out, meta = ring.pop() if ring else (None, None)
+            af = engine.render_async(scale_mode, fixed_bound, readout_time=int(readout), out=out, meta=meta)
+            af.index = frame_index
+            pending.append(af)
+            frame_index += 1
+            return
         frame = engine.render(scale_mode, fixed_bound, readout_time=int(readout))
         if frame_sink is not None:
             frame_sink(frame_index, frame)
@@ -730,7 +810,7 @@ def run(
             ts = block.t
             pos = 0
             while next_r is not None and next_r <= ts[-1]:
-                idx = int(np.searchsorted(ts, next_r, side="left"))
+                idx = int(np.searchsorted(ts, _time_key(next_r, ts.dtype), side="left"))
                 if idx > pos:
                     engine.process_array(block.slice(pos, idx))
                     pos = idx
@@ -742,6 +822,8 @@ def run(
             while next_r is not None:
                 emit(next_r)
                 next_r = next(times, None)
+        while pending:
+            deliver(pending.popleft())
     finally:
         if diag is not None:
             diag.close()

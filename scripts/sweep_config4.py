@@ -33,6 +33,8 @@ ap.add_argument("--events", type=int, default=20_000_000)
 ap.add_argument("--max-packets", type=int, default=3000)
 ap.add_argument("--cpu-seconds", type=float, default=4.0, help="CPU reference budget per point")
 ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "config4_sweep.json"))
+ap.add_argument("--sync", action="store_true", help="render_device (read-out on the caller's stream) instead of "
+                                                   "render_async (behind the blur stage, next packet overlapping)")
 a = ap.parse_args()
 
 geom = SensorGeometry(1280, 720)
@@ -41,6 +43,7 @@ xd = torch.from_numpy(ev.x.view(np.int16)).cuda()
 yd = torch.from_numpy(ev.y.view(np.int16)).cuda()
 pd = torch.from_numpy(ev.p).cuda()
 frame = torch.empty((geom.height, geom.width), dtype=torch.uint8, device="cuda")
+meta = torch.empty(4, dtype=torch.float64, device="cuda")
 rows = []
 for spatial in (True, False):
     params = compute_params(40.0, Fraction(1, 2), geom, spatial_enabled=spatial)
@@ -55,15 +58,27 @@ for spatial in (True, False):
             eng.render_device("robust", out=frame)
         eng.reset()
         torch.cuda.synchronize()
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(n_pk + 1)]
-        evs[0].record()
-        for i, p in enumerate(pk):
-            eng.process_array(p)
-            eng.render_device("robust", out=frame)
-            evs[i + 1].record()
-        torch.cuda.synchronize()
-        total_ms = evs[0].elapsed_time(evs[-1])
-        lat = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(n_pk)]) * 1e3   # us per packet
+        if a.sync:
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(n_pk + 1)]
+            evs[0].record()
+            for i, p in enumerate(pk):
+                eng.process_array(p)
+                eng.render_device("robust", out=frame)
+                evs[i + 1].record()
+            torch.cuda.synchronize()
+            total_ms = evs[0].elapsed_time(evs[-1])
+            lat = np.array([evs[i].elapsed_time(evs[i + 1]) for i in range(n_pk)]) * 1e3   # us per packet
+        else:
+            # packet i: from its submission on the stream to its frame in HBM
+            starts = [torch.cuda.Event(enable_timing=True) for _ in range(n_pk)]
+            ready = []
+            for i, p in enumerate(pk):
+                starts[i].record()
+                eng.process_array(p)
+                ready.append(eng.render_async("robust", out=frame, meta=meta).event)
+            torch.cuda.synchronize()
+            total_ms = starts[0].elapsed_time(ready[-1])
+            lat = np.array([starts[i].elapsed_time(ready[i]) for i in range(n_pk)]) * 1e3
         # reference CPU path at the same cadence on a prefix
         from oracle import oracle as orc
         ref = orc.OracleEngine(geom.width, geom.height, params)
@@ -82,7 +97,8 @@ for spatial in (True, False):
         rows.append(row)
         print(json.dumps(row), flush=True)
         eng.close()
-out = {"config": "config4:1280x720 texture, read-out (robust, render_device) after every packet",
+out = {"config": "config4:1280x720 texture, robust read-out after every packet (%s)" %
+       ("render_device, on the caller's stream" if a.sync else "render_async, behind the packet's blur stage"),
        "note": "prefix of the 50M-event stream per point (events/packets columns); latency = process + read-out "
                "per packet, CUDA events on the stream; CPU reference = C oracle port, one core, same cadence, "
                "time-boxed prefix", "rows": rows}
