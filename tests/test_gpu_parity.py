@@ -192,19 +192,26 @@ def test_pinned_host_packets_direct_copy():
 
 
 def test_graph_and_streamed_batches_agree(monkeypatch):
-    """Small batches replay a captured CUDA graph, large ones stream on two
-    streams; forcing either form gives the same (oracle-exact) state."""
+    """Small batches replay captured CUDA graphs, large ones stream on two
+    streams; every form gives the same (oracle-exact) state."""
     from paper_2510_20071_b200.pipeline import ReconstructionEngine
     geom, params, ev, ref = _oracle_stream("texture_noise_hot", 320, 240, 300_000, 30_000, True, seed=9)
     want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
                 qx=ref.qx, qy=ref.qy, qs=ref.qs)
-    for graphs in ("1", "0"):
+    # graphs=1: small batches stream with their front end replayed as a graph;
+    # full=1: one whole-batch graph (serial schedule); graphs=0: every kernel
+    # streamed; async: read-outs behind the blur stage (render_async)
+    for graphs, full, read in (("1", "0", "sync"), ("1", "1", "sync"), ("0", "0", "sync"), ("1", "0", "async")):
         monkeypatch.setenv("FIBAR_GRAPHS", graphs)
+        monkeypatch.setenv("FIBAR_FULL_GRAPHS", full)
         eng = ReconstructionEngine(geom, params)
         for a in range(0, len(ev), 30_000):
             eng.process_array(ev.slice(a, min(len(ev), a + 30_000)))
-            eng.render("robust")          # a read-out per packet: one batch per packet
-        assert_state(eng, want, f"graphs={graphs}")
+            if read == "sync":
+                eng.render("robust")          # a read-out per packet: one batch per packet
+            else:
+                eng.render_async("robust")
+        assert_state(eng, want, f"graphs={graphs} full={full} {read}")
         eng.close()
 
 
