@@ -461,12 +461,6 @@ __device__ __forceinline__ void blur_lanes(const Ctx &x) {
   unsigned p = FIBAR_NONE, okm = 0, pend = 0, runpos = FIBAR_NONE;
   unsigned tnt = 0;   // halo bands: the value read a not-yet-final halo value (TAINT_HI or 0)
   unsigned val[9];
-#ifdef FIBAR_RUN_PREFETCH
-  // the first positions of the run this item rebuilds, loaded while its taps
-  // are still pending: the rebuild then costs no round trip after the blur
-  unsigned prb[FIBAR_RUN_PREFETCH];
-  float ptt[FIBAR_RUN_PREFETCH];
-#endif
   bool exhausted = false;
   // the warp draws 32 items at a time from the global ticket and hands them
   // to its free lanes in order (one contended atomic per 32 items); every
@@ -523,14 +517,6 @@ __device__ __forceinline__ void blur_lanes(const Ctx &x) {
             val[7] = n2.y;
             val[8] = n2.z;
             runpos = n2.w;
-#ifdef FIBAR_RUN_PREFETCH
-#pragma unroll
-            for (int u = 0; u < FIBAR_RUN_PREFETCH; ++u) {
-              const bool in = runpos != FIBAR_NONE && runpos + u < b.B;
-              prb[u] = in ? __ldcg(&x.posrec[runpos + u].runbase) : FIBAR_NONE;
-              ptt[u] = in ? __ldcg(&x.t2[runpos + u]) : 0.0f;
-            }
-#endif
             if (x.dbg_g) {
               unsigned long long tt;
               asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
@@ -582,27 +568,7 @@ __device__ __forceinline__ void blur_lanes(const Ctx &x) {
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
           x.dbg_t[p] = tt;
         }
-#ifdef FIBAR_RUN_PREFETCH
-        if (runpos != FIBAR_NONE && okm != HALO_OKM) {
-          float v2 = v;
-          bool cont = true;
-#pragma unroll
-          for (int u = 0; u < FIBAR_RUN_PREFETCH; ++u) {
-            if (!cont || prb[u] != p) {
-              cont = false;
-              continue;
-            }
-            v2 = faddr(fmulr(x.beta, v2), ptt[u]);
-            x.posrec[runpos + u].val = v2;
-            st_relaxed_u64(&x.mv64[runpos + u], ((unsigned long long)hi << 32) | __float_as_uint(v2));
-          }
-          if (cont) materialise_run(x, b, p, runpos + FIBAR_RUN_PREFETCH, v2, hi);
-        } else if (runpos != FIBAR_NONE) {
-          materialise_run(x, b, p, runpos, v, hi);
-        }
-#else
         if (runpos != FIBAR_NONE) materialise_run(x, b, p, runpos, v, hi);
-#endif
         p = FIBAR_NONE;
       } else if (x.blur_sleep) {
         __nanosleep(x.blur_sleep);
