@@ -773,7 +773,8 @@ def run(
     # packets while earlier frames are copied back.
     pipelined = diag is None and hasattr(engine, "render_async")
     pending = collections.deque()
-    ring = []
+    # pinned frame buffers, kept on the engine across run() calls
+    ring = engine.__dict__.setdefault("_run_frame_pool", []) if pipelined else []
 
     def deliver(af) -> None:
         frame = af.frame()
