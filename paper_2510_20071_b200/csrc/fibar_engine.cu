@@ -204,6 +204,11 @@ struct fibar_engine {
   int nsm = 148;
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
+  // batches up to this size use 32-event speculation chunks: a small batch
+  // leaves most SMs idle, so shorter serial chunk runs win over the extra
+  // anchors and re-runs (config 3, 100k batches: 214 -> 227 Mev/s; 1M-event
+  // batches keep 64: 1173 vs 1018 Mev/s at 32).  FIBAR_CHUNK fixes one size.
+  long long small_chunk_max = 1LL << 18;
   int twarm = 256;
   bool serial = false;   // FIBAR_SERIAL: blur stage on the engine stream (no overlap; for measurement)
   unsigned blur_sleep = 0;
@@ -274,7 +279,7 @@ struct fibar_engine {
     x.mv64 = mv64;
     x.prep = prep2[par];
     x.colist = colist;
-    x.chunk = chunk;
+    x.chunk = n_raw <= small_chunk_max ? std::min(chunk, 32) : chunk;
     x.twarm = twarm;
     x.debug = debug;
     x.blur_sleep = blur_sleep;
@@ -367,7 +372,7 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   x.raw_p = rp0;
   const int nb = (int)((n_raw + TPB - 1) / TPB);
   if (g->spatial) {
-    const int T = (int)((n_raw + g->chunk - 1) / g->chunk);
+    const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
     fibar_launch(L, "seg_marks", k_seg_marks, nb, TPB, 0, s, x);
     fibar_launch(L, "link", k_link, nb, TPB, 0, s, x);
     fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
@@ -777,7 +782,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   g->key_bits = ceil_log2(g->n_tiles * g->A);
   // window-speculation tuning knobs (results never depend on them; the verifier
   // re-runs any chunk whose speculative start was wrong)
-  if (const char *v = getenv("FIBAR_CHUNK")) g->chunk = std::max(CHUNK_MIN, atoi(v));
+  if (const char *v = getenv("FIBAR_CHUNK")) {
+    g->chunk = std::max(CHUNK_MIN, atoi(v));
+    g->small_chunk_max = 0;
+  }
   if (const char *v = getenv("FIBAR_WARM")) g->warm = std::max(0, atoi(v));
   if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
   if (const char *v = getenv("FIBAR_SERIAL")) g->serial = atoi(v) != 0;
