@@ -27,29 +27,52 @@ __global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, l
     for (int u = 0; u < t; ++u)
       if (pref[u] == pref[t]) act[t] = false;
   }
-  for (int i = threadIdx.x; i < 4 * 2048; i += TPB) (&h[0][0])[i] = 0;
+  // only the distinct targets' histograms are used (pass 0: one; later
+  // passes: usually two), so only those are cleared, merged and read back
+#pragma unroll
+  for (int t = 0; t < 4; ++t)
+    if (act[t])
+      for (int i = threadIdx.x; i < 2048; i += TPB) h[t][i] = 0;
   __syncthreads();
   // brightness values cluster in a few top digits, so equal digits within a
   // warp are combined first (one shared atomic per distinct digit and target)
   const long long stride = (long long)gridDim.x * TPB;
   const long long n_round = (n + 31) & ~31LL;
-  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n_round; i += stride) {
-    const bool in = i < n;
-    const unsigned k = in ? order_key(l[i]) : 0u;
-    const unsigned d = (k >> shift) & dmask;
+  // SEL_UNROLL values per thread are loaded before any is binned, so a
+  // thread waits on one memory round trip per SEL_UNROLL values
+  constexpr int SEL_UNROLL = 8;
+  for (long long i0 = (long long)blockIdx.x * TPB + threadIdx.x; i0 < n_round; i0 += SEL_UNROLL * stride) {
+    unsigned kk[SEL_UNROLL];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      if (!act[t]) continue;   // warp-uniform
-      const bool mine = in && (k & hmask) == pref[t];
-      const unsigned key = mine ? d : 0xFFFFFFFFu;
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      if (mine && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&h[t][d], (unsigned)__popc(peers));
+    for (int u = 0; u < SEL_UNROLL; ++u) {
+      const long long i = i0 + u * stride;
+      kk[u] = i < n ? order_key(__ldg(&l[i])) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < SEL_UNROLL; ++u) {
+      const long long i = i0 + u * stride;
+      if (i >= n_round) break;   // warp-uniform (n_round and stride are multiples of 32)
+      const bool in = i < n;
+      const unsigned k = kk[u];
+      const unsigned d = (k >> shift) & dmask;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        if (!act[t]) continue;   // warp-uniform
+        const bool mine = in && (k & hmask) == pref[t];
+        const unsigned key = mine ? d : 0xFFFFFFFFu;
+        const unsigned peers = __match_any_sync(0xffffffffu, key);
+        if (mine && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&h[t][d], (unsigned)__popc(peers));
+      }
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 4 * 2048; i += TPB) {
-    const unsigned v = (&h[0][0])[i];
-    if (v) atomicAdd(&(&sel->hist[0][0])[i], v);
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    if (!act[t]) continue;
+    for (int i = threadIdx.x; i < 2048; i += TPB) {
+      const unsigned v = h[t][i];
+      if (v) atomicAdd(&sel->hist[t][i], v);
+    }
   }
   __threadfence();
   __shared__ bool last;
@@ -58,9 +81,13 @@ __global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, l
   if (!last) return;
   __threadfence();
   // totals into shared memory (and the global table cleared for the next pass)
-  for (int i = threadIdx.x; i < 4 * 2048; i += TPB) {
-    (&h[0][0])[i] = __ldcg(&(&sel->hist[0][0])[i]);
-    (&sel->hist[0][0])[i] = 0u;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    if (!act[t]) continue;
+    for (int i = threadIdx.x; i < 2048; i += TPB) {
+      h[t][i] = __ldcg(&sel->hist[t][i]);
+      sel->hist[t][i] = 0u;
+    }
   }
   __syncthreads();
   // one warp per target: the digit holding its remaining rank
