@@ -128,6 +128,33 @@ class BandedReconstructionEngine:
         return int(t.item()), ob
 
 
+def _slice(block, a, b):
+    if hasattr(block, "slice"):
+        return block.slice(a, b)
+    from .pipeline import DeviceEventArray
+    return DeviceEventArray(block.x[a:b], block.y[a:b], block.p[a:b], None if block.t is None else block.t[a:b])
+
+
+def _concat(blocks):
+    from .core import EventArray
+    if all(hasattr(b, "slice") for b in blocks):
+        return EventArray.concatenate(blocks)
+    import torch
+    from .pipeline import DeviceEventArray
+    dev = next(b.x.device for b in blocks if not hasattr(b, "slice"))
+
+    def col(b, name):   # a host packet's column as a device tensor (x, y as int16 bits)
+        v = getattr(b, name)
+        if hasattr(b, "slice"):
+            v = torch.from_numpy(v.view(np.int16) if v.dtype == np.uint16 else v).to(dev)
+        return v.to(torch.int8) if name == "p" else v.to(torch.int16) if v.dtype != torch.int16 else v
+
+    ts = [b.t for b in blocks]
+    t = None if any(v is None for v in ts) else np.concatenate(ts)
+    return DeviceEventArray(torch.cat([col(b, "x") for b in blocks]), torch.cat([col(b, "y") for b in blocks]),
+                            torch.cat([col(b, "p") for b in blocks]), t)
+
+
 # A value word of the halo exchange: bit 63 = tainted, bits 0-31 = float32 bits.
 TAINTED = -(1 << 63)
 
@@ -175,12 +202,13 @@ class HaloBandEngine:
 
     # -- ingest ----------------------------------------------------------------
     def process_array(self, block) -> None:
-        """Queue a packet; full batches run at once (halo rounds included)."""
+        """Queue a packet (EventArray or DeviceEventArray); full batches run at
+        once (halo rounds included)."""
         n = len(block)
         off = 0
         while off < n:
             take = min(n - off, self.batch_events - self._pending_n)
-            self._pending.append(block.slice(off, off + take) if (off or take < n) else block)
+            self._pending.append(_slice(block, off, off + take) if (off or take < n) else block)
             self._pending_n += take
             off += take
             if self._pending_n == self.batch_events:
@@ -191,8 +219,7 @@ class HaloBandEngine:
             self._run_pending()
 
     def _run_pending(self) -> None:
-        from .core import EventArray
-        blk = self._pending[0] if len(self._pending) == 1 else EventArray.concatenate(self._pending)
+        blk = self._pending[0] if len(self._pending) == 1 else _concat(self._pending)
         self._pending, self._pending_n = [], 0
         self.rounds.append(self._run_batch(blk))
 

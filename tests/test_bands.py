@@ -264,9 +264,15 @@ def test_halo_band_engine_single_rank_and_render():
     ev = workloads.moving_texture(120, 90, 100_000, seed=6)
     ref = orc.OracleEngine(120, 90, params)
     eng = bands.HaloBandEngine(geom, params, rank=0, world=1, batch_events=30_000)
-    for blk in workloads.packets(ev, 7_000):
+    from paper_2510_20071_b200.pipeline import DeviceEventArray
+    for i, blk in enumerate(workloads.packets(ev, 7_000)):
         ref.process_array(blk.t, blk.x, blk.y, blk.p)
-        eng.process_array(blk)
+        if i % 2:   # host and device packets, split across batch boundaries
+            eng.process_array(blk)
+        else:
+            eng.process_array(DeviceEventArray(torch.from_numpy(blk.x.view(np.int16)).cuda(),
+                                               torch.from_numpy(blk.y.view(np.int16)).cuda(),
+                                               torch.from_numpy(blk.p).cuda(), blk.t))
     assert torch.equal(eng.gather_l().cpu().reshape(-1), torch.from_numpy(ref.l))
     fr = eng.render("robust")
     px, b, _ = ref.render("robust")
