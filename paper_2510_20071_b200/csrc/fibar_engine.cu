@@ -185,6 +185,8 @@ struct fibar_engine {
   CUgreenCtx gctx = nullptr;
   cudaStream_t gstream = nullptr;
   cudaEvent_t evP = nullptr, evG = nullptr;
+  cudaEvent_t evT = nullptr;   // temporal_on_blur: the replay + batch end of the newest batch
+  bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
   bool graphs_on = true;
@@ -466,11 +468,29 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     if (rc) return rc;
   }
   if (g->spatial) {
-    // the replay reads the brightness the previous batch's blur stage finishes
-    if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
-    fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
-    fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
-    fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
+    // The temporal replay reads the brightness the previous batch's blur
+    // stage finishes.  Streamed (temporal_on_blur): it runs first on the blur
+    // stream itself, so the cycle blur(k) -> final(k) -> replay(k+1) ->
+    // prep(k+1) -> blur(k+1) crosses no stream; the engine stream waits for
+    // it (evT) before the next front end (whose links read the replay's
+    // last-touch tables and batch_end's event count).
+    const bool t_on_b = !graph && !g->serial && !g->halo && g->temporal_on_blur;
+    if (t_on_b) {
+      cudaStream_t bs = g->bstream;
+      CK(cudaEventRecord(g->evF[par], s));
+      CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
+      L.stream = bs;
+      fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, bs, x);
+      fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, bs, x);
+      fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, bs, x);
+      CK(cudaEventRecord(g->evT, bs));
+      CK(cudaStreamWaitEvent(s, g->evT, 0));
+    } else {
+      if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
+      fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
+      fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
+      fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
+    }
     if (g->halo) {
       // halo band: the item lists of the exchanged rows and the tap
       // resolution; the host then drives the blur rounds (fibar_halo_round)
@@ -487,7 +507,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     }
     // blur stage on its own stream: overlaps the next batch's front end
     cudaStream_t bs = (g->serial || graph) ? s : g->bstream;
-    if (!graph) {
+    if (!graph && !t_on_b) {
       CK(cudaEventRecord(g->evF[par], s));
       CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
     }
@@ -825,6 +845,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     cudaGetLastError();
   }
   if (const char *v = getenv("FIBAR_PDL")) g->L.pdl = atoi(v) != 0;
+  if (const char *v = getenv("FIBAR_TEMPORAL_ON_BLUR")) g->temporal_on_blur = atoi(v) != 0;
   g->full_graphs = !g->spatial;
   if (const char *v = getenv("FIBAR_FULL_GRAPHS")) g->full_graphs = atoi(v) != 0;
   {
@@ -922,6 +943,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       if (const char *v = getenv("FIBAR_BLUR_PRIO")) hi = atoi(v) ? hi : lo;
       cudaStreamCreateWithPriority(&g->bstream, cudaStreamNonBlocking, hi);
     }
+    cudaEventCreateWithFlags(&g->evT, cudaEventDisableTiming);
     for (int c = 0; c < 2; ++c) {
       cudaEventCreateWithFlags(&g->evF[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evB[c], cudaEventDisableTiming);
@@ -1005,7 +1027,7 @@ int fibar_destroy(fibar_engine *g) {
     cudaStreamDestroy(g->gstream);
   }
   if (g->gctx) green_api().ctxDestroy(g->gctx);
-  for (cudaEvent_t ev : {g->evP, g->evG})
+  for (cudaEvent_t ev : {g->evP, g->evG, g->evT})
     if (ev) cudaEventDestroy(ev);
   delete g;
   return 0;
