@@ -19,6 +19,10 @@ constexpr int TPB = 256;
 #define FIBAR_BLUR_MINB 1
 #endif
 constexpr int BLUR_MINB = FIBAR_BLUR_MINB;   // k_blur: min resident blocks per SM (register cap)
+#ifndef FIBAR_PREP_MINB
+#define FIBAR_PREP_MINB 4
+#endif
+constexpr int PREP_MINB = FIBAR_PREP_MINB;   // k_blur_prep: min resident blocks per SM
 constexpr unsigned ITEM_CARRIED_ONLY = 1u;   // Item.pad flag
 constexpr int IN_ITEMS = 8;
 constexpr int IN_TILE = TPB * IN_ITEMS;
@@ -145,7 +149,7 @@ __global__ void __launch_bounds__(TPB) k_posinfo(Ctx x);
 __global__ void __launch_bounds__(TPB) k_temporal(Ctx x);
 __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x);
 __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x);
-__global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x);
+__global__ void __launch_bounds__(TPB, PREP_MINB) k_blur_prep(Ctx x);
 __global__ void __launch_bounds__(TPB, BLUR_MINB) k_blur(Ctx x);
 __global__ void __launch_bounds__(TPB) k_blur_halo(Ctx x);   // halo-band engines
 __global__ void __launch_bounds__(TPB) k_final(Ctx x);

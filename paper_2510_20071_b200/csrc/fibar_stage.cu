@@ -315,7 +315,7 @@ __device__ __forceinline__ void prep_item(const Ctx &x, unsigned p);
 // pixels without events.  Neighbouring threads then resolve neighbouring
 // pixels' 3x3 taps, so the random pixel / position records they read are
 // shared in L1 instead of fetched again from L2.
-__global__ void __launch_bounds__(TPB, 4) k_blur_prep(Ctx x) {
+__global__ void __launch_bounds__(TPB, PREP_MINB) k_blur_prep(Ctx x) {
   pdl_wait();
   const long long B = x.bs->B;
   const long long q = (long long)blockIdx.x * TPB + threadIdx.x;
