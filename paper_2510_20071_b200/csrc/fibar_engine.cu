@@ -148,6 +148,7 @@ struct fibar_engine {
            *vb2[2] = {nullptr, nullptr}, *hist = nullptr;
   uint2 *dp = nullptr;
   unsigned *S = nullptr;
+  unsigned *pmap = nullptr;
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
   BlurPrep *prep = nullptr;            // = prep2[0] (debug reads)
   BlurPrep *prep2[2] = {nullptr, nullptr};   // per batch parity: k_popj of batch k+1 writes while batch k blurs
@@ -274,6 +275,7 @@ struct fibar_engine {
     x.sidx = sidx;
     x.dp = dp;
     x.S = S;
+    x.pmap = pmap;
     x.item = item2[par];
     x.posrec = posrec2[par];
     x.t2 = t2_2[par];
@@ -385,6 +387,7 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
     fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
     fibar_launch(L, "window_fix", k_window_fix, 1, 1024, 0, s, x);
+    fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
     fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
     fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
   }
@@ -954,6 +957,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->rnext, g->R);
     rc |= dalloc(&g->dp, Bc);
     rc |= dalloc(&g->S, Bc);
+    rc |= dalloc(&g->pmap, npop_cap);
     rc |= dalloc(&g->bv64, npop_cap);
     rc |= dalloc(&g->mv64, Bc);
     rc |= dalloc(&g->prep2[0], npop_cap);
@@ -995,7 +999,7 @@ int fibar_destroy(fibar_engine *g) {
   if (g->bstream) cudaStreamSynchronize(g->bstream);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
-                  g->dp, g->S, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->sel, g->frame,
+                  g->dp, g->S, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);

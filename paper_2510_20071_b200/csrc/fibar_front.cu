@@ -931,6 +931,32 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
 // Every window entry popped in this batch becomes an item, in pop order (the
 // order the reference blurs them, _kernels.py:152-189).  An entry is stale iff
 // its pixel has no later event up to the popping event.
+// Event jj pops the evictions [S[jj-1], S[jj]) (S is the window start after
+// each event): one thread per event writes jj for its range, ranges longer
+// than a warp (a collapsing window) written by the whole warp.  Replaces a
+// binary search of S per eviction.
+__global__ void __launch_bounds__(TPB) k_popj_map(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const unsigned jj = blockIdx.x * TPB + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  unsigned lo = 0, hi = 0;
+  if (jj < B) {
+    lo = jj == 0 ? 0u : x.S[jj - 1];
+    hi = x.S[jj];
+  }
+  if (hi - lo <= 32)
+    for (unsigned p = lo; p < hi; ++p) x.pmap[p] = jj;
+  unsigned m = __ballot_sync(0xffffffffu, hi - lo > 32);
+  while (m) {
+    const int L = __ffs(m) - 1;
+    const unsigned l0 = __shfl_sync(0xffffffffu, lo, L), h0 = __shfl_sync(0xffffffffu, hi, L);
+    const unsigned j0 = __shfl_sync(0xffffffffu, jj, L);
+    for (unsigned p = l0 + lane; p < h0; p += 32) x.pmap[p] = j0;
+    m &= m - 1;
+  }
+}
+
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
   pdl_wait();
   const long long B = x.bs->B;
@@ -939,12 +965,7 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
   const unsigned p = blockIdx.x * TPB + threadIdx.x;   // one thread per eviction (balanced)
   unsigned nst = 0;
   if (p < npop) {
-    // popping event: the first jj with S[jj] > p (S is non-decreasing)
-    unsigned lo = 0, hi = (unsigned)B - 1;
-    while (lo < hi) {
-      const unsigned mid = (lo + hi) >> 1;
-      if (__ldg(&x.S[mid]) > p) hi = mid; else lo = mid + 1;
-    }
+    const unsigned lo = x.pmap[p];   // popping event (k_popj_map)
     const long long k = s_start + p;
     const long long j = E0 + lo;
     const bool stale = (unsigned long long)x.rnext[(unsigned long long)k & x.Rm].x > (unsigned long long)(j - k);

@@ -84,6 +84,7 @@ struct Ctx {
   const unsigned *skey, *sidx;    // sorted keys / batch-local event index
   uint2 *dp;
   unsigned *S;
+  unsigned *pmap;   // per eviction: the batch-relative event that pops it (k_popj_map)
   Item *item;
   PosRec *posrec;
   float *t2;
@@ -144,6 +145,7 @@ __global__ void __launch_bounds__(TPB) k_fp(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run(Ctx x);
 __global__ void __launch_bounds__(1024) k_window_fix(Ctx x);
+__global__ void __launch_bounds__(TPB) k_popj_map(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x);
 __global__ void __launch_bounds__(TPB) k_posinfo(Ctx x);
 __global__ void __launch_bounds__(TPB) k_temporal(Ctx x);
