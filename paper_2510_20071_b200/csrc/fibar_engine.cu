@@ -386,6 +386,7 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
     fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
+    fibar_launch(L, "window_check", k_window_check, (T + TPB - 1) / TPB, TPB, 0, s, x);
     fibar_launch(L, "window_fix", k_window_fix, 1, 1024, 0, s, x);
     fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
     fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);

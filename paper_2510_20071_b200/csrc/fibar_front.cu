@@ -104,6 +104,9 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->ticket = 0;
     b->nlong = 0;
     b->nco = 0;
+    b->nbad = 0;
+    b->qlo = 0x7FFFFFFFFFFFFFFFLL;
+    b->qhi = -1;
     s->epoch += 1;
     b->epoch = s->epoch;
     b->epoch0 = s->epoch;
@@ -822,6 +825,40 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
 // predecessor's current end (read before the round writes anything), until
 // every boundary agrees; each round makes at least the first disagreeing
 // chunk exact.  Then publish the batch's final window state.
+// Every chunk boundary checked at once over the whole grid, and the targets'
+// extrema reduced, so that k_window_fix (one block) only loops when a
+// speculative start was wrong.
+__global__ void __launch_bounds__(TPB) k_window_check(Ctx x) {
+  pdl_wait();
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int c = blockIdx.x * TPB + threadIdx.x;
+  long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
+  unsigned bad = 0;
+  if (c < T) {
+    const ChunkRec q = x.ch[c];
+    lo = q.qlo;
+    hi = q.qhi;
+    if (c > 0) {
+      const ChunkRec &p = x.ch[c - 1];
+      bad = q.st_s != p.en_s || q.st_q != p.en_q;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0) {
+    if (bad) atomicAdd(&x.bs->nbad, bad);
+    if (hi >= 0) {
+      atomicMin((unsigned long long *)&x.bs->qlo, (unsigned long long)lo);
+      atomicMax((long long *)&x.bs->qhi, hi);
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
   pdl_wait();
   __shared__ int n_bad;
@@ -830,7 +867,8 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const long long E0 = x.bs->E0, s_start = x.bs->s_start;
   int rounds = 0, reruns = 0;
-  while (true) {
+  const bool fast = x.bs->nbad == 0;   // k_window_check found every boundary exact
+  while (!fast) {
     if (threadIdx.x == 0) n_bad = 0;
     __syncthreads();
     // each thread owns chunks threadIdx.x + 1024*i; snapshot predecessors first
@@ -883,9 +921,16 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
     __syncthreads();
   }
   long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
-  for (int c = threadIdx.x; c < T; c += 1024) {
-    lo = min(lo, x.ch[c].qlo);
-    hi = max(hi, x.ch[c].qhi);
+  if (fast) {
+    if (threadIdx.x == 0) {
+      lo = x.bs->qlo;
+      hi = x.bs->qhi;
+    }
+  } else {
+    for (int c = threadIdx.x; c < T; c += 1024) {
+      lo = min(lo, x.ch[c].qlo);
+      hi = max(hi, x.ch[c].qhi);
+    }
   }
   int rr = __reduce_add_sync(0xffffffffu, reruns);
 #pragma unroll

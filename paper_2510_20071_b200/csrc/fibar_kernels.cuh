@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc);
 __global__ void __launch_bounds__(TPB) k_fp(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run(Ctx x);
+__global__ void __launch_bounds__(TPB) k_window_check(Ctx x);
 __global__ void __launch_bounds__(1024) k_window_fix(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj_map(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x);
