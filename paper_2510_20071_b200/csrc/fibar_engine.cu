@@ -152,7 +152,9 @@ struct fibar_engine {
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
   BlurPrep *prep = nullptr;            // = prep2[0] (debug reads)
   BlurPrep *prep2[2] = {nullptr, nullptr};   // per batch parity: k_popj of batch k+1 writes while batch k blurs
-  unsigned *colist = nullptr;
+  // carried-only stale items, per batch parity: k_popj of batch k+2 may run
+  // while batch k+1's tap resolution still reads its list
+  unsigned *colist2[2] = {nullptr, nullptr};
   Item *item2[2] = {nullptr, nullptr};
   PosRec *posrec2[2] = {nullptr, nullptr};
   float *t2_2[2] = {nullptr, nullptr};
@@ -282,7 +284,7 @@ struct fibar_engine {
     x.bv64 = bv64;
     x.mv64 = mv64;
     x.prep = prep2[par];
-    x.colist = colist;
+    x.colist = colist2[par];
     x.chunk = n_raw <= small_chunk_max ? std::min(chunk, 32) : chunk;
     x.twarm = twarm;
     x.debug = debug;
@@ -964,7 +966,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->prep2[0], npop_cap);
     rc |= dalloc(&g->prep2[1], npop_cap);
     g->prep = g->prep2[0];
-    rc |= dalloc(&g->colist, n + 1);
+    rc |= dalloc(&g->colist2[0], n + 1);
+    rc |= dalloc(&g->colist2[1], n + 1);
     rc |= dalloc(&g->anc, T * NCAND);
     rc |= dalloc(&g->anc2, T * NFINE);
     rc |= dalloc(&g->anc0, T);
@@ -1000,7 +1003,7 @@ int fibar_destroy(fibar_engine *g) {
   if (g->bstream) cudaStreamSynchronize(g->bstream);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
-                  g->dp, g->S, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->sel, g->frame,
+                  g->dp, g->S, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
