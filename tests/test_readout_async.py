@@ -66,3 +66,37 @@ def test_run_pipelined_frames_match_oracle():
         px, bounds, _ = ref.render("robust")
         assert np.array_equal(got[k].pixels, px), k
         assert got[k].bounds == bounds and got[k].readout_time == r
+
+
+@pytest.mark.gpu
+def test_render_async_then_reset_and_reuse():
+    """A read-out still in flight when the engine is reset or read: the frame is
+    the pre-reset state, and the engine afterwards matches a fresh one."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2510_20071_b200.pipeline import DeviceEventArray, ReconstructionEngine
+    geom = SensorGeometry(256, 192)
+    params = compute_params(40.0, Fraction(1, 2), geom)
+    ev = workloads.moving_texture(256, 192, 300_000, seed=21)
+    xd = torch.from_numpy(ev.x.view(np.int16)).cuda()
+    yd = torch.from_numpy(ev.y.view(np.int16)).cuda()
+    pd = torch.from_numpy(ev.p).cuda()
+    eng = ReconstructionEngine(geom, params, batch_capacity=1 << 16)
+    ref = orc.OracleEngine(256, 192, params)
+    for s in range(0, 200_000, 50_000):
+        eng.process_array(DeviceEventArray(xd[s:s + 50_000], yd[s:s + 50_000], pd[s:s + 50_000]))
+        ref.process_array(ev.t[s:s + 50_000], ev.x[s:s + 50_000], ev.y[s:s + 50_000], ev.p[s:s + 50_000])
+    af = eng.render_async("robust")
+    assert np.array_equal(eng.l, ref.l)        # a state read joins the read-out
+    eng.reset()
+    px, bounds, _ = ref.render("robust")
+    fr = af.frame()
+    assert np.array_equal(fr.pixels, px) and fr.bounds == bounds
+    ref2 = orc.OracleEngine(256, 192, params)
+    for s in range(0, 300_000, 30_000):
+        eng.process_array(DeviceEventArray(xd[s:s + 30_000], yd[s:s + 30_000], pd[s:s + 30_000]))
+        ref2.process_array(ev.t[s:s + 30_000], ev.x[s:s + 30_000], ev.y[s:s + 30_000], ev.p[s:s + 30_000])
+        eng.render_async("fixed", 0.5)
+    st = eng.state_arrays()
+    for k in ("p_bar", "l", "active_count", "tile_count", "qx", "qy", "qs"):
+        assert np.array_equal(st[k], getattr(ref2, k)), k
