@@ -70,8 +70,8 @@ def parse():
     ap.add_argument("--profile-only", action="store_true", help="one step, for ncu launch lists")
     ap.add_argument("--bands", action="store_true",
                     help="row bands (filter OFF: the default at N>1; filter ON: halo bands instead of replicas)")
-    ap.add_argument("--halo", type=int, default=8, help="halo rows of the filter-ON row bands")
-    ap.add_argument("--halo-batch", type=int, default=1 << 18, help="events per halo-band batch")
+    ap.add_argument("--halo", type=int, default=16, help="halo rows of the filter-ON row bands")
+    ap.add_argument("--halo-batch", type=int, default=1 << 20, help="events per halo-band batch")
     return ap.parse_args()
 
 

@@ -174,7 +174,7 @@ class HaloBandEngine:
     """
 
     def __init__(self, geometry: SensorGeometry, params: FilterParams, *, rank: int, world: int, group=None,
-                 halo: int = 8, batch_events: int = 1 << 18, engine_factory=None, **engine_kw):
+                 halo: int = 16, batch_events: int = 1 << 20, engine_factory=None, **engine_kw):
         if not params.spatial_enabled:
             raise ConfigError("halo bands are for the spatial filter (filter OFF: BandedReconstructionEngine)")
         self.geometry = geometry
