@@ -62,7 +62,7 @@ def parse():
     ap.add_argument("--events", type=int, default=None, help="override the config's event count")
     ap.add_argument("--packet", type=int, default=None)
     ap.add_argument("--filter", default=None, choices=("on", "off"))
-    ap.add_argument("--batch-cap", type=int, default=1 << 20)
+    ap.add_argument("--batch-cap", type=int, default=0, help="device batch capacity (0: the engine's default)")
     ap.add_argument("--readout", default=None, choices=("end", "packet"),
                     help="robust read-out at the end of the stream or after every packet (config default)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -208,6 +208,7 @@ def run_ours(args, rank, world, dist):
     yd = torch.from_numpy(ev.y.view(np.int16)).to(dev)
     pd = torch.from_numpy(ev.p).to(dev)
     eng = ReconstructionEngine(geom, params, batch_capacity=args.batch_cap)
+    args.batch_cap = eng._bcap   # the effective device batch capacity
     stream = torch.cuda.current_stream(dev)
     frame = torch.empty((geom.height, geom.width), dtype=torch.uint8, device=dev)
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
