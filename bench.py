@@ -178,11 +178,11 @@ def kernel_bytes(name, B, P, D, n_pix):
 def committed_traffic(kernel: str, batch_cap: int, config: int):
     """DRAM bytes per launch of `kernel` from the latest committed ncu --set full
     capture (profiles/rNN*_traffic.json, latest round tag, written by scripts/summarize_ncu.py from
-    `bench.py --profile-only`: config 2, 1M-event device batches); None for any
-    other workload or batch size, or when no capture is committed."""
+    `bench.py --profile-only`: config 2 at the default device batch); None for any
+    other workload or an explicit batch size, or when no capture is committed."""
     import glob
     import json
-    if batch_cap != 1 << 20 or config != 2:
+    if batch_cap or config != 2:   # an explicit --batch-cap: not the captured workload
         return None
     files = sorted(glob.glob(os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "*_traffic.json")))
     for f in reversed(files):
@@ -208,6 +208,7 @@ def run_ours(args, rank, world, dist):
     yd = torch.from_numpy(ev.y.view(np.int16)).to(dev)
     pd = torch.from_numpy(ev.p).to(dev)
     eng = ReconstructionEngine(geom, params, batch_capacity=args.batch_cap)
+    cap_explicit = args.batch_cap
     args.batch_cap = eng._bcap   # the effective device batch capacity
     stream = torch.cuda.current_stream(dev)
     frame = torch.empty((geom.height, geom.width), dtype=torch.uint8, device=dev)
@@ -324,7 +325,7 @@ def run_ours(args, rank, world, dist):
     roofline = {
         "bound": "hbm", "kernel": dname, "achieved": achieved, "peak": peak, "peak_source": peak_kind,
         "unit": "GB/s", "frac": (achieved / peak) if achieved else None,
-        "traffic": committed_traffic(dname, args.batch_cap, args.config),
+        "traffic": committed_traffic(dname, cap_explicit, args.config),
         "share_of_step": dms / tot_ms if tot_ms else None, "mean_launch_us": launch_s * 1e6,
         "bytes_per_launch": bytes_launch,
     }
