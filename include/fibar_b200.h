@@ -165,6 +165,9 @@ int fibar_profile_read(fibar_engine *eng, int32_t max_entries, char *names, int3
 int fibar_debug_times(fibar_engine *eng, uint64_t *done_ns, uint64_t *grab_ns, int64_t n);
 /* Debug only: the blur items' resolved-tap records of the last batch (80 B each). */
 int fibar_debug_prep(fibar_engine *eng, void *out, int64_t n);
+/* debug: globaltimer stamps (ns) of the last read-out's phases, CTA 0
+ * (16 slots; zero unless the library was built with FIBAR_RO_TIMES) */
+int fibar_debug_readout_times(fibar_engine *eng, uint64_t ts[16]);
 /* Copy the float32 brightness grid (after running coalesced events) to dst
  * (dst_mem: FIBAR_MEM_DEVICE, asynchronous; or FIBAR_MEM_HOST, synchronous). */
 int fibar_copy_brightness(fibar_engine *eng, float *dst, int32_t dst_mem);

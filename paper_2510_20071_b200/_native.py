@@ -24,7 +24,7 @@ FIBAR_RENDER_FIXED = 1
 EXPORTED = (
     "fibar_create", "fibar_destroy", "fibar_set_stream", "fibar_reset", "fibar_process", "fibar_flush",
     "fibar_render", "fibar_read_qs", "fibar_counters", "fibar_read_state", "fibar_stats",
-    "fibar_brightness_ptr", "fibar_last_error", "fibar_profile", "fibar_profile_read", "fibar_pending", "fibar_debug_times", "fibar_debug_prep", "fibar_render_grid", "fibar_copy_brightness", "fibar_decode_evf1",
+    "fibar_brightness_ptr", "fibar_last_error", "fibar_profile", "fibar_profile_read", "fibar_pending", "fibar_debug_times", "fibar_debug_prep", "fibar_debug_readout_times", "fibar_render_grid", "fibar_copy_brightness", "fibar_decode_evf1",
     "fibar_count_events", "fibar_pixel_trace", "fibar_pixel_trace_iir",
     "fibar_halo_batch", "fibar_halo_round", "fibar_halo_finish", "fibar_render_async",
 )
@@ -89,6 +89,7 @@ def load(path: str | None = None):
         "fibar_pending": ([P, P, P], C.c_int),
         "fibar_debug_times": ([P, P, P, i64], C.c_int),
         "fibar_debug_prep": ([P, P, i64], C.c_int),
+        "fibar_debug_readout_times": ([P, P], C.c_int),
         "fibar_render_grid": ([P, i64, i32, f64, P, i32, P, P, P], C.c_int),
         "fibar_copy_brightness": ([P, P, i32], C.c_int),
         "fibar_decode_evf1": ([P, i64, i32, i32, C.c_uint64, P, P, P, P, P, P], C.c_int),

@@ -22,8 +22,8 @@
 //                                            order (_kernels.py:173-189), dataflow over a
 //                                            persistent grid polling (epoch | value) words
 //   final      k_final / k_batch_end         end-of-batch brightness, counters
-//   read-out   k_sel_init / k_sel_hist /     exact percentile select + float64 map
-//              k_render_map                  (pipeline.py:562-584)
+//   read-out   k_readout                     exact percentile select + float64 map in one
+//                                            cooperative kernel (pipeline.py:247-269)
 //
 // Filter ON, the blur stage of batch k runs on a second stream while batch k+1's
 // front end runs; small batches replay a captured CUDA graph
@@ -36,6 +36,7 @@
 #include <cmath>
 #include <algorithm>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include <cuda.h>
@@ -683,6 +684,7 @@ int render_core(Launcher &L, const float *l, long long n, int32_t mode, double f
   if (mode != FIBAR_RENDER_FIXED && mode != FIBAR_RENDER_ROBUST) return fail(FIBAR_E_CONFIG, "unknown scale mode");
   cudaStream_t s = L.stream;
   double g_lo = 0, g_hi = 0;
+  uint4 ranks = make_uint4(0u, 0u, 0u, 0u);
   if (mode == FIBAR_RENDER_ROBUST) {
     // virtual index (n-1)*q, neighbours floor / floor+1, clamped at the top
     const double qs[2] = {1.0 / 100.0, 99.0 / 100.0};
@@ -707,15 +709,38 @@ int render_core(Launcher &L, const float *l, long long n, int32_t mode, double f
     }
     g_lo = gam[0];
     g_hi = gam[1];
-    fibar_launch(L, "sel_init", k_sel_init, 1, 1, 0, s, sel, rk[0], rk[1], rk[2], rk[3]);
-    const int grid = nsm * 2;
-    for (int pass = 0; pass < 3; ++pass)
-      fibar_launch(L, "sel_hist", k_sel_hist, grid, TPB, 0, s, l, n, sel, pass, g_lo, g_hi);
-  } else {
-    fibar_launch(L, "sel_bounds", k_sel_bounds, 1, 1, 0, s, sel, g_lo, g_hi, mode, fixed_bound);
+    ranks = make_uint4(rk[0], rk[1], rk[2], rk[3]);
   }
   uint8_t *dst = out_mem == FIBAR_MEM_DEVICE ? out : frame;
-  fibar_launch(L, "render_map", k_render_map, nsm * 4, TPB, 0, s, l, n, sel, dst);
+  // one cooperative launch, one CTA per SM (fewer for small grids), each CTA
+  // holding its slice of keys on chip when it fits (k_readout)
+  const long long grid0 = std::max(1LL, std::min((long long)nsm, (n + 2047) / 2048));
+  const long long slice = ((n + grid0 - 1) / grid0 + 3) & ~3LL;
+  const int grid = (int)((n + slice - 1) / slice);
+  const int on_chip = slice * 4 <= RO_SMEM_MAX ? 1 : 0;
+  {
+    static unsigned long long attr_set = 0;   // per device: dynamic shared memory opt-in done
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 64 && !(attr_set >> dev & 1ull)) {
+      CK(cudaFuncSetAttribute(k_readout, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RO_SMEM_MAX));
+      attr_set |= 1ull << dev;
+    }
+  }
+  L.begin("readout");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(RO_TPB);
+  cfg.dynamicSmemBytes = on_chip ? (size_t)slice * 4 : 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CK(cudaLaunchKernelEx(&cfg, k_readout, l, (long long)n, sel, (int)mode, fixed_bound, ranks, g_lo, g_hi, dst, slice,
+                        on_chip));
+  L.end();
   CK(cudaGetLastError());
   if (out_mem != FIBAR_MEM_DEVICE) CK(cudaMemcpyAsync(out, frame, n, cudaMemcpyDeviceToHost, s));
   if (bounds || degenerate || out_mem != FIBAR_MEM_DEVICE) {
@@ -1263,29 +1288,41 @@ int fibar_render_async(fibar_engine *g, int32_t mode, double fixed_bound, uint8_
 
 int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_bound, uint8_t *out, int32_t out_mem,
                       double *bounds, int32_t *degenerate, void *stream) {
-  static SelState *sel = nullptr;
-  static uint8_t *frame = nullptr;
-  static long long cap = 0;
-  static Launcher L;
-  static int nsm = 0;
+  // read-out scratch per device, one caller at a time (the scratch is shared
+  // by every stream of that device)
+  struct Scratch {
+    SelState *sel = nullptr;
+    uint8_t *frame = nullptr;
+    long long cap = 0;
+    int nsm = 0;
+  };
+  static Scratch per_dev[64];
+  static std::mutex mu;
   if (!l_dev || n < 1) return fail(FIBAR_E_CONFIG, "empty grid");
-  if (!sel) {
-    int rc = dalloc(&sel, 1);
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(FIBAR_E_CONFIG, "device index out of range");
+  std::lock_guard<std::mutex> lock(mu);
+  Scratch &sc = per_dev[dev];
+  if (!sc.sel) {
+    int rc = dalloc(&sc.sel, 1);
     if (rc) return rc;
-    CK(cudaMemset(sel, 0, sizeof(SelState)));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    CK(cudaMemset(sc.sel, 0, sizeof(SelState)));
+    cudaDeviceGetAttribute(&sc.nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  if (out_mem != FIBAR_MEM_DEVICE && n > cap) {
-    if (frame) cudaFree(frame);
-    frame = nullptr;
-    int rc = dalloc(&frame, n);
+  if (out_mem != FIBAR_MEM_DEVICE && n > sc.cap) {
+    if (sc.frame) cudaFree(sc.frame);
+    sc.frame = nullptr;
+    int rc = dalloc(&sc.frame, n);
     if (rc) return rc;
-    cap = n;
+    sc.cap = n;
   }
+  Launcher L;
   L.stream = (cudaStream_t)stream;
-  return render_core(L, l_dev, n, mode, fixed_bound, out, out_mem, bounds, degenerate, sel, frame, nsm);
+  int rc = render_core(L, l_dev, n, mode, fixed_bound, out, out_mem, bounds, degenerate, sc.sel, sc.frame, sc.nsm);
+  if (!rc && !(bounds || degenerate || out_mem != FIBAR_MEM_DEVICE))
+    CK(cudaStreamSynchronize(L.stream));   // the scratch is reused by the next caller
+  return rc;
 }
 
 int fibar_read_qs(fibar_engine *g, int64_t qs[10]) {
@@ -1452,6 +1489,14 @@ int fibar_debug_prep(fibar_engine *g, void *out, int64_t n) {
   join_blur(g);
   CK(cudaStreamSynchronize(g->L.stream));
   CK(cudaMemcpy(out, g->prep, sizeof(BlurPrep) * n, cudaMemcpyDeviceToHost));
+  return 0;
+}
+
+int fibar_debug_readout_times(fibar_engine *g, uint64_t ts[16]) {
+  if (!g || !ts) return fail(FIBAR_E_CONFIG, "null argument");
+  join_blur(g);
+  CK(cudaStreamSynchronize(g->L.stream));
+  CK(cudaMemcpy(ts, g->sel->ts, sizeof(uint64_t) * 16, cudaMemcpyDeviceToHost));
   return 0;
 }
 

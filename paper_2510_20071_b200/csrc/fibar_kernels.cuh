@@ -44,14 +44,25 @@ struct ChunkRec {
   long long qlo, qhi;                            // extrema of the targets set inside the chunk
 };
 
+// read-out scratch (k_readout): the bounds first (copied to the host as
+// {lo, hi, degenerate}), the grid barrier, what the last CTA publishes, and two
+// sets of radix histograms (one per launch parity: a launch clears the set the
+// next one uses)
+struct alignas(16) SelCounters {
+  unsigned hist[3][4][2048];      // [pass][target][digit]
+};
 struct SelState {
-  unsigned prefix[4];
-  unsigned rank[4];
-  unsigned hist[4][2048];
   double lo, hi;
   int degenerate;
-  unsigned done;   // blocks finished with the current histogram pass
+  unsigned parity;
+  unsigned bar_count, bar_gen;
+  unsigned pad0[2];
+  alignas(16) unsigned bc[12];    // published by the last CTA: prefixes, residual ranks
+  unsigned long long ts[16];      // FIBAR_RO_TIMES: CTA 0's phase stamps
+  SelCounters cur[2];
 };
+constexpr int RO_TPB = 512;                  // k_readout: threads per CTA (one CTA per SM)
+constexpr long long RO_SMEM_MAX = 160 << 10;  // slice keys kept on chip up to this many bytes
 
 struct Ctx {
   int W, H, ts, tiles_x, A;
@@ -162,10 +173,7 @@ __global__ void __launch_bounds__(TPB) k_halo_write(Ctx x, const unsigned *cnt, 
 __global__ void k_halo_epoch(Ctx x);
 __global__ void __launch_bounds__(TPB) k_halo_collect(Ctx x, const unsigned *hlist, long long n_in, long long n_out,
                                                       unsigned long long *out);
-__global__ void __launch_bounds__(TPB) k_sel_hist(const float *__restrict__ l, long long n, SelState *sel, int pass, double g_lo, double g_hi);
-__global__ void k_sel_init(SelState *sel, unsigned r0, unsigned r1, unsigned r2, unsigned r3);
-__global__ void k_sel_bounds(SelState *sel, double g_lo, double g_hi, int mode, double fixed_bound);
-__global__ void __launch_bounds__(TPB) k_render_map(const float *__restrict__ l, long long n, const SelState *__restrict__ sel, uint8_t *__restrict__ out);
+__global__ void __launch_bounds__(RO_TPB, 1) k_readout(const float *__restrict__ l, long long n, SelState *sel, int mode, double fixed_bound, uint4 ranks, double g_lo, double g_hi, uint8_t *__restrict__ out, long long slice, int on_chip);
 __global__ void __launch_bounds__(TPB) k_evf1_decode(const uint4 *__restrict__ rec2, const uint2 *__restrict__ rec1, long long nrec, int W, int H, uint16_t *__restrict__ xo, uint16_t *__restrict__ yo, int8_t *__restrict__ po, unsigned *__restrict__ dto, unsigned long long *__restrict__ bsum, unsigned long long *__restrict__ first_bad);
 __global__ void __launch_bounds__(1024) k_evf1_block_scan(unsigned long long *bsum, int nb, unsigned long long t_base);
 __global__ void __launch_bounds__(TPB) k_evf1_times(const unsigned *__restrict__ dt, long long nrec, const unsigned long long *__restrict__ bofs, unsigned long long *__restrict__ t);
