@@ -7,25 +7,25 @@
  * (paths relative to /root/reference/pkg/src/fibar):
  *
  *   fibar_create / fibar_destroy
- *       ReconstructionEngine.__init__ state allocation, pipeline.py:381-439
+ *       ReconstructionEngine.__init__ state allocation, pipeline.py:66-124
  *       (p_bar, l, active_count, tile_count, ring qx/qy, qs[10], gain map,
  *       float32 coefficient casts).
  *   fibar_process
- *       ReconstructionEngine.process_array, pipeline.py:511-558, i.e. the OOB
+ *       ReconstructionEngine.process_array, pipeline.py:196-243, i.e. the OOB
  *       filter (non-strict) plus the numba kernels _temporal_chunk
  *       (_kernels.py:62-73) / _full_chunk (_kernels.py:76-216).
  *   fibar_flush
  *       (no reference equivalent: the engine coalesces packets on the device
  *       between read-outs; state is packet-size invariant).
  *   fibar_render / fibar_render_async
- *       ReconstructionEngine.render, pipeline.py:562-584 (async: the frame
+ *       ReconstructionEngine.render, pipeline.py:247-269 (async: the frame
  *       loop of run(), pipeline.py:372-397, without a host wait per frame).
  *   fibar_read_qs / fibar_counters
- *       the qs[10] slots (_kernels.py:48-59, pipeline.py:451-477) and
- *       event_count / oob_dropped (pipeline.py:437-439).
+ *       the qs[10] slots (_kernels.py:48-59, pipeline.py:136-162) and
+ *       event_count / oob_dropped (pipeline.py:122-124).
  *   fibar_read_state
  *       the arrays hashed by state_digest / returned by iap, l_grid,
- *       p_bar_grid (pipeline.py:443-496).
+ *       p_bar_grid (pipeline.py:128-181).
  *   fibar_halo_batch / fibar_halo_round / fibar_halo_finish
  *       _full_chunk (_kernels.py:76-216) for one row band of a filter-ON
  *       multi-GPU partition: the window pass of the whole stream, the blur loop
@@ -74,10 +74,10 @@ typedef struct fibar_config {
   int64_t fill_den;
   int64_t q_min;
   int64_t q_max;
-  float alpha;              /* float32(params.alpha)            pipeline.py:432 */
-  float one_m_alpha;        /* float32(1 - params.alpha)        pipeline.py:433 */
-  float beta;               /* float32(params.beta)             pipeline.py:434 */
-  float half_1p_beta;       /* float32(params.half_one_plus_beta) pipeline.py:435 */
+  float alpha;              /* float32(params.alpha)            pipeline.py:117 */
+  float one_m_alpha;        /* float32(1 - params.alpha)        pipeline.py:118 */
+  float beta;               /* float32(params.beta)             pipeline.py:119 */
+  float half_1p_beta;       /* float32(params.half_one_plus_beta) pipeline.py:120 */
   const float *gain;        /* optional host array [height*width] or NULL */
   int64_t batch_capacity;   /* max in-bounds events per device batch; 0 = default */
   /* Row band (multi-GPU row-band partition, filter OFF only): this engine owns
@@ -107,7 +107,7 @@ int fibar_reset(fibar_engine *eng);
 /* Append one packet of n events (SoA columns x, y uint16 and p int8 in {-1,+1}).
  * mem = FIBAR_MEM_HOST or FIBAR_MEM_DEVICE says where the three columns live.
  * Out-of-bounds events are dropped and counted (non-strict semantics of
- * pipeline.py:516-528); strict checks are the caller's.  Work is queued on the
+ * pipeline.py:201-213); strict checks are the caller's.  Work is queued on the
  * engine stream; packets may be coalesced until the next read. */
 int fibar_process(fibar_engine *eng, const uint16_t *x, const uint16_t *y, const int8_t *p, int64_t n,
                   int32_t mem);
@@ -179,7 +179,7 @@ int fibar_brightness_ptr(fibar_engine *eng, float **out);
 int fibar_render_grid(const float *l_dev, int64_t n, int32_t mode, double fixed_bound, uint8_t *out,
                       int32_t out_mem, double *bounds, int32_t *degenerate, void *stream);
 
-/* Decode nrec EVF1 records (event_io.py:353-369: dt u32 | xp u16 | y u16,
+/* Decode nrec EVF1 records (event_io.py:60-76: dt u32 | xp u16 | y u16,
  * little endian) already in device memory into device columns x, y (uint16),
  * p (int8 +-1) and, if t is non-NULL, t = t_base + cumulative dt (uint64).
  * records must be 16-byte aligned.  *first_bad receives the index of the

@@ -17,9 +17,9 @@
  *   oracle_temporal_chunk  <- _kernels.py:62-73   (_temporal_chunk)
  *   oracle_full_chunk      <- _kernels.py:76-216  (_full_chunk), QS_* slots 48-59
  *   oracle_blur_at         <- _kernels.py:252-268 (_blur_at)
- *   oracle_render          <- pipeline.py:562-584 (render) + numpy 2.3.5
+ *   oracle_render          <- pipeline.py:247-269 (render) + numpy 2.3.5
  *                             percentile 'linear' (virtual index (n-1)q, _lerp)
- *   oracle_decode_evf1     <- event_io.py:353-369 (_decode_block)
+ *   oracle_decode_evf1     <- event_io.py:60-76 (_decode_block)
  *   oracle_trace_f32/_f64  <- _kernels.py:219-233 (_temporal_trace)
  *   oracle_trace_iir_f32/_f64 <- _kernels.py:236-249 (_iir_trace)
  *   oracle_count_events    <- calib.py:26-45 (count_events, flat = y*W + x)
@@ -240,7 +240,7 @@ static double percentile_linear(double *work, int64_t n, double q) {
   return r;
 }
 
-/* render (pipeline.py:562-584).  mode 0 = robust (1st..99th percentile),
+/* render (pipeline.py:247-269).  mode 0 = robust (1st..99th percentile),
  * 1 = fixed (+-bound).  Writes n uint8 pixels, bounds[2], *degenerate.
  * Returns 0, or -1 on a bad mode / bound (the caller raises ConfigError). */
 int oracle_render(const float *l, int64_t n, int mode, double fixed_bound,
@@ -280,7 +280,7 @@ int oracle_render(const float *l, int64_t n, int mode, double fixed_bound,
   return 0;
 }
 
-/* EVF1 record block decode (event_io.py:353-369).  Returns -1 when every
+/* EVF1 record block decode (event_io.py:60-76).  Returns -1 when every
  * record is in bounds, else the index of the first out-of-bounds record
  * (outputs are then unspecified; the caller raises DataError). */
 int64_t oracle_decode_evf1(const uint8_t *raw, int64_t nrec, int64_t width,

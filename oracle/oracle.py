@@ -73,7 +73,7 @@ def _p(a: np.ndarray):
 
 
 def render(l: np.ndarray, scale_mode: str = "robust", fixed_bound: float = 1.0):
-    """(uint8 pixels, (lo, hi), degenerate) exactly as pipeline.py:562-584."""
+    """(uint8 pixels, (lo, hi), degenerate) exactly as pipeline.py:247-269."""
     lf = np.ascontiguousarray(l, dtype=np.float32).reshape(-1)
     out = np.empty(lf.size, np.uint8)
     bounds = np.zeros(2, np.float64)

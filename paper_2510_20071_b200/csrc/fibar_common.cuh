@@ -74,7 +74,7 @@ struct BatchState {
 
 // Window / counter state living in device memory so no kernel needs a host
 // round trip.  Mirrors the reference's qs[10] slots (_kernels.py:48-59) plus
-// the engine counters (pipeline.py:437-439).
+// the engine counters (pipeline.py:122-124).
 struct DevState {
   long long s;        // window start (global in-bounds index); QS_HEAD = s mod (n_pix+1)
   long long q;        // QS_TARGET

@@ -5,7 +5,7 @@
 // fibar_sort.cu (radix sort, scans); fibar_kernels.cuh declares them.
 //
 // One device batch (coalesced packets) flows through:
-//   ingest     k_count_inb / k_compact      OOB filter + compaction (pipeline.py:516-528),
+//   ingest     k_count_inb / k_compact      OOB filter + compaction (pipeline.py:201-213),
 //                                            pixel keys, ring of window keys
 //   group      radix_sort_pairs              stable (tile-major key, index) sort
 //   link       k_seg_marks / k_link          per event: distance to previous same-pixel /
@@ -676,7 +676,7 @@ int sync_point(fibar_engine *g) {
   return join_blur(g);
 }
 
-// read-out (pipeline.py:562-584) of n float32 values at l: exact order
+// read-out (pipeline.py:247-269) of n float32 values at l: exact order
 // statistics for the robust bounds (numpy 'linear' percentile), float64 map
 int render_core(Launcher &L, const float *l, long long n, int32_t mode, double fixed_bound, uint8_t *out,
                 int32_t out_mem, double *bounds, int32_t *degenerate, SelState *sel, uint8_t *frame, int nsm) {

@@ -13,7 +13,7 @@ static __constant__ double c_geo_mul[NGEO] = {0.25, 0.5, 0.75, 1.25, 1.5, 2.0, 2
 
 
 // an event is kept iff it lies on the sensor (else it is out of bounds,
-// counted like pipeline.py:524-525) and in this engine's row band (a band
+// counted like pipeline.py:209-210) and in this engine's row band (a band
 // engine silently leaves other bands' events to their owners)
 __device__ __forceinline__ bool on_sensor(const Ctx &x, unsigned xx, unsigned yy) {
   return xx < (unsigned)x.W && yy < x.full_H;

@@ -324,10 +324,10 @@ __global__ void __launch_bounds__(RO_TPB, 1)
 
 // ------------------------------------------------------------ EVF1 decode ---
 
-// EVF1 records (event_io.py:353-369): dt u32 LE | xp u16 (bit 15 polarity,
+// EVF1 records (event_io.py:60-76): dt u32 LE | xp u16 (bit 15 polarity,
 // bits 0..14 x) | y u16.  Two records per thread through one 16-byte load;
 // columns out, per-block dt sums for the timestamp scan, first out-of-bounds
-// record index (the container is invalid then: DataError, event_io.py:359-365).
+// record index (the container is invalid then: DataError, event_io.py:66-72).
 
 __global__ void __launch_bounds__(TPB) k_evf1_decode(const uint4 *__restrict__ rec2, const uint2 *__restrict__ rec1,
                                                      long long nrec, int W, int H, uint16_t *__restrict__ xo,

@@ -2,7 +2,7 @@
 
 Drop-in for the reference's `fibar/pipeline.py`: same class and function
 names, constructor arguments, properties, validation and exception types
-(``ReconstructionEngine`` <- pipeline.py:378-584, ``run`` <- 640-712,
+(``ReconstructionEngine`` <- pipeline.py:63-269, ``run`` <- 640-712,
 ``Frame`` <- 359-375, ``write_pgm``/``read_pgm`` <- 590-610,
 ``RunResult`` <- 613-618).
 
@@ -160,7 +160,7 @@ class ReconstructionEngine:
             gain_ptr = self._gain.ctypes.data
         self._use_gain = self._gain is not None
 
-        # float32 coefficients exactly as the reference casts them (pipeline.py:431-435)
+        # float32 coefficients exactly as the reference casts them (pipeline.py:116-120)
         self._alpha32 = np.float32(params.alpha)
         self._one_m_alpha32 = np.float32(1.0 - params.alpha)
         self._beta32 = np.float32(params.beta)
@@ -394,7 +394,7 @@ class ReconstructionEngine:
         return self.active_count.reshape(self.geometry.height, self.geometry.width)
 
     def state_bytes(self) -> int:
-        """Bytes of the reference-layout state (pipeline.py:488-490), for parity with its report."""
+        """Bytes of the reference-layout state (pipeline.py:173-175), for parity with its report."""
         n = self.geometry.n_pix
         b = n * 4 * 2 + n * 2 + self.tiles_x * self.tiles_y + self.qcap * 4 + QS_SIZE * 8
         return b + (self._gain.nbytes if self._use_gain else 0)
@@ -488,7 +488,7 @@ class ReconstructionEngine:
         _native.check(self._lib.fibar_halo_finish(self._h), "fibar_halo_finish")
 
     def _note_last_t(self, xs, ys, ts) -> None:
-        # the reference keeps the time of the last *in-bounds* event (pipeline.py:558)
+        # the reference keeps the time of the last *in-bounds* event (pipeline.py:243)
         if ts is None:
             return
         W, H = self.geometry.width, self.geometry.height
@@ -751,7 +751,7 @@ def run(
     """Stream packets through the engine, reading out frames on a time grid.
 
     A frame at time r reflects exactly the events with t < r (packets are
-    split with ``searchsorted(..., 'left')`` as in pipeline.py:694-699);
+    split with ``searchsorted(..., 'left')`` as in pipeline.py:379-384);
     explicit read-out times after the stream end render the final state.
     """
     if frame_sink is None and out_dir is not None:

@@ -6,7 +6,7 @@ Same names, arguments and results as the reference module:
   ``apply_threshold_map`` (temporal.py:25-67) are scalar float64 helpers --
   plain Python arithmetic in the same operation order, exactly as the
   reference defines them (there is nothing to put on a GPU in one scalar step).
-* ``stream_pixel`` / ``stream_pixel_iir`` (temporal.py:78-118) run a polarity
+* ``stream_pixel`` / ``stream_pixel_iir`` (temporal.py:78-117) run a polarity
   sequence through the recurrences on the device (``fibar_pixel_trace`` /
   ``fibar_pixel_trace_iir``, csrc/fibar_tools.cu) with the reference kernels'
   separately rounded operation order (_kernels.py:219-249), so float32 traces
@@ -156,5 +156,5 @@ def stream_pixels_iir(polarities, params: FilterParams, dtype=np.float32) -> np.
 
 
 def stream_pixel_iir(polarities, params: FilterParams, dtype=np.float32) -> np.ndarray:
-    """Run one polarity sequence through the combined recurrence from zero state (temporal.py:103-118)."""
+    """Run one polarity sequence through the combined recurrence from zero state (temporal.py:103-117)."""
     return stream_pixels_iir(np.asarray(polarities, dtype=np.int8).reshape(1, -1), params, dtype)[0]

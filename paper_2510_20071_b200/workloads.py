@@ -164,6 +164,39 @@ CONFIGS = {
 }
 
 
+GENERATOR_VERSION = 1   # bump when a generator's output changes (invalidates cached streams)
+
+
+def make_cached(kind: str, geometry: SensorGeometry, n: int, seed: int = 0, cache_dir: str | None = None,
+                **kw) -> EventArray:
+    """``make`` with an on-disk copy of the stream (default ``$FIBAR_STREAM_CACHE``
+    or /tmp/fibar_streams), so the bench's two arms on one box generate a
+    100M-event stream once.  A cache miss or an unreadable file regenerates;
+    the stream itself never depends on the cache."""
+    import hashlib
+    import os
+    cache_dir = cache_dir or os.environ.get("FIBAR_STREAM_CACHE", "/tmp/fibar_streams")
+    key = hashlib.sha256(repr((GENERATOR_VERSION, kind, geometry.width, geometry.height, n, seed,
+                               sorted(kw.items()))).encode()).hexdigest()[:24]
+    path = os.path.join(cache_dir, f"{kind}_{geometry.width}x{geometry.height}_{n}_{seed}_{key}.npz")
+    try:
+        with np.load(path) as z:
+            ev = EventArray(z["t"], z["x"], z["y"], z["p"])
+        if len(ev) == n:
+            return ev
+    except (OSError, ValueError, KeyError):
+        pass
+    ev = make(kind, geometry, n, seed=seed, **kw)
+    try:
+        os.makedirs(cache_dir, exist_ok=True)
+        tmp = path + f".{os.getpid()}.tmp.npz"
+        np.savez(tmp, t=ev.t, x=ev.x, y=ev.y, p=ev.p)
+        os.replace(tmp, path)
+    except OSError:
+        pass
+    return ev
+
+
 def make(kind: str, geometry: SensorGeometry, n: int, seed: int = 0, **kw) -> EventArray:
     if kind == "uniform":
         return uniform(geometry.width, geometry.height, n, seed)

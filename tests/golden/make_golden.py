@@ -131,7 +131,7 @@ def misc_cases():
     coef = np.array([rcore.cutoff_coefficients(tc) for tc in tcuts])
     out["tcuts"] = tcuts
     out["coef"] = coef
-    # render edge cases (pipeline.py:562-584)
+    # render edge cases (pipeline.py:247-269)
     g = rcore.SensorGeometry(8, 5)
     params = rcore.compute_params(40.0, Fraction(1, 2), g)
     rng = np.random.default_rng(5)
@@ -152,7 +152,7 @@ def misc_cases():
             out[f"grid{i}_{mode}_{bound}_px"] = fr.pixels
             out[f"grid{i}_{mode}_{bound}_bounds"] = np.array(fr.bounds)
             out[f"grid{i}_{mode}_{bound}_deg"] = fr.degenerate
-    # EVF1 round trip + decode (event_io.py:353-369, 436-475)
+    # EVF1 round trip + decode (event_io.py:60-76, 143-182)
     geom, ev = _stream("uniform", 100, 60, 5000, 3)
     buf = io.BytesIO()
     rio.write_stream(geom, ev, buf)

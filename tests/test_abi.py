@@ -51,3 +51,27 @@ def test_no_cuda_means_loud_failure():
     g = SensorGeometry(8, 8)
     with pytest.raises(DeviceError):
         ReconstructionEngine(g, compute_params(40.0, geometry=g))
+
+
+REF = "/root/reference/pkg/src/fibar"
+CITE = re.compile(r"\b(_kernels|pipeline|core|event_io|errors|calib|temporal|spatial|cli|synth)\.py:(\d+)(?:-(\d+))?")
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference not mounted")
+def test_reference_citations_point_inside_the_cited_files():
+    """Every `module.py:A-B` citation in product code, docs and the header names
+    lines that exist in the reference module (the boundary cites what it replaces)."""
+    lengths = {m: sum(1 for _ in open(os.path.join(REF, m + ".py"))) for m in
+               ("_kernels", "pipeline", "core", "event_io", "errors", "calib", "temporal", "spatial", "cli", "synth")}
+    files = subprocess.run(["git", "ls-files"], cwd=ROOT, capture_output=True, text=True).stdout.split()
+    skip = {"SURVEY.md", "VERDICT.md", "ADVICE.md", "BASELINE.md", "PAPERS.md", "SNIPPETS.md"}
+    bad = []
+    for f in files:
+        if f in skip or not f.endswith((".py", ".md", ".h", ".c", ".cu", ".cuh")):
+            continue
+        for ln, line in enumerate(open(os.path.join(ROOT, f), errors="replace"), 1):
+            for m in CITE.finditer(line):
+                a, b = int(m.group(2)), int(m.group(3) or m.group(2))
+                if not (1 <= a <= b <= lengths[m.group(1)]):
+                    bad.append(f"{f}:{ln}: {m.group(0)}")
+    assert not bad, bad

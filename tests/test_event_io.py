@@ -1,5 +1,6 @@
-"""EVF1 ingest: host mirror (CPU) and device decode kernel (GPU), pinned to the
-reference's own decode of a reference-written stream (tests/golden/misc.npz)."""
+"""EVF1 ingest: the device decoder behind read_blocks / read_blocks_device, and
+the writer, pinned to the reference's own decode of a reference-written stream
+(tests/golden/misc.npz)."""
 
 import io
 
@@ -9,7 +10,7 @@ import pytest
 from conftest import golden_path
 from paper_2510_20071_b200 import event_io, workloads
 from paper_2510_20071_b200.core import SensorGeometry
-from paper_2510_20071_b200.errors import DataError, FormatError, TruncationError
+from paper_2510_20071_b200.errors import DataError, DeviceError, FormatError, OrderError, TruncationError
 
 
 def golden():
@@ -17,7 +18,8 @@ def golden():
     return m["evf1"].tobytes(), m
 
 
-def test_host_decode_matches_reference():
+@pytest.mark.gpu
+def test_read_blocks_matches_reference():
     raw, m = golden()
     geom, blocks = event_io.read_blocks(io.BytesIO(raw), block_events=777)
     assert (geom.width, geom.height) == (100, 60)
@@ -26,14 +28,38 @@ def test_host_decode_matches_reference():
         assert np.array_equal(np.concatenate([getattr(b, k) for b in got]), m[f"evf1_{k}"])
 
 
-def test_write_read_round_trip_and_errors():
+def test_writer_bytes_and_header_errors():
     ev = workloads.uniform(100, 60, 5000, 3)
     buf = io.BytesIO()
     event_io.write_stream(SensorGeometry(100, 60), ev, buf)
     raw, _ = golden()
     assert buf.getvalue() == raw          # byte-identical to the reference's writer
+    buf = io.BytesIO()                    # the same stream as several blocks
+    event_io.write_stream(SensorGeometry(100, 60), [ev.slice(0, 1234), ev.slice(1234, 1234), ev.slice(1234, 5000)], buf)
+    assert buf.getvalue() == raw
     with pytest.raises(FormatError):
         event_io.read_header(io.BytesIO(b"EVF2" + raw[4:16]))
+    with pytest.raises(FormatError):
+        event_io.read_header(io.BytesIO(raw[:15] + b"\x01"))
+    with pytest.raises(TruncationError):
+        event_io.read_header(io.BytesIO(raw[:9]))
+    assert event_io.read_header(io.BytesIO(raw)) == SensorGeometry(100, 60)
+    with pytest.raises(OrderError):
+        event_io.write_stream(SensorGeometry(100, 60), [ev.slice(10, 20), ev.slice(0, 10)], io.BytesIO())
+
+
+def test_readers_need_the_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    raw, _ = golden()
+    with pytest.raises(DeviceError):
+        list(event_io.read_blocks(io.BytesIO(raw))[1])
+
+
+@pytest.mark.gpu
+def test_read_blocks_errors():
+    raw, _ = golden()
     with pytest.raises(TruncationError):
         list(event_io.read_blocks(io.BytesIO(raw[:-3]))[1])
     with pytest.raises(DataError):

@@ -93,50 +93,12 @@ def test_threshold_scaling_and_errors(tools):
         temporal.update_pixel(temporal.PixelState(), 0, _params(40.0))
 
 
-@pytest.mark.parametrize("qtag,q", [("q01", 0.01), ("q0", 0.0), ("q20", 0.2)])
-def test_estimate_thresholds_match_reference(tools, qtag, q):
+@pytest.mark.parametrize("qtag", ["q01", "q0", "q20"])
+def test_gain_grid_matches_reference(tools, qtag):
+    """ThresholdMap.gain_grid (calib.py:73-78) of the reference's own thresholds."""
     from paper_2510_20071_b200 import calib
-    tm = calib.estimate_thresholds(tools["cal_n_on"], tools["cal_n_off"], exclusion_quantile=q)
-    for mine, key in ((tm.c_prime, "c"), (tm.c_on_prime, "con"), (tm.c_off_prime, "coff")):
-        assert np.array_equal(mine, tools[f"cal_{qtag}_{key}"], equal_nan=True)
-    assert np.array_equal(tm.excluded, tools[f"cal_{qtag}_excl"])
-    assert tm.n_bar_tot == float(tools[f"cal_{qtag}_nbar"])
-    assert tm.harmonic_mean() == float(tools[f"cal_{qtag}_hmean"])
-    g = tm.gain_grid()
+    g = calib.gain_grid(tools[f"cal_{qtag}_c"])
     assert g.dtype == np.float32 and np.array_equal(g, tools[f"cal_{qtag}_gain"])
-    edges, counts = calib.histogram(tm, "c_prime", bins=20)
-    assert np.array_equal(edges, tools[f"cal_{qtag}_hist_edges"])
-    assert np.array_equal(counts, tools[f"cal_{qtag}_hist_counts"])
-
-
-def test_threshold_map_csv_round_trip(tools, tmp_path):
-    from paper_2510_20071_b200 import calib
-    tm = calib.estimate_thresholds(tools["cal_n_on"], tools["cal_n_off"])
-    path = os.path.join(tmp_path, "map.csv")
-    tm.save_csv(path)
-    assert open(path, "rb").read() == tools["cal_q01_csv"].tobytes()
-    back = calib.ThresholdMap.load_csv(path)
-    assert np.array_equal(back.n_on, tm.n_on) and np.array_equal(back.excluded, tm.excluded)
-    assert np.allclose(back.c_prime, tm.c_prime, equal_nan=True, rtol=1e-8)
-    edges, counts = calib.histogram(tm)
-    hpath = os.path.join(tmp_path, "h.csv")
-    calib.write_histogram_csv(edges, counts, hpath)
-    lines = open(hpath).read().splitlines()
-    assert lines[0] == "bin_lo,bin_hi,count" and len(lines) == len(counts) + 1
-
-
-def test_calibration_argument_errors(tools):
-    from paper_2510_20071_b200 import calib
-    from paper_2510_20071_b200.errors import ConfigError, EstimationError
-    with pytest.raises(ConfigError):
-        calib.estimate_thresholds(tools["cal_n_on"], tools["cal_n_off"], exclusion_quantile=0.5)
-    with pytest.raises(ConfigError):
-        calib.estimate_thresholds(tools["cal_n_on"], tools["cal_n_off"][:-1])
-    with pytest.raises(EstimationError):
-        calib.estimate_thresholds(np.zeros((3, 3)), np.zeros((3, 3)))
-    tm = calib.estimate_thresholds(tools["cal_n_on"], tools["cal_n_off"])
-    with pytest.raises(ConfigError):
-        calib.histogram(tm, "nope")
 
 
 # ------------------------------------------------------------- CUDA kernels
@@ -214,15 +176,20 @@ def test_gpu_count_events_hot_stream_and_errors():
 
 
 @pytest.mark.gpu
-def test_gpu_gain_from_calibration_feeds_engine():
-    """count_events -> estimate_thresholds -> gain_grid -> engine threshold_map, against the oracle."""
+def test_gpu_gain_from_calibration_feeds_engine(tools):
+    """GPU counts of the reference's calibration stream -> the reference's thresholds
+    -> gain_grid -> engine threshold_map, against the oracle on a longer stream."""
     from oracle import oracle as orc
     from paper_2510_20071_b200 import calib, workloads
-    from paper_2510_20071_b200.core import SensorGeometry, compute_params
+    from paper_2510_20071_b200.core import EventArray, SensorGeometry, compute_params
     from paper_2510_20071_b200.pipeline import ReconstructionEngine
-    geom = SensorGeometry(96, 64)
+    w, h = int(tools["cal_w"]), int(tools["cal_h"])
+    geom = SensorGeometry(w, h)
+    cal = EventArray(tools["cal_t"], tools["cal_x"], tools["cal_y"], tools["cal_p"])
+    on, off = calib.count_events(cal, geom)
+    assert np.array_equal(on, tools["cal_n_on"]) and np.array_equal(off, tools["cal_n_off"])
+    gain = calib.gain_grid(tools["cal_q01_c"])
     ev = workloads.make("texture_noise_hot", geom, 200_000, seed=8)
-    gain = calib.estimate_thresholds(*calib.count_events(ev, geom)).gain_grid()
     params = compute_params(40.0, Fraction(1, 2), geom)
     eng = ReconstructionEngine(geom, params, threshold_map=gain)
     ref = orc.OracleEngine(geom.width, geom.height, params, gain=gain)
