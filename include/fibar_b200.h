@@ -143,6 +143,15 @@ int fibar_counters(fibar_engine *eng, int64_t *event_count, int64_t *oob_dropped
 int fibar_read_state(fibar_engine *eng, float *p_bar, float *l, uint16_t *active, uint8_t *tiles,
                      uint16_t *qx, uint16_t *qy);
 
+/* Parity surface for the stale mask (runs pending packets first): the stale
+ * episodes of the most recent device batch, in pop order -- the in-bounds
+ * index of the event whose trim made the pixel stale and the pixel (row-major,
+ * engine rows) -- i.e. the per-event blurred-pixel list of the reference's
+ * SpatialFilter.on_event (spatial.py:165-207) / the stale branch of
+ * _kernels.py:160-172 for that batch.  *n_out = the count; fails if it
+ * exceeds cap.  Filter ON only (else *n_out = 0). */
+int fibar_debug_stale_items(fibar_engine *eng, int64_t *event_idx, uint32_t *pixel, int64_t cap, int64_t *n_out);
+
 /* Diagnostics (runs pending packets first): stats[0] = device kernel launches
  * so far, [1] = device batches, [2] = speculative window chunks, [3] = chunks
  * re-run by the verifier, [4] = pops (window evictions) processed, [5] =

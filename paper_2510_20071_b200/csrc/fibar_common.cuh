@@ -68,8 +68,11 @@ struct BatchState {
   unsigned nlong;      // long pixel segments
   unsigned nco;        // stale items of pixels with no events in the batch (listed by k_popj)
   unsigned epoch0;     // the batch's first epoch (halo bands: one more per exchange round)
-  unsigned nbad;       // chunk boundaries k_window_check found inexact
-  long long qlo, qhi;  // extrema of the targets set in the batch (k_window_check)
+  unsigned nbad;       // (unused)
+  long long qlo, qhi;  // extrema of the targets set in the batch (k_window_verify)
+  unsigned vbar;       // k_window_verify: grid-barrier arrivals of this batch's launch
+  unsigned vcnt[2];    // k_window_verify: disagreeing chunks listed in the round (by round parity)
+  unsigned vpad;
 };
 
 // Window / counter state living in device memory so no kernel needs a host

@@ -12,7 +12,7 @@
 //                                            same-tile event; per ring slot: distance to next
 //   window     k_anchor / k_anchor_scan /    the reference's FIFO window (_kernels.py:132-205)
 //              k_fp / k_anchor2 /            reproduced exactly by chunked speculation +
-//              k_window_run / k_window_fix   verification
+//              k_window_run / k_window_verify verification
 //   stale      k_popj                        eviction event of every popped entry; stale iff
 //                                            the pixel has no later event before its eviction
 //   temporal   k_posinfo / k_temporal_runs / per-pixel in-order replay of the two-stage IIR
@@ -162,6 +162,7 @@ struct fibar_engine {
   int2 *anc = nullptr, *anc2 = nullptr, *anc0 = nullptr;
   long long *lc = nullptr, *lu = nullptr;
   ChunkRec *ch = nullptr;
+  VRec *vl = nullptr;
   SelState *sel = nullptr;
   uint8_t *frame = nullptr;
   unsigned *cnt_tmp = nullptr, *tcnt_tmp = nullptr;
@@ -206,10 +207,12 @@ struct fibar_engine {
   int blur_grid_serial = 148;
   cudaEvent_t evF[2] = {nullptr, nullptr}, evB[2] = {nullptr, nullptr};
   int last_b = -1;   // parity of the newest batch with a blur stage in flight
+  int last_par = -1;  // parity of the newest batch (fibar_debug_stale_items)
   bool b_used[2] = {false, false};
   int nsm = 148;
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
+  bool warm_set = false;   // FIBAR_WARM given: used for every batch size
   // batches up to this size use 32-event speculation chunks: a small batch
   // leaves most SMs idle, so shorter serial chunk runs win over the extra
   // anchors and re-runs (config 3, 100k batches: 214 -> 227 Mev/s; 1M-event
@@ -292,7 +295,7 @@ struct fibar_engine {
     x.blur_sleep = blur_sleep;
     x.dbg_t = dbg_t;
     x.dbg_g = dbg_g;
-    x.warm = warm;
+    x.warm = (n_raw <= small_chunk_max && !warm_set) ? std::min(warm, 24) : warm;
     x.halo = halo;
     x.hreg0 = halo ? hreg0 : 0;
     x.hreg1 = halo ? hreg1 : H;
@@ -308,6 +311,7 @@ struct fibar_engine {
     x.lc = lc;
     x.lu = lu;
     x.ch = ch;
+    x.vl = vl;
     return x;
   }
 };
@@ -389,8 +393,9 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
     fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
-    fibar_launch(L, "window_check", k_window_check, (T + TPB - 1) / TPB, TPB, 0, s, x);
-    fibar_launch(L, "window_fix", k_window_fix, 1, 1024, 0, s, x);
+    // cooperative (grid barriers between its rounds' phases); a small grid, so
+    // its CTAs fit beside the blur stage running on the other stream
+    fibar_launch_coop(L, "window_verify", k_window_verify, std::max(1, std::min(64, g->nsm / 2)), VF_TPB, 0, s, x);
     fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
     fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
     fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
@@ -447,6 +452,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
                   cudaEvent_t used_ev, int par, bool graph) {
   Launcher &L = g->L;
   cudaStream_t s = L.stream;
+  g->last_par = par;
   // this parity's buffers are free once the batch two back finished its blur stage
   if (!graph && g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
   Ctx x{};
@@ -475,12 +481,16 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     if (rc) return rc;
   }
   if (g->spatial) {
+    // The batch's counters (event count, stale count, candidate set) close on
+    // the engine stream: the next front end reads them.  Its links read the
+    // last-touch tables, which k_link already advanced; so the next front end
+    // never waits for this batch's temporal replay or blur stage (only, two
+    // batches on, for the buffers of its parity).
+    fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
     // The temporal replay reads the brightness the previous batch's blur
     // stage finishes.  Streamed (temporal_on_blur): it runs first on the blur
     // stream itself, so the cycle blur(k) -> final(k) -> replay(k+1) ->
-    // prep(k+1) -> blur(k+1) crosses no stream; the engine stream waits for
-    // it (evT) before the next front end (whose links read the replay's
-    // last-touch tables and batch_end's event count).
+    // prep(k+1) -> blur(k+1) crosses no stream.
     const bool t_on_b = !graph && !g->serial && !g->halo && g->temporal_on_blur;
     if (t_on_b) {
       cudaStream_t bs = g->bstream;
@@ -489,14 +499,10 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       L.stream = bs;
       fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, bs, x);
       fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, bs, x);
-      fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, bs, x);
-      CK(cudaEventRecord(g->evT, bs));
-      CK(cudaStreamWaitEvent(s, g->evT, 0));
     } else {
       if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
       fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
       fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
-      fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
     }
     if (g->halo) {
       // halo band: the item lists of the exchanged rows and the tap
@@ -625,6 +631,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   }
   CK(cudaGraphLaunch(hit->exec, s));
   L.launches += hit->kernels;
+  g->last_par = 0;   // whole-batch graphs use the parity-0 buffers
   g->batches++;
   return 0;
 }
@@ -843,7 +850,12 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     g->chunk = std::max(CHUNK_MIN, atoi(v));
     g->small_chunk_max = 0;
   }
-  if (const char *v = getenv("FIBAR_WARM")) g->warm = std::max(0, atoi(v));
+  // small batches (<= small_chunk_max) warm up 24 events: the cooperative
+  // verifier re-runs the extra misses cheaply (config 3: 265 -> 273 Mev/s)
+  if (const char *v = getenv("FIBAR_WARM")) {
+    g->warm = std::max(0, atoi(v));
+    g->warm_set = true;
+  }
   if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
   if (const char *v = getenv("FIBAR_SERIAL")) g->serial = atoi(v) != 0;
   // The blur dataflow kernel runs in a CUDA green context of 24 SMs (5
@@ -1005,6 +1017,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->lc, T);
     rc |= dalloc(&g->lu, T);
     rc |= dalloc(&g->ch, T);
+    rc |= dalloc(&g->vl, T);
   }
   if (g->halo) {
     const long long nbh = (Bc + n + 2 + TPB - 1) / TPB;
@@ -1034,7 +1047,7 @@ int fibar_destroy(fibar_engine *g) {
   if (g->bstream) cudaStreamSynchronize(g->bstream);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
-                  g->dp, g->S, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->sel, g->frame,
+                  g->dp, g->S, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1347,6 +1360,34 @@ int fibar_read_qs(fibar_engine *g, int64_t qs[10]) {
     qs[1] = 0;
   }
   return 0;
+}
+
+int fibar_debug_stale_items(fibar_engine *g, int64_t *event_idx, uint32_t *pixel, int64_t cap, int64_t *n_out) {
+  if (!g || !n_out) return fail(FIBAR_E_CONFIG, "null argument");
+  int rc = sync_point(g);
+  if (rc) return rc;
+  *n_out = 0;
+  if (!g->spatial || g->last_par < 0) return 0;
+  const int par = g->last_par;
+  BatchState bs;
+  CK(cudaMemcpyAsync(&bs, g->bsd + par, sizeof(BatchState), cudaMemcpyDeviceToHost, g->L.stream));
+  CK(cudaStreamSynchronize(g->L.stream));
+  if (bs.npop <= 0) return 0;
+  std::vector<Item> items((size_t)bs.npop);
+  CK(cudaMemcpyAsync(items.data(), g->item2[par], sizeof(Item) * (size_t)bs.npop, cudaMemcpyDeviceToHost,
+                     g->L.stream));
+  CK(cudaStreamSynchronize(g->L.stream));
+  long long k = 0;
+  for (const Item &it : items) {
+    if (it.pix == FIBAR_NONE) continue;
+    if (k < cap) {
+      if (event_idx) event_idx[k] = bs.E0 + (long long)it.jrel;
+      if (pixel) pixel[k] = it.pix;
+    }
+    ++k;
+  }
+  *n_out = k;
+  return k > cap ? fail(FIBAR_E_CONFIG, "stale item buffer too small") : 0;
 }
 
 int fibar_counters(fibar_engine *g, int64_t *event_count, int64_t *oob_dropped) {

@@ -105,6 +105,9 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->nlong = 0;
     b->nco = 0;
     b->nbad = 0;
+    b->vbar = 0;
+    b->vcnt[0] = 0;
+    b->vcnt[1] = 0;
     b->qlo = 0x7FFFFFFFFFFFFFFFLL;
     b->qhi = -1;
     s->epoch += 1;
@@ -155,11 +158,13 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
   // tile links: latest earlier / earliest later event in the tile segment
   const uint2 tr = x.ptt[t];
   long long prev_t = -1, next_t = -1;
+  unsigned tmax = 0;   // the tile's latest event of the batch (its new last-touch)
   if (tr.y - tr.x <= 64) {
     unsigned best_lo = 0, best_hi = 0xFFFFFFFFu;
     bool have_lo = false;
     for (unsigned q = tr.x; q < tr.y; ++q) {
       unsigned o = x.sidx[q];
+      tmax = max(tmax, o);
       if (o < jj) {
         if (!have_lo || o > best_lo) best_lo = o;
         have_lo = true;
@@ -179,6 +184,7 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
         if (xx >= x.W) break;
         const PixRec r = x.pt[(unsigned)yy * x.W + xx];
         if (r.end <= r.st) continue;
+        tmax = max(tmax, x.sidx[r.end - 1]);   // a pixel's events are in stream order
         // first position in [st, end) with sidx >= jj
         unsigned lo = r.st, hi = r.end;
         while (lo < hi) {
@@ -195,7 +201,12 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
     }
   }
   const bool first_tile = prev_t < 0;
-  if (first_tile) prev_t = x.last_tile[t];
+  if (first_tile) {
+    // the tile's earliest event of the batch is the only one reading the
+    // tile's last-touch; it also writes the batch's value for the next batch
+    prev_t = x.last_tile[t];
+    x.last_tile[t] = E0 + tmax;
+  }
 
   x.dp[jj] = make_uint2(dist32(j, prev_p), dist32(j, prev_t));
   x.rnext[(unsigned long long)j & x.Rm] =
@@ -206,10 +217,14 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
     // the pixel's exact in-window event count at batch start; the count seen
     // by its t-th event this batch is at most wcnt + t, so a batch can only
     // reach the cap if wcnt + seglen > 65535 -- flag that (never misses).
-    const unsigned seglen = x.pt[c].end - (unsigned)i;
+    const unsigned pend = x.pt[c].end;
+    const unsigned seglen = pend - (unsigned)i;
     const unsigned wc = x.wcnt[c];
     if ((unsigned long long)wc + seglen > 65535ull) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);
     x.wcnt[c] = wc + seglen;
+    // the pixel's last-touch for the next batch (read above by this thread
+    // alone), so the next front end never waits for this batch's replay
+    x.plast[c] = E0 + x.sidx[pend - 1];
   }
   if (first_pix && pre_last >= lo_ok && pre_last >= 0) {
     long long d = j - pre_last;
@@ -258,11 +273,23 @@ __device__ __forceinline__ long long regulate(const Ctx &x, long long len, long 
 }
 
 // the same for the serial window run's 32-bit state: (len * nt) as one wide
-// multiply, num * A folded on the host, an approximate float quotient (a few
-// units off at most below 2^24) fixed up exactly in integers
+// multiply, num * A folded on the host.  With q_max < 2^22 (every sensor up to
+// 4.19M pixels) the quotient below the clamp is < 2^22, so a float estimate
+// N * rcp(D) is within 1 of N / D (four roundings of 2^-24 each) and one
+// integer fix-up each way makes it the exact floor: a short dependency chain
+// instead of a double division.  Larger q_max: the exact double quotient.
 __device__ __forceinline__ unsigned regulate32(const Ctx &x, unsigned len, unsigned np, unsigned nt) {
   const unsigned long long N = (unsigned long long)len * nt * (unsigned long long)x.numA;
   const unsigned long long D = (unsigned long long)x.den * np;
+  const unsigned qmax = (unsigned)x.qmax, qmin = (unsigned)x.qmin;
+  if (x.qmax < (1LL << 22)) {
+    if ((unsigned long long)(qmax + 1) * D <= N) return qmax;
+    unsigned q = (unsigned)__fmul_rn(__ull2float_rn(N), __frcp_rn(__ull2float_rn(D)));
+    q = q > qmax + 1 ? qmax + 1 : q;
+    if ((unsigned long long)q * D > N) --q;
+    else if ((unsigned long long)(q + 1) * D <= N) ++q;
+    return q < qmin ? qmin : (q > qmax ? qmax : q);
+  }
   if (N < (1ull << 53)) {
     // exact in one double division: N and D convert exactly, and for a
     // non-integer N/D the distance to the next integer (>= 1/D) exceeds the
@@ -723,11 +750,17 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
     const bool big = hi - lo > 8;
     if (jr < br) wpops += hi - lo;
     if (!big && hi > lo) {
-      for (unsigned k = lo; k < hi; ++k) {
-        const uint2 rr = x.rnext[(bslot + k) & rm];
-        const unsigned dd = jr - k;
-        np -= rr.x > dd;
-        nt -= rr.y > dd;
+      // up to 8 entries, four independent loads in flight per round
+      for (unsigned k = lo; k < hi; k += 4) {
+        uint2 rr[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) rr[u] = k + u < hi ? x.rnext[(bslot + k + u) & rm] : make_uint2(0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const unsigned dd = jr - (k + u);
+          np -= rr[u].x > dd;
+          nt -= rr[u].y > dd;
+        }
       }
       sr = hi;
     }
@@ -824,131 +857,167 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
 // re-run, in parallel, every chunk whose start disagrees with its
 // predecessor's current end (read before the round writes anything), until
 // every boundary agrees; each round makes at least the first disagreeing
-// chunk exact.  Then publish the batch's final window state.
-// Every chunk boundary checked at once over the whole grid, and the targets'
-// extrema reduced, so that k_window_fix (one block) only loops when a
-// speculative start was wrong.
-__global__ void __launch_bounds__(TPB) k_window_check(Ctx x) {
-  pdl_wait();
-  const long long B = x.bs->B;
-  const int T = (int)((B + x.chunk - 1) / x.chunk);
-  const int c = blockIdx.x * TPB + threadIdx.x;
-  long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
-  unsigned bad = 0;
-  if (c < T) {
-    const ChunkRec q = x.ch[c];
-    lo = q.qlo;
-    hi = q.qhi;
-    if (c > 0) {
-      const ChunkRec &p = x.ch[c - 1];
-      bad = q.st_s != p.en_s || q.st_q != p.en_q;
+// chunk exact, so this is exact by induction whatever the guesses.  Then the
+// targets' extrema are reduced and the batch's final window state published.
+//
+// One cooperative launch (grid barriers between the phases of a round): every
+// boundary is checked by the whole grid, and each re-run is done by one warp
+// that stages the chunk's links dp[b, e) and the ring next-links of the
+// evictions it will most likely make, [s, s + VF_RN), in shared memory with
+// coalesced loads, after which lane 0 steps the recurrence from shared memory.
+constexpr int VF_DP = 64;     // >= the largest chunk
+constexpr int VF_RN = 128;    // staged ring entries per re-run
+
+__device__ __forceinline__ void vf_barrier(BatchState *bs, unsigned k) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&bs->vbar) : "memory");
+    while (ld_acquire_u32(&bs->vbar) < k * gridDim.x) {
     }
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) {
-    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
-    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
-  }
-  bad = __reduce_add_sync(0xffffffffu, bad);
-  if ((threadIdx.x & 31) == 0) {
-    if (bad) atomicAdd(&x.bs->nbad, bad);
-    if (hi >= 0) {
-      atomicMin((unsigned long long *)&x.bs->qlo, (unsigned long long)lo);
-      atomicMax((long long *)&x.bs->qhi, hi);
-    }
-  }
+  __syncthreads();
 }
 
-__global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
+__device__ void rerun_chunk_staged(const Ctx &x, WState &w, long long b, long long e, long long E0, long long s_start,
+                                   uint2 *sdp, uint2 *srn, long long &qlo, long long &qhi) {
+  const int lane = threadIdx.x & 31;
+  const long long rn0 = w.s;
+  for (int i = lane; i < (int)(e - b); i += 32) sdp[i] = x.dp[b - E0 + i];
+  uint2 rr[VF_RN / 32];
+#pragma unroll
+  for (int u = 0; u < VF_RN / 32; ++u) rr[u] = x.rnext[(unsigned long long)(rn0 + lane + 32 * u) & x.Rm];
+#pragma unroll
+  for (int u = 0; u < VF_RN / 32; ++u) srn[lane + 32 * u] = rr[u];
+  __syncwarp();
+  if (lane == 0) {
+    for (long long j = b; j < e; ++j) {
+      const uint2 d = sdp[j - b];
+      const unsigned long long js = (unsigned long long)(j - w.s);
+      w.npix += (unsigned long long)d.x > js;
+      w.ntiles += (unsigned long long)d.y > js;
+      long long len = j - w.s + 1;
+      if (len > w.q) {
+        const long long snew = j + 1 - w.q;
+        long long np = w.npix, nt = w.ntiles;
+        for (long long k = w.s; k < snew; ++k) {
+          const long long o = k - rn0;
+          const uint2 r = o < VF_RN ? srn[o] : x.rnext[(unsigned long long)k & x.Rm];
+          const unsigned long long dd = (unsigned long long)(j - k);
+          np -= (unsigned long long)r.x > dd;
+          nt -= (unsigned long long)r.y > dd;
+        }
+        w.npix = np;
+        w.ntiles = nt;
+        w.s = snew;
+        len = w.q;
+      }
+      if (++w.evctr >= x.every) {
+        w.evctr = 0;
+        if (w.npix >= 1 && w.ntiles >= 1) {
+          const long long qn = (x.qmax < (1LL << 22) && len < (1LL << 32))
+                                   ? (long long)regulate32(x, (unsigned)len, (unsigned)w.npix, (unsigned)w.ntiles)
+                                   : regulate(x, len, w.npix, w.ntiles);
+          w.q = qn;
+          qlo = min(qlo, qn);
+          qhi = max(qhi, qn);
+        }
+      }
+      x.S[j - E0] = (unsigned)(w.s - s_start);
+    }
+  }
+  __syncwarp();
+}
+
+__global__ void __launch_bounds__(VF_TPB) k_window_verify(Ctx x) {
   pdl_wait();
-  __shared__ int n_bad;
-  __shared__ long long red_lo[32], red_hi[32];
-  const long long B = x.bs->B;
+  constexpr int NW = VF_TPB / 32;
+  __shared__ uint2 sdp[NW][VF_DP];
+  __shared__ uint2 srn[NW][VF_RN];
+  __shared__ long long red_lo[NW], red_hi[NW];
+  BatchState *bs = x.bs;
+  const long long B = bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
-  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
-  int rounds = 0, reruns = 0;
-  const bool fast = x.bs->nbad == 0;   // k_window_check found every boundary exact
-  while (!fast) {
-    if (threadIdx.x == 0) n_bad = 0;
-    __syncthreads();
-    // each thread owns chunks threadIdx.x + 1024*i; snapshot predecessors first
-    constexpr int MAXC = 64;
-    int mine[MAXC];
-    ChunkRec pre[1];
-    int nm = 0;
-    for (int c = 1 + threadIdx.x; c < T && nm < MAXC; c += 1024) {
+  const long long E0 = bs->E0, s_start = bs->s_start;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const long long tid = (long long)blockIdx.x * VF_TPB + threadIdx.x, nthr = (long long)gridDim.x * VF_TPB;
+  const long long gw = (long long)blockIdx.x * NW + wid, nwarps = (long long)gridDim.x * NW;
+  unsigned nbar = 0;
+  int rounds = 0;
+  long long reruns = 0;
+  for (;; ++rounds) {
+    unsigned *cnt = &bs->vcnt[rounds & 1];
+    if (tid == 0) bs->vcnt[(rounds + 1) & 1] = 0;   // the next round's list (its last reader passed a barrier)
+    for (long long c = 1 + tid; c < T; c += nthr) {
       const ChunkRec &p = x.ch[c - 1];
       const ChunkRec &q = x.ch[c];
-      if (q.st_s != p.en_s || q.st_q != p.en_q) mine[nm++] = c;
+      if (q.st_s != p.en_s || q.st_q != p.en_q) {
+        const unsigned i = atomicAdd(cnt, 1u);
+        VRec v;
+        v.s = p.en_s;
+        v.q = p.en_q;
+        v.np = p.en_np;
+        v.nt = p.en_nt;
+        v.ev = p.en_ev;
+        v.c = (int)c;
+        v.pad = 0;
+        x.vl[i] = v;
+      }
     }
-    if (nm) atomicAdd(&n_bad, nm);
-    __syncthreads();
-    if (n_bad == 0) break;
-    // read every rerun's start state before any write of this round
-    long long ss[MAXC], sq[MAXC], snp[MAXC], snt[MAXC], sev[MAXC];
-    (void)pre;
-    for (int i = 0; i < nm; ++i) {
-      const ChunkRec &p = x.ch[mine[i] - 1];
-      ss[i] = p.en_s;
-      sq[i] = p.en_q;
-      snp[i] = p.en_np;
-      snt[i] = p.en_nt;
-      sev[i] = p.en_ev;
-    }
-    __syncthreads();
-    for (int i = 0; i < nm; ++i) {
-      const int m = mine[i];
-      WState w{ss[i], sq[i], snp[i], snt[i], sev[i]};
+    vf_barrier(bs, ++nbar);
+    const unsigned n = ld_relaxed_u32(cnt);
+    if (n == 0) break;
+    reruns += n;
+    for (long long i = gw; i < n; i += nwarps) {
+      const VRec v = x.vl[i];
+      WState w{v.s, v.q, v.np, v.nt, v.ev};
       long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
-      const long long b = E0 + (long long)m * x.chunk;
+      const long long b = E0 + (long long)v.c * x.chunk;
       const long long e = min(E0 + B, b + x.chunk);
-      run_window(x, w, b, e, E0, s_start, true, qlo, qhi);
-      ChunkRec r;
-      r.st_s = ss[i];
-      r.st_q = sq[i];
-      r.en_s = w.s;
-      r.en_q = w.q;
-      r.en_np = w.npix;
-      r.en_nt = w.ntiles;
-      r.en_ev = w.evctr;
-      r.qlo = qlo;
-      r.qhi = qhi;
-      x.ch[m] = r;
+      rerun_chunk_staged(x, w, b, e, E0, s_start, sdp[wid], srn[wid], qlo, qhi);
+      if (lane == 0) {
+        ChunkRec r;
+        r.st_s = v.s;
+        r.st_q = v.q;
+        r.en_s = w.s;
+        r.en_q = w.q;
+        r.en_np = w.npix;
+        r.en_nt = w.ntiles;
+        r.en_ev = w.evctr;
+        r.qlo = qlo;
+        r.qhi = qhi;
+        x.ch[v.c] = r;
+      }
     }
-    reruns += nm;
-    ++rounds;
-    __threadfence_block();
-    __syncthreads();
+    vf_barrier(bs, ++nbar);
   }
+  // the targets' extrema over every chunk
   long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
-  if (fast) {
-    if (threadIdx.x == 0) {
-      lo = x.bs->qlo;
-      hi = x.bs->qhi;
-    }
-  } else {
-    for (int c = threadIdx.x; c < T; c += 1024) {
-      lo = min(lo, x.ch[c].qlo);
-      hi = max(hi, x.ch[c].qhi);
-    }
+  for (long long c = tid; c < T; c += nthr) {
+    lo = min(lo, x.ch[c].qlo);
+    hi = max(hi, x.ch[c].qhi);
   }
-  int rr = __reduce_add_sync(0xffffffffu, reruns);
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
   }
-  if ((threadIdx.x & 31) == 0) {
-    red_lo[threadIdx.x >> 5] = lo;
-    red_hi[threadIdx.x >> 5] = hi;
-    if (rr) atomicAdd((unsigned long long *)&x.st->mismatch, (unsigned long long)rr);
+  if (lane == 0) {
+    red_lo[wid] = lo;
+    red_hi[wid] = hi;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 0; w < 32; ++w) {
+    for (int w = 1; w < NW; ++w) {
       lo = min(lo, red_lo[w]);
       hi = max(hi, red_hi[w]);
     }
+    if (hi >= 0) {
+      atomicMin((unsigned long long *)&bs->qlo, (unsigned long long)lo);
+      atomicMax((long long *)&bs->qhi, hi);
+    }
+  }
+  vf_barrier(bs, ++nbar);
+  if (tid == 0) {
     DevState *s = x.st;
     if (T > 0) {
       const ChunkRec &r = x.ch[T - 1];
@@ -957,17 +1026,18 @@ __global__ void __launch_bounds__(1024) k_window_fix(Ctx x) {
       s->npix = r.en_np;
       s->ntiles = r.en_nt;
       s->evctr = r.en_ev;
-      if (hi >= 0) {
-        s->qtmin = min(s->qtmin, lo);
-        s->qtmax = max(s->qtmax, hi);
+      if (bs->qhi >= 0) {
+        s->qtmin = min(s->qtmin, bs->qlo);
+        s->qtmax = max(s->qtmax, bs->qhi);
       }
       s->pops += r.en_s - s_start;
-      x.bs->npop = r.en_s - s_start;
+      bs->npop = r.en_s - s_start;
     } else {
-      x.bs->npop = 0;
+      bs->npop = 0;
     }
     s->chunks += T;
     s->fix_rounds += rounds;
+    s->mismatch += reruns;
   }
 }
 

@@ -76,6 +76,25 @@ inline void fibar_launch(Launcher &L, const char *name, void (*kern)(KArgs...), 
   L.end();
 }
 
+// A cooperative launch (all CTAs co-resident: the kernel has grid barriers).
+template <typename... KArgs, typename... Args>
+inline void fibar_launch_coop(Launcher &L, const char *name, void (*kern)(KArgs...), dim3 grid, dim3 block,
+                              size_t smem, cudaStream_t s, Args &&...args) {
+  L.begin(name);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  L.end();
+}
+
 // first statement of every kernel launched by fibar_launch: wait until the
 // previous kernel on the stream has completed and its writes are visible
 // (a no-op for launches without the PDL attribute)

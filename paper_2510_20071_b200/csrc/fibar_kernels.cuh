@@ -38,6 +38,14 @@ constexpr int EV_TILE = TPB * EV_PER_THREAD;
 constexpr unsigned HALO_OKM = 1u << 9;
 constexpr unsigned TAINT_HI = 0x80000000u;   // taint bit of a value word's high half (bit 63)
 
+// a chunk the window verifier re-runs, with its predecessor's end state as
+// read before the round writes anything
+struct VRec {
+  long long s, q, np, nt, ev;
+  int c, pad;
+};
+constexpr int VF_TPB = 256;   // k_window_verify: threads per CTA (one warp per re-run)
+
 struct ChunkRec {
   long long st_s, st_q;                          // state after event b_c - 1 (speculative start)
   long long en_s, en_q, en_np, en_nt, en_ev;     // state after the chunk's last event
@@ -117,6 +125,7 @@ struct Ctx {
   int2 *anc0;   // per chunk: distinct counts of the no-pop window [s_start, a_c - 1]
   long long *lc, *lu;
   ChunkRec *ch;
+  VRec *vl;
 };
 
 struct BatchScalars {
@@ -155,8 +164,7 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc);
 __global__ void __launch_bounds__(TPB) k_fp(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run(Ctx x);
-__global__ void __launch_bounds__(TPB) k_window_check(Ctx x);
-__global__ void __launch_bounds__(1024) k_window_fix(Ctx x);
+__global__ void __launch_bounds__(VF_TPB) k_window_verify(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj_map(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x);
 __global__ void __launch_bounds__(TPB) k_posinfo(Ctx x);

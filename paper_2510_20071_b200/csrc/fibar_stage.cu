@@ -128,10 +128,6 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
     }
   }
   x.pbar[c] = pb;
-  // last-touch tables for the next batch's links (the blur stage never reads them)
-  const long long elast = x.bs->E0 + x.sidx[end - 1];
-  x.plast[c] = elast;
-  atomicMax(&x.last_tile[key / x.A], elast);
 }
 
 // Long pixel segments (hot pixels: thousands of events per batch) replayed by
@@ -248,12 +244,7 @@ __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
       __syncthreads();
       continue;
     }
-    if (tid == 0) {
-      x.pbar[c] = fpb;
-      const long long elast = x.bs->E0 + x.sidx[end - 1];
-      x.plast[c] = elast;
-      atomicMax(&x.last_tile[x.skey[st] / x.A], elast);
-    }
+    if (tid == 0) x.pbar[c] = fpb;
     // blur bookkeeping: which blur each position builds on (last stale event
     // before it in the segment, or the pixel's carried blur)
     unsigned last = FIBAR_NONE;

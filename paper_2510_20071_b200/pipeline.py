@@ -405,6 +405,19 @@ class ReconstructionEngine:
         d["qs"] = self.qs
         return d
 
+    def stale_items(self) -> tuple[np.ndarray, np.ndarray]:
+        """Stale episodes of the most recent device batch (runs pending packets
+        first): (in-bounds event index, pixel) in pop order, the reference's
+        per-event blurred-pixel list (spatial.py:165-207) for that batch."""
+        cap = max(1024, self._bcap + self.geometry.n_pix)
+        j = np.empty(cap, np.int64)
+        pix = np.empty(cap, np.uint32)
+        n = C.c_int64(0)
+        self._sync_stream()
+        _native.check(self._lib.fibar_debug_stale_items(self._h, j.ctypes.data, pix.ctypes.data, cap, C.byref(n)),
+                      "fibar_debug_stale_items")
+        return j[: n.value].copy(), pix[: n.value].astype(np.int64)
+
     def state_digest(self) -> str:
         d = self.state_arrays()
         h = hashlib.sha256()
@@ -747,12 +760,20 @@ def run(
     frame_sink: Callable[[int, Frame], None] | None = None,
     out_dir=None,
     diagnostics_path=None,
+    async_frames: bool = True,
 ) -> RunResult:
     """Stream packets through the engine, reading out frames on a time grid.
 
     A frame at time r reflects exactly the events with t < r (packets are
     split with ``searchsorted(..., 'left')`` as in pipeline.py:379-384);
     explicit read-out times after the stream end render the final state.
+
+    With ``async_frames`` (default, and only without diagnostics) frames are
+    rendered asynchronously and handed to ``frame_sink`` in order up to
+    ``_RUN_DEPTH`` read-outs late, i.e. after later packets were submitted: the
+    frame's pixels are exact, but a sink that reads engine state (counters,
+    ``l``) sees a later state than the reference's loop would show.  Pass
+    ``async_frames=False`` for the reference's call order (render, then sink).
     """
     if frame_sink is None and out_dir is not None:
         os.makedirs(out_dir, exist_ok=True)
@@ -771,7 +792,7 @@ def run(
     # out asynchronously (render_async into a small ring of pinned buffers) and
     # handed to the sink in order as they land, so the GPU runs the next
     # packets while earlier frames are copied back.
-    pipelined = diag is None and hasattr(engine, "render_async")
+    pipelined = async_frames and diag is None and hasattr(engine, "render_async")
     pending = collections.deque()
     # pinned frame buffers, kept on the engine across run() calls
     ring = engine.__dict__.setdefault("_run_frame_pool", []) if pipelined else []
@@ -826,6 +847,10 @@ def run(
         while pending:
             deliver(pending.popleft())
     finally:
+        # on an error, frames still in flight are copying into pinned buffers
+        # that torch does not track: wait for them before the buffers go
+        while pending:
+            pending.popleft().event.synchronize()
         if diag is not None:
             diag.close()
     ec, ob = engine._counters()

@@ -236,12 +236,15 @@ def test_launch_modes_agree(monkeypatch):
 
 @pytest.mark.parametrize("kind,w,h,n,packet,kw", [
     # hot pixels at config-3 geometry: long segments, several 1M-event batches
-    ("texture_noise_hot", 1280, 720, 3_000_000, 100_000, {}),
+    ("texture_noise_hot", 1280, 720, 3_000_000, 100_000, dict(bcap=1 << 20)),
+    # the default (non-power-of-two) 1280x720 batch of 3,735,552 events, more
+    # than two of them: carried stale items and last-touch tables across batches
+    ("texture_noise_hot", 1280, 720, 8_000_000, 1_000_000, {}),
     # variants at scale: tile side 3, fill 2/3, regulate_every 2, a gain map, blur off
     ("texture", 640, 480, 2_500_000, 50_000, dict(tile_side=3, fill=Fraction(2, 3), regulate_every=2, gain=True)),
     ("texture", 640, 480, 2_500_000, 250_000, dict(blur=False)),
-    # config-5 geometry: a window larger than a device batch (warp-counted collapses)
-    ("texture", 2560, 1440, 3_000_000, 1_000_000, {}),
+    # config-5 geometry: a window (~1.2M events) larger than a device batch (warp-counted collapses)
+    ("texture", 2560, 1440, 3_000_000, 1_000_000, dict(bcap=1 << 20)),
 ])
 def test_large_streams_match_oracle(kind, w, h, n, packet, kw):
     from oracle import oracle as orc
@@ -255,7 +258,8 @@ def test_large_streams_match_oracle(kind, w, h, n, packet, kw):
     if kw.get("gain"):
         gain = np.random.default_rng(4).uniform(0.6, 1.6, (h, w)).astype(np.float32)
     every, blur = kw.get("regulate_every", 1), kw.get("blur", True)
-    eng = ReconstructionEngine(geom, params, threshold_map=gain, regulate_every=every, blur_enabled=blur)
+    eng = ReconstructionEngine(geom, params, threshold_map=gain, regulate_every=every, blur_enabled=blur,
+                               batch_capacity=kw.get("bcap", 0))
     ref = orc.OracleEngine(w, h, params, gain=gain, regulate_every=every, blur_enabled=blur)
     for a in range(0, n, packet):
         b = min(n, a + packet)
@@ -267,3 +271,54 @@ def test_large_streams_match_oracle(kind, w, h, n, packet, kw):
     fr = eng.render("robust")
     px, bounds, deg = ref.render("robust")
     assert np.array_equal(fr.pixels, px) and fr.bounds == bounds
+
+
+def test_golden_stale_mask_per_batch(golden_case):
+    """The CUDA stale items (popping event, pixel), batch by batch, equal the
+    reference's per-event blurred-pixel list (SpatialFilter.on_event,
+    spatial.py:165-207) recorded in the goldens -- the stale mask bit-exact."""
+    from paper_2510_20071_b200.core import EventArray
+    name, g = golden_case
+    if "stale_j" not in g:
+        pytest.skip("filter-OFF golden")
+    eng = make_engine(g)
+    n = len(g["x"])
+    P = int(g["packet"]) if int(g["packet"]) else n
+    js, pxs = [], []
+    for a in range(0, n, P):
+        b = min(n, a + P)
+        eng.process_array(EventArray(g["t"][a:b], g["x"][a:b], g["y"][a:b], g["p"][a:b]))
+        j, pix = eng.stale_items()   # one device batch per packet
+        js.append(j)
+        pxs.append(pix)
+    j, pix = np.concatenate(js), np.concatenate(pxs)
+    assert np.array_equal(j, g["stale_j"]), (name, len(j), len(g["stale_j"]))
+    assert np.array_equal(pix, g["stale_pix"]), name
+    assert eng.stale_count == len(g["stale_j"])
+
+
+def test_small_packets_720p_frame_by_frame():
+    """600 packets of 1k events at 1280x720 (texture + noise + hot pixels), a
+    robust read-out after every packet, each frame equal to the oracle's."""
+    from oracle import oracle as orc
+    from paper_2510_20071_b200 import workloads
+    from paper_2510_20071_b200.core import SensorGeometry, compute_params
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    geom = SensorGeometry(1280, 720)
+    ev = workloads.make("texture_noise_hot", geom, 600_000, seed=31)
+    params = compute_params(40.0, Fraction(1, 2), geom)
+    eng = ReconstructionEngine(geom, params)
+    ref = orc.OracleEngine(geom.width, geom.height, params)
+    bad = []
+    for k, a in enumerate(range(0, len(ev), 1000)):
+        blk = ev.slice(a, a + 1000)
+        eng.process_array(blk)
+        ref.process_array(blk.t, blk.x, blk.y, blk.p)
+        fr = eng.render("robust")
+        px, bounds, deg = ref.render("robust")
+        if not (np.array_equal(fr.pixels, px) and fr.bounds == bounds and fr.degenerate == deg):
+            bad.append(k)
+    assert not bad, f"frames differ at packets {bad[:10]}"
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, "720p 1k packets")
