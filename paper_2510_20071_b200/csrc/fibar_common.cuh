@@ -70,8 +70,7 @@ struct BatchState {
   unsigned epoch0;     // the batch's first epoch (halo bands: one more per exchange round)
   unsigned nbad;       // (unused)
   long long qlo, qhi;  // extrema of the targets set in the batch (k_window_verify)
-  unsigned vbar;       // k_window_verify: grid-barrier arrivals of this batch's launch
-  unsigned vcnt[2];    // k_window_verify: disagreeing chunks listed in the round (by round parity)
+  unsigned vcnt[3];    // k_window_verify: chunks listed for a round (rotating by round)
   unsigned vpad;
 };
 

@@ -148,7 +148,7 @@ struct fibar_engine {
   unsigned *ka2[2] = {nullptr, nullptr}, *va2[2] = {nullptr, nullptr}, *kb2[2] = {nullptr, nullptr},
            *vb2[2] = {nullptr, nullptr}, *hist = nullptr;
   uint2 *dp = nullptr;
-  unsigned *S = nullptr;
+  unsigned *S = nullptr, *Qt = nullptr;
   unsigned *pmap = nullptr;
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
   BlurPrep *prep = nullptr;            // = prep2[0] (debug reads)
@@ -213,6 +213,7 @@ struct fibar_engine {
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
   bool warm_set = false;   // FIBAR_WARM given: used for every batch size
+  bool sort_cluster_ok = false;   // batches <= CS_MAX sort in one cluster (FIBAR_SORT_CLUSTER=0: off)
   // batches up to this size use 32-event speculation chunks: a small batch
   // leaves most SMs idle, so shorter serial chunk runs win over the extra
   // anchors and re-runs (config 3, 100k batches: 214 -> 227 Mev/s; 1M-event
@@ -281,6 +282,7 @@ struct fibar_engine {
     x.sidx = sidx;
     x.dp = dp;
     x.S = S;
+    x.Qt = Qt;
     x.pmap = pmap;
     x.item = item2[par];
     x.posrec = posrec2[par];
@@ -295,7 +297,7 @@ struct fibar_engine {
     x.blur_sleep = blur_sleep;
     x.dbg_t = dbg_t;
     x.dbg_g = dbg_g;
-    x.warm = (n_raw <= small_chunk_max && !warm_set) ? std::min(warm, 24) : warm;
+    x.warm = (n_raw <= small_chunk_max && !warm_set) ? std::min(warm, 32) : warm;
     x.halo = halo;
     x.hreg0 = halo ? hreg0 : 0;
     x.hreg1 = halo ? hreg1 : H;
@@ -372,8 +374,13 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
   fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
-  where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
-                           g->key_bits);
+  // small batches: the whole sort in one thread-block cluster (on chip)
+  where = g->sort_cluster_ok ? sort_pairs_cluster(L, g->ka2[par], g->kb2[par], g->vb2[par], &g->bsd[par].B, n_raw,
+                                                  g->key_bits)
+                             : -1;
+  if (where < 0)
+    where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
+                             g->key_bits);
   L.stream = s_saved;
   const unsigned *skey = where ? g->kb2[par] : g->ka2[par];
   const unsigned *sidx = where ? g->vb2[par] : g->va2[par];
@@ -393,9 +400,8 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
     fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
-    // cooperative (grid barriers between its rounds' phases); a small grid, so
-    // its CTAs fit beside the blur stage running on the other stream
-    fibar_launch_coop(L, "window_verify", k_window_verify, std::max(1, std::min(64, g->nsm / 2)), VF_TPB, 0, s, x);
+    // one cluster (cluster barriers between its rounds' phases)
+    fibar_launch_cluster(L, "window_verify", k_window_verify, VF_CTAS, VF_TPB, 0, s, x);
     fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
     fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
     fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
@@ -779,6 +785,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   *out = nullptr;
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(FIBAR_E_NODEVICE, "no CUDA device");
+  // the window verifier is one 16-CTA cluster (beyond the portable 8)
+  CK(cudaFuncSetAttribute(k_window_verify, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  static int cluster_sort_state = -1;   // per process: the cluster sort's opt-ins done and usable
+  if (cluster_sort_state < 0) cluster_sort_state = sort_cluster_init() ? 1 : 0;
   if (cfg->width < 2 || cfg->height < 2) return fail(FIBAR_E_CONFIG, "geometry must be at least 2x2");
   if (cfg->tile_side < 2) return fail(FIBAR_E_CONFIG, "tile_side must be >= 2");
   if (cfg->regulate_every < 1) return fail(FIBAR_E_CONFIG, "regulate_every must be >= 1");
@@ -850,8 +860,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     g->chunk = std::max(CHUNK_MIN, atoi(v));
     g->small_chunk_max = 0;
   }
-  // small batches (<= small_chunk_max) warm up 24 events: the cooperative
-  // verifier re-runs the extra misses cheaply (config 3: 265 -> 273 Mev/s)
+  // small batches (<= small_chunk_max) warm up 32 events: the verifier
+  // re-runs the extra misses cheaply (config 3: 270 -> 280 Mev/s)
+  g->sort_cluster_ok = cluster_sort_state == 1;
+  if (const char *v = getenv("FIBAR_SORT_CLUSTER")) g->sort_cluster_ok = g->sort_cluster_ok && atoi(v) != 0;
   if (const char *v = getenv("FIBAR_WARM")) {
     g->warm = std::max(0, atoi(v));
     g->warm_set = true;
@@ -1003,6 +1015,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->rnext, g->R);
     rc |= dalloc(&g->dp, Bc);
     rc |= dalloc(&g->S, Bc);
+    rc |= dalloc(&g->Qt, Bc);
     rc |= dalloc(&g->pmap, npop_cap);
     rc |= dalloc(&g->bv64, npop_cap);
     rc |= dalloc(&g->mv64, Bc);
@@ -1017,7 +1030,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->lc, T);
     rc |= dalloc(&g->lu, T);
     rc |= dalloc(&g->ch, T);
-    rc |= dalloc(&g->vl, T);
+    rc |= dalloc(&g->vl, 2 * T);   // the verifier's lists, by round parity
   }
   if (g->halo) {
     const long long nbh = (Bc + n + 2 + TPB - 1) / TPB;
@@ -1047,7 +1060,7 @@ int fibar_destroy(fibar_engine *g) {
   if (g->bstream) cudaStreamSynchronize(g->bstream);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
-                  g->dp, g->S, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
+                  g->dp, g->S, g->Qt, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);

@@ -20,19 +20,60 @@ __device__ __forceinline__ bool on_sensor(const Ctx &x, unsigned xx, unsigned yy
 }
 __device__ __forceinline__ bool in_band(const Ctx &x, unsigned yy) { return yy - x.band_y0 < (unsigned)x.H; }
 
+// a thread's IN_ITEMS consecutive packet entries: one 16-byte load per
+// coordinate column and one 8-byte load of polarities when the packet is
+// aligned (lanes take consecutive 16-byte pieces: coalesced), else scalar
+__device__ __forceinline__ void load_in(const Ctx &x, long long base, unsigned (&xx)[IN_ITEMS],
+                                        unsigned (&yy)[IN_ITEMS], int (&pp)[IN_ITEMS], bool with_p) {
+  static_assert(IN_ITEMS == 8, "vector ingest assumes 8 entries per thread");
+  const bool vec = base + IN_ITEMS <= x.n_raw && ((reinterpret_cast<uintptr_t>(x.raw_x + base) |
+                                                   reinterpret_cast<uintptr_t>(x.raw_y + base)) & 15) == 0 &&
+                   (!with_p || (reinterpret_cast<uintptr_t>(x.raw_p + base) & 7) == 0);
+  if (vec) {
+    const uint4 vx = *reinterpret_cast<const uint4 *>(x.raw_x + base);
+    const uint4 vy = *reinterpret_cast<const uint4 *>(x.raw_y + base);
+    const unsigned wx[4] = {vx.x, vx.y, vx.z, vx.w}, wy[4] = {vy.x, vy.y, vy.z, vy.w};
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      xx[2 * r] = wx[r] & 0xFFFFu;
+      xx[2 * r + 1] = wx[r] >> 16;
+      yy[2 * r] = wy[r] & 0xFFFFu;
+      yy[2 * r + 1] = wy[r] >> 16;
+    }
+    if (with_p) {
+      const uint2 vp = *reinterpret_cast<const uint2 *>(x.raw_p + base);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        pp[r] = (int)(int8_t)(vp.x >> (8 * r));
+        pp[4 + r] = (int)(int8_t)(vp.y >> (8 * r));
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < IN_ITEMS; ++r) {
+    const long long i = base + r;
+    const bool in = i < x.n_raw;
+    xx[r] = in ? x.raw_x[i] : 0xFFFFu;   // off the sensor: never kept
+    yy[r] = in ? x.raw_y[i] : 0xFFFFu;
+    if (with_p) pp[r] = in ? x.raw_p[i] : 0;
+  }
+}
+
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
   pdl_wait();
   __shared__ unsigned wsum[TPB / 32], woob[TPB / 32];
   const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
   unsigned cnt = 0, oob = 0;
+  unsigned xs[IN_ITEMS], ys[IN_ITEMS];
+  int ps[IN_ITEMS];
+  load_in(x, base, xs, ys, ps, false);
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
-    long long i = base + r;
-    if (i < x.n_raw) {
-      const unsigned xx = x.raw_x[i], yy = x.raw_y[i];
-      const bool ok = on_sensor(x, xx, yy);
+    if (base + r < x.n_raw) {
+      const bool ok = on_sensor(x, xs[r], ys[r]);
       oob += !ok;
-      cnt += ok && in_band(x, yy);
+      cnt += ok && in_band(x, ys[r]);
     }
   }
   cnt = __reduce_add_sync(0xffffffffu, cnt);
@@ -62,10 +103,12 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
   bool keep[IN_ITEMS];
   unsigned cnt = 0;
+  unsigned xs[IN_ITEMS], ys[IN_ITEMS];
+  int ps[IN_ITEMS];
+  load_in(x, base, xs, ys, ps, true);
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
-    long long i = base + r;
-    keep[r] = i < x.n_raw && on_sensor(x, x.raw_x[i], x.raw_y[i]) && in_band(x, x.raw_y[i]);
+    keep[r] = base + r < x.n_raw && on_sensor(x, xs[r], ys[r]) && in_band(x, ys[r]);
     cnt += keep[r];
   }
   unsigned incl = cnt;
@@ -82,14 +125,13 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
     if (!keep[r]) continue;
-    long long i = base + r;
-    const unsigned xx = x.raw_x[i], yy = x.raw_y[i] - x.band_y0;
+    const unsigned xx = xs[r], yy = ys[r] - x.band_y0;
     const unsigned key = yy * (unsigned)x.W + xx;
     const unsigned tile = (yy / x.ts) * (unsigned)x.tiles_x + xx / x.ts;
     const unsigned sub = (yy % x.ts) * x.ts + xx % x.ts;
     x.ekey[pos] = key;
     x.tkey[pos] = tile * (unsigned)x.A + sub;
-    x.epol[pos] = x.raw_p[i];
+    x.epol[pos] = (int8_t)ps[r];
     if (x.spatial) x.rkey[(unsigned long long)(E0 + pos) & x.Rm] = key;
     ++pos;
   }
@@ -105,7 +147,6 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->nlong = 0;
     b->nco = 0;
     b->nbad = 0;
-    b->vbar = 0;
     b->vcnt[0] = 0;
     b->vcnt[1] = 0;
     b->qlo = 0x7FFFFFFFFFFFFFFFLL;
@@ -822,7 +863,10 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
           }
         }
       }
-      if (jr >= br) x.S[jr - e0r] = sr;
+      if (jr >= br) {
+        x.S[jr - e0r] = sr;
+        x.Qt[jr - e0r] = q;
+      }
     }
   }
   w.s = base + sr;
@@ -860,78 +904,120 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
 // chunk exact, so this is exact by induction whatever the guesses.  Then the
 // targets' extrema are reduced and the batch's final window state published.
 //
-// One cooperative launch (grid barriers between the phases of a round): every
-// boundary is checked by the whole grid, and each re-run is done by one warp
-// that stages the chunk's links dp[b, e) and the ring next-links of the
-// evictions it will most likely make, [s, s + VF_RN), in shared memory with
-// coalesced loads, after which lane 0 steps the recurrence from shared memory.
+// One thread-block cluster (VF_CTAS CTAs, hardware cluster barriers between
+// the phases of a round): every boundary is checked by the whole cluster, and
+// each re-run is done by one warp that stages the chunk's links dp[b, e) and
+// the ring next-links of the evictions it will most likely make,
+// [s, s + VF_RN), in shared memory with coalesced loads, after which lane 0
+// steps the recurrence from shared memory.
 constexpr int VF_DP = 64;     // >= the largest chunk
 constexpr int VF_RN = 128;    // staged ring entries per re-run
 
-__device__ __forceinline__ void vf_barrier(BatchState *bs, unsigned k) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&bs->vbar) : "memory");
-    while (ld_acquire_u32(&bs->vbar) < k * gridDim.x) {
-    }
-  }
-  __syncthreads();
+// cluster-wide barrier; release / acquire at cluster scope also orders the
+// CTAs' global-memory accesses
+__device__ __forceinline__ void vf_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
-__device__ void rerun_chunk_staged(const Ctx &x, WState &w, long long b, long long e, long long E0, long long s_start,
-                                   uint2 *sdp, uint2 *srn, long long &qlo, long long &qhi) {
+// 32-bit state relative to the batch's start window (every index in play is
+// within B + window of it), as in k_window_run.  The speculative run recorded
+// (S, Qt) -- window start and target after each of the chunk's events; a
+// re-run that reaches the same (s, q) after some event has merged with that
+// trajectory (the distinct counts are functions of (s, j), the regulation
+// counter of j), so the rest of the chunk and its end state stand as they are:
+// the re-run stops there (regulation every event only).  Returns whether it
+// merged.
+__device__ bool rerun_chunk_staged(const Ctx &x, WState &w, long long b, long long e, long long E0, long long s_start,
+                                   uint2 *sdp, uint2 *srn, uint2 *ssq, long long &qlo, long long &qhi) {
   const int lane = threadIdx.x & 31;
   const long long rn0 = w.s;
-  for (int i = lane; i < (int)(e - b); i += 32) sdp[i] = x.dp[b - E0 + i];
+  for (int i = lane; i < (int)(e - b); i += 32) {
+    sdp[i] = x.dp[b - E0 + i];
+    ssq[i] = make_uint2(x.S[b - E0 + i], x.Qt[b - E0 + i]);
+  }
   uint2 rr[VF_RN / 32];
 #pragma unroll
   for (int u = 0; u < VF_RN / 32; ++u) rr[u] = x.rnext[(unsigned long long)(rn0 + lane + 32 * u) & x.Rm];
 #pragma unroll
   for (int u = 0; u < VF_RN / 32; ++u) srn[lane + 32 * u] = rr[u];
   __syncwarp();
+  unsigned merged_at = 0xFFFFFFFFu;
   if (lane == 0) {
-    for (long long j = b; j < e; ++j) {
-      const uint2 d = sdp[j - b];
-      const unsigned long long js = (unsigned long long)(j - w.s);
-      w.npix += (unsigned long long)d.x > js;
-      w.ntiles += (unsigned long long)d.y > js;
-      long long len = j - w.s + 1;
-      if (len > w.q) {
-        const long long snew = j + 1 - w.q;
-        long long np = w.npix, nt = w.ntiles;
-        for (long long k = w.s; k < snew; ++k) {
-          const long long o = k - rn0;
-          const uint2 r = o < VF_RN ? srn[o] : x.rnext[(unsigned long long)k & x.Rm];
-          const unsigned long long dd = (unsigned long long)(j - k);
-          np -= (unsigned long long)r.x > dd;
-          nt -= (unsigned long long)r.y > dd;
+    const unsigned bslot = (unsigned)((unsigned long long)s_start & x.Rm), rm = (unsigned)x.Rm;
+    const unsigned r0 = (unsigned)(rn0 - s_start);   // first staged entry, relative
+    const unsigned br = (unsigned)(b - s_start), er = (unsigned)(e - s_start), e0r = (unsigned)(E0 - s_start);
+    const unsigned every = (unsigned)x.every;
+    unsigned sr = (unsigned)(w.s - s_start), q = (unsigned)w.q, ev = (unsigned)w.evctr;
+    int np = (int)w.npix, nt = (int)w.ntiles;
+    unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0;
+#pragma unroll 1
+    for (unsigned jr = br; jr < er; ++jr) {
+      const uint2 d = sdp[jr - br];
+      const unsigned js = jr - sr;
+      np += d.x > js;
+      nt += d.y > js;
+      if (js >= q) {   // the trim pops [sr, jr + 1 - q)
+        const unsigned hi = jr + 1 - q;
+#pragma unroll 1
+        for (unsigned k = sr; k < hi; ++k) {
+          const unsigned o = k - r0;
+          const uint2 r = o < (unsigned)VF_RN ? srn[o] : x.rnext[(bslot + k) & rm];
+          const unsigned dd = jr - k;
+          np -= r.x > dd;
+          nt -= r.y > dd;
         }
-        w.npix = np;
-        w.ntiles = nt;
-        w.s = snew;
-        len = w.q;
+        sr = hi;
       }
-      if (++w.evctr >= x.every) {
-        w.evctr = 0;
-        if (w.npix >= 1 && w.ntiles >= 1) {
-          const long long qn = (x.qmax < (1LL << 22) && len < (1LL << 32))
-                                   ? (long long)regulate32(x, (unsigned)len, (unsigned)w.npix, (unsigned)w.ntiles)
-                                   : regulate(x, len, w.npix, w.ntiles);
-          w.q = qn;
-          qlo = min(qlo, qn);
-          qhi = max(qhi, qn);
+      if (++ev >= every) {
+        ev = 0;
+        if (np >= 1 && nt >= 1) {
+          q = regulate32(x, jr - sr + 1, (unsigned)np, (unsigned)nt);
+          qlo32 = min(qlo32, q);
+          qhi32 = max(qhi32, q);
         }
       }
-      x.S[j - E0] = (unsigned)(w.s - s_start);
+      const uint2 old = ssq[jr - br];
+      if (every == 1 && old.x == sr && old.y == q) {
+        merged_at = jr - br;
+        break;
+      }
+      x.S[jr - e0r] = sr;
+      x.Qt[jr - e0r] = q;
+    }
+    w.s = s_start + sr;
+    w.q = q;
+    w.npix = np;
+    w.ntiles = nt;
+    w.evctr = ev;
+    if (qhi32 > 0) {
+      qlo = qlo32;
+      qhi = qhi32;
+    }
+  }
+  merged_at = __shfl_sync(0xffffffffu, merged_at, 0);
+  if (merged_at != 0xFFFFFFFFu) {
+    // the chunk's targets after the merge are the recorded ones
+    unsigned lo = 0xFFFFFFFFu, hi = 0;
+    for (unsigned i = merged_at + 1 + lane; i < (unsigned)(e - b); i += 32) {
+      lo = min(lo, ssq[i].y);
+      hi = max(hi, ssq[i].y);
+    }
+    lo = __reduce_min_sync(0xffffffffu, lo);
+    hi = __reduce_max_sync(0xffffffffu, hi);
+    if (hi > 0) {
+      qlo = min(qlo, (long long)lo);
+      qhi = max(qhi, (long long)hi);
     }
   }
   __syncwarp();
+  return merged_at != 0xFFFFFFFFu;
 }
 
-__global__ void __launch_bounds__(VF_TPB) k_window_verify(Ctx x) {
+__global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x) {
   pdl_wait();
   constexpr int NW = VF_TPB / 32;
   __shared__ uint2 sdp[NW][VF_DP];
+  __shared__ uint2 ssq[NW][VF_DP];
   __shared__ uint2 srn[NW][VF_RN];
   __shared__ long long red_lo[NW], red_hi[NW];
   BatchState *bs = x.bs;
@@ -941,54 +1027,71 @@ __global__ void __launch_bounds__(VF_TPB) k_window_verify(Ctx x) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const long long tid = (long long)blockIdx.x * VF_TPB + threadIdx.x, nthr = (long long)gridDim.x * VF_TPB;
   const long long gw = (long long)blockIdx.x * NW + wid, nwarps = (long long)gridDim.x * NW;
-  unsigned nbar = 0;
   int rounds = 0;
   long long reruns = 0;
-  for (;; ++rounds) {
-    unsigned *cnt = &bs->vcnt[rounds & 1];
-    if (tid == 0) bs->vcnt[(rounds + 1) & 1] = 0;   // the next round's list (its last reader passed a barrier)
-    for (long long c = 1 + tid; c < T; c += nthr) {
-      const ChunkRec &p = x.ch[c - 1];
-      const ChunkRec &q = x.ch[c];
-      if (q.st_s != p.en_s || q.st_q != p.en_q) {
-        const unsigned i = atomicAdd(cnt, 1u);
-        VRec v;
-        v.s = p.en_s;
-        v.q = p.en_q;
-        v.np = p.en_np;
-        v.nt = p.en_nt;
-        v.ev = p.en_ev;
-        v.c = (int)c;
-        v.pad = 0;
-        x.vl[i] = v;
-      }
+  // round 0 lists every disagreeing boundary; a re-run that did not merge
+  // with its recorded trajectory changed its end state, so it lists its
+  // successor for the next round itself (with that end state as the start)
+  for (long long c = 1 + tid; c < T; c += nthr) {
+    const ChunkRec &p = x.ch[c - 1];
+    const ChunkRec &q = x.ch[c];
+    if (q.st_s != p.en_s || q.st_q != p.en_q) {
+      const unsigned i = atomicAdd(&bs->vcnt[0], 1u);
+      VRec v;
+      v.s = p.en_s;
+      v.q = p.en_q;
+      v.np = p.en_np;
+      v.nt = p.en_nt;
+      v.ev = p.en_ev;
+      v.c = (int)c;
+      v.pad = 0;
+      x.vl[i] = v;
     }
-    vf_barrier(bs, ++nbar);
-    const unsigned n = ld_relaxed_u32(cnt);
+  }
+  vf_barrier();
+  for (;; ++rounds) {
+    const unsigned n = ld_relaxed_u32(&bs->vcnt[rounds % 3]);
     if (n == 0) break;
     reruns += n;
+    if (tid == 0) bs->vcnt[(rounds + 2) % 3] = 0;   // for round r + 2 (its last reader passed a barrier)
+    const VRec *in = x.vl + (long long)(rounds & 1) * T;
+    VRec *out = x.vl + (long long)((rounds + 1) & 1) * T;
+    unsigned *out_cnt = &bs->vcnt[(rounds + 1) % 3];
     for (long long i = gw; i < n; i += nwarps) {
-      const VRec v = x.vl[i];
+      const VRec v = in[i];
       WState w{v.s, v.q, v.np, v.nt, v.ev};
       long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
       const long long b = E0 + (long long)v.c * x.chunk;
       const long long e = min(E0 + B, b + x.chunk);
-      rerun_chunk_staged(x, w, b, e, E0, s_start, sdp[wid], srn[wid], qlo, qhi);
+      const bool merged = rerun_chunk_staged(x, w, b, e, E0, s_start, sdp[wid], srn[wid], ssq[wid], qlo, qhi);
       if (lane == 0) {
-        ChunkRec r;
+        ChunkRec r = x.ch[v.c];   // merged: the recorded end state stands
         r.st_s = v.s;
         r.st_q = v.q;
-        r.en_s = w.s;
-        r.en_q = w.q;
-        r.en_np = w.npix;
-        r.en_nt = w.ntiles;
-        r.en_ev = w.evctr;
+        if (!merged) {
+          r.en_s = w.s;
+          r.en_q = w.q;
+          r.en_np = w.npix;
+          r.en_nt = w.ntiles;
+          r.en_ev = w.evctr;
+          if (v.c + 1 < T) {
+            VRec nx;
+            nx.s = w.s;
+            nx.q = w.q;
+            nx.np = w.npix;
+            nx.nt = w.ntiles;
+            nx.ev = w.evctr;
+            nx.c = v.c + 1;
+            nx.pad = 0;
+            out[atomicAdd(out_cnt, 1u)] = nx;
+          }
+        }
         r.qlo = qlo;
         r.qhi = qhi;
         x.ch[v.c] = r;
       }
     }
-    vf_barrier(bs, ++nbar);
+    vf_barrier();
   }
   // the targets' extrema over every chunk
   long long lo = 0x7FFFFFFFFFFFFFFFLL, hi = -1;
@@ -1016,7 +1119,7 @@ __global__ void __launch_bounds__(VF_TPB) k_window_verify(Ctx x) {
       atomicMax((long long *)&bs->qhi, hi);
     }
   }
-  vf_barrier(bs, ++nbar);
+  vf_barrier();
   if (tid == 0) {
     DevState *s = x.st;
     if (T > 0) {

@@ -76,21 +76,26 @@ inline void fibar_launch(Launcher &L, const char *name, void (*kern)(KArgs...), 
   L.end();
 }
 
-// A cooperative launch (all CTAs co-resident: the kernel has grid barriers).
+// A launch of one thread-block cluster of grid.x CTAs (the kernel uses
+// cluster barriers), with programmatic dependent launch like fibar_launch.
 template <typename... KArgs, typename... Args>
-inline void fibar_launch_coop(Launcher &L, const char *name, void (*kern)(KArgs...), dim3 grid, dim3 block,
-                              size_t smem, cudaStream_t s, Args &&...args) {
+inline void fibar_launch_cluster(Launcher &L, const char *name, void (*kern)(KArgs...), int ctas, dim3 block,
+                                 size_t smem, cudaStream_t s, Args &&...args) {
   L.begin(name);
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = grid;
+  cfg.gridDim = dim3(ctas);
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = ctas;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = L.pdl ? 2 : 1;
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
   L.end();
 }
@@ -104,6 +109,15 @@ __device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
 }
+
+// one-cluster sort of small batches (fibar_sort.cu)
+constexpr int CS_CTAS = 16;                    // CTAs in the cluster (non-portable size)
+constexpr int CS_THREADS = 256;                // threads per CTA (one per digit)
+constexpr int CS_CAP = 8192;                   // pairs per CTA
+constexpr long long CS_MAX = (long long)CS_CTAS * CS_CAP;   // 131072
+int sort_pairs_cluster(Launcher &L, const unsigned *k_a, unsigned *k_b, unsigned *v_b, const long long *n_dev,
+                       long long n_max, int bits);
+bool sort_cluster_init();
 
 int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, unsigned *v_b, unsigned *hist,
                      const long long *n_dev, long long n_max, int bits);

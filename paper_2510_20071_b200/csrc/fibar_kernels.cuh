@@ -45,6 +45,7 @@ struct VRec {
   int c, pad;
 };
 constexpr int VF_TPB = 256;   // k_window_verify: threads per CTA (one warp per re-run)
+constexpr int VF_CTAS = 16;   // k_window_verify: CTAs in its one cluster (non-portable size)
 
 struct ChunkRec {
   long long st_s, st_q;                          // state after event b_c - 1 (speculative start)
@@ -103,6 +104,7 @@ struct Ctx {
   const unsigned *skey, *sidx;    // sorted keys / batch-local event index
   uint2 *dp;
   unsigned *S;
+  unsigned *Qt;     // per batch event: the window target after it (k_window_run / k_window_verify)
   unsigned *pmap;   // per eviction: the batch-relative event that pops it (k_popj_map)
   Item *item;
   PosRec *posrec;
@@ -164,7 +166,7 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc);
 __global__ void __launch_bounds__(TPB) k_fp(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run(Ctx x);
-__global__ void __launch_bounds__(VF_TPB) k_window_verify(Ctx x);
+__global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj_map(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x);
 __global__ void __launch_bounds__(TPB) k_posinfo(Ctx x);
