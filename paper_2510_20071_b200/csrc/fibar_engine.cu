@@ -213,7 +213,6 @@ struct fibar_engine {
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
   bool warm_set = false;   // FIBAR_WARM given: used for every batch size
-  bool sort_cluster_ok = false;   // batches <= CS_MAX sort in one cluster (FIBAR_SORT_CLUSTER=0: off)
   // batches up to this size use 32-event speculation chunks: a small batch
   // leaves most SMs idle, so shorter serial chunk runs win over the extra
   // anchors and re-runs (config 3, 100k batches: 214 -> 227 Mev/s; 1M-event
@@ -374,13 +373,8 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
   fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
-  // small batches: the whole sort in one thread-block cluster (on chip)
-  where = g->sort_cluster_ok ? sort_pairs_cluster(L, g->ka2[par], g->kb2[par], g->vb2[par], &g->bsd[par].B, n_raw,
-                                                  g->key_bits)
-                             : -1;
-  if (where < 0)
-    where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
-                             g->key_bits);
+  where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
+                           g->key_bits);
   L.stream = s_saved;
   const unsigned *skey = where ? g->kb2[par] : g->ka2[par];
   const unsigned *sidx = where ? g->vb2[par] : g->va2[par];
@@ -787,8 +781,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(FIBAR_E_NODEVICE, "no CUDA device");
   // the window verifier is one 16-CTA cluster (beyond the portable 8)
   CK(cudaFuncSetAttribute(k_window_verify, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  static int cluster_sort_state = -1;   // per process: the cluster sort's opt-ins done and usable
-  if (cluster_sort_state < 0) cluster_sort_state = sort_cluster_init() ? 1 : 0;
+
   if (cfg->width < 2 || cfg->height < 2) return fail(FIBAR_E_CONFIG, "geometry must be at least 2x2");
   if (cfg->tile_side < 2) return fail(FIBAR_E_CONFIG, "tile_side must be >= 2");
   if (cfg->regulate_every < 1) return fail(FIBAR_E_CONFIG, "regulate_every must be >= 1");
@@ -862,8 +855,6 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   }
   // small batches (<= small_chunk_max) warm up 32 events: the verifier
   // re-runs the extra misses cheaply (config 3: 270 -> 280 Mev/s)
-  g->sort_cluster_ok = cluster_sort_state == 1;
-  if (const char *v = getenv("FIBAR_SORT_CLUSTER")) g->sort_cluster_ok = g->sort_cluster_ok && atoi(v) != 0;
   if (const char *v = getenv("FIBAR_WARM")) {
     g->warm = std::max(0, atoi(v));
     g->warm_set = true;

@@ -347,45 +347,19 @@ __device__ __forceinline__ unsigned regulate32(const Ctx &x, unsigned len, unsig
   return (unsigned)(q < x.qmin ? x.qmin : (q > x.qmax ? x.qmax : q));
 }
 
+// regulate() through the 32-bit form whenever the operands fit (always for
+// sensors up to 4.19M pixels): no double division on the candidate paths
+__device__ __forceinline__ long long regulate_fast(const Ctx &x, long long len, long long np, long long nt) {
+  if (len < (1LL << 32) && np < (1LL << 32) && nt < (1LL << 32))
+    return (long long)regulate32(x, (unsigned)len, (unsigned)np, (unsigned)nt);
+  return regulate(x, len, np, nt);
+}
+
 // The reference's per-event queue bookkeeping (_kernels.py:132-205) restated on
 // the suffix window [s, j]: the push of event j activates its pixel / tile iff
 // its previous same-pixel / same-tile event lies before s; the trim pops
 // [s, j+1-q) and each popped k deactivates iff its next occurrence lies after j.
-// Scalar form, used by the verifier's re-runs.
-__device__ void run_window(const Ctx &x, WState &w, long long jf, long long jt, long long E0, long long s_start,
-                           bool write, long long &qlo, long long &qhi) {
-  for (long long j = jf; j < jt; ++j) {
-    const uint2 d = x.dp[j - E0];
-    const unsigned long long js = (unsigned long long)(j - w.s);
-    w.npix += (unsigned long long)d.x > js;
-    w.ntiles += (unsigned long long)d.y > js;
-    long long len = j - w.s + 1;
-    if (len > w.q) {
-      const long long snew = j + 1 - w.q;
-      long long np = w.npix, nt = w.ntiles;
-      for (long long k = w.s; k < snew; ++k) {
-        const uint2 r = x.rnext[(unsigned long long)k & x.Rm];
-        const unsigned long long dd = (unsigned long long)(j - k);
-        np -= (unsigned long long)r.x > dd;
-        nt -= (unsigned long long)r.y > dd;
-      }
-      w.npix = np;
-      w.ntiles = nt;
-      w.s = snew;
-      len = w.q;
-    }
-    if (++w.evctr >= x.every) {
-      w.evctr = 0;
-      if (w.npix >= 1 && w.ntiles >= 1) {
-        const long long qn = regulate(x, len, w.npix, w.ntiles);
-        w.q = qn;
-        qlo = min(qlo, qn);
-        qhi = max(qhi, qn);
-      }
-    }
-    if (write) x.S[j - E0] = (unsigned)(w.s - s_start);
-  }
-}
+// k_window_run steps it per chunk lane, the verifier's re-runs per warp.
 
 // Exact distinct-pixel / distinct-tile counts for every chunk's candidate
 // windows [max(s_start, a_c - L_i), a_c - 1], as deltas from the previous
@@ -580,7 +554,7 @@ __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
   for (int i = 0; i < nc; ++i) {
     const long long len = a - max(s0, a - cand_len(x, q0, i));
     const int2 cnt = x.anc[(long long)c * NCAND + i];
-    const long long f = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) - len : -1;
+    const long long f = (cnt.x >= 1 && cnt.y >= 1) ? regulate_fast(x, len, cnt.x, cnt.y) - len : -1;
     int k = i;   // insertion by length
     while (k > 0 && lens[k - 1] > len) {
       lens[k] = lens[k - 1];
@@ -718,7 +692,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
         const long long sc = fine_start(x, s_start0, a, center, unit, j);
         const int2 cnt = x.anc2[(long long)c * NFINE + j];
         const long long len = a - sc;
-        if (cnt.x >= 1 && cnt.y >= 1 && regulate(x, len, cnt.x, cnt.y) >= len) jstar = j;
+        if (cnt.x >= 1 && cnt.y >= 1 && regulate_fast(x, len, cnt.x, cnt.y) >= len) jstar = j;
       }
       const int g = jstar + 1 < NFINE ? jstar + 1 : NFINE - 1;
       int2 cnt = x.anc2[(long long)c * NFINE + g];
@@ -728,14 +702,14 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
       // state is the no-pop window [s_start, a - 1] whenever that is stable
       const int2 c0 = x.anc0[c];
       const long long len0 = a - s_start0;
-      if (c0.x >= 1 && c0.y >= 1 && regulate(x, len0, c0.x, c0.y) >= len0) {
+      if (c0.x >= 1 && c0.y >= 1 && regulate_fast(x, len0, c0.x, c0.y) >= len0) {
         w.s = s_start0;
         cnt = c0;
       }
       w.npix = cnt.x;
       w.ntiles = cnt.y;
       const long long len = a - w.s;
-      w.q = (cnt.x >= 1 && cnt.y >= 1) ? regulate(x, len, cnt.x, cnt.y) : len;
+      w.q = (cnt.x >= 1 && cnt.y >= 1) ? regulate_fast(x, len, cnt.x, cnt.y) : len;
       if (x.debug) {
         long long bn = 0, bt = 0;
         for (long long k = w.s; k < a; ++k) {

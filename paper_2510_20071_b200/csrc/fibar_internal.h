@@ -110,15 +110,6 @@ __device__ __forceinline__ void pdl_wait() {
 #endif
 }
 
-// one-cluster sort of small batches (fibar_sort.cu)
-constexpr int CS_CTAS = 16;                    // CTAs in the cluster (non-portable size)
-constexpr int CS_THREADS = 256;                // threads per CTA (one per digit)
-constexpr int CS_CAP = 8192;                   // pairs per CTA
-constexpr long long CS_MAX = (long long)CS_CTAS * CS_CAP;   // 131072
-int sort_pairs_cluster(Launcher &L, const unsigned *k_a, unsigned *k_b, unsigned *v_b, const long long *n_dev,
-                       long long n_max, int bits);
-bool sort_cluster_init();
-
 int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, unsigned *v_b, unsigned *hist,
                      const long long *n_dev, long long n_max, int bits);
 

@@ -7,8 +7,6 @@
 //
 // The batch size lives in device memory (after OOB compaction), so every
 // kernel is launched for the host-side upper bound and reads the real count.
-#include <cooperative_groups.h>
-
 #include "fibar_common.cuh"
 #include "fibar_internal.h"
 
@@ -185,180 +183,6 @@ int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, u
     fibar_launch(L, "rs_scatter", k_rs_scatter, nblocks, RS_THREADS, 0, L.stream, ki, vi, ko, vo, n_dev, shift, hist, nblocks);
   }
   return (passes % 2) == 1 ? 1 : 0;
-}
-
-// --- small batches: the whole sort inside one thread-block cluster ----------
-//
-// A batch of up to CS_MAX pairs fits in the distributed shared memory of one
-// 16-CTA cluster (CS_CAP pairs per CTA, double buffered).  Every 8-bit LSD
-// pass runs on chip: per-warp digit counts (match_any), the cluster-wide digit
-// offsets read from the other CTAs' histograms through DSMEM, then each warp
-// ranks its pairs in order and stores each one straight into the destination
-// CTA's other buffer.  Two cluster barriers per pass, one launch per sort
-// instead of three per pass, and no global traffic between passes.
-namespace cg = cooperative_groups;
-
-__global__ void __launch_bounds__(CS_THREADS, 1) k_sort_cluster(const unsigned *__restrict__ keys_in,
-                                                                 const long long *__restrict__ n_dev, int passes,
-                                                                 unsigned *__restrict__ keys_out,
-                                                                 unsigned *__restrict__ vals_out) {
-  pdl_wait();
-  cg::cluster_group cluster = cg::this_cluster();
-  extern __shared__ __align__(16) unsigned cs_smem[];
-  constexpr int NW = CS_THREADS / 32;
-  // two buffers of (keys[CS_CAP], vals[CS_CAP]), then the counters
-  unsigned *wcnt = cs_smem + 4 * CS_CAP;    // [NW][256]: per-warp digit counts, then their exclusive prefix
-  unsigned *hist = wcnt + NW * 256;         // [256]: this CTA's digit totals (read by the other CTAs)
-  unsigned *off = hist + 256;               // [256]: this CTA's first global position per digit
-  unsigned *wsum = off + 256;               // [NW + 1]: scan scratch
-  const int r = (int)cluster.block_rank();
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  const long long n = *n_dev;
-  const int cap = (int)((n + CS_CTAS - 1) / CS_CTAS);   // pairs per CTA (the last may hold fewer)
-  const int mine = (int)max(0LL, min((long long)cap, n - (long long)r * cap));
-  const int ipw = (cap + NW * 32 - 1) / (NW * 32) * 32;   // pairs per warp, whole rounds
-  for (int i = tid; i < mine; i += CS_THREADS) {
-    cs_smem[i] = keys_in[(long long)r * cap + i];
-    cs_smem[CS_CAP + i] = (unsigned)((long long)r * cap + i);
-  }
-  const unsigned lt = (1u << lane) - 1u;
-  int cur = 0;
-  for (int ps = 0; ps < passes; ++ps) {
-    const int shift = ps * 8;
-    const unsigned *kin = cs_smem + cur * 2 * CS_CAP, *vin = kin + CS_CAP;
-    unsigned *kout = cs_smem + (cur ^ 1) * 2 * CS_CAP, *vout = kout + CS_CAP;
-    for (int i = tid; i < NW * 256; i += CS_THREADS) wcnt[i] = 0;
-    __syncthreads();
-    // per-warp digit counts, in the warp's pair order
-    const int w0 = wid * ipw;
-    for (int k = w0 + lane; k < w0 + ipw; k += 32) {
-      const bool valid = k < mine;
-      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-      if (valid) {
-        const unsigned d = (kin[k] >> shift) & 255u;
-        const unsigned peers = __match_any_sync(vmask, d);
-        if ((peers & lt) == 0) wcnt[wid * 256 + d] += __popc(peers);
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    // exclusive prefix over the warps per digit; the CTA's digit totals
-    {
-      unsigned run = 0;
-      for (int w = 0; w < NW; ++w) {
-        const unsigned t = wcnt[w * 256 + tid];
-        wcnt[w * 256 + tid] = run;
-        run += t;
-      }
-      hist[tid] = run;
-    }
-    cluster.sync();   // (A) every CTA's histogram is visible in the cluster
-    {
-      // digit tid: totals over the cluster and the part of the CTAs before this one
-      unsigned tot = 0, before = 0;
-#pragma unroll 4
-      for (int q = 0; q < CS_CTAS; ++q) {
-        const unsigned h = *cluster.map_shared_rank(hist + tid, q);
-        tot += h;
-        before += q < r ? h : 0u;
-      }
-      // exclusive scan of the totals over the 256 digits
-      unsigned inc = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const unsigned t = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += t;
-      }
-      if (lane == 31) wsum[wid] = inc;
-      __syncthreads();
-      unsigned wofs = 0;
-      for (int w = 0; w < wid; ++w) wofs += wsum[w];
-      off[tid] = wofs + inc - tot + before;
-    }
-    __syncthreads();
-    // rank in order and store each pair into its destination CTA's other buffer
-    for (int k = w0 + lane; k < w0 + ipw; k += 32) {
-      const bool valid = k < mine;
-      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
-      if (valid) {
-        const unsigned key = kin[k], val = vin[k];
-        const unsigned d = (key >> shift) & 255u;
-        const unsigned peers = __match_any_sync(vmask, d);
-        const unsigned before = wcnt[wid * 256 + d];
-        const unsigned pos = off[d] + before + __popc(peers & lt);
-        __syncwarp(vmask);
-        if ((peers & lt) == 0) wcnt[wid * 256 + d] = before + __popc(peers);
-        const int dst = (int)(pos / (unsigned)cap), slot = (int)(pos % (unsigned)cap);
-        *cluster.map_shared_rank(kout + slot, dst) = key;
-        *cluster.map_shared_rank(vout + slot, dst) = val;
-      }
-      __syncwarp();
-    }
-    cluster.sync();   // (B) every pair has landed; histograms may be rewritten
-    cur ^= 1;
-  }
-  for (int i = tid; i < mine; i += CS_THREADS) {
-    keys_out[(long long)r * cap + i] = cs_smem[cur * 2 * CS_CAP + i];
-    vals_out[(long long)r * cap + i] = cs_smem[cur * 2 * CS_CAP + CS_CAP + i];
-  }
-}
-
-// the dynamic shared memory k_sort_cluster needs per CTA
-size_t sort_cluster_smem() { return sizeof(unsigned) * (4 * CS_CAP + (CS_THREADS / 32) * 256 + 512 + 64); }
-
-// Small batches (n_max <= CS_MAX) sorted by one cluster: the result goes to
-// (k_b, v_b).  Returns 1 (the buffer pair holding the result), or -1 when the
-// cluster form is unavailable (the caller runs radix_sort_pairs).
-int sort_pairs_cluster(Launcher &L, const unsigned *k_a, unsigned *k_b, unsigned *v_b, const long long *n_dev,
-                       long long n_max, int bits) {
-  if (n_max > CS_MAX) return -1;
-  const int passes = bits <= 0 ? 1 : (bits + 7) / 8;
-  L.begin("sort_cluster");
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CS_CTAS);
-  cfg.blockDim = dim3(CS_THREADS);
-  cfg.dynamicSmemBytes = sort_cluster_smem();
-  cfg.stream = L.stream;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS_CTAS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = L.pdl ? 2 : 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, k_sort_cluster, k_a, n_dev, passes, k_b, v_b);
-  L.end();
-  return e == cudaSuccess ? 1 : -1;
-}
-
-// once per process: the cluster sort's shared-memory and cluster-size opt-ins;
-// false when this device cannot run one such cluster
-bool sort_cluster_init() {
-  if (cudaFuncSetAttribute(k_sort_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sort_cluster_smem()) !=
-          cudaSuccess ||
-      cudaFuncSetAttribute(k_sort_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(CS_CTAS);
-  cfg.blockDim = dim3(CS_THREADS);
-  cfg.dynamicSmemBytes = sort_cluster_smem();
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = CS_CTAS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  int nclusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&nclusters, k_sort_cluster, &cfg) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return nclusters >= 1;
 }
 
 // --- multi-block exclusive scan (reduce / scan partials / scan + offset) ---
