@@ -143,7 +143,11 @@ struct fibar_engine {
   int8_t *raw_p = nullptr;
   unsigned *blockcnt = nullptr;
   unsigned *ekey2[2] = {nullptr, nullptr};
-  int8_t *epol = nullptr, *spol = nullptr;
+  // polarities in stream order (per batch parity: the next batch's ingest may
+  // run while this one's front end reads them) and in pixel-sorted order (per
+  // parity: the temporal replay on the blur stream reads them while the next
+  // front end writes its own)
+  int8_t *epol2[2] = {nullptr, nullptr}, *spol2[2] = {nullptr, nullptr};
   uint2 *longseg = nullptr;
   unsigned *ka2[2] = {nullptr, nullptr}, *va2[2] = {nullptr, nullptr}, *kb2[2] = {nullptr, nullptr},
            *vb2[2] = {nullptr, nullptr}, *hist = nullptr;
@@ -190,7 +194,11 @@ struct fibar_engine {
   CUgreenCtx gctx = nullptr;
   cudaStream_t gstream = nullptr;
   cudaEvent_t evP = nullptr, evG = nullptr;
-  cudaEvent_t evT = nullptr;   // temporal_on_blur: the replay + batch end of the newest batch
+  cudaEvent_t evT = nullptr;   // (unused)
+  // streamed filter-ON batches: the front end's ingest + sort (astream) and
+  // window part (fstream), so batch k+1's ingest overlaps batch k's window pass
+  cudaStream_t astream = nullptr, fstream = nullptr;
+  cudaEvent_t evIn = nullptr, evCp = nullptr, evA[2] = {nullptr, nullptr};
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
@@ -273,8 +281,8 @@ struct fibar_engine {
     x.n_raw = n_raw;
     x.blockcnt = blockcnt;
     x.ekey = ekey2[par];
-    x.epol = epol;
-    x.spol = spol;
+    x.epol = epol2[par];
+    x.spol = spol2[par];
     x.longseg = longseg;
     x.tkey = ka2[par];
     x.skey = skey;
@@ -356,33 +364,39 @@ int init_state(fibar_engine *g) {
   return 0;
 }
 
-// The front end of a batch on stream s: ingest (OOB filter, compaction), the
-// pixel sort and, filter ON, segments, links, the window pass, the stale items
-// and the per-position info.  Returns the batch context (sorted keys) in x.
-int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
-                  cudaEvent_t used_ev, int par, cudaStream_t s, Ctx &x, int &where) {
+// The front end of a batch, in two parts.
+// Ingest (stream s): the OOB filter, compaction and the pixel sort -- it reads
+// only the batch's own events, so it may run ahead of the previous batch's
+// window pass.  Returns where the sorted pairs are.
+int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                   cudaEvent_t used_ev, int par, cudaStream_t s, int &where) {
   Launcher &L = g->L;
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
-  x = g->ctx(nullptr, nullptr, n_raw, par);
+  Ctx x = g->ctx(nullptr, nullptr, n_raw, par);
   x.raw_x = rx0;
   x.raw_y = ry0;
   x.raw_p = rp0;
-  fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
   cudaStream_t s_saved = L.stream;
   L.stream = s;
+  fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
   fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
-  if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
+  if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw packet may be refilled / freed from here on
   where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
                            g->key_bits);
   L.stream = s_saved;
-  const unsigned *skey = where ? g->kb2[par] : g->ka2[par];
-  const unsigned *sidx = where ? g->vb2[par] : g->va2[par];
-  x = g->ctx(skey, sidx, n_raw, par);
-  x.raw_x = rx0;
-  x.raw_y = ry0;
-  x.raw_p = rp0;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// The rest (stream s, after the previous batch's front end): the batch opens
+// against the window state, then (filter ON) segments, links, the window pass,
+// the stale items and the per-position info.  Returns the batch context in x.
+int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s, Ctx &x) {
+  Launcher &L = g->L;
+  x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
   const int nb = (int)((n_raw + TPB - 1) / TPB);
+  fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);
   if (g->spatial) {
     const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
     fibar_launch(L, "seg_marks", k_seg_marks, nb, TPB, 0, s, x);
@@ -404,12 +418,29 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   return 0;
 }
 
-// The captured front end for (n_raw, par), reading the fixed input buffers
-// gx/gy/gp; captured on first use (nullptr on failure).
-GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
+// Both parts on one stream (serial schedules, whole-batch graphs, halo bands).
+int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                  cudaEvent_t used_ev, int par, cudaStream_t s, Ctx &x, int &where) {
+  int rc = enqueue_ingest(g, rx0, ry0, rp0, n_raw, used_ev, par, s, where);
+  if (rc) return rc;
+  cudaStream_t s_saved = g->L.stream;
+  g->L.stream = s;
+  rc = enqueue_window(g, n_raw, par, where, s, x);
+  g->L.stream = s_saved;
+  x.raw_x = rx0;
+  x.raw_y = ry0;
+  x.raw_p = rp0;
+  return rc;
+}
+
+// A captured part of the front end for (n_raw, par): kind 1 the ingest
+// (reading the fixed input buffers gx/gy/gp), kind 2 the window part (given
+// where the ingest graph leaves the sorted pairs).  Captured on first use
+// (nullptr on failure).
+GraphEntry *front_graph(fibar_engine *g, int kind, long long n_raw, int par, int where) {
   for (auto &ge : g->graphs)
-    if (ge.kind == 1 && ge.n == n_raw && ge.par == par) return &ge;
-  if (g->graphs.size() >= 16) {   // small cache: drop the oldest
+    if (ge.kind == kind && ge.n == n_raw && ge.par == par) return &ge;
+  if (g->graphs.size() >= 32) {   // small cache: drop the oldest
     cudaGraphExecDestroy(g->graphs.front().exec);
     g->graphs.erase(g->graphs.begin());
   }
@@ -419,17 +450,19 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   cudaStream_t s0 = L.stream;
   cudaGraph_t graph = nullptr;
   GraphEntry ge;
+  ge.where = where;
   Ctx x{};
   if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
     cudaGetLastError();
     return nullptr;
   }
   L.stream = g->capstream;
-  const int rc = enqueue_front(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, x, ge.where);
+  const int rc = kind == 1 ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where)
+                           : enqueue_window(g, n_raw, par, where, g->capstream, x);
   L.stream = s0;
   cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
   ge.n = n_raw;
-  ge.kind = 1;
+  ge.kind = kind;
   ge.par = par;
   ge.kernels = L.launches - l0;
   L.launches = l0;
@@ -448,44 +481,80 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
 // the second stream, cross-batch events).  graph == true: everything on the
 // engine stream with parity-0 buffers and no events, the form captured into a
 // CUDA graph for small batches (see run_batch_raw).
+//
+// Streamed, filter ON: the front end's two parts run on the engine's own
+// streams.  The ingest (astream) waits for the packet (the caller's stream at
+// the call) and for its parity's buffers (the blur stage two batches back);
+// the window part (fstream) waits for the ingest and runs after the previous
+// batch's window part.  So batch k+1's ingest and sort overlap batch k's
+// window pass.  The caller's stream waits for the ingest's read of the packet.
 int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
                   cudaEvent_t used_ev, int par, bool graph) {
   Launcher &L = g->L;
-  cudaStream_t s = L.stream;
+  const cudaStream_t u = L.stream;   // the caller's stream
   g->last_par = par;
-  // this parity's buffers are free once the batch two back finished its blur stage
-  if (!graph && g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
+  const bool split = !graph && g->spatial && !g->serial && !g->halo && g->temporal_on_blur;
+  cudaStream_t s = split ? g->fstream : u;   // the window part's stream
   Ctx x{};
   int where = 0;
   const int nb = (int)((n_raw + TPB - 1) / TPB);
-  if (g->spatial && !graph && g->graphs_on && !L.prof && n_raw <= g->graph_max) {
-    // a small streamed batch: its front end (ingest .. stale items, ~25
-    // kernels) replays one CUDA graph per (size, parity) from fixed input
-    // buffers, so the host issues a handful of calls per batch while the blur
-    // stage still overlaps the next batch as below
-    CK(cudaMemcpyAsync(g->gx, rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(g->gy, ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
-    CK(cudaMemcpyAsync(g->gp, rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, s));
-    if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
-    GraphEntry *ge = front_graph(g, n_raw, par);
-    if (!ge) return g_err.empty() ? fail(FIBAR_E_CUDA, "front-end graph capture failed") : FIBAR_E_CUDA;
-    CK(cudaGraphLaunch(ge->exec, s));
-    L.launches += ge->kernels;
-    where = ge->where;
-    x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
-    x.raw_x = g->gx;
-    x.raw_y = g->gy;
-    x.raw_p = g->gp;
+  if (split) {
+    cudaStream_t sa = g->astream;
+    CK(cudaEventRecord(g->evIn, u));
+    CK(cudaStreamWaitEvent(sa, g->evIn, 0));
+    if (g->b_used[par]) CK(cudaStreamWaitEvent(sa, g->evB[par], 0));   // this parity's buffers are free
+    const bool small = g->graphs_on && !L.prof && n_raw <= g->graph_max;
+    if (small) {
+      // a small batch: each part replays one CUDA graph per (size, parity),
+      // the ingest from fixed input buffers
+      CK(cudaMemcpyAsync(g->gx, rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, sa));
+      CK(cudaMemcpyAsync(g->gy, ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, sa));
+      CK(cudaMemcpyAsync(g->gp, rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, sa));
+      CK(cudaEventRecord(g->evCp, sa));
+      if (used_ev) CK(cudaEventRecord(used_ev, sa));
+      GraphEntry *gi = front_graph(g, 1, n_raw, par, 0);
+      if (!gi) return g_err.empty() ? fail(FIBAR_E_CUDA, "front-end graph capture failed") : FIBAR_E_CUDA;
+      where = gi->where;
+      GraphEntry *gw = front_graph(g, 2, n_raw, par, where);
+      if (!gw) return g_err.empty() ? fail(FIBAR_E_CUDA, "front-end graph capture failed") : FIBAR_E_CUDA;
+      CK(cudaGraphLaunch(gi->exec, sa));
+      L.launches += gi->kernels;
+      CK(cudaEventRecord(g->evA[par], sa));
+      CK(cudaStreamWaitEvent(s, g->evA[par], 0));
+      CK(cudaGraphLaunch(gw->exec, s));
+      L.launches += gw->kernels;
+      x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+      x.raw_x = g->gx;
+      x.raw_y = g->gy;
+      x.raw_p = g->gp;
+    } else {
+      int rc = enqueue_ingest(g, rx0, ry0, rp0, n_raw, used_ev, par, sa, where);
+      if (rc) return rc;
+      CK(cudaEventRecord(g->evCp, sa));
+      CK(cudaEventRecord(g->evA[par], sa));
+      CK(cudaStreamWaitEvent(s, g->evA[par], 0));
+      L.stream = s;
+      rc = enqueue_window(g, n_raw, par, where, s, x);
+      L.stream = u;
+      if (rc) return rc;
+      x.raw_x = rx0;
+      x.raw_y = ry0;
+      x.raw_p = rp0;
+    }
+    CK(cudaStreamWaitEvent(u, g->evCp, 0));   // the caller may reuse the packet after the ingest read it
+    L.stream = s;
   } else {
+    // this parity's buffers are free once the batch two back finished its blur stage
+    if (!graph && g->spatial && g->b_used[par]) CK(cudaStreamWaitEvent(s, g->evB[par], 0));
     int rc = enqueue_front(g, rx0, ry0, rp0, n_raw, used_ev, par, s, x, where);
     if (rc) return rc;
   }
   if (g->spatial) {
     // The batch's counters (event count, stale count, candidate set) close on
-    // the engine stream: the next front end reads them.  Its links read the
-    // last-touch tables, which k_link already advanced; so the next front end
-    // never waits for this batch's temporal replay or blur stage (only, two
-    // batches on, for the buffers of its parity).
+    // the front end's stream: the next front end reads them.  Its links read
+    // the last-touch tables, which k_link already advanced; so the next front
+    // end never waits for this batch's temporal replay or blur stage (only,
+    // two batches on, for the buffers of its parity).
     fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
     // The temporal replay reads the brightness the previous batch's blur
     // stage finishes.  Streamed (temporal_on_blur): it runs first on the blur
@@ -515,6 +584,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, s, x);
       g->hnb = nbh;
       g->hctx = x;
+      L.stream = u;
       CK(cudaGetLastError());
       return 0;
     }
@@ -543,7 +613,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       }
     }
     fibar_launch(L, "final", k_final, g->nsm * 8, TPB, 0, bs, x);
-    L.stream = s;
+    L.stream = u;
     if (!graph) {
       CK(cudaEventRecord(g->evB[par], bs));
       g->b_used[par] = true;
@@ -555,6 +625,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
     fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
   }
+  L.stream = u;
   CK(cudaGetLastError());
   return 0;
 }
@@ -954,8 +1025,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->gy, g->graph_max);
     rc |= dalloc(&g->gp, g->graph_max);
   }
-  rc |= dalloc(&g->epol, Bc);
-  rc |= dalloc(&g->spol, Bc);
+  for (int b = 0; b < 2; ++b) {
+    rc |= dalloc(&g->epol2[b], Bc);
+    rc |= dalloc(&g->spol2[b], Bc);
+  }
   rc |= dalloc(&g->longseg, 16384);
   rc |= dalloc(&g->bsd, 2);
   if (!rc) cudaMemset(g->bsd, 0, 2 * sizeof(BatchState));
@@ -999,7 +1072,12 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     for (int c = 0; c < 2; ++c) {
       cudaEventCreateWithFlags(&g->evF[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evB[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evA[c], cudaEventDisableTiming);
     }
+    cudaEventCreateWithFlags(&g->evIn, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&g->evCp, cudaEventDisableTiming);
+    cudaStreamCreateWithFlags(&g->astream, cudaStreamNonBlocking);
+    cudaStreamCreateWithFlags(&g->fstream, cudaStreamNonBlocking);
     rc |= dalloc(&g->last_tile, g->n_tiles);
     rc |= dalloc(&g->ptt, g->n_tiles);
     rc |= dalloc(&g->rkey, g->R);
@@ -1048,9 +1126,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
-  if (g->bstream) cudaStreamSynchronize(g->bstream);
+  for (cudaStream_t st : {g->astream, g->fstream, g->bstream})
+    if (st) cudaStreamSynchronize(st);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
-                  g->raw_y, g->raw_p, g->blockcnt, g->epol, g->spol, g->longseg, g->hist,
+                  g->raw_y, g->raw_p, g->blockcnt, g->epol2[0], g->epol2[1], g->spol2[0], g->spol2[1], g->longseg, g->hist,
                   g->dp, g->S, g->Qt, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
@@ -1078,6 +1157,10 @@ int fibar_destroy(fibar_engine *g) {
   for (void *q : {(void *)g->gx, (void *)g->gy, (void *)g->gp})
     if (q) cudaFree(q);
   if (g->bstream) cudaStreamDestroy(g->bstream);
+  for (cudaStream_t st : {g->astream, g->fstream})
+    if (st) cudaStreamDestroy(st);
+  for (cudaEvent_t ev : {g->evIn, g->evCp, g->evA[0], g->evA[1]})
+    if (ev) cudaEventDestroy(ev);
   if (g->gstream) {
     cudaStreamSynchronize(g->gstream);
     cudaStreamDestroy(g->gstream);

@@ -99,7 +99,6 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   pdl_wait();
   __shared__ unsigned wsum[TPB / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const long long E0 = x.st->E;
   const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
   bool keep[IN_ITEMS];
   unsigned cnt = 0;
@@ -132,15 +131,14 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     x.ekey[pos] = key;
     x.tkey[pos] = tile * (unsigned)x.A + sub;
     x.epol[pos] = (int8_t)ps[r];
-    if (x.spatial) x.rkey[(unsigned long long)(E0 + pos) & x.Rm] = key;
     ++pos;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    DevState *s = x.st;
+    // the batch's own scalars; what depends on the window state (E0, s_start,
+    // epoch) is set by k_batch_begin, so ingest may run ahead of the previous
+    // batch's window pass
     BatchState *b = x.bs;
-    b->E0 = s->E;
     b->B = x.blockcnt[nblocks];
-    b->s_start = s->s;
     b->npop = 0;
     b->stale_batch = 0;
     b->ticket = 0;
@@ -151,10 +149,20 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->vcnt[1] = 0;
     b->qlo = 0x7FFFFFFFFFFFFFFFLL;
     b->qhi = -1;
-    s->epoch += 1;
-    b->epoch = s->epoch;
-    b->epoch0 = s->epoch;
   }
+}
+
+// Opens the batch against the engine state the previous batch left: its first
+// event index, the window start and a fresh blur epoch.
+__global__ void k_batch_begin(Ctx x) {
+  pdl_wait();
+  DevState *s = x.st;
+  BatchState *b = x.bs;
+  b->E0 = s->E;
+  b->s_start = s->s;
+  s->epoch += 1;
+  b->epoch = s->epoch;
+  b->epoch0 = s->epoch;
 }
 
 // ------------------------------------------------------------------ link ---
@@ -167,6 +175,7 @@ __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x) {
   const unsigned k = x.skey[i];
   const unsigned jj = x.sidx[i];
   const unsigned c = x.ekey[jj];
+  x.rkey[(unsigned long long)(x.bs->E0 + jj) & x.Rm] = c;   // the window ring's key of event jj
   const bool head = i == 0 || x.skey[i - 1] != k;
   const bool tail = i == B - 1 || x.skey[i + 1] != k;
   if (head) x.pt[c].st = (unsigned)i;

@@ -158,6 +158,7 @@ __device__ __forceinline__ float order_unkey(unsigned k) {
 // kernels (launched by fibar_engine.cu)
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks);
 __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
+__global__ void k_batch_begin(Ctx x);
 __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x);
 __global__ void __launch_bounds__(TPB) k_link(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x);
