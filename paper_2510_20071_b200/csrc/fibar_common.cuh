@@ -72,6 +72,7 @@ struct BatchState {
   long long qlo, qhi;  // extrema of the targets set in the batch (k_window_verify)
   unsigned vcnt[3];    // k_window_verify: chunks listed for a round (rotating by round)
   unsigned vpad;
+  long long n_raw;     // raw events of the batch, set by k_stage (graphs are captured per size class)
 };
 
 // Window / counter state living in device memory so no kernel needs a host
@@ -107,6 +108,7 @@ struct DevState {
   int geo, geo_next;     // window candidates: geometric set needed (this / next batch)
   unsigned nlong, nlong_pad;   // long pixel segments of the batch
   long long dbg_bad;           // FIBAR_DEBUG_WINDOW: anchor counts that disagreed with a serial recount
+  long long Ein;               // in-bounds events ingested (the ingest's running E, ahead of E)
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {

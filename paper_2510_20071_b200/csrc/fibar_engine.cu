@@ -109,11 +109,16 @@ int ceil_log2(long long v) {
 
 }  // namespace
 
+// small batches' front-end graphs are captured per size class of this many events
+constexpr long long GRAPH_CLASS = 16384;
+
 struct GraphEntry {
   long long n;               // batch size the graph was captured for
   long long kernels;         // kernels per replay (the launch counter)
-  cudaGraphExec_t exec;
-  int kind = 0;              // 0: whole batch (serial schedule), 1: front end of the streamed schedule
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphExec_t exec2 = nullptr;   // kind 1: the window part (exec: the ingest)
+  long long kernels2 = 0;
+  int kind = 0;              // 0: whole batch (serial schedule), 1: front end of the streamed schedule (two parts)
   int par = 0;               // kind 1: the batch parity whose buffers it uses
   int where = 0;             // kind 1: which radix-sort buffer holds the sorted keys
 };
@@ -136,7 +141,7 @@ struct fibar_engine {
   unsigned *wcnt = nullptr;
   BatchState *bsd = nullptr;   // [2]
   long long *last_tile = nullptr;
-  uint2 *ptt = nullptr;
+  uint2 *ptt2[2] = {nullptr, nullptr};   // tile segments, per batch parity
   unsigned *rkey = nullptr;
   uint2 *rnext = nullptr;
   uint16_t *raw_x = nullptr, *raw_y = nullptr;
@@ -151,7 +156,7 @@ struct fibar_engine {
   uint2 *longseg = nullptr;
   unsigned *ka2[2] = {nullptr, nullptr}, *va2[2] = {nullptr, nullptr}, *kb2[2] = {nullptr, nullptr},
            *vb2[2] = {nullptr, nullptr}, *hist = nullptr;
-  uint2 *dp = nullptr;
+  uint2 *dp2[2] = {nullptr, nullptr};    // per-event link distances, per batch parity
   unsigned *S = nullptr, *Qt = nullptr;
   unsigned *pmap = nullptr;
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
@@ -185,6 +190,10 @@ struct fibar_engine {
   const uint16_t *zx = nullptr, *zy = nullptr;  // pending zero-copy device range (contiguous device packets)
   const int8_t *zp = nullptr;
   long long zn = 0;
+  // pending non-contiguous device packets, gathered into device staging set
+  // `cur` (k_gather) when the batch is full or at a flush point
+  GatherTable gt{};
+  long long dfill = 0;
   long long batches = 0;
   // filter ON: batch k's blur stage (blur_prep, blur, final) runs on bstream
   // while batch k+1's front end runs on the engine stream; per-batch buffers
@@ -271,7 +280,7 @@ struct fibar_engine {
     x.wcnt = wcnt;
     x.bs = bsd ? bsd + par : nullptr;
     x.last_tile = last_tile;
-    x.ptt = ptt;
+    x.ptt = ptt2[par];
     x.rkey = rkey;
     x.rnext = rnext;
     x.Rm = (unsigned long long)(R - 1);
@@ -279,6 +288,7 @@ struct fibar_engine {
     x.raw_y = raw_y;
     x.raw_p = raw_p;
     x.n_raw = n_raw;
+    x.n_raw_dev = nullptr;
     x.blockcnt = blockcnt;
     x.ekey = ekey2[par];
     x.epol = epol2[par];
@@ -287,7 +297,7 @@ struct fibar_engine {
     x.tkey = ka2[par];
     x.skey = skey;
     x.sidx = sidx;
-    x.dp = dp;
+    x.dp = dp2[par];
     x.S = S;
     x.Qt = Qt;
     x.pmap = pmap;
@@ -360,38 +370,51 @@ int init_state(fibar_engine *g) {
   }
   g->zn = 0;
   g->hfill = 0;
+  g->dfill = 0;
+  g->gt.n = 0;
   CK(cudaGetLastError());
   return 0;
 }
 
 // The front end of a batch, in two parts.
-// Ingest (stream s): the OOB filter, compaction and the pixel sort -- it reads
-// only the batch's own events, so it may run ahead of the previous batch's
-// window pass.  Returns where the sorted pairs are.
+// Ingest (stream s): the OOB filter, compaction, the pixel sort and (filter
+// ON) segments and links -- it reads the batch's own events and the previous
+// batch's links, never the previous window pass, so it may run ahead of it.
+// Returns where the sorted pairs are.
 int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
-                   cudaEvent_t used_ev, int par, cudaStream_t s, int &where) {
+                   cudaEvent_t used_ev, int par, cudaStream_t s, int &where, const long long *n_dev = nullptr) {
   Launcher &L = g->L;
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
   Ctx x = g->ctx(nullptr, nullptr, n_raw, par);
   x.raw_x = rx0;
   x.raw_y = ry0;
   x.raw_p = rp0;
+  x.n_raw_dev = n_dev;   // n_raw is then the size class's upper bound
   cudaStream_t s_saved = L.stream;
   L.stream = s;
   fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
   scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
   fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw packet may be refilled / freed from here on
+  fibar_launch(L, "ingest_end", k_ingest_end, 1, 1, 0, s, x);
   where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
                            g->key_bits);
+  if (g->spatial) {
+    // segments and links: they read the previous batch's links (last-touch
+    // tables), never its window pass
+    x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+    const int nb = (int)((n_raw + TPB - 1) / TPB);
+    fibar_launch(L, "seg_marks", k_seg_marks, nb, TPB, 0, s, x);
+    fibar_launch(L, "link", k_link, nb, TPB, 0, s, x);
+  }
   L.stream = s_saved;
   CK(cudaGetLastError());
   return 0;
 }
 
 // The rest (stream s, after the previous batch's front end): the batch opens
-// against the window state, then (filter ON) segments, links, the window pass,
-// the stale items and the per-position info.  Returns the batch context in x.
+// against the window state, then (filter ON) the window pass, the stale items
+// and the per-position info.  Returns the batch context in x.
 int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s, Ctx &x) {
   Launcher &L = g->L;
   x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
@@ -399,8 +422,6 @@ int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStr
   fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);
   if (g->spatial) {
     const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
-    fibar_launch(L, "seg_marks", k_seg_marks, nb, TPB, 0, s, x);
-    fibar_launch(L, "link", k_link, nb, TPB, 0, s, x);
     fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
     fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, g->anc, NCAND);
@@ -433,45 +454,61 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   return rc;
 }
 
-// A captured part of the front end for (n_raw, par): kind 1 the ingest
-// (reading the fixed input buffers gx/gy/gp), kind 2 the window part (given
-// where the ingest graph leaves the sorted pairs).  Captured on first use
-// (nullptr on failure).
-GraphEntry *front_graph(fibar_engine *g, int kind, long long n_raw, int par, int where) {
+// The captured front end for a size class (n_raw: the class's upper bound)
+// and a parity, as two graphs: exec the ingest (reading the fixed input
+// buffers gx/gy/gp and the batch's raw count that k_stage leaves in the
+// batch state), exec2 the window part.  Every kernel reads the batch's real
+// counts from device memory, so one capture serves the whole class.  One
+// cache entry holds both graphs, so evicting an entry never splits a pair.
+// Captured on first use (nullptr on failure).
+GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   for (auto &ge : g->graphs)
-    if (ge.kind == kind && ge.n == n_raw && ge.par == par) return &ge;
-  if (g->graphs.size() >= 32) {   // small cache: drop the oldest
+    if (ge.kind == 1 && ge.n == n_raw && ge.par == par) return &ge;
+  if (g->graphs.size() >= 16) {   // small cache: drop the oldest (freed once its launches finish)
     cudaGraphExecDestroy(g->graphs.front().exec);
+    if (g->graphs.front().exec2) cudaGraphExecDestroy(g->graphs.front().exec2);
     g->graphs.erase(g->graphs.begin());
   }
   if (!g->capstream && cudaStreamCreateWithFlags(&g->capstream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
   Launcher &L = g->L;
-  const long long l0 = L.launches;
   cudaStream_t s0 = L.stream;
-  cudaGraph_t graph = nullptr;
   GraphEntry ge;
-  ge.where = where;
-  Ctx x{};
-  if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
-  }
-  L.stream = g->capstream;
-  const int rc = kind == 1 ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where)
-                           : enqueue_window(g, n_raw, par, where, g->capstream, x);
-  L.stream = s0;
-  cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
   ge.n = n_raw;
-  ge.kind = kind;
+  ge.kind = 1;
   ge.par = par;
-  ge.kernels = L.launches - l0;
-  L.launches = l0;
-  if (rc == 0 && ce == cudaSuccess) ce = cudaGraphInstantiate(&ge.exec, graph, 0);
-  if (graph) cudaGraphDestroy(graph);
-  if (rc || ce != cudaSuccess) {
-    cudaGetLastError();
-    g->graphs_on = false;   // capture impossible here: stream every kernel from now on
-    return nullptr;
+  for (int part = 0; part < 2; ++part) {
+    const long long l0 = L.launches;
+    cudaGraph_t graph = nullptr;
+    Ctx x{};
+    if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      cudaGetLastError();
+      if (ge.exec) cudaGraphExecDestroy(ge.exec);
+      return nullptr;
+    }
+    L.stream = g->capstream;
+    const int rc = part == 0 ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where,
+                                              &g->bsd[par].n_raw)
+                             : enqueue_window(g, n_raw, par, ge.where, g->capstream, x);
+    L.stream = s0;
+    cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
+    cudaGraphExec_t exec = nullptr;
+    if (rc == 0 && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    const long long k = L.launches - l0;
+    L.launches = l0;
+    if (rc || ce != cudaSuccess) {
+      cudaGetLastError();
+      if (ge.exec) cudaGraphExecDestroy(ge.exec);
+      g->graphs_on = false;   // capture impossible here: stream every kernel from now on
+      return nullptr;
+    }
+    if (part == 0) {
+      ge.exec = exec;
+      ge.kernels = k;
+    } else {
+      ge.exec2 = exec;
+      ge.kernels2 = k;
+    }
   }
   g->graphs.push_back(ge);
   return &g->graphs.back();
@@ -505,24 +542,24 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     if (g->b_used[par]) CK(cudaStreamWaitEvent(sa, g->evB[par], 0));   // this parity's buffers are free
     const bool small = g->graphs_on && !L.prof && n_raw <= g->graph_max;
     if (small) {
-      // a small batch: each part replays one CUDA graph per (size, parity),
-      // the ingest from fixed input buffers
-      CK(cudaMemcpyAsync(g->gx, rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, sa));
-      CK(cudaMemcpyAsync(g->gy, ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, sa));
-      CK(cudaMemcpyAsync(g->gp, rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, sa));
+      // a small batch: each part replays one CUDA graph per (size class,
+      // parity), the ingest from fixed input buffers (k_stage fills them and
+      // the batch's raw count)
+      const long long cls = std::min(g->graph_max, (n_raw + GRAPH_CLASS - 1) / GRAPH_CLASS * GRAPH_CLASS);
+      const int nbs = (int)std::max(1LL, std::min((long long)g->nsm * 2, (n_raw / 8 + TPB - 1) / TPB));
+      fibar_launch(L, "stage", k_stage, nbs, TPB, 0, sa, rx0, ry0, rp0, (long long)n_raw, g->gx, g->gy, g->gp,
+                   &g->bsd[par].n_raw);
       CK(cudaEventRecord(g->evCp, sa));
       if (used_ev) CK(cudaEventRecord(used_ev, sa));
-      GraphEntry *gi = front_graph(g, 1, n_raw, par, 0);
-      if (!gi) return g_err.empty() ? fail(FIBAR_E_CUDA, "front-end graph capture failed") : FIBAR_E_CUDA;
-      where = gi->where;
-      GraphEntry *gw = front_graph(g, 2, n_raw, par, where);
-      if (!gw) return g_err.empty() ? fail(FIBAR_E_CUDA, "front-end graph capture failed") : FIBAR_E_CUDA;
-      CK(cudaGraphLaunch(gi->exec, sa));
-      L.launches += gi->kernels;
+      const GraphEntry *ge = front_graph(g, cls, par);
+      if (!ge) return g_err.empty() ? fail(FIBAR_E_CUDA, "front-end graph capture failed") : FIBAR_E_CUDA;
+      where = ge->where;
+      CK(cudaGraphLaunch(ge->exec, sa));
+      L.launches += ge->kernels;
       CK(cudaEventRecord(g->evA[par], sa));
       CK(cudaStreamWaitEvent(s, g->evA[par], 0));
-      CK(cudaGraphLaunch(gw->exec, s));
-      L.launches += gw->kernels;
+      CK(cudaGraphLaunch(ge->exec2, s));
+      L.launches += ge->kernels2;
       x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
       x.raw_x = g->gx;
       x.raw_y = g->gy;
@@ -656,10 +693,11 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
   GraphEntry *hit = nullptr;
   for (auto &ge : g->graphs)
-    if (ge.n == n_raw) hit = &ge;
+    if (ge.kind == 0 && ge.n == n_raw) hit = &ge;
   if (!hit) {
     if (g->graphs.size() >= 8) {   // small cache: drop the oldest size
       cudaGraphExecDestroy(g->graphs.front().exec);
+      if (g->graphs.front().exec2) cudaGraphExecDestroy(g->graphs.front().exec2);
       g->graphs.erase(g->graphs.begin());
     }
     // captured on a private stream (the caller's may be the legacy default
@@ -736,8 +774,43 @@ int launch_host_batch(fibar_engine *g) {
   return run_batch_raw(g, g->sx[c], g->sy[c], g->sp_[c], n, g->ev_used[c]);
 }
 
-// run everything pending (zero-copy device range, then staged host packets)
+// gather the pending device packets into staging set `cur` and run them
+int flush_gather(fibar_engine *g) {
+  if (g->dfill == 0) return 0;
+  const int c = g->cur;
+  const long long n = g->dfill;
+  Launcher &L = g->L;
+  CK(cudaStreamWaitEvent(L.stream, g->ev_used[c], 0));   // the staging set's previous batch has read it
+  fibar_launch(L, "gather", k_gather, g->gt.n, TPB, 0, L.stream, g->gt, g->sx[c], g->sy[c], g->sp_[c]);
+  g->gt.n = 0;
+  g->dfill = 0;
+  g->cur ^= 1;
+  return run_batch_raw(g, g->sx[c], g->sy[c], g->sp_[c], n, g->ev_used[c]);
+}
+
+// add a device packet (part) to the gather table
+int gather_add(fibar_engine *g, const uint16_t *x, const uint16_t *y, const int8_t *p, long long n) {
+  GatherTable &t = g->gt;
+  if (t.n > 0) {   // contiguous with the previous entry: extend it
+    GatherEntry &e = t.e[t.n - 1];
+    if (x == e.x + e.n && y == e.y + e.n && p == e.p + e.n) {
+      e.n += n;
+      g->dfill += n;
+      return 0;
+    }
+  }
+  t.e[t.n++] = GatherEntry{x, y, p, n, g->dfill};
+  g->dfill += n;
+  return 0;
+}
+
+// run everything pending (zero-copy device range or gathered device packets,
+// then staged host packets)
 int run_batch(fibar_engine *g) {
+  if (g->dfill > 0) {
+    int rc = flush_gather(g);
+    if (rc) return rc;
+  }
   if (g->zn > 0) {
     const long long n = g->zn;
     g->zn = 0;
@@ -978,7 +1051,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     const double steps = (r > 0.0 && r < 1.0) ? 24.0 * std::log(2.0) / -std::log(r) : 1024.0;
     g->twarm = (int)std::min(2048.0, std::max(64.0, std::ceil(1.6 * steps)));
   }
-  g->R = 1LL << ceil_log2(n + 1 + g->Bcap);
+  // the window plus two batches (the next batch's ingest writes its ring keys
+  // while this batch's window pass still reads)
+  g->R = 1LL << ceil_log2(n + 1 + 2 * g->Bcap);
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1079,10 +1154,12 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     cudaStreamCreateWithFlags(&g->astream, cudaStreamNonBlocking);
     cudaStreamCreateWithFlags(&g->fstream, cudaStreamNonBlocking);
     rc |= dalloc(&g->last_tile, g->n_tiles);
-    rc |= dalloc(&g->ptt, g->n_tiles);
+    rc |= dalloc(&g->ptt2[0], g->n_tiles);
+    rc |= dalloc(&g->ptt2[1], g->n_tiles);
     rc |= dalloc(&g->rkey, g->R);
     rc |= dalloc(&g->rnext, g->R);
-    rc |= dalloc(&g->dp, Bc);
+    rc |= dalloc(&g->dp2[0], Bc);
+    rc |= dalloc(&g->dp2[1], Bc);
     rc |= dalloc(&g->S, Bc);
     rc |= dalloc(&g->Qt, Bc);
     rc |= dalloc(&g->pmap, npop_cap);
@@ -1128,9 +1205,9 @@ int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
   for (cudaStream_t st : {g->astream, g->fstream, g->bstream})
     if (st) cudaStreamSynchronize(st);
-  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt, g->rkey, g->rnext, g->raw_x,
+  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt2[0], g->ptt2[1], g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->epol2[0], g->epol2[1], g->spol2[0], g->spol2[1], g->longseg, g->hist,
-                  g->dp, g->S, g->Qt, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
+                  g->dp2[0], g->dp2[1], g->S, g->Qt, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1152,7 +1229,10 @@ int fibar_destroy(fibar_engine *g) {
     if (g->evB[c]) cudaEventDestroy(g->evB[c]);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
-  for (auto &ge : g->graphs) cudaGraphExecDestroy(ge.exec);
+  for (auto &ge : g->graphs) {
+    cudaGraphExecDestroy(ge.exec);
+    if (ge.exec2) cudaGraphExecDestroy(ge.exec2);
+  }
   if (g->capstream) cudaStreamDestroy(g->capstream);
   for (void *q : {(void *)g->gx, (void *)g->gy, (void *)g->gp})
     if (q) cudaFree(q);
@@ -1196,11 +1276,23 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
       if (rc) return rc;
     }
     while (off < n) {
-      if (g->zn > 0 && !(x + off == g->zx + g->zn && y + off == g->zy + g->zn && p + off == g->zp + g->zn)) {
+      const bool contiguous = g->zn > 0 && x + off == g->zx + g->zn && y + off == g->zy + g->zn && p + off == g->zp + g->zn;
+      if (g->zn > 0 && !contiguous) {
+        // a packet elsewhere in memory: the pending in-place range and what
+        // follows are gathered into the device staging set instead
         const long long zn = g->zn;
         g->zn = 0;
-        int rc = run_batch_raw(g, g->zx, g->zy, g->zp, zn, nullptr);
-        if (rc) return rc;
+        gather_add(g, g->zx, g->zy, g->zp, zn);
+      }
+      if (g->dfill > 0) {
+        const long long take = std::min((long long)n - off, g->Bcap - g->dfill);
+        gather_add(g, x + off, y + off, p + off, take);
+        off += take;
+        if (g->dfill == g->Bcap || g->gt.n == GATHER_MAX) {
+          int rc = flush_gather(g);
+          if (rc) return rc;
+        }
+        continue;
       }
       if (g->zn == 0) {
         g->zx = x + off;
@@ -1219,7 +1311,7 @@ int fibar_process(fibar_engine *g, const uint16_t *x, const uint16_t *y, const i
     }
     return 0;
   }
-  if (g->zn > 0) {
+  if (g->zn > 0 || g->dfill > 0) {
     int rc = run_batch(g);
     if (rc) return rc;
   }
@@ -1334,7 +1426,7 @@ int fibar_flush(fibar_engine *g) {
 
 int fibar_pending(fibar_engine *g, int64_t *device_events, int64_t *staged_events) {
   if (!g) return fail(FIBAR_E_CONFIG, "null engine");
-  if (device_events) *device_events = g->zn;
+  if (device_events) *device_events = g->zn + g->dfill;   // device packets still read from where they are
   if (staged_events) *staged_events = g->hfill;
   return 0;
 }

@@ -23,10 +23,12 @@ __device__ __forceinline__ bool in_band(const Ctx &x, unsigned yy) { return yy -
 // a thread's IN_ITEMS consecutive packet entries: one 16-byte load per
 // coordinate column and one 8-byte load of polarities when the packet is
 // aligned (lanes take consecutive 16-byte pieces: coalesced), else scalar
-__device__ __forceinline__ void load_in(const Ctx &x, long long base, unsigned (&xx)[IN_ITEMS],
+__device__ __forceinline__ long long raw_count(const Ctx &x) { return x.n_raw_dev ? *x.n_raw_dev : x.n_raw; }
+
+__device__ __forceinline__ void load_in(const Ctx &x, long long n_raw, long long base, unsigned (&xx)[IN_ITEMS],
                                         unsigned (&yy)[IN_ITEMS], int (&pp)[IN_ITEMS], bool with_p) {
   static_assert(IN_ITEMS == 8, "vector ingest assumes 8 entries per thread");
-  const bool vec = base + IN_ITEMS <= x.n_raw && ((reinterpret_cast<uintptr_t>(x.raw_x + base) |
+  const bool vec = base + IN_ITEMS <= n_raw && ((reinterpret_cast<uintptr_t>(x.raw_x + base) |
                                                    reinterpret_cast<uintptr_t>(x.raw_y + base)) & 15) == 0 &&
                    (!with_p || (reinterpret_cast<uintptr_t>(x.raw_p + base) & 7) == 0);
   if (vec) {
@@ -53,7 +55,7 @@ __device__ __forceinline__ void load_in(const Ctx &x, long long base, unsigned (
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
     const long long i = base + r;
-    const bool in = i < x.n_raw;
+    const bool in = i < n_raw;
     xx[r] = in ? x.raw_x[i] : 0xFFFFu;   // off the sensor: never kept
     yy[r] = in ? x.raw_y[i] : 0xFFFFu;
     if (with_p) pp[r] = in ? x.raw_p[i] : 0;
@@ -65,12 +67,13 @@ __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
   __shared__ unsigned wsum[TPB / 32], woob[TPB / 32];
   const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
   unsigned cnt = 0, oob = 0;
+  const long long n_raw = raw_count(x);
   unsigned xs[IN_ITEMS], ys[IN_ITEMS];
   int ps[IN_ITEMS];
-  load_in(x, base, xs, ys, ps, false);
+  load_in(x, n_raw, base, xs, ys, ps, false);
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
-    if (base + r < x.n_raw) {
+    if (base + r < n_raw) {
       const bool ok = on_sensor(x, xs[r], ys[r]);
       oob += !ok;
       cnt += ok && in_band(x, ys[r]);
@@ -102,12 +105,13 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   const long long base = (long long)blockIdx.x * IN_TILE + threadIdx.x * IN_ITEMS;
   bool keep[IN_ITEMS];
   unsigned cnt = 0;
+  const long long n_raw = raw_count(x);
   unsigned xs[IN_ITEMS], ys[IN_ITEMS];
   int ps[IN_ITEMS];
-  load_in(x, base, xs, ys, ps, true);
+  load_in(x, n_raw, base, xs, ys, ps, true);
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
-    keep[r] = base + r < x.n_raw && on_sensor(x, xs[r], ys[r]) && in_band(x, ys[r]);
+    keep[r] = base + r < n_raw && on_sensor(x, xs[r], ys[r]) && in_band(x, ys[r]);
     cnt += keep[r];
   }
   unsigned incl = cnt;
@@ -152,13 +156,75 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   }
 }
 
-// Opens the batch against the engine state the previous batch left: its first
-// event index, the window start and a fresh blur epoch.
+// A small batch's packet into the fixed input buffers its captured ingest
+// graph reads, with the batch's raw count (graphs are captured per size class,
+// sized for the class's upper bound, and read the real count here).
+__global__ void __launch_bounds__(TPB) k_stage(const uint16_t *sx, const uint16_t *sy, const int8_t *sp, long long n,
+                                               uint16_t *dx, uint16_t *dy, int8_t *dp, long long *n_dev) {
+  pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n;
+  const bool vec = ((reinterpret_cast<uintptr_t>(sx) | reinterpret_cast<uintptr_t>(sy)) & 15) == 0 &&
+                   (reinterpret_cast<uintptr_t>(sp) & 7) == 0;
+  const long long stride = (long long)gridDim.x * TPB;
+  long long i0 = 0;
+  if (vec) {
+    const long long nv = n / 8;
+    for (long long v = (long long)blockIdx.x * TPB + threadIdx.x; v < nv; v += stride) {
+      reinterpret_cast<uint4 *>(dx)[v] = reinterpret_cast<const uint4 *>(sx)[v];
+      reinterpret_cast<uint4 *>(dy)[v] = reinterpret_cast<const uint4 *>(sy)[v];
+      reinterpret_cast<uint2 *>(dp)[v] = reinterpret_cast<const uint2 *>(sp)[v];
+    }
+    i0 = nv * 8;
+  }
+  for (long long i = i0 + (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += stride) {
+    dx[i] = sx[i];
+    dy[i] = sy[i];
+    dp[i] = sp[i];
+  }
+}
+
+// Non-contiguous device packets into the device staging set: one CTA per
+// packet (grid-stride within it), 16-byte vector copies when the source and
+// destination line up, element copies otherwise.
+__global__ void __launch_bounds__(TPB) k_gather(const GatherTable tab, uint16_t *dx, uint16_t *dy, int8_t *dp) {
+  pdl_wait();
+  const GatherEntry e = tab.e[blockIdx.x];
+  const bool vec = ((reinterpret_cast<uintptr_t>(e.x) | reinterpret_cast<uintptr_t>(e.y) |
+                     reinterpret_cast<uintptr_t>(dx + e.dst) | reinterpret_cast<uintptr_t>(dy + e.dst)) & 15) == 0 &&
+                   ((reinterpret_cast<uintptr_t>(e.p) | reinterpret_cast<uintptr_t>(dp + e.dst)) & 7) == 0;
+  long long i0 = 0;
+  if (vec) {
+    const long long nv = e.n / 8;   // 8 events: 16 B of x, 16 B of y, 8 B of p
+    for (long long v = threadIdx.x; v < nv; v += TPB) {
+      reinterpret_cast<uint4 *>(dx + e.dst)[v] = reinterpret_cast<const uint4 *>(e.x)[v];
+      reinterpret_cast<uint4 *>(dy + e.dst)[v] = reinterpret_cast<const uint4 *>(e.y)[v];
+      reinterpret_cast<uint2 *>(dp + e.dst)[v] = reinterpret_cast<const uint2 *>(e.p)[v];
+    }
+    i0 = nv * 8;
+  }
+  for (long long i = i0 + threadIdx.x; i < e.n; i += TPB) {
+    dx[e.dst + i] = e.x[i];
+    dy[e.dst + i] = e.y[i];
+    dp[e.dst + i] = e.p[i];
+  }
+}
+
+// The batch's first event index, from the ingest's own running count (so the
+// ingest, segments and links may run ahead of the previous window pass).
+__global__ void k_ingest_end(Ctx x) {
+  pdl_wait();
+  DevState *s = x.st;
+  BatchState *b = x.bs;
+  b->E0 = s->Ein;
+  s->Ein += b->B;
+}
+
+// Opens the batch's window part against the state the previous batch left:
+// the window start and a fresh blur epoch.
 __global__ void k_batch_begin(Ctx x) {
   pdl_wait();
   DevState *s = x.st;
   BatchState *b = x.bs;
-  b->E0 = s->E;
   b->s_start = s->s;
   s->epoch += 1;
   b->epoch = s->epoch;
@@ -269,9 +335,10 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
     // reach the cap if wcnt + seglen > 65535 -- flag that (never misses).
     const unsigned pend = x.pt[c].end;
     const unsigned seglen = pend - (unsigned)i;
-    const unsigned wc = x.wcnt[c];
+    // (atomic: the previous batch's eviction pass may be subtracting meanwhile;
+    // a count not yet decremented only makes the check more conservative)
+    const unsigned wc = atomicAdd(&x.wcnt[c], seglen);
     if ((unsigned long long)wc + seglen > 65535ull) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);
-    x.wcnt[c] = wc + seglen;
     // the pixel's last-touch for the next batch (read above by this thread
     // alone), so the next front end never waits for this batch's replay
     x.plast[c] = E0 + x.sidx[pend - 1];

@@ -47,6 +47,19 @@ struct VRec {
 constexpr int VF_TPB = 256;   // k_window_verify: threads per CTA (one warp per re-run)
 constexpr int VF_CTAS = 16;   // k_window_verify: CTAs in its one cluster (non-portable size)
 
+// device packets gathered into the device staging set (non-contiguous
+// packets coalesced into one batch): the table travels as a kernel parameter
+constexpr int GATHER_MAX = 256;
+struct GatherEntry {
+  const uint16_t *x, *y;
+  const int8_t *p;
+  long long n, dst;
+};
+struct GatherTable {
+  int n;
+  GatherEntry e[GATHER_MAX];
+};
+
 struct ChunkRec {
   long long st_s, st_q;                          // state after event b_c - 1 (speculative start)
   long long en_s, en_q, en_np, en_nt, en_ev;     // state after the chunk's last event
@@ -95,7 +108,8 @@ struct Ctx {
   unsigned long long Rm;
   const uint16_t *raw_x, *raw_y;
   const int8_t *raw_p;
-  long long n_raw;
+  long long n_raw;                // raw events (an upper bound when n_raw_dev is set)
+  const long long *n_raw_dev;     // the batch's raw event count in device memory, or null
   unsigned *blockcnt;
   unsigned *ekey;
   int8_t *epol, *spol;
@@ -159,6 +173,10 @@ __device__ __forceinline__ float order_unkey(unsigned k) {
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks);
 __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
 __global__ void k_batch_begin(Ctx x);
+__global__ void k_ingest_end(Ctx x);
+__global__ void __launch_bounds__(TPB) k_stage(const uint16_t *sx, const uint16_t *sy, const int8_t *sp, long long n,
+                                               uint16_t *dx, uint16_t *dy, int8_t *dp, long long *n_dev);
+__global__ void __launch_bounds__(TPB) k_gather(const GatherTable tab, uint16_t *dx, uint16_t *dy, int8_t *dp);
 __global__ void __launch_bounds__(TPB) k_seg_marks(Ctx x);
 __global__ void __launch_bounds__(TPB) k_link(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x);

@@ -322,3 +322,58 @@ def test_small_packets_720p_frame_by_frame():
     want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
                 qx=ref.qx, qy=ref.qy, qs=ref.qs)
     assert_state(eng, want, "720p 1k packets")
+
+
+def test_separate_device_packets_are_gathered():
+    """Device packets in separate allocations (a real device stream) are
+    gathered into device batches (k_gather) instead of running one batch per
+    packet, mixed with contiguous views and host packets; state stays exact."""
+    import torch
+    from paper_2510_20071_b200.pipeline import DeviceEventArray, ReconstructionEngine
+    geom, params, ev, ref = _oracle_stream("texture_noise_hot", 320, 240, 400_000, 400_000, True, seed=13)
+    eng = ReconstructionEngine(geom, params, batch_capacity=1 << 17)
+    b0 = eng.stats()["batches"]
+    keep = []
+    cuts = list(range(0, 300_000, 7_500)) + [300_000]
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        cols = [torch.from_numpy(ev.x[a:b].view(np.int16)).cuda(), torch.from_numpy(ev.y[a:b].view(np.int16)).cuda(),
+                torch.from_numpy(ev.p[a:b].copy()).cuda()]
+        keep.append(cols)   # separate allocations, so never address-contiguous
+        eng.process_array(DeviceEventArray(*cols))
+    big = [torch.from_numpy(ev.x[300_000:].view(np.int16)).cuda(), torch.from_numpy(ev.y[300_000:].view(np.int16)).cuda(),
+           torch.from_numpy(ev.p[300_000:].copy()).cuda()]
+    for a in range(0, 60_000, 20_000):   # contiguous views of one buffer, then a host packet
+        eng.process_array(DeviceEventArray(big[0][a:a + 20_000], big[1][a:a + 20_000], big[2][a:a + 20_000]))
+    eng.process_array(ev.slice(360_000, 400_000))
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, "gathered device packets")
+    assert eng.stats()["batches"] - b0 <= 6   # 400k events in 128k-event batches, not one per packet
+
+
+def test_many_batch_sizes_cycle_the_graph_cache():
+    """Small batches of 40 distinct sizes (more than the front-end graph cache
+    holds): captures, evictions and replays of the two-part front end, with a
+    read-out after every batch; state and frames stay oracle-exact."""
+    from oracle import oracle as orc
+    from paper_2510_20071_b200 import workloads
+    from paper_2510_20071_b200.core import SensorGeometry, compute_params
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    geom = SensorGeometry(160, 120)
+    ev = workloads.make("texture_noise_hot", geom, 240_000, seed=17)
+    params = compute_params(40.0, Fraction(1, 2), geom)
+    eng = ReconstructionEngine(geom, params)
+    ref = orc.OracleEngine(160, 120, params)
+    a = 0
+    for k in range(40):
+        b = min(len(ev), a + 3000 + 37 * k)
+        blk = ev.slice(a, b)
+        eng.process_array(blk)
+        ref.process_array(blk.t, blk.x, blk.y, blk.p)
+        af = eng.render_async("robust")
+        px, _, _ = ref.render("robust")
+        assert np.array_equal(af.frame().pixels, px), k
+        a = b
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, "graph cache cycling")
