@@ -73,6 +73,8 @@ struct BatchState {
   unsigned vcnt[3];    // k_window_verify: chunks listed for a round (rotating by round)
   unsigned vpad;
   long long n_raw;     // raw events of the batch, set by k_stage (graphs are captured per size class)
+  unsigned nclosed;    // k_posinfo blocks done (the last one closes the batch)
+  unsigned npad;
 };
 
 // Window / counter state living in device memory so no kernel needs a host

@@ -109,6 +109,10 @@ int ceil_log2(long long v) {
 
 }  // namespace
 
+// buffer sets for batches in flight (ingest of k+2 may run while k's window
+// part and k-1's blur stage run), indexed by batch % NPAR
+constexpr int NPAR = 3;
+
 // small batches' front-end graphs are captured per size class of this many events
 constexpr long long GRAPH_CLASS = 16384;
 
@@ -136,38 +140,37 @@ struct fibar_engine {
   bool spatial = true, blur_on = true, use_gain = false;
   DevState *st = nullptr;
   float *pbar = nullptr, *l = nullptr, *gain = nullptr;
-  PixRec *pt2[2] = {nullptr, nullptr};
+  PixRec *pt2[NPAR] = {};
   long long *plast = nullptr;
   unsigned *wcnt = nullptr;
-  BatchState *bsd = nullptr;   // [2]
+  BatchState *bsd = nullptr;   // [NPAR]
   long long *last_tile = nullptr;
-  uint2 *ptt2[2] = {nullptr, nullptr};   // tile segments, per batch parity
+  uint2 *ptt2[NPAR] = {};   // tile segments, per batch parity
   unsigned *rkey = nullptr;
   uint2 *rnext = nullptr;
   uint16_t *raw_x = nullptr, *raw_y = nullptr;
   int8_t *raw_p = nullptr;
   unsigned *blockcnt = nullptr;
-  unsigned *ekey2[2] = {nullptr, nullptr};
+  unsigned *ekey2[NPAR] = {};
   // polarities in stream order (per batch parity: the next batch's ingest may
   // run while this one's front end reads them) and in pixel-sorted order (per
   // parity: the temporal replay on the blur stream reads them while the next
   // front end writes its own)
-  int8_t *epol2[2] = {nullptr, nullptr}, *spol2[2] = {nullptr, nullptr};
+  int8_t *epol2[NPAR] = {}, *spol2[NPAR] = {};
   uint2 *longseg = nullptr;
-  unsigned *ka2[2] = {nullptr, nullptr}, *va2[2] = {nullptr, nullptr}, *kb2[2] = {nullptr, nullptr},
-           *vb2[2] = {nullptr, nullptr}, *hist = nullptr;
-  uint2 *dp2[2] = {nullptr, nullptr};    // per-event link distances, per batch parity
+  unsigned *ka2[NPAR] = {}, *va2[NPAR] = {}, *kb2[NPAR] = {}, *vb2[NPAR] = {}, *hist = nullptr;
+  uint2 *dp2[NPAR] = {};    // per-event link distances, per batch parity
   unsigned *S = nullptr, *Qt = nullptr;
   unsigned *pmap = nullptr;
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
   BlurPrep *prep = nullptr;            // = prep2[0] (debug reads)
-  BlurPrep *prep2[2] = {nullptr, nullptr};   // per batch parity: k_popj of batch k+1 writes while batch k blurs
+  BlurPrep *prep2[NPAR] = {};   // per batch parity: k_popj of batch k+1 writes while batch k blurs
   // carried-only stale items, per batch parity: k_popj of batch k+2 may run
   // while batch k+1's tap resolution still reads its list
-  unsigned *colist2[2] = {nullptr, nullptr};
-  Item *item2[2] = {nullptr, nullptr};
-  PosRec *posrec2[2] = {nullptr, nullptr};
-  float *t2_2[2] = {nullptr, nullptr};
+  unsigned *colist2[NPAR] = {};
+  Item *item2[NPAR] = {};
+  PosRec *posrec2[NPAR] = {};
+  float *t2_2[NPAR] = {};
   int2 *anc = nullptr, *anc2 = nullptr, *anc0 = nullptr;
   long long *lc = nullptr, *lu = nullptr;
   ChunkRec *ch = nullptr;
@@ -207,7 +210,7 @@ struct fibar_engine {
   // streamed filter-ON batches: the front end's ingest + sort (astream) and
   // window part (fstream), so batch k+1's ingest overlaps batch k's window pass
   cudaStream_t astream = nullptr, fstream = nullptr;
-  cudaEvent_t evIn = nullptr, evCp = nullptr, evA[2] = {nullptr, nullptr};
+  cudaEvent_t evIn = nullptr, evCp = nullptr, evA[NPAR] = {};
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
@@ -222,10 +225,10 @@ struct fibar_engine {
   uint16_t *gx = nullptr, *gy = nullptr;
   int8_t *gp = nullptr;
   int blur_grid_serial = 148;
-  cudaEvent_t evF[2] = {nullptr, nullptr}, evB[2] = {nullptr, nullptr};
+  cudaEvent_t evF[NPAR] = {}, evB[NPAR] = {};
   int last_b = -1;   // parity of the newest batch with a blur stage in flight
   int last_par = -1;  // parity of the newest batch (fibar_debug_stale_items)
-  bool b_used[2] = {false, false};
+  bool b_used[NPAR] = {};
   int nsm = 148;
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
@@ -355,12 +358,12 @@ int init_state(fibar_engine *g) {
   cudaStream_t s = g->L.stream;
   join_blur(g);
   g->last_b = -1;
-  g->b_used[0] = g->b_used[1] = false;
+  for (bool &u : g->b_used) u = false;
   fibar_launch(g->L, "init", k_init_state, 1, 1, 0, s, g->st, g->q0);
   CK(cudaMemsetAsync(g->pbar, 0, sizeof(float) * g->n_pix, s));
   CK(cudaMemsetAsync(g->l, 0, sizeof(float) * g->n_pix, s));
   if (g->spatial) {
-    fibar_launch(g->L, "init", k_init_pt, g->nsm * 4, TPB, 0, s, g->pt2[0], g->pt2[1], g->plast, g->n_pix);
+    for (int c = 0; c < NPAR; ++c) fibar_launch(g->L, "init", k_init_pt, g->nsm * 4, TPB, 0, s, g->pt2[c], g->plast, g->n_pix);
     fibar_launch(g->L, "init", k_fill_ll, g->nsm * 4, TPB, 0, s, g->last_tile, g->n_tiles, -1);
     CK(cudaMemsetAsync(g->rkey, 0, sizeof(unsigned) * g->R, s));
     CK(cudaMemsetAsync(g->wcnt, 0, sizeof(unsigned) * g->n_pix, s));
@@ -419,13 +422,12 @@ int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStr
   Launcher &L = g->L;
   x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
   const int nb = (int)((n_raw + TPB - 1) / TPB);
-  fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);
+  if (!g->spatial) fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);   // (filter ON: in k_anchor)
   if (g->spatial) {
     const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
     fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
     fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, g->anc, NCAND);
-    fibar_launch(L, "fp", k_fp, (T + TPB - 1) / TPB, TPB, 0, s, x);
     fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
     fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
     fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
@@ -433,7 +435,7 @@ int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStr
     fibar_launch_cluster(L, "window_verify", k_window_verify, VF_CTAS, VF_TPB, 0, s, x);
     fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
     fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
-    fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
+    fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x, 1);   // its last block closes the batch
   }
   CK(cudaGetLastError());
   return 0;
@@ -587,12 +589,11 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     if (rc) return rc;
   }
   if (g->spatial) {
-    // The batch's counters (event count, stale count, candidate set) close on
-    // the front end's stream: the next front end reads them.  Its links read
-    // the last-touch tables, which k_link already advanced; so the next front
-    // end never waits for this batch's temporal replay or blur stage (only,
-    // two batches on, for the buffers of its parity).
-    fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
+    // The batch's counters (event count, stale count, candidate set) closed
+    // at the end of the window part (k_posinfo): the next front end reads
+    // them.  Its links read the last-touch tables, which k_link already
+    // advanced; so the next front end never waits for this batch's temporal
+    // replay or blur stage (only, two batches on, for its parity's buffers).
     // The temporal replay reads the brightness the previous batch's blur
     // stage finishes.  Streamed (temporal_on_blur): it runs first on the blur
     // stream itself, so the cycle blur(k) -> final(k) -> replay(k+1) ->
@@ -657,7 +658,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       g->last_b = par;
     }
   } else {
-    fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x);
+    fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x, 0);
     fibar_launch(L, "temporal", k_temporal, nb, TPB, 0, s, x);
     fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
     fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
@@ -677,7 +678,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   Launcher &L = g->L;
   cudaStream_t s = L.stream;
   if (!g->graphs_on || L.prof || n_raw > g->graph_max || !g->full_graphs) {
-    const int par = g->spatial ? (int)(g->batches & 1) : 0;
+    const int par = g->spatial ? (int)(g->batches % NPAR) : 0;
     int rc = enqueue_batch(g, rx0, ry0, rp0, n_raw, used_ev, par, false);
     if (rc) return rc;
     g->batches++;
@@ -686,7 +687,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   // graph form: after every earlier blur stage (it reuses parity-0 buffers)
   join_blur(g);
   g->last_b = -1;
-  g->b_used[0] = g->b_used[1] = false;
+  for (bool &u : g->b_used) u = false;
   CK(cudaMemcpyAsync(g->gx, rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
   CK(cudaMemcpyAsync(g->gy, ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
   CK(cudaMemcpyAsync(g->gp, rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, s));
@@ -1051,9 +1052,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     const double steps = (r > 0.0 && r < 1.0) ? 24.0 * std::log(2.0) / -std::log(r) : 1024.0;
     g->twarm = (int)std::min(2048.0, std::max(64.0, std::ceil(1.6 * steps)));
   }
-  // the window plus two batches (the next batch's ingest writes its ring keys
-  // while this batch's window pass still reads)
-  g->R = 1LL << ceil_log2(n + 1 + 2 * g->Bcap);
+  // the window plus NPAR batches (the ingest of later batches writes their
+  // ring keys while this batch's window pass still reads)
+  g->R = 1LL << ceil_log2(n + 1 + NPAR * g->Bcap);
   int dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&g->nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -1100,14 +1101,15 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->gy, g->graph_max);
     rc |= dalloc(&g->gp, g->graph_max);
   }
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < NPAR; ++b) {
+    if (b > 0 && !g->spatial) break;   // filter off: one batch at a time
     rc |= dalloc(&g->epol2[b], Bc);
     rc |= dalloc(&g->spol2[b], Bc);
   }
   rc |= dalloc(&g->longseg, 16384);
-  rc |= dalloc(&g->bsd, 2);
-  if (!rc) cudaMemset(g->bsd, 0, 2 * sizeof(BatchState));
-  for (int c = 0; c < 2; ++c) {
+  rc |= dalloc(&g->bsd, NPAR);
+  if (!rc) cudaMemset(g->bsd, 0, NPAR * sizeof(BatchState));
+  for (int c = 0; c < NPAR; ++c) {
     // the filter-off path runs every batch on one stream: one set suffices
     const bool own = c == 0 || g->spatial;
     if (own) {
@@ -1127,7 +1129,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     if (!rc) cudaMemcpy(g->gain, cfg->gain, sizeof(float) * n, cudaMemcpyHostToDevice);
   }
   if (g->spatial) {
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < NPAR; ++c) {
       rc |= dalloc(&g->pt2[c], n);
       rc |= dalloc(&g->item2[c], npop_cap);
       rc |= dalloc(&g->t2_2[c], Bc);
@@ -1144,32 +1146,38 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       cudaStreamCreateWithPriority(&g->bstream, cudaStreamNonBlocking, hi);
     }
     cudaEventCreateWithFlags(&g->evT, cudaEventDisableTiming);
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < NPAR; ++c) {
       cudaEventCreateWithFlags(&g->evF[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evB[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evA[c], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&g->evIn, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g->evCp, cudaEventDisableTiming);
-    cudaStreamCreateWithFlags(&g->astream, cudaStreamNonBlocking);
-    cudaStreamCreateWithFlags(&g->fstream, cudaStreamNonBlocking);
+    {
+      // the window part is the critical chain (latency-bound, small grids):
+      // its blocks go first when SM slots free up (FIBAR_FRONT_PRIO=0: off)
+      int lo = 0, hi = 0;
+      cudaDeviceGetStreamPriorityRange(&lo, &hi);
+      int fp = hi;
+      if (const char *v = getenv("FIBAR_FRONT_PRIO")) fp = atoi(v) ? hi : lo;
+      cudaStreamCreateWithPriority(&g->fstream, cudaStreamNonBlocking, fp);
+      cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, lo);
+    }
     rc |= dalloc(&g->last_tile, g->n_tiles);
-    rc |= dalloc(&g->ptt2[0], g->n_tiles);
-    rc |= dalloc(&g->ptt2[1], g->n_tiles);
+    for (int c = 0; c < NPAR; ++c) rc |= dalloc(&g->ptt2[c], g->n_tiles);
     rc |= dalloc(&g->rkey, g->R);
     rc |= dalloc(&g->rnext, g->R);
-    rc |= dalloc(&g->dp2[0], Bc);
-    rc |= dalloc(&g->dp2[1], Bc);
+    for (int c = 0; c < NPAR; ++c) rc |= dalloc(&g->dp2[c], Bc);
     rc |= dalloc(&g->S, Bc);
     rc |= dalloc(&g->Qt, Bc);
     rc |= dalloc(&g->pmap, npop_cap);
     rc |= dalloc(&g->bv64, npop_cap);
     rc |= dalloc(&g->mv64, Bc);
-    rc |= dalloc(&g->prep2[0], npop_cap);
-    rc |= dalloc(&g->prep2[1], npop_cap);
+    for (int c = 0; c < NPAR; ++c) {
+      rc |= dalloc(&g->prep2[c], npop_cap);
+      rc |= dalloc(&g->colist2[c], n + 1);
+    }
     g->prep = g->prep2[0];
-    rc |= dalloc(&g->colist2[0], n + 1);
-    rc |= dalloc(&g->colist2[1], n + 1);
     rc |= dalloc(&g->anc, T * NCAND);
     rc |= dalloc(&g->anc2, T * NFINE);
     rc |= dalloc(&g->anc0, T);
@@ -1205,9 +1213,9 @@ int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
   for (cudaStream_t st : {g->astream, g->fstream, g->bstream})
     if (st) cudaStreamSynchronize(st);
-  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->ptt2[0], g->ptt2[1], g->rkey, g->rnext, g->raw_x,
-                  g->raw_y, g->raw_p, g->blockcnt, g->epol2[0], g->epol2[1], g->spol2[0], g->spol2[1], g->longseg, g->hist,
-                  g->dp2[0], g->dp2[1], g->S, g->Qt, g->pmap, g->bv64, g->mv64, g->prep2[0], g->prep2[1], g->colist2[0], g->colist2[1], g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
+  void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->rkey, g->rnext, g->raw_x,
+                  g->raw_y, g->raw_p, g->blockcnt, g->longseg, g->hist,
+                  g->S, g->Qt, g->pmap, g->bv64, g->mv64, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1221,12 +1229,14 @@ int fibar_destroy(fibar_engine *g) {
     if (g->hp[c]) cudaFreeHost(g->hp[c]);
     if (g->ev_h2d[c]) cudaEventDestroy(g->ev_h2d[c]);
     if (g->ev_used[c]) cudaEventDestroy(g->ev_used[c]);
+  }
+  for (int c = 0; c < NPAR; ++c) {
     void *per[] = {g->pt2[c], g->ekey2[c], g->ka2[c], g->va2[c], g->kb2[c], g->vb2[c], g->item2[c], g->posrec2[c],
-                   g->t2_2[c]};
+                   g->t2_2[c], g->ptt2[c], g->dp2[c], g->prep2[c], g->colist2[c], g->epol2[c], g->spol2[c]};
     for (void *p : per)
       if (p) cudaFree(p);
-    if (g->evF[c]) cudaEventDestroy(g->evF[c]);
-    if (g->evB[c]) cudaEventDestroy(g->evB[c]);
+    for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evA[c]})
+      if (ev) cudaEventDestroy(ev);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
   for (auto &ge : g->graphs) {
@@ -1239,7 +1249,7 @@ int fibar_destroy(fibar_engine *g) {
   if (g->bstream) cudaStreamDestroy(g->bstream);
   for (cudaStream_t st : {g->astream, g->fstream})
     if (st) cudaStreamDestroy(st);
-  for (cudaEvent_t ev : {g->evIn, g->evCp, g->evA[0], g->evA[1]})
+  for (cudaEvent_t ev : {g->evIn, g->evCp})
     if (ev) cudaEventDestroy(ev);
   if (g->gstream) {
     cudaStreamSynchronize(g->gstream);
@@ -1376,7 +1386,7 @@ int fibar_halo_batch(fibar_engine *g, const uint16_t *x, const uint16_t *y, cons
       y = g->sy[0];
       p = g->sp_[0];
     }
-    const int par = (int)(g->batches & 1);
+    const int par = (int)(g->batches % NPAR);
     rc = enqueue_batch(g, x, y, p, n, nullptr, par, false);
     if (rc) return rc;
     unsigned tot[5];

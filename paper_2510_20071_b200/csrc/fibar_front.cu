@@ -153,6 +153,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->vcnt[1] = 0;
     b->qlo = 0x7FFFFFFFFFFFFFFFLL;
     b->qhi = -1;
+    b->nclosed = 0;
   }
 }
 
@@ -220,15 +221,20 @@ __global__ void k_ingest_end(Ctx x) {
 }
 
 // Opens the batch's window part against the state the previous batch left:
-// the window start and a fresh blur epoch.
-__global__ void k_batch_begin(Ctx x) {
-  pdl_wait();
+// the window start and a fresh blur epoch (k_batch_begin, or the first thread
+// of the front end's k_anchor).
+__device__ __forceinline__ void open_batch(const Ctx &x) {
   DevState *s = x.st;
   BatchState *b = x.bs;
   b->s_start = s->s;
   s->epoch += 1;
   b->epoch = s->epoch;
   b->epoch0 = s->epoch;
+}
+
+__global__ void k_batch_begin(Ctx x) {
+  pdl_wait();
+  open_batch(x);
 }
 
 // ------------------------------------------------------------------ link ---
@@ -442,12 +448,13 @@ __device__ __forceinline__ long long regulate_fast(const Ctx &x, long long len, 
 // chunk's window of the same candidate (one warp per chunk).
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) open_batch(x);   // (its values are read from the next kernel on)
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
   if (c >= T) return;
-  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
+  const long long E0 = x.bs->E0, s0 = x.st->s, q0 = x.st->q;
   const int nc = x.st->geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
   const long long a = chunk_warm_start(x, E0, c);
   const long long Jc = a - 1;
@@ -611,17 +618,13 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
 // that fixed point and never far beyond it, so the first unstable fine
 // candidate above the largest stable one is a start that collapses onto the
 // true trajectory within a handful of events, with few evictions.
-__global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
-  pdl_wait();
-  const long long B = x.bs->B;
-  const int T = (int)((B + x.chunk - 1) / x.chunk);
-  const int c = blockIdx.x * TPB + threadIdx.x;
-  if (c >= T) return;
+__device__ void fixed_point(const Ctx &x, int c, long long &Lout, long long &uout, bool &unsettled) {
   const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
   const long long a = chunk_warm_start(x, E0, c);
+  unsettled = false;
   if (c == 0 || a == E0) {
-    x.lc[c] = a - s0;
-    x.lu[c] = 32;
+    Lout = a - s0;
+    uout = 32;
     return;
   }
   const int nc = x.st->geo ? NCAND : NLIN;
@@ -666,9 +669,9 @@ __global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
   // stays well inside their span; a window still growing from the batch start
   // (clamped) is unsettled too: its target can run far from q0 next batch
   const bool clamped = len_lo >= 0 && len_hi < 0 && len_lo == a - s0;
-  if (clamped || L < q0 + c_lin_off[0] / 2 || L > q0 + c_lin_off[NLIN - 1] / 2) x.st->geo_next = 1;
-  x.lc[c] = L;
-  x.lu[c] = unit;
+  unsettled = clamped || L < q0 + c_lin_off[0] / 2 || L > q0 + c_lin_off[NLIN - 1] / 2;
+  Lout = L;
+  uout = unit;
 }
 
 __device__ __forceinline__ long long fine_start(const Ctx &x, long long s0, long long a, long long center,
@@ -692,8 +695,18 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
   const long long ac = chunk_warm_start(x, E0, c);
   const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
   const long long Jc = ac - 1, Jp = ap - 1;
-  const long long lcc = x.lc[c], lcp = c == 1 ? 0 : x.lc[c - 1];
-  const long long luc = x.lu[c], lup = c == 1 ? 32 : x.lu[c - 1];
+  // the regulator's fixed points of this chunk (lane 0) and the previous one
+  // (lane 1), from the coarse counts; this chunk's goes to the window run
+  long long fpL = 0, fpU = 32;
+  bool uns = false;
+  if (lane < 2 && !(lane == 1 && c == 1)) fixed_point(x, c - lane, fpL, fpU, uns);
+  if (lane == 0) {
+    x.lc[c] = fpL;
+    x.lu[c] = fpU;
+    if (uns) x.st->geo_next = 1;
+  }
+  const long long lcc = __shfl_sync(0xffffffffu, fpL, 0), lcp = c == 1 ? 0 : __shfl_sync(0xffffffffu, fpL, 1);
+  const long long luc = __shfl_sync(0xffffffffu, fpU, 0), lup = c == 1 ? 32 : __shfl_sync(0xffffffffu, fpU, 1);
   long long sp[NFINE];
   int cp[NFINE], ct[NFINE];
 #pragma unroll

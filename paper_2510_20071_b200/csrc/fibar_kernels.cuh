@@ -182,13 +182,12 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x);
 __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc);
-__global__ void __launch_bounds__(TPB) k_fp(Ctx x);
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run(Ctx x);
 __global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj_map(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x);
-__global__ void __launch_bounds__(TPB) k_posinfo(Ctx x);
+__global__ void __launch_bounds__(TPB) k_posinfo(Ctx x, int close);
 __global__ void __launch_bounds__(TPB) k_temporal(Ctx x);
 __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x);
 __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x);
@@ -211,6 +210,6 @@ __global__ void k_tile_counts(Ctx x, const unsigned *cnt, unsigned *tcnt);
 __global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy);
 __global__ void k_init_state(DevState *s, long long q0);
 __global__ void k_fill_ll(long long *p, long long n, long long v);
-__global__ void k_init_pt(PixRec *p0, PixRec *p1, long long *plast, long long n);
+__global__ void k_init_pt(PixRec *p, long long *plast, long long n);
 
 }  // namespace fibar

@@ -496,7 +496,7 @@ __global__ void k_fill_ll(long long *p, long long n, long long v) {
   pdl_wait();
   for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) p[i] = v;
 }
-__global__ void k_init_pt(PixRec *p0, PixRec *p1, long long *plast, long long n) {
+__global__ void k_init_pt(PixRec *p, long long *plast, long long n) {
   pdl_wait();
   for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
     PixRec r;
@@ -504,8 +504,7 @@ __global__ void k_init_pt(PixRec *p0, PixRec *p1, long long *plast, long long n)
     r.end = 0;
     r.carried = FIBAR_NONE;
     r.pad0 = 0;
-    p0[i] = r;
-    p1[i] = r;
+    p[i] = r;
     plast[i] = -1;
   }
 }

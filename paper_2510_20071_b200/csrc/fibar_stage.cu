@@ -9,23 +9,53 @@ namespace fibar {
 // Per sorted position, fully parallel: the event's polarity gathered into
 // sorted order and (filter ON) whether the event is evicted stale in this
 // batch -- the random loads the serial per-pixel replay would otherwise wait on.
-__global__ void __launch_bounds__(TPB) k_posinfo(Ctx x) {
+// the batch's counters into the engine state (k_batch_end, or the last block
+// of the front end's final k_posinfo)
+__device__ __forceinline__ void close_batch(const Ctx &x) {
+  DevState *s = x.st;
+  const BatchState *bsp = x.bs;
+  if (x.spatial && bsp->B > 0) {
+    s->geo = s->geo_next;
+    s->geo_next = 0;
+  }
+  s->E += bsp->B;
+  if (x.spatial) {
+    s->stale += bsp->stale_batch;
+    if (x.blur_on) s->blur += bsp->stale_batch;
+  }
+}
+
+// close != 0: the last block to finish also closes the batch (saves a launch
+// on the front end's critical chain)
+__global__ void __launch_bounds__(TPB) k_posinfo(Ctx x, int close) {
   pdl_wait();
   const long long B = x.bs->B;
   const long long i = (long long)blockIdx.x * TPB + threadIdx.x;
-  if (i >= B) return;
-  const unsigned jj = x.sidx[i];
-  x.spol[i] = x.epol[jj];
-  if (!x.spatial) return;
-  const long long E0 = x.bs->E0, s_start = x.bs->s_start;
-  const long long s_end = s_start + x.S[B - 1];
-  const long long e = E0 + jj;
-  unsigned bidx = FIBAR_NONE;
-  if (e < s_end) {
-    const unsigned q = (unsigned)(e - s_start);
-    if (x.item[q].pix != FIBAR_NONE) bidx = q;
+  if (i < B) {
+    const unsigned jj = x.sidx[i];
+    x.spol[i] = x.epol[jj];
+    if (x.spatial) {
+      const long long E0 = x.bs->E0, s_start = x.bs->s_start;
+      const long long s_end = s_start + x.S[B - 1];
+      const long long e = E0 + jj;
+      unsigned bidx = FIBAR_NONE;
+      if (e < s_end) {
+        const unsigned q = (unsigned)(e - s_start);
+        if (x.item[q].pix != FIBAR_NONE) bidx = q;
+      }
+      *reinterpret_cast<uint2 *>(&x.posrec[i]) = make_uint2(jj, bidx);
+    }
   }
-  *reinterpret_cast<uint2 *>(&x.posrec[i]) = make_uint2(jj, bidx);
+  if (close) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      if (atomicAdd(&x.bs->nclosed, 1u) == gridDim.x - 1) {
+        __threadfence();
+        close_batch(x);
+      }
+    }
+  }
 }
 
 // One thread per pixel segment replays its events in stream order with the
@@ -685,17 +715,7 @@ __global__ void __launch_bounds__(TPB) k_halo_collect(Ctx x, const unsigned *hli
 
 __global__ void k_batch_end(Ctx x) {
   pdl_wait();
-  DevState *s = x.st;
-  const BatchState *bsp = x.bs;
-  if (x.spatial && bsp->B > 0) {
-    s->geo = s->geo_next;
-    s->geo_next = 0;
-  }
-  s->E += bsp->B;
-  if (x.spatial) {
-    s->stale += bsp->stale_batch;
-    if (x.blur_on) s->blur += bsp->stale_batch;
-  }
+  close_batch(x);
 }
 
 
