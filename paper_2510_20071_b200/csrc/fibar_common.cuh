@@ -74,7 +74,7 @@ struct BatchState {
   unsigned vpad;
   long long n_raw;     // raw events of the batch, set by k_stage (graphs are captured per size class)
   unsigned nclosed;    // k_posinfo blocks done (the last one closes the batch)
-  unsigned npad;
+  int geo_next;        // a fixed point of this batch lay far from its candidates: the next batch adds the geometric ones
 };
 
 // Window / counter state living in device memory so no kernel needs a host
@@ -107,7 +107,7 @@ struct DevState {
   long long warm_pops;   // evictions replayed during speculative warm-ups (stats)
   long long coop_iters;  // warp-cooperative eviction-count steps (stats)
   long long fix_rounds;  // verifier rounds (stats)
-  int geo, geo_next;     // window candidates: geometric set needed (this / next batch)
+  int geo, geo_unused;   // window candidates: geometric set needed (set by the previous batch's verifier)
   unsigned nlong, nlong_pad;   // long pixel segments of the batch
   long long dbg_bad;           // FIBAR_DEBUG_WINDOW: anchor counts that disagreed with a serial recount
   long long Ein;               // in-bounds events ingested (the ingest's running E, ahead of E)

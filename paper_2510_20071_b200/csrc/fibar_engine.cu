@@ -122,6 +122,8 @@ struct GraphEntry {
   cudaGraphExec_t exec = nullptr;
   cudaGraphExec_t exec2 = nullptr;   // kind 1: the window part (exec: the ingest)
   long long kernels2 = 0;
+  cudaGraphExec_t exec3 = nullptr;   // kind 1: the eviction pass
+  long long kernels3 = 0;
   int kind = 0;              // 0: whole batch (serial schedule), 1: front end of the streamed schedule (two parts)
   int par = 0;               // kind 1: the batch parity whose buffers it uses
   int where = 0;             // kind 1: which radix-sort buffer holds the sorted keys
@@ -160,8 +162,10 @@ struct fibar_engine {
   uint2 *longseg = nullptr;
   unsigned *ka2[NPAR] = {}, *va2[NPAR] = {}, *kb2[NPAR] = {}, *vb2[NPAR] = {}, *hist = nullptr;
   uint2 *dp2[NPAR] = {};    // per-event link distances, per batch parity
-  unsigned *S = nullptr, *Qt = nullptr;
-  unsigned *pmap = nullptr;
+  // window starts / targets after each event and the eviction -> popping-event
+  // map, per batch parity (the eviction pass of batch k runs beside the window
+  // pass of batch k+1)
+  unsigned *S2[NPAR] = {}, *Qt2[NPAR] = {}, *pmap2[NPAR] = {};
   unsigned long long *bv64 = nullptr, *mv64 = nullptr;
   BlurPrep *prep = nullptr;            // = prep2[0] (debug reads)
   BlurPrep *prep2[NPAR] = {};   // per batch parity: k_popj of batch k+1 writes while batch k blurs
@@ -211,6 +215,10 @@ struct fibar_engine {
   // window part (fstream), so batch k+1's ingest overlaps batch k's window pass
   cudaStream_t astream = nullptr, fstream = nullptr;
   cudaEvent_t evIn = nullptr, evCp = nullptr, evA[NPAR] = {};
+  // ... and the eviction pass (pstream) after the window part (evV), beside
+  // the next batch's window part
+  cudaStream_t pstream = nullptr;
+  cudaEvent_t evV[NPAR] = {};
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
@@ -301,9 +309,9 @@ struct fibar_engine {
     x.skey = skey;
     x.sidx = sidx;
     x.dp = dp2[par];
-    x.S = S;
-    x.Qt = Qt;
-    x.pmap = pmap;
+    x.S = S2[par];
+    x.Qt = Qt2[par];
+    x.pmap = pmap2[par];
     x.item = item2[par];
     x.posrec = posrec2[par];
     x.t2 = t2_2[par];
@@ -415,9 +423,9 @@ int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, co
   return 0;
 }
 
-// The rest (stream s, after the previous batch's front end): the batch opens
-// against the window state, then (filter ON) the window pass, the stale items
-// and the per-position info.  Returns the batch context in x.
+// The window part (stream s, after the previous batch's window part): the
+// batch opens against the window state, then (filter ON) the anchors, the
+// speculative run and the verifier.  Returns the batch context in x.
 int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s, Ctx &x) {
   Launcher &L = g->L;
   x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
@@ -433,10 +441,22 @@ int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStr
     fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
     // one cluster (cluster barriers between its rounds' phases)
     fibar_launch_cluster(L, "window_verify", k_window_verify, VF_CTAS, VF_TPB, 0, s, x);
-    fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
-    fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
-    fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x, 1);   // its last block closes the batch
   }
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// The eviction pass (stream s, after the window part; filter ON): each popped
+// entry's popping event, the stale items, the per-position info; its last
+// block closes the batch.  It reads only this batch's window trajectory, so it
+// runs beside the next batch's window part.
+int enqueue_post(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s) {
+  Launcher &L = g->L;
+  Ctx x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+  const int nb = (int)((n_raw + TPB - 1) / TPB);
+  fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
+  fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
+  fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x, 1);   // its last block closes the batch
   CK(cudaGetLastError());
   return 0;
 }
@@ -449,6 +469,7 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   cudaStream_t s_saved = g->L.stream;
   g->L.stream = s;
   rc = enqueue_window(g, n_raw, par, where, s, x);
+  if (!rc && g->spatial) rc = enqueue_post(g, n_raw, par, where, s);
   g->L.stream = s_saved;
   x.raw_x = rx0;
   x.raw_y = ry0;
@@ -467,8 +488,8 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   for (auto &ge : g->graphs)
     if (ge.kind == 1 && ge.n == n_raw && ge.par == par) return &ge;
   if (g->graphs.size() >= 16) {   // small cache: drop the oldest (freed once its launches finish)
-    cudaGraphExecDestroy(g->graphs.front().exec);
-    if (g->graphs.front().exec2) cudaGraphExecDestroy(g->graphs.front().exec2);
+    for (cudaGraphExec_t e : {g->graphs.front().exec, g->graphs.front().exec2, g->graphs.front().exec3})
+      if (e) cudaGraphExecDestroy(e);
     g->graphs.erase(g->graphs.begin());
   }
   if (!g->capstream && cudaStreamCreateWithFlags(&g->capstream, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
@@ -478,19 +499,21 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   ge.n = n_raw;
   ge.kind = 1;
   ge.par = par;
-  for (int part = 0; part < 2; ++part) {
+  for (int part = 0; part < 3; ++part) {
     const long long l0 = L.launches;
     cudaGraph_t graph = nullptr;
     Ctx x{};
     if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
-      if (ge.exec) cudaGraphExecDestroy(ge.exec);
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2})
+        if (e) cudaGraphExecDestroy(e);
       return nullptr;
     }
     L.stream = g->capstream;
-    const int rc = part == 0 ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where,
-                                              &g->bsd[par].n_raw)
-                             : enqueue_window(g, n_raw, par, ge.where, g->capstream, x);
+    const int rc = part == 0   ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where,
+                                                &g->bsd[par].n_raw)
+                   : part == 1 ? enqueue_window(g, n_raw, par, ge.where, g->capstream, x)
+                               : enqueue_post(g, n_raw, par, ge.where, g->capstream);
     L.stream = s0;
     cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
     cudaGraphExec_t exec = nullptr;
@@ -500,16 +523,20 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     L.launches = l0;
     if (rc || ce != cudaSuccess) {
       cudaGetLastError();
-      if (ge.exec) cudaGraphExecDestroy(ge.exec);
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2})
+        if (e) cudaGraphExecDestroy(e);
       g->graphs_on = false;   // capture impossible here: stream every kernel from now on
       return nullptr;
     }
     if (part == 0) {
       ge.exec = exec;
       ge.kernels = k;
-    } else {
+    } else if (part == 1) {
       ge.exec2 = exec;
       ge.kernels2 = k;
+    } else {
+      ge.exec3 = exec;
+      ge.kernels3 = k;
     }
   }
   g->graphs.push_back(ge);
@@ -562,6 +589,10 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaStreamWaitEvent(s, g->evA[par], 0));
       CK(cudaGraphLaunch(ge->exec2, s));
       L.launches += ge->kernels2;
+      CK(cudaEventRecord(g->evV[par], s));
+      CK(cudaStreamWaitEvent(g->pstream, g->evV[par], 0));
+      CK(cudaGraphLaunch(ge->exec3, g->pstream));
+      L.launches += ge->kernels3;
       x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
       x.raw_x = g->gx;
       x.raw_y = g->gy;
@@ -576,11 +607,18 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       rc = enqueue_window(g, n_raw, par, where, s, x);
       L.stream = u;
       if (rc) return rc;
+      CK(cudaEventRecord(g->evV[par], s));
+      CK(cudaStreamWaitEvent(g->pstream, g->evV[par], 0));
+      L.stream = g->pstream;
+      rc = enqueue_post(g, n_raw, par, where, g->pstream);
+      L.stream = u;
+      if (rc) return rc;
       x.raw_x = rx0;
       x.raw_y = ry0;
       x.raw_p = rp0;
     }
     CK(cudaStreamWaitEvent(u, g->evCp, 0));   // the caller may reuse the packet after the ingest read it
+    s = g->pstream;   // the batch's front end ends with the eviction pass
     L.stream = s;
   } else {
     // this parity's buffers are free once the batch two back finished its blur stage
@@ -1150,6 +1188,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       cudaEventCreateWithFlags(&g->evF[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evB[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evA[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evV[c], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&g->evIn, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g->evCp, cudaEventDisableTiming);
@@ -1161,6 +1200,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       int fp = hi;
       if (const char *v = getenv("FIBAR_FRONT_PRIO")) fp = atoi(v) ? hi : lo;
       cudaStreamCreateWithPriority(&g->fstream, cudaStreamNonBlocking, fp);
+      cudaStreamCreateWithPriority(&g->pstream, cudaStreamNonBlocking, fp);
       cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, lo);
     }
     rc |= dalloc(&g->last_tile, g->n_tiles);
@@ -1168,9 +1208,11 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->rkey, g->R);
     rc |= dalloc(&g->rnext, g->R);
     for (int c = 0; c < NPAR; ++c) rc |= dalloc(&g->dp2[c], Bc);
-    rc |= dalloc(&g->S, Bc);
-    rc |= dalloc(&g->Qt, Bc);
-    rc |= dalloc(&g->pmap, npop_cap);
+    for (int c = 0; c < NPAR; ++c) {
+      rc |= dalloc(&g->S2[c], Bc);
+      rc |= dalloc(&g->Qt2[c], Bc);
+      rc |= dalloc(&g->pmap2[c], npop_cap);
+    }
     rc |= dalloc(&g->bv64, npop_cap);
     rc |= dalloc(&g->mv64, Bc);
     for (int c = 0; c < NPAR; ++c) {
@@ -1211,11 +1253,11 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
-  for (cudaStream_t st : {g->astream, g->fstream, g->bstream})
+  for (cudaStream_t st : {g->astream, g->fstream, g->pstream, g->bstream})
     if (st) cudaStreamSynchronize(st);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->longseg, g->hist,
-                  g->S, g->Qt, g->pmap, g->bv64, g->mv64, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
+                  g->bv64, g->mv64, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1232,22 +1274,22 @@ int fibar_destroy(fibar_engine *g) {
   }
   for (int c = 0; c < NPAR; ++c) {
     void *per[] = {g->pt2[c], g->ekey2[c], g->ka2[c], g->va2[c], g->kb2[c], g->vb2[c], g->item2[c], g->posrec2[c],
-                   g->t2_2[c], g->ptt2[c], g->dp2[c], g->prep2[c], g->colist2[c], g->epol2[c], g->spol2[c]};
+                   g->t2_2[c], g->ptt2[c], g->dp2[c], g->prep2[c], g->colist2[c], g->epol2[c], g->spol2[c],
+                   g->S2[c], g->Qt2[c], g->pmap2[c]};
     for (void *p : per)
       if (p) cudaFree(p);
-    for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evA[c]})
+    for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evA[c], g->evV[c]})
       if (ev) cudaEventDestroy(ev);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
-  for (auto &ge : g->graphs) {
-    cudaGraphExecDestroy(ge.exec);
-    if (ge.exec2) cudaGraphExecDestroy(ge.exec2);
-  }
+  for (auto &ge : g->graphs)
+    for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3})
+      if (e) cudaGraphExecDestroy(e);
   if (g->capstream) cudaStreamDestroy(g->capstream);
   for (void *q : {(void *)g->gx, (void *)g->gy, (void *)g->gp})
     if (q) cudaFree(q);
   if (g->bstream) cudaStreamDestroy(g->bstream);
-  for (cudaStream_t st : {g->astream, g->fstream})
+  for (cudaStream_t st : {g->astream, g->fstream, g->pstream})
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t ev : {g->evIn, g->evCp})
     if (ev) cudaEventDestroy(ev);

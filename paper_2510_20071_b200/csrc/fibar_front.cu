@@ -154,6 +154,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->qlo = 0x7FFFFFFFFFFFFFFFLL;
     b->qhi = -1;
     b->nclosed = 0;
+    b->geo_next = 0;
   }
 }
 
@@ -703,7 +704,7 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
   if (lane == 0) {
     x.lc[c] = fpL;
     x.lu[c] = fpU;
-    if (uns) x.st->geo_next = 1;
+    if (uns) x.bs->geo_next = 1;
   }
   const long long lcc = __shfl_sync(0xffffffffu, fpL, 0), lcp = c == 1 ? 0 : __shfl_sync(0xffffffffu, fpL, 1);
   const long long luc = __shfl_sync(0xffffffffu, fpU, 0), lup = c == 1 ? 32 : __shfl_sync(0xffffffffu, fpU, 1);
@@ -1204,6 +1205,8 @@ __global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x) {
     s->chunks += T;
     s->fix_rounds += rounds;
     s->mismatch += reruns;
+    // the next batch's candidate set (its anchors run right after this kernel)
+    if (B > 0) s->geo = bs->geo_next;
   }
 }
 

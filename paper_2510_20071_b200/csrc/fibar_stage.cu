@@ -14,10 +14,6 @@ namespace fibar {
 __device__ __forceinline__ void close_batch(const Ctx &x) {
   DevState *s = x.st;
   const BatchState *bsp = x.bs;
-  if (x.spatial && bsp->B > 0) {
-    s->geo = s->geo_next;
-    s->geo_next = 0;
-  }
   s->E += bsp->B;
   if (x.spatial) {
     s->stale += bsp->stale_batch;
