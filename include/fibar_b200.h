@@ -152,6 +152,13 @@ int fibar_read_state(fibar_engine *eng, float *p_bar, float *l, uint16_t *active
  * exceeds cap.  Filter ON only (else *n_out = 0). */
 int fibar_debug_stale_items(fibar_engine *eng, int64_t *event_idx, uint32_t *pixel, int64_t cap, int64_t *n_out);
 
+/* Measurement: with FIBAR_TRACE=1 set at creation, timing events are recorded
+ * at the stream-part boundaries of every streamed batch (labels 0/1 ingest
+ * start/end, 2/3 window part, 4/5 eviction pass, 6/7 blur stage, 8 read-out
+ * end).  Returns (batch index, label, ms since the first mark) and clears them;
+ * synchronises the device. */
+int fibar_debug_trace(fibar_engine *eng, int64_t cap, int64_t *batch, int32_t *label, double *ms, int64_t *n_out);
+
 /* Diagnostics (runs pending packets first): stats[0] = device kernel launches
  * so far, [1] = device batches, [2] = speculative window chunks, [3] = chunks
  * re-run by the verifier, [4] = pops (window evictions) processed, [5] =

@@ -75,6 +75,8 @@ struct BatchState {
   long long n_raw;     // raw events of the batch, set by k_stage (graphs are captured per size class)
   unsigned nclosed;    // k_posinfo blocks done (the last one closes the batch)
   int geo_next;        // a fixed point of this batch lay far from its candidates: the next batch adds the geometric ones
+  int gpad;
+  long long s_pred;    // the window start the batch's anchors counted from (DevState.pred_s when they ran)
 };
 
 // Window / counter state living in device memory so no kernel needs a host
@@ -111,6 +113,11 @@ struct DevState {
   unsigned nlong, nlong_pad;   // long pixel segments of the batch
   long long dbg_bad;           // FIBAR_DEBUG_WINDOW: anchor counts that disagreed with a serial recount
   long long Ein;               // in-bounds events ingested (the ingest's running E, ahead of E)
+  // the next batch's anchors run before this batch's verifier: they count
+  // candidate windows against the speculative end state of this batch's last
+  // chunk (exact distinct counts for that window, whatever the verifier finds)
+  long long pred_s, pred_q, pred_np, pred_nt;
+  int pred_geo, pred_pad;
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {

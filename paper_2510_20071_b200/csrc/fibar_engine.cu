@@ -124,6 +124,8 @@ struct GraphEntry {
   long long kernels2 = 0;
   cudaGraphExec_t exec3 = nullptr;   // kind 1: the eviction pass
   long long kernels3 = 0;
+  cudaGraphExec_t exec4 = nullptr;   // kind 1: the anchors (exec2: run + verifier)
+  long long kernels4 = 0;
   int kind = 0;              // 0: whole batch (serial schedule), 1: front end of the streamed schedule (two parts)
   int par = 0;               // kind 1: the batch parity whose buffers it uses
   int where = 0;             // kind 1: which radix-sort buffer holds the sorted keys
@@ -219,6 +221,27 @@ struct fibar_engine {
   // the next batch's window part
   cudaStream_t pstream = nullptr;
   cudaEvent_t evV[NPAR] = {};
+  // ... and the anchors (nstream) after the ingest (evA) and the previous
+  // batch's run (evR), beside the previous batch's verifier
+  cudaStream_t nstream = nullptr;
+  cudaEvent_t evN[NPAR] = {}, evR[NPAR] = {};
+  int r_par = -1;   // buffer set of the newest batch whose run recorded evR (-1: none since reset)
+  // FIBAR_TRACE=1: timing events at the stream parts' boundaries of every
+  // streamed batch (fibar_debug_trace reads them; measurement only)
+  bool trace = false;
+  struct TraceRec {
+    long long batch;
+    int label;
+    cudaEvent_t ev;
+  };
+  std::vector<TraceRec> tr;
+  void mark(int label, cudaStream_t st) {
+    if (!trace || tr.size() >= 200000) return;
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, st);
+    tr.push_back(TraceRec{batches, label, e});
+  }
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
@@ -383,6 +406,7 @@ int init_state(fibar_engine *g) {
   g->hfill = 0;
   g->dfill = 0;
   g->gt.n = 0;
+  g->r_par = -1;
   CK(cudaGetLastError());
   return 0;
 }
@@ -426,24 +450,57 @@ int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, co
 // The window part (stream s, after the previous batch's window part): the
 // batch opens against the window state, then (filter ON) the anchors, the
 // speculative run and the verifier.  Returns the batch context in x.
-int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s, Ctx &x) {
+// The window part in two pieces.  Anchors (filter ON): exact distinct counts
+// of every chunk's candidate windows, counted against the previous batch's
+// predicted end state, so they may run beside the previous batch's verifier.
+int enqueue_anchors(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s) {
+  Launcher &L = g->L;
+  Ctx x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+  const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
+  fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
+  fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
+  fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, g->anc, NCAND);
+  fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
+  fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
+  CK(cudaGetLastError());
+  return 0;
+}
+
+// ... then (after the previous batch's verifier) the speculative run and the
+// verifier; ev_run (if given) is recorded between them: the next batch's
+// anchors read the run's predicted end state and overwrite its candidates.
+int enqueue_chain(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s, Ctx &x, cudaEvent_t ev_run) {
   Launcher &L = g->L;
   x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
-  const int nb = (int)((n_raw + TPB - 1) / TPB);
-  if (!g->spatial) fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);   // (filter ON: in k_anchor)
-  if (g->spatial) {
+  if (!g->spatial) {
+    fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);   // (filter ON: in k_window_run)
+  } else {
     const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
-    fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
-    fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
-    fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, g->anc, NCAND);
-    fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
-    fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
     fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
+    // an external event-record node when captured (the next batch's anchors,
+    // on another stream, wait on it)
+    if (ev_run) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      CK(cudaStreamIsCapturing(s, &cs));
+      if (cs == cudaStreamCaptureStatusActive)
+        CK(cudaEventRecordWithFlags(ev_run, s, cudaEventRecordExternal));
+      else
+        CK(cudaEventRecord(ev_run, s));
+    }
     // one cluster (cluster barriers between its rounds' phases)
     fibar_launch_cluster(L, "window_verify", k_window_verify, VF_CTAS, VF_TPB, 0, s, x);
   }
   CK(cudaGetLastError());
   return 0;
+}
+
+// Both pieces on one stream.
+int enqueue_window(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s, Ctx &x) {
+  if (g->spatial) {
+    int rc = enqueue_anchors(g, n_raw, par, where, s);
+    if (rc) return rc;
+  }
+  return enqueue_chain(g, n_raw, par, where, s, x, nullptr);
 }
 
 // The eviction pass (stream s, after the window part; filter ON): each popped
@@ -488,7 +545,8 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   for (auto &ge : g->graphs)
     if (ge.kind == 1 && ge.n == n_raw && ge.par == par) return &ge;
   if (g->graphs.size() >= 16) {   // small cache: drop the oldest (freed once its launches finish)
-    for (cudaGraphExec_t e : {g->graphs.front().exec, g->graphs.front().exec2, g->graphs.front().exec3})
+    for (cudaGraphExec_t e : {g->graphs.front().exec, g->graphs.front().exec2, g->graphs.front().exec3,
+                              g->graphs.front().exec4})
       if (e) cudaGraphExecDestroy(e);
     g->graphs.erase(g->graphs.begin());
   }
@@ -499,21 +557,22 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   ge.n = n_raw;
   ge.kind = 1;
   ge.par = par;
-  for (int part = 0; part < 3; ++part) {
+  for (int part = 0; part < 4; ++part) {
     const long long l0 = L.launches;
     cudaGraph_t graph = nullptr;
     Ctx x{};
     if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
-      for (cudaGraphExec_t e : {ge.exec, ge.exec2})
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3})
         if (e) cudaGraphExecDestroy(e);
       return nullptr;
     }
     L.stream = g->capstream;
     const int rc = part == 0   ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where,
                                                 &g->bsd[par].n_raw)
-                   : part == 1 ? enqueue_window(g, n_raw, par, ge.where, g->capstream, x)
-                               : enqueue_post(g, n_raw, par, ge.where, g->capstream);
+                   : part == 1 ? enqueue_chain(g, n_raw, par, ge.where, g->capstream, x, g->evR[par])
+                   : part == 2 ? enqueue_post(g, n_raw, par, ge.where, g->capstream)
+                               : enqueue_anchors(g, n_raw, par, ge.where, g->capstream);
     L.stream = s0;
     cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
     cudaGraphExec_t exec = nullptr;
@@ -523,7 +582,7 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     L.launches = l0;
     if (rc || ce != cudaSuccess) {
       cudaGetLastError();
-      for (cudaGraphExec_t e : {ge.exec, ge.exec2})
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3})
         if (e) cudaGraphExecDestroy(e);
       g->graphs_on = false;   // capture impossible here: stream every kernel from now on
       return nullptr;
@@ -534,9 +593,12 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     } else if (part == 1) {
       ge.exec2 = exec;
       ge.kernels2 = k;
-    } else {
+    } else if (part == 2) {
       ge.exec3 = exec;
       ge.kernels3 = k;
+    } else {
+      ge.exec4 = exec;
+      ge.kernels4 = k;
     }
   }
   g->graphs.push_back(ge);
@@ -569,6 +631,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     CK(cudaEventRecord(g->evIn, u));
     CK(cudaStreamWaitEvent(sa, g->evIn, 0));
     if (g->b_used[par]) CK(cudaStreamWaitEvent(sa, g->evB[par], 0));   // this parity's buffers are free
+    g->mark(0, sa);   // trace labels: 0/1 ingest start/end, 2/3 window part, 4/5 eviction pass, 6/7 blur stage
     const bool small = g->graphs_on && !L.prof && n_raw <= g->graph_max;
     if (small) {
       // a small batch: each part replays one CUDA graph per (size class,
@@ -585,14 +648,27 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       where = ge->where;
       CK(cudaGraphLaunch(ge->exec, sa));
       L.launches += ge->kernels;
+      g->mark(1, sa);
       CK(cudaEventRecord(g->evA[par], sa));
-      CK(cudaStreamWaitEvent(s, g->evA[par], 0));
-      CK(cudaGraphLaunch(ge->exec2, s));
+      // anchors after the ingest and the previous batch's run
+      cudaStream_t sn = g->nstream;
+      CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
+      if (g->r_par >= 0) CK(cudaStreamWaitEvent(sn, g->evR[g->r_par], 0));
+      CK(cudaGraphLaunch(ge->exec4, sn));
+      L.launches += ge->kernels4;
+      CK(cudaEventRecord(g->evN[par], sn));
+      CK(cudaStreamWaitEvent(s, g->evN[par], 0));
+      g->mark(2, s);
+      CK(cudaGraphLaunch(ge->exec2, s));   // (records evR[par] after the run)
       L.launches += ge->kernels2;
+      g->r_par = par;
+      g->mark(3, s);
       CK(cudaEventRecord(g->evV[par], s));
       CK(cudaStreamWaitEvent(g->pstream, g->evV[par], 0));
+      g->mark(4, g->pstream);
       CK(cudaGraphLaunch(ge->exec3, g->pstream));
       L.launches += ge->kernels3;
+      g->mark(5, g->pstream);
       x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
       x.raw_x = g->gx;
       x.raw_y = g->gy;
@@ -602,11 +678,20 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       if (rc) return rc;
       CK(cudaEventRecord(g->evCp, sa));
       CK(cudaEventRecord(g->evA[par], sa));
-      CK(cudaStreamWaitEvent(s, g->evA[par], 0));
-      L.stream = s;
-      rc = enqueue_window(g, n_raw, par, where, s, x);
+      cudaStream_t sn = g->nstream;
+      CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
+      if (g->r_par >= 0) CK(cudaStreamWaitEvent(sn, g->evR[g->r_par], 0));
+      L.stream = sn;
+      rc = enqueue_anchors(g, n_raw, par, where, sn);
       L.stream = u;
       if (rc) return rc;
+      CK(cudaEventRecord(g->evN[par], sn));
+      CK(cudaStreamWaitEvent(s, g->evN[par], 0));
+      L.stream = s;
+      rc = enqueue_chain(g, n_raw, par, where, s, x, g->evR[par]);
+      L.stream = u;
+      if (rc) return rc;
+      g->r_par = par;
       CK(cudaEventRecord(g->evV[par], s));
       CK(cudaStreamWaitEvent(g->pstream, g->evV[par], 0));
       L.stream = g->pstream;
@@ -641,6 +726,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       cudaStream_t bs = g->bstream;
       CK(cudaEventRecord(g->evF[par], s));
       CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
+      g->mark(6, bs);
       L.stream = bs;
       fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, bs, x);
       fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, bs, x);
@@ -674,9 +760,11 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     if (g->blur_on) {
       const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
       fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, bs, x);
-      if (g->gstream && !graph) {
+      if (g->gstream && !graph && n_raw > g->small_chunk_max) {
         // the blur dataflow alone on its own SM partition (green context):
         // its polling no longer shares SMs with the next batch's front end
+        // (large batches; a small batch's blur stage is the critical chain
+        // and takes the whole GPU: config 3, 374 -> 389 Mev/s)
         CK(cudaEventRecord(g->evP, bs));
         CK(cudaStreamWaitEvent(g->gstream, g->evP, 0));
         L.stream = g->gstream;
@@ -691,6 +779,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "final", k_final, g->nsm * 8, TPB, 0, bs, x);
     L.stream = u;
     if (!graph) {
+      g->mark(7, bs);
       CK(cudaEventRecord(g->evB[par], bs));
       g->b_used[par] = true;
       g->last_b = par;
@@ -1038,6 +1127,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   }
   // small batches (<= small_chunk_max) warm up 32 events: the verifier
   // re-runs the extra misses cheaply (config 3: 270 -> 280 Mev/s)
+  if (const char *v = getenv("FIBAR_TRACE")) g->trace = atoi(v) != 0;
   if (const char *v = getenv("FIBAR_WARM")) {
     g->warm = std::max(0, atoi(v));
     g->warm_set = true;
@@ -1189,6 +1279,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       cudaEventCreateWithFlags(&g->evB[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evA[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evV[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evN[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evR[c], cudaEventDisableTiming);
     }
     cudaEventCreateWithFlags(&g->evIn, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&g->evCp, cudaEventDisableTiming);
@@ -1201,6 +1293,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       if (const char *v = getenv("FIBAR_FRONT_PRIO")) fp = atoi(v) ? hi : lo;
       cudaStreamCreateWithPriority(&g->fstream, cudaStreamNonBlocking, fp);
       cudaStreamCreateWithPriority(&g->pstream, cudaStreamNonBlocking, fp);
+      cudaStreamCreateWithPriority(&g->nstream, cudaStreamNonBlocking, fp);
       cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, lo);
     }
     rc |= dalloc(&g->last_tile, g->n_tiles);
@@ -1253,7 +1346,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
-  for (cudaStream_t st : {g->astream, g->fstream, g->pstream, g->bstream})
+  for (cudaStream_t st : {g->astream, g->nstream, g->fstream, g->pstream, g->bstream})
     if (st) cudaStreamSynchronize(st);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->longseg, g->hist,
@@ -1278,18 +1371,18 @@ int fibar_destroy(fibar_engine *g) {
                    g->S2[c], g->Qt2[c], g->pmap2[c]};
     for (void *p : per)
       if (p) cudaFree(p);
-    for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evA[c], g->evV[c]})
+    for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evA[c], g->evV[c], g->evN[c], g->evR[c]})
       if (ev) cudaEventDestroy(ev);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
   for (auto &ge : g->graphs)
-    for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3})
+    for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4})
       if (e) cudaGraphExecDestroy(e);
   if (g->capstream) cudaStreamDestroy(g->capstream);
   for (void *q : {(void *)g->gx, (void *)g->gy, (void *)g->gp})
     if (q) cudaFree(q);
   if (g->bstream) cudaStreamDestroy(g->bstream);
-  for (cudaStream_t st : {g->astream, g->fstream, g->pstream})
+  for (cudaStream_t st : {g->astream, g->nstream, g->fstream, g->pstream})
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t ev : {g->evIn, g->evCp})
     if (ev) cudaEventDestroy(ev);
@@ -1519,6 +1612,7 @@ int fibar_render_async(fibar_engine *g, int32_t mode, double fixed_bound, uint8_
     if (e != cudaSuccess) rc = cuda_fail(e, "render_async meta");
   }
   if (!rc && on_blur) {
+    g->mark(8, rs);   // 8: read-out end
     cudaError_t e = cudaEventRecord(g->evB[g->last_b], rs);   // later batches order after the read-out
     if (e != cudaSuccess) rc = cuda_fail(e, "render_async event");
   }
@@ -1619,6 +1713,24 @@ int fibar_debug_stale_items(fibar_engine *g, int64_t *event_idx, uint32_t *pixel
   }
   *n_out = k;
   return k > cap ? fail(FIBAR_E_CONFIG, "stale item buffer too small") : 0;
+}
+
+int fibar_debug_trace(fibar_engine *g, int64_t cap, int64_t *batch, int32_t *label, double *ms, int64_t *n_out) {
+  if (!g || !n_out) return fail(FIBAR_E_CONFIG, "null argument");
+  CK(cudaDeviceSynchronize());
+  const long long n = (long long)g->tr.size();
+  *n_out = n;
+  for (long long i = 0; i < n && i < cap; ++i) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, g->tr[0].ev, g->tr[i].ev);
+    batch[i] = g->tr[i].batch;
+    label[i] = g->tr[i].label;
+    ms[i] = t;
+  }
+  for (auto &r : g->tr) cudaEventDestroy(r.ev);
+  g->tr.clear();
+  cudaGetLastError();
+  return 0;
 }
 
 int fibar_counters(fibar_engine *g, int64_t *event_count, int64_t *oob_dropped) {

@@ -449,14 +449,15 @@ __device__ __forceinline__ long long regulate_fast(const Ctx &x, long long len, 
 // chunk's window of the same candidate (one warp per chunk).
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 0) open_batch(x);   // (its values are read from the next kernel on)
+  // counted against the previous batch's predicted end state (DevState.pred_*)
+  if (blockIdx.x == 0 && threadIdx.x == 0) x.bs->s_pred = x.st->pred_s;   // read from the next kernel on
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
   if (c >= T) return;
-  const long long E0 = x.bs->E0, s0 = x.st->s, q0 = x.st->q;
-  const int nc = x.st->geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
+  const long long E0 = x.bs->E0, s0 = x.st->pred_s, q0 = x.st->pred_q;
+  const int nc = x.st->pred_geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
   const long long a = chunk_warm_start(x, E0, c);
   const long long Jc = a - 1;
   const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
@@ -517,8 +518,8 @@ __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   if (T < 2) return;
   const int i = blockIdx.y;
-  if (i >= (x.st->geo ? NCAND : NLIN)) return;
-  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
+  if (i >= (x.st->pred_geo ? NCAND : NLIN)) return;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_pred, q0 = x.st->pred_q;
   const long long a = chunk_warm_start(x, E0, 1);
   const long long Jc = a - 1;
   const long long sn = max(s0, a - cand_len(x, q0, i));
@@ -562,7 +563,7 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
     i = 0;
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int2 carry = make_int2((int)x.st->npix, (int)x.st->ntiles);
+  int2 carry = make_int2((int)x.st->pred_np, (int)x.st->pred_nt);
   for (int base = 1; base < T; base += 1024 * PER) {
     const int c0 = base + threadIdx.x * PER;
     int2 v[PER];
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
 // candidate above the largest stable one is a start that collapses onto the
 // true trajectory within a handful of events, with few evictions.
 __device__ void fixed_point(const Ctx &x, int c, long long &Lout, long long &uout, bool &unsettled) {
-  const long long E0 = x.bs->E0, s0 = x.bs->s_start, q0 = x.st->q;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_pred, q0 = x.st->pred_q;
   const long long a = chunk_warm_start(x, E0, c);
   unsettled = false;
   if (c == 0 || a == E0) {
@@ -628,7 +629,7 @@ __device__ void fixed_point(const Ctx &x, int c, long long &Lout, long long &uou
     uout = 32;
     return;
   }
-  const int nc = x.st->geo ? NCAND : NLIN;
+  const int nc = x.st->pred_geo ? NCAND : NLIN;
   long long lens[NCAND], fs[NCAND];
 #pragma unroll 1
   for (int i = 0; i < nc; ++i) {
@@ -692,7 +693,7 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
   if (c >= T) return;
-  const long long E0 = x.bs->E0, s0 = x.bs->s_start;
+  const long long E0 = x.bs->E0, s0 = x.bs->s_pred;
   const long long ac = chunk_warm_start(x, E0, c);
   const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
   const long long Jc = ac - 1, Jp = ap - 1;
@@ -754,6 +755,10 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
 
 __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    open_batch(x);                        // the batch's true start (after the previous verifier)
+    x.st->pred_geo = x.bs->geo_next;      // the next batch's candidate set
+  }
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int c = blockIdx.x * 128 + threadIdx.x;
@@ -762,14 +767,15 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   const bool valid = c < T;
   const DevState s = *x.st;
   const long long E0 = x.bs->E0;
-  const long long s_start0 = x.bs->s_start;
+  const long long s_true = s.s;             // chunk 0 starts exactly here
+  const long long s_start0 = x.bs->s_pred;  // the anchors' start: candidate windows are clamped to it
   const long long b = E0 + (long long)c * x.chunk;
   const long long e = valid ? min(E0 + B, b + x.chunk) : b;
   const long long a = valid ? chunk_warm_start(x, E0, c) : b;
   WState w{0, 1, 0, 0, 0};
   if (valid) {
     if (a == E0) {
-      w.s = s_start0;
+      w.s = s_true;
       w.q = s.q;
       w.npix = s.npix;
       w.ntiles = s.ntiles;
@@ -820,8 +826,11 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   const unsigned n_my = (unsigned)(e - a);
   const unsigned n_max = __reduce_max_sync(0xffffffffu, n_my);
   // 32-bit state relative to the batch's start window (every index in play is
-  // within B + window of it); ring slots as (slot of s_start + offset) & Rm
-  const long long base = s_start0;
+  // within B + window of it); ring slots as (slot of s_start + offset) & Rm.
+  // S / Qt are stored relative to the true start (a lane whose trajectory is
+  // still behind it is invalid and will be re-run by the verifier)
+  const long long base = min(s_start0, s_true);
+  const unsigned sofs = (unsigned)(s_true - base);
   const unsigned bslot = (unsigned)((unsigned long long)base & x.Rm);
   const unsigned rm = (unsigned)x.Rm;
   unsigned sr = (unsigned)(w.s - base);
@@ -928,7 +937,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
         }
       }
       if (jr >= br) {
-        x.S[jr - e0r] = sr;
+        x.S[jr - e0r] = sr - sofs;
         x.Qt[jr - e0r] = q;
       }
     }
@@ -958,6 +967,13 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   r.qlo = qlo;
   r.qhi = qhi;
   x.ch[c] = r;
+  if (c == T - 1) {   // the next batch's anchors count against this speculative end
+    DevState *d = x.st;
+    d->pred_s = w.s;
+    d->pred_q = w.q;
+    d->pred_np = w.npix;
+    d->pred_nt = w.ntiles;
+  }
 }
 
 // Verify chunk boundaries: a chunk is exact once its speculative start state
@@ -991,9 +1007,13 @@ __device__ __forceinline__ void vf_barrier() {
 // counter of j), so the rest of the chunk and its end state stand as they are:
 // the re-run stops there (regulation every event only).  Returns whether it
 // merged.
-__device__ bool rerun_chunk_staged(const Ctx &x, WState &w, long long b, long long e, long long E0, long long s_start,
-                                   uint2 *sdp, uint2 *srn, uint2 *ssq, long long &qlo, long long &qhi) {
+// Returns 0: re-run, end changed; 1: merged with the recorded trajectory;
+// 2: skipped (its start lies behind the batch's true start: an invalid
+// trajectory's end, re-run once that predecessor is)
+__device__ int rerun_chunk_staged(const Ctx &x, WState &w, long long b, long long e, long long E0, long long s_start,
+                                  uint2 *sdp, uint2 *srn, uint2 *ssq, long long &qlo, long long &qhi) {
   const int lane = threadIdx.x & 31;
+  if (w.s < s_start) return 2;
   const long long rn0 = w.s;
   for (int i = lane; i < (int)(e - b); i += 32) {
     sdp[i] = x.dp[b - E0 + i];
@@ -1074,7 +1094,7 @@ __device__ bool rerun_chunk_staged(const Ctx &x, WState &w, long long b, long lo
     }
   }
   __syncwarp();
-  return merged_at != 0xFFFFFFFFu;
+  return merged_at != 0xFFFFFFFFu ? 1 : 0;
 }
 
 __global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x) {
@@ -1127,8 +1147,9 @@ __global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x) {
       long long qlo = 0x7FFFFFFFFFFFFFFFLL, qhi = -1;
       const long long b = E0 + (long long)v.c * x.chunk;
       const long long e = min(E0 + B, b + x.chunk);
-      const bool merged = rerun_chunk_staged(x, w, b, e, E0, s_start, sdp[wid], srn[wid], ssq[wid], qlo, qhi);
-      if (lane == 0) {
+      const int how = rerun_chunk_staged(x, w, b, e, E0, s_start, sdp[wid], srn[wid], ssq[wid], qlo, qhi);
+      const bool merged = how == 1;
+      if (lane == 0 && how != 2) {
         ChunkRec r = x.ch[v.c];   // merged: the recorded end state stands
         r.st_s = v.s;
         r.st_q = v.q;

@@ -490,6 +490,8 @@ __global__ void k_init_state(DevState *s, long long q0) {
   s->qtmin = q0;
   s->qtmax = q0;
   s->epoch = 1;
+  s->pred_q = q0;
+  s->pred_geo = 1;
 }
 
 __global__ void k_fill_ll(long long *p, long long n, long long v) {
