@@ -74,9 +74,14 @@ struct BatchState {
   unsigned vpad;
   long long n_raw;     // raw events of the batch, set by k_stage (graphs are captured per size class)
   unsigned nclosed;    // k_posinfo blocks done (the last one closes the batch)
-  int geo_next;        // a fixed point of this batch lay far from its candidates: the next batch adds the geometric ones
-  int gpad;
-  long long s_pred;    // the window start the batch's anchors counted from (DevState.pred_s when they ran)
+  int geo_next;        // (unused)
+  // The state the batch's anchors count their candidate windows against: a
+  // predicted window at the batch start with exact distinct counts, written by
+  // the previous batch's anchors (k_predict) -- so anchors never wait for the
+  // previous window run or verifier.  p_geo: add the geometric candidates.
+  int p_geo;
+  long long p_s, p_q, p_np, p_nt;
+  long long s_anchor;  // p_s as the batch's anchors used it (k_window_run reads this copy)
 };
 
 // Window / counter state living in device memory so no kernel needs a host
@@ -113,11 +118,7 @@ struct DevState {
   unsigned nlong, nlong_pad;   // long pixel segments of the batch
   long long dbg_bad;           // FIBAR_DEBUG_WINDOW: anchor counts that disagreed with a serial recount
   long long Ein;               // in-bounds events ingested (the ingest's running E, ahead of E)
-  // the next batch's anchors run before this batch's verifier: they count
-  // candidate windows against the speculative end state of this batch's last
-  // chunk (exact distinct counts for that window, whatever the verifier finds)
-  long long pred_s, pred_q, pred_np, pred_nt;
-  int pred_geo, pred_pad;
+
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {

@@ -177,8 +177,10 @@ struct fibar_engine {
   Item *item2[NPAR] = {};
   PosRec *posrec2[NPAR] = {};
   float *t2_2[NPAR] = {};
-  int2 *anc = nullptr, *anc2 = nullptr, *anc0 = nullptr;
-  long long *lc = nullptr, *lu = nullptr;
+  // window candidates, per buffer set (a batch's anchors run while the
+  // previous batch's window run still reads its own)
+  int2 *anc3[NPAR] = {}, *anc23[NPAR] = {}, *anc03[NPAR] = {};
+  long long *lc3[NPAR] = {}, *lu3[NPAR] = {};
   ChunkRec *ch = nullptr;
   VRec *vl = nullptr;
   SelState *sel = nullptr;
@@ -264,6 +266,7 @@ struct fibar_engine {
   int blur_grid = 148;
   int chunk = 64, warm = 64, debug = 0;
   bool warm_set = false;   // FIBAR_WARM given: used for every batch size
+  int run_smem = 0;        // FIBAR_RUN_SMEM: dynamic shared memory reserved by each k_window_run block (experiment)
   // batches up to this size use 32-event speculation chunks: a small batch
   // leaves most SMs idle, so shorter serial chunk runs win over the extra
   // anchors and re-runs (config 3, 100k batches: 214 -> 227 Mev/s; 1M-event
@@ -313,6 +316,7 @@ struct fibar_engine {
     x.plast = plast;
     x.wcnt = wcnt;
     x.bs = bsd ? bsd + par : nullptr;
+    x.bsn = bsd ? bsd + (par + 1) % NPAR : nullptr;
     x.last_tile = last_tile;
     x.ptt = ptt2[par];
     x.rkey = rkey;
@@ -358,11 +362,11 @@ struct fibar_engine {
     x.hout_bot = hout_bot;
     x.hslot = hslot;
     x.hin = nullptr;
-    x.anc = anc;
-    x.anc2 = anc2;
-    x.anc0 = anc0;
-    x.lc = lc;
-    x.lu = lu;
+    x.anc = anc3[par];
+    x.anc2 = anc23[par];
+    x.anc0 = anc03[par];
+    x.lc = lc3[par];
+    x.lu = lu3[par];
     x.ch = ch;
     x.vl = vl;
     return x;
@@ -390,7 +394,7 @@ int init_state(fibar_engine *g) {
   join_blur(g);
   g->last_b = -1;
   for (bool &u : g->b_used) u = false;
-  fibar_launch(g->L, "init", k_init_state, 1, 1, 0, s, g->st, g->q0);
+  fibar_launch(g->L, "init", k_init_state, 1, 1, 0, s, g->st, g->q0, g->bsd, NPAR);
   CK(cudaMemsetAsync(g->pbar, 0, sizeof(float) * g->n_pix, s));
   CK(cudaMemsetAsync(g->l, 0, sizeof(float) * g->n_pix, s));
   if (g->spatial) {
@@ -456,12 +460,14 @@ int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, co
 int enqueue_anchors(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s) {
   Launcher &L = g->L;
   Ctx x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+  // chunks 1..T: chunk T ends at the batch end (the next batch's prediction)
   const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
-  fibar_launch(L, "anchor", k_anchor, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
+  fibar_launch(L, "anchor", k_anchor, (int)(((long long)(T + 1) * 32 + TPB - 1) / TPB), TPB, 0, s, x);
   fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
-  fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, g->anc, NCAND);
-  fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)T * 32 + TPB - 1) / TPB), TPB, 0, s, x);
-  fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, g->anc2, NFINE);
+  fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, x.anc, NCAND);
+  fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)(T + 1) * 32 + TPB - 1) / TPB), TPB, 0, s, x);
+  fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, x.anc2, NFINE);
+  fibar_launch(L, "predict", k_predict, 1, 1, 0, s, x);
   CK(cudaGetLastError());
   return 0;
 }
@@ -476,7 +482,7 @@ int enqueue_chain(fibar_engine *g, long long n_raw, int par, int where, cudaStre
     fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);   // (filter ON: in k_window_run)
   } else {
     const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
-    fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, 0, s, x);
+    fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, (size_t)g->run_smem, s, x);
     // an external event-record node when captured (the next batch's anchors,
     // on another stream, wait on it)
     if (ev_run) {
@@ -570,7 +576,7 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     L.stream = g->capstream;
     const int rc = part == 0   ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where,
                                                 &g->bsd[par].n_raw)
-                   : part == 1 ? enqueue_chain(g, n_raw, par, ge.where, g->capstream, x, g->evR[par])
+                   : part == 1 ? enqueue_chain(g, n_raw, par, ge.where, g->capstream, x, nullptr)
                    : part == 2 ? enqueue_post(g, n_raw, par, ge.where, g->capstream)
                                : enqueue_anchors(g, n_raw, par, ge.where, g->capstream);
     L.stream = s0;
@@ -653,7 +659,6 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       // anchors after the ingest and the previous batch's run
       cudaStream_t sn = g->nstream;
       CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
-      if (g->r_par >= 0) CK(cudaStreamWaitEvent(sn, g->evR[g->r_par], 0));
       CK(cudaGraphLaunch(ge->exec4, sn));
       L.launches += ge->kernels4;
       CK(cudaEventRecord(g->evN[par], sn));
@@ -680,7 +685,6 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaEventRecord(g->evA[par], sa));
       cudaStream_t sn = g->nstream;
       CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
-      if (g->r_par >= 0) CK(cudaStreamWaitEvent(sn, g->evR[g->r_par], 0));
       L.stream = sn;
       rc = enqueue_anchors(g, n_raw, par, where, sn);
       L.stream = u;
@@ -688,7 +692,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaEventRecord(g->evN[par], sn));
       CK(cudaStreamWaitEvent(s, g->evN[par], 0));
       L.stream = s;
-      rc = enqueue_chain(g, n_raw, par, where, s, x, g->evR[par]);
+      rc = enqueue_chain(g, n_raw, par, where, s, x, nullptr);
       L.stream = u;
       if (rc) return rc;
       g->r_par = par;
@@ -1128,6 +1132,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // small batches (<= small_chunk_max) warm up 32 events: the verifier
   // re-runs the extra misses cheaply (config 3: 270 -> 280 Mev/s)
   if (const char *v = getenv("FIBAR_TRACE")) g->trace = atoi(v) != 0;
+  if (const char *v = getenv("FIBAR_RUN_SMEM")) {
+    g->run_smem = std::max(0, atoi(v));
+    if (g->run_smem > 48 * 1024) cudaFuncSetAttribute(k_window_run, cudaFuncAttributeMaxDynamicSharedMemorySize, g->run_smem);
+  }
   if (const char *v = getenv("FIBAR_WARM")) {
     g->warm = std::max(0, atoi(v));
     g->warm_set = true;
@@ -1313,11 +1321,13 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       rc |= dalloc(&g->colist2[c], n + 1);
     }
     g->prep = g->prep2[0];
-    rc |= dalloc(&g->anc, T * NCAND);
-    rc |= dalloc(&g->anc2, T * NFINE);
-    rc |= dalloc(&g->anc0, T);
-    rc |= dalloc(&g->lc, T);
-    rc |= dalloc(&g->lu, T);
+    for (int c = 0; c < NPAR; ++c) {
+      rc |= dalloc(&g->anc3[c], (T + 1) * NCAND);
+      rc |= dalloc(&g->anc23[c], (T + 1) * NFINE);
+      rc |= dalloc(&g->anc03[c], T + 1);
+      rc |= dalloc(&g->lc3[c], T + 1);
+      rc |= dalloc(&g->lu3[c], T + 1);
+    }
     rc |= dalloc(&g->ch, T);
     rc |= dalloc(&g->vl, 2 * T);   // the verifier's lists, by round parity
   }
@@ -1350,7 +1360,7 @@ int fibar_destroy(fibar_engine *g) {
     if (st) cudaStreamSynchronize(st);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p, g->blockcnt, g->longseg, g->hist,
-                  g->bv64, g->mv64, g->anc, g->anc2, g->anc0, g->lc, g->lu, g->ch, g->vl, g->sel, g->frame,
+                  g->bv64, g->mv64, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1368,7 +1378,7 @@ int fibar_destroy(fibar_engine *g) {
   for (int c = 0; c < NPAR; ++c) {
     void *per[] = {g->pt2[c], g->ekey2[c], g->ka2[c], g->va2[c], g->kb2[c], g->vb2[c], g->item2[c], g->posrec2[c],
                    g->t2_2[c], g->ptt2[c], g->dp2[c], g->prep2[c], g->colist2[c], g->epol2[c], g->spol2[c],
-                   g->S2[c], g->Qt2[c], g->pmap2[c]};
+                   g->S2[c], g->Qt2[c], g->pmap2[c], g->anc3[c], g->anc23[c], g->anc03[c], g->lc3[c], g->lu3[c]};
     for (void *p : per)
       if (p) cudaFree(p);
     for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evA[c], g->evV[c], g->evN[c], g->evR[c]})

@@ -154,7 +154,6 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->qlo = 0x7FFFFFFFFFFFFFFFLL;
     b->qhi = -1;
     b->nclosed = 0;
-    b->geo_next = 0;
   }
 }
 
@@ -370,6 +369,12 @@ __device__ __forceinline__ long long chunk_warm_start(const Ctx &x, long long E0
   return max(E0, E0 + (long long)c * x.chunk - x.warm);
 }
 
+// where chunk c's candidate windows end: its warm-up start, or for the extra
+// chunk c == T (the prediction for the next batch) the batch's end
+__device__ __forceinline__ long long anchor_at(const Ctx &x, long long E0, long long B, int c, int T) {
+  return c < T ? chunk_warm_start(x, E0, c) : E0 + B;
+}
+
 // coarse candidate i: a dense linear grid around the batch-start target q0
 // plus a geometric one that reaches windows far from it (cold start, scene change)
 __device__ __forceinline__ long long cand_len(const Ctx &x, long long q0, int i) {
@@ -449,18 +454,22 @@ __device__ __forceinline__ long long regulate_fast(const Ctx &x, long long len, 
 // chunk's window of the same candidate (one warp per chunk).
 __global__ void __launch_bounds__(TPB) k_anchor(Ctx x) {
   pdl_wait();
-  // counted against the previous batch's predicted end state (DevState.pred_*)
-  if (blockIdx.x == 0 && threadIdx.x == 0) x.bs->s_pred = x.st->pred_s;   // read from the next kernel on
+  // counted against the predicted start state (bs->p_*); chunks 1..T, T being
+  // the batch end (the next batch's prediction)
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    x.bsn->p_geo = 0;              // set by k_anchor2 if a fixed point is unsettled
+    x.bs->s_anchor = x.bs->p_s;    // (the window run reads this copy: p_s is rewritten three batches on)
+  }
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
-  if (c >= T) return;
-  const long long E0 = x.bs->E0, s0 = x.st->pred_s, q0 = x.st->pred_q;
-  const int nc = x.st->pred_geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
-  const long long a = chunk_warm_start(x, E0, c);
+  if (c > T) return;
+  const long long E0 = x.bs->E0, s0 = x.bs->p_s, q0 = x.bs->p_q;
+  const int nc = x.bs->p_geo ? NCAND : NLIN;   // geometric candidates only after an unsettled batch
+  const long long a = anchor_at(x, E0, B, c, T);
   const long long Jc = a - 1;
-  const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
+  const long long ap = c == 1 ? E0 : anchor_at(x, E0, B, c - 1, T);
   const long long Jp = ap - 1;
   int cp[NCAND], ct[NCAND];
   int c0p = 0, c0t = 0;   // the no-pop window [s0, Jc] (a growing window: no eviction yet in the batch)
@@ -516,11 +525,11 @@ __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x) {
   __shared__ int red[2][TPB / 32];
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
-  if (T < 2) return;
+  if (T < 1) return;
   const int i = blockIdx.y;
-  if (i >= (x.st->pred_geo ? NCAND : NLIN)) return;
-  const long long E0 = x.bs->E0, s0 = x.bs->s_pred, q0 = x.st->pred_q;
-  const long long a = chunk_warm_start(x, E0, 1);
+  if (i >= (x.bs->p_geo ? NCAND : NLIN)) return;
+  const long long E0 = x.bs->E0, s0 = x.bs->p_s, q0 = x.bs->p_q;
+  const long long a = anchor_at(x, E0, B, 1, T);
   const long long Jc = a - 1;
   const long long sn = max(s0, a - cand_len(x, q0, i));
   int cp = 0, ct = 0;
@@ -563,14 +572,14 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
     i = 0;
   }
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  int2 carry = make_int2((int)x.st->pred_np, (int)x.st->pred_nt);
-  for (int base = 1; base < T; base += 1024 * PER) {
+  int2 carry = make_int2((int)x.bs->p_np, (int)x.bs->p_nt);
+  for (int base = 1; base <= T; base += 1024 * PER) {
     const int c0 = base + threadIdx.x * PER;
     int2 v[PER];
     int2 tsum = make_int2(0, 0);
 #pragma unroll
     for (int r = 0; r < PER; ++r) {
-      v[r] = c0 + r < T ? anc[(long long)(c0 + r) * nc + i] : make_int2(0, 0);
+      v[r] = c0 + r <= T ? anc[(long long)(c0 + r) * nc + i] : make_int2(0, 0);
       tsum.x += v[r].x;
       tsum.y += v[r].y;
     }
@@ -605,7 +614,7 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
     for (int r = 0; r < PER; ++r) {
       run.x += v[r].x;
       run.y += v[r].y;
-      if (c0 + r < T) anc[(long long)(c0 + r) * nc + i] = run;
+      if (c0 + r <= T) anc[(long long)(c0 + r) * nc + i] = run;
     }
     carry.x += wt[32].x;
     carry.y += wt[32].y;
@@ -620,16 +629,16 @@ __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc) 
 // that fixed point and never far beyond it, so the first unstable fine
 // candidate above the largest stable one is a start that collapses onto the
 // true trajectory within a handful of events, with few evictions.
-__device__ void fixed_point(const Ctx &x, int c, long long &Lout, long long &uout, bool &unsettled) {
-  const long long E0 = x.bs->E0, s0 = x.bs->s_pred, q0 = x.st->pred_q;
-  const long long a = chunk_warm_start(x, E0, c);
+__device__ void fixed_point(const Ctx &x, int c, int T, long long &Lout, long long &uout, bool &unsettled) {
+  const long long E0 = x.bs->E0, s0 = x.bs->p_s, q0 = x.bs->p_q;
+  const long long a = anchor_at(x, E0, x.bs->B, c, T);
   unsettled = false;
   if (c == 0 || a == E0) {
     Lout = a - s0;
     uout = 32;
     return;
   }
-  const int nc = x.st->pred_geo ? NCAND : NLIN;
+  const int nc = x.bs->p_geo ? NCAND : NLIN;
   long long lens[NCAND], fs[NCAND];
 #pragma unroll 1
   for (int i = 0; i < nc; ++i) {
@@ -692,20 +701,20 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31;
   const int c = (int)((blockIdx.x * (long long)TPB + threadIdx.x) >> 5) + 1;
-  if (c >= T) return;
-  const long long E0 = x.bs->E0, s0 = x.bs->s_pred;
-  const long long ac = chunk_warm_start(x, E0, c);
-  const long long ap = c == 1 ? E0 : chunk_warm_start(x, E0, c - 1);
+  if (c > T) return;   // chunks 1..T (T: the batch end, for the next batch's prediction)
+  const long long E0 = x.bs->E0, s0 = x.bs->p_s;
+  const long long ac = anchor_at(x, E0, B, c, T);
+  const long long ap = c == 1 ? E0 : anchor_at(x, E0, B, c - 1, T);
   const long long Jc = ac - 1, Jp = ap - 1;
   // the regulator's fixed points of this chunk (lane 0) and the previous one
   // (lane 1), from the coarse counts; this chunk's goes to the window run
   long long fpL = 0, fpU = 32;
   bool uns = false;
-  if (lane < 2 && !(lane == 1 && c == 1)) fixed_point(x, c - lane, fpL, fpU, uns);
+  if (lane < 2 && !(lane == 1 && c == 1)) fixed_point(x, c - lane, T, fpL, fpU, uns);
   if (lane == 0) {
     x.lc[c] = fpL;
     x.lu[c] = fpU;
-    if (uns) x.bs->geo_next = 1;
+    if (uns) x.bsn->p_geo = 1;
   }
   const long long lcc = __shfl_sync(0xffffffffu, fpL, 0), lcp = c == 1 ? 0 : __shfl_sync(0xffffffffu, fpL, 1);
   const long long luc = __shfl_sync(0xffffffffu, fpU, 0), lup = c == 1 ? 32 : __shfl_sync(0xffffffffu, fpU, 1);
@@ -746,6 +755,49 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
   }
 }
 
+// The next batch's start prediction: the batch-end "chunk" T's start chosen
+// exactly as k_window_run chooses a chunk start (the first unstable fine
+// candidate above the largest stable one, or the no-pop window when stable),
+// with its exact counts and regulated target.  One thread.
+__global__ void k_predict(Ctx x) {
+  pdl_wait();
+  BatchState *b = x.bs, *n = x.bsn;
+  const long long B = b->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  if (T == 0) {   // an empty batch: the same start
+    n->p_s = b->p_s;
+    n->p_q = b->p_q;
+    n->p_np = b->p_np;
+    n->p_nt = b->p_nt;
+    n->p_geo = b->p_geo;
+    return;
+  }
+  const long long s0 = b->p_s, a = b->E0 + B;
+  const long long center = x.lc[T], unit = x.lu[T];
+  int jstar = -1;
+#pragma unroll 1
+  for (int j = 0; j < NFINE; ++j) {
+    const long long sc = fine_start(x, s0, a, center, unit, j);
+    const int2 cnt = x.anc2[(long long)T * NFINE + j];
+    const long long len = a - sc;
+    if (cnt.x >= 1 && cnt.y >= 1 && regulate_fast(x, len, cnt.x, cnt.y) >= len) jstar = j;
+  }
+  const int g = jstar + 1 < NFINE ? jstar + 1 : NFINE - 1;
+  int2 cnt = x.anc2[(long long)T * NFINE + g];
+  long long ss = fine_start(x, s0, a, center, unit, g);
+  const int2 c0 = x.anc0[T];
+  const long long len0 = a - s0;
+  if (c0.x >= 1 && c0.y >= 1 && regulate_fast(x, len0, c0.x, c0.y) >= len0) {
+    ss = s0;
+    cnt = c0;
+  }
+  const long long len = a - ss;
+  n->p_s = ss;
+  n->p_q = (cnt.x >= 1 && cnt.y >= 1) ? regulate_fast(x, len, cnt.x, cnt.y) : len;
+  n->p_np = cnt.x;
+  n->p_nt = cnt.y;
+}
+
 // One lane per chunk, the warp stepping its lanes' events in lockstep.  Each
 // lane starts from the longest candidate window just past the regulator's
 // fixed point (a too-long window collapses to the true one within a few
@@ -755,10 +807,7 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
 
 __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   pdl_wait();
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    open_batch(x);                        // the batch's true start (after the previous verifier)
-    x.st->pred_geo = x.bs->geo_next;      // the next batch's candidate set
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) open_batch(x);   // the batch's true start (after the previous verifier)
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int c = blockIdx.x * 128 + threadIdx.x;
@@ -768,7 +817,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   const DevState s = *x.st;
   const long long E0 = x.bs->E0;
   const long long s_true = s.s;             // chunk 0 starts exactly here
-  const long long s_start0 = x.bs->s_pred;  // the anchors' start: candidate windows are clamped to it
+  const long long s_start0 = x.bs->s_anchor;   // the anchors' start: candidate windows are clamped to it
   const long long b = E0 + (long long)c * x.chunk;
   const long long e = valid ? min(E0 + B, b + x.chunk) : b;
   const long long a = valid ? chunk_warm_start(x, E0, c) : b;
@@ -967,13 +1016,6 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   r.qlo = qlo;
   r.qhi = qhi;
   x.ch[c] = r;
-  if (c == T - 1) {   // the next batch's anchors count against this speculative end
-    DevState *d = x.st;
-    d->pred_s = w.s;
-    d->pred_q = w.q;
-    d->pred_np = w.npix;
-    d->pred_nt = w.ntiles;
-  }
 }
 
 // Verify chunk boundaries: a chunk is exact once its speculative start state
@@ -1226,8 +1268,7 @@ __global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x) {
     s->chunks += T;
     s->fix_rounds += rounds;
     s->mismatch += reruns;
-    // the next batch's candidate set (its anchors run right after this kernel)
-    if (B > 0) s->geo = bs->geo_next;
+
   }
 }
 

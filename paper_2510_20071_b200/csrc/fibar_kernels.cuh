@@ -96,6 +96,7 @@ struct Ctx {
   int use_gain, blur_on, spatial;
   DevState *st;
   BatchState *bs;     // this batch's scalars (parity buffer)
+  BatchState *bsn;    // the next batch's (its anchors' predicted start state is written here)
   long long *plast;   // per pixel: last event index before the batch
   unsigned *wcnt;     // per pixel: exact in-window event count (saturation check)
   float *pbar, *l;
@@ -174,6 +175,7 @@ __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks);
 __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
 __global__ void k_batch_begin(Ctx x);
 __global__ void k_ingest_end(Ctx x);
+__global__ void k_predict(Ctx x);
 __global__ void __launch_bounds__(TPB) k_stage(const uint16_t *sx, const uint16_t *sy, const int8_t *sp, long long n,
                                                uint16_t *dx, uint16_t *dy, int8_t *dp, long long *n_dev);
 __global__ void __launch_bounds__(TPB) k_gather(const GatherTable tab, uint16_t *dx, uint16_t *dy, int8_t *dp);
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(TPB) k_evf1_times(const unsigned *__restrict__
 __global__ void k_active_counts(Ctx x, unsigned *cnt);
 __global__ void k_tile_counts(Ctx x, const unsigned *cnt, unsigned *tcnt);
 __global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy);
-__global__ void k_init_state(DevState *s, long long q0);
+__global__ void k_init_state(DevState *s, long long q0, BatchState *bs, int nbs);
 __global__ void k_fill_ll(long long *p, long long n, long long v);
 __global__ void k_init_pt(PixRec *p, long long *plast, long long n);
 

@@ -482,16 +482,21 @@ __global__ void k_ring_xy(Ctx x, uint16_t *qx, uint16_t *qy) {
   }
 }
 
-__global__ void k_init_state(DevState *s, long long q0) {
+__global__ void k_init_state(DevState *s, long long q0, BatchState *bs, int nbs) {
   pdl_wait();
+  for (int i = 0; i < nbs; ++i) {   // every batch's anchors may start from the initial state
+    bs[i].p_s = 0;
+    bs[i].p_q = q0;
+    bs[i].p_np = 0;
+    bs[i].p_nt = 0;
+    bs[i].p_geo = 1;
+  }
   memset(s, 0, sizeof(DevState));
   s->geo = 1;
   s->q = q0;
   s->qtmin = q0;
   s->qtmax = q0;
   s->epoch = 1;
-  s->pred_q = q0;
-  s->pred_geo = 1;
 }
 
 __global__ void k_fill_ll(long long *p, long long n, long long v) {

@@ -126,18 +126,24 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
   if (carry != FIBAR_NONE) x.item[carry].runpos = (unsigned)i;
   float pb = x.pbar[c], lv = x.l[c];
   const float g = x.use_gain ? x.gain[c] : 1.0f;
-  for (long long pos = i; pos < end; pos += GROUP) {
-    int8_t pol[GROUP];
-    unsigned bidx[GROUP];
+  // inputs in groups of RGROUP positions, the next group's loads in flight
+  // while this group's chain runs (a segment of hundreds of events runs at
+  // the arithmetic chain's speed, not one L2 round trip per group)
+  constexpr int RGROUP = 16;
+  int8_t pa[RGROUP], pbuf[RGROUP];
+  unsigned ba[RGROUP], bbuf[RGROUP];
+  auto load = [&](long long q0, int8_t (&pol)[RGROUP], unsigned (&bi)[RGROUP]) {
 #pragma unroll
-    for (int u = 0; u < GROUP; ++u) {
-      const long long q = pos + u;
+    for (int u = 0; u < RGROUP; ++u) {
+      const long long q = q0 + u;
       pol[u] = q < end ? x.spol[q] : (int8_t)0;
-      bidx[u] = q < end ? x.posrec[q].bidx : FIBAR_NONE;
+      bi[u] = q < end ? x.posrec[q].bidx : FIBAR_NONE;
     }
+  };
+  auto step = [&](long long q0, const int8_t (&pol)[RGROUP], const unsigned (&bi)[RGROUP]) {
 #pragma unroll
-    for (int u = 0; u < GROUP; ++u) {
-      const long long q = pos + u;
+    for (int u = 0; u < RGROUP; ++u) {
+      const long long q = q0 + u;
       if (q >= end) break;
       const float p = (float)pol[u];
       pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
@@ -147,11 +153,23 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
       lv = faddr(fmulr(x.beta, lv), tt);
       x.t2[q] = tt;
       *reinterpret_cast<uint2 *>(&x.posrec[q].runbase) = make_uint2(carry, __float_as_uint(lv));
-      if (bidx[u] != FIBAR_NONE) {
-        carry = bidx[u];
-        if (q + 1 < end) x.item[bidx[u]].runpos = (unsigned)(q + 1);
+      if (bi[u] != FIBAR_NONE) {
+        carry = bi[u];
+        if (q + 1 < end) x.item[bi[u]].runpos = (unsigned)(q + 1);
       }
     }
+  };
+  long long pos = i;
+  load(pos, pa, ba);
+  while (pos < end) {
+    const long long nx = pos + RGROUP;
+    if (nx < end) load(nx, pbuf, bbuf);
+    step(pos, pa, ba);
+    if (nx >= end) break;
+    const long long nn = nx + RGROUP;
+    if (nn < end) load(nn, pa, ba);
+    step(nx, pbuf, bbuf);
+    pos = nn;
   }
   x.pbar[c] = pb;
 }
@@ -175,23 +193,39 @@ __device__ __forceinline__ void iir_step(const Ctx &x, float &pb, float &lv, flo
 }
 
 // replay [q0, q1) from (pb, lv), writing the per-position outputs; inputs are
-// loaded GROUP at a time so the chain waits on one load per group
+// loaded PGROUP at a time with the next group's loads in flight while this
+// group's chain runs
 __device__ __forceinline__ void replay_piece(const Ctx &x, long long q0, long long q1, float &pb, float &lv, float g,
                                              bool write) {
-  for (long long q = q0; q < q1; q += GROUP) {
-    int8_t pol[GROUP];
+  constexpr int PGROUP = 16;
+  int8_t pa[PGROUP], pbuf[PGROUP];
+  auto load = [&](long long s0, int8_t (&pol)[PGROUP]) {
 #pragma unroll
-    for (int u = 0; u < GROUP; ++u) pol[u] = q + u < q1 ? x.spol[q + u] : (int8_t)0;
+    for (int u = 0; u < PGROUP; ++u) pol[u] = s0 + u < q1 ? x.spol[s0 + u] : (int8_t)0;
+  };
+  auto step = [&](long long s0, const int8_t (&pol)[PGROUP]) {
 #pragma unroll
-    for (int u = 0; u < GROUP; ++u) {
-      if (q + u >= q1) break;
+    for (int u = 0; u < PGROUP; ++u) {
+      if (s0 + u >= q1) break;
       float tt;
       iir_step(x, pb, lv, (float)pol[u], g, tt);
       if (write && x.spatial) {
-        x.t2[q + u] = tt;
-        x.posrec[q + u].val = lv;
+        x.t2[s0 + u] = tt;
+        x.posrec[s0 + u].val = lv;
       }
     }
+  };
+  long long q = q0;
+  if (q < q1) load(q, pa);
+  while (q < q1) {
+    const long long nx = q + PGROUP;
+    if (nx < q1) load(nx, pbuf);
+    step(q, pa);
+    if (nx >= q1) break;
+    const long long nn = nx + PGROUP;
+    if (nn < q1) load(nn, pa);
+    step(nx, pbuf);
+    q = nn;
   }
 }
 
