@@ -267,6 +267,7 @@ struct fibar_engine {
   int chunk = 64, warm = 64, debug = 0;
   bool warm_set = false;   // FIBAR_WARM given: used for every batch size
   int run_smem = 0;        // FIBAR_RUN_SMEM: dynamic shared memory reserved by each k_window_run block (experiment)
+  int vf_ctas = VF_CTAS;   // FIBAR_VF_CTAS: CTAs of the verifier's cluster (<= 16)
   // batches up to this size use 32-event speculation chunks: a small batch
   // leaves most SMs idle, so shorter serial chunk runs win over the extra
   // anchors and re-runs (config 3, 100k batches: 214 -> 227 Mev/s; 1M-event
@@ -494,7 +495,7 @@ int enqueue_chain(fibar_engine *g, long long n_raw, int par, int where, cudaStre
         CK(cudaEventRecord(ev_run, s));
     }
     // one cluster (cluster barriers between its rounds' phases)
-    fibar_launch_cluster(L, "window_verify", k_window_verify, VF_CTAS, VF_TPB, 0, s, x);
+    fibar_launch_cluster(L, "window_verify", k_window_verify, g->vf_ctas, VF_TPB, 0, s, x);
   }
   CK(cudaGetLastError());
   return 0;
@@ -1132,6 +1133,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // small batches (<= small_chunk_max) warm up 32 events: the verifier
   // re-runs the extra misses cheaply (config 3: 270 -> 280 Mev/s)
   if (const char *v = getenv("FIBAR_TRACE")) g->trace = atoi(v) != 0;
+  if (const char *v = getenv("FIBAR_VF_CTAS")) g->vf_ctas = std::min(16, std::max(1, atoi(v)));
   if (const char *v = getenv("FIBAR_RUN_SMEM")) {
     g->run_smem = std::max(0, atoi(v));
     if (g->run_smem > 48 * 1024) cudaFuncSetAttribute(k_window_run, cudaFuncAttributeMaxDynamicSharedMemorySize, g->run_smem);
@@ -1300,8 +1302,11 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       int fp = hi;
       if (const char *v = getenv("FIBAR_FRONT_PRIO")) fp = atoi(v) ? hi : lo;
       cudaStreamCreateWithPriority(&g->fstream, cudaStreamNonBlocking, fp);
-      cudaStreamCreateWithPriority(&g->pstream, cudaStreamNonBlocking, fp);
-      cudaStreamCreateWithPriority(&g->nstream, cudaStreamNonBlocking, fp);
+      // the eviction pass and the anchors run beside the chain: low priority
+      int op = lo;
+      if (const char *v = getenv("FIBAR_SIDE_PRIO")) op = atoi(v) ? hi : lo;
+      cudaStreamCreateWithPriority(&g->pstream, cudaStreamNonBlocking, op);
+      cudaStreamCreateWithPriority(&g->nstream, cudaStreamNonBlocking, op);
       cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, lo);
     }
     rc |= dalloc(&g->last_tile, g->n_tiles);
