@@ -190,10 +190,17 @@ def kernel_bytes(name, B, P, D, NB, n_pix):
     return table.get(name)
 
 
+def workload_class(name: str) -> str:
+    """The workload string without its event count: per-launch traffic of a
+    device batch does not depend on how long the stream is."""
+    parts = name.split(",")
+    return ",".join(p for p in parts if not p.endswith("M events"))
+
+
 def committed_traffic(kernel: str, workload_name: str, batch_cap: int):
     """DRAM bytes per launch of `kernel` from the latest committed ncu --set full
     capture (profiles/*_traffic.json, written by scripts/summarize_ncu.py) --
-    only when that capture was taken on this exact workload and device batch."""
+    only when that capture was taken on this workload class and device batch."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
     for f in reversed(files):
@@ -201,7 +208,7 @@ def committed_traffic(kernel: str, workload_name: str, batch_cap: int):
             d = json.load(open(f))
         except (OSError, ValueError):
             continue
-        if d.get("workload") != workload_name or d.get("device_batch_cap") != batch_cap:
+        if d.get("workload_class") != workload_class(workload_name) or d.get("device_batch_cap") != batch_cap:
             continue
         v = d.get("bytes_per_launch", {}).get(kernel)
         if v:
@@ -317,6 +324,8 @@ def run_ours(args, rank, world, dist):
     if args.profile_only:
         step_device()
         torch.cuda.synchronize()
+        print(json.dumps({"workload_class": workload_class(name), "device_batch_cap": args.batch_cap,
+                          "batches": eng.stats()["batches"]}))
         return None
 
     # host arm: pinned host columns, numpy views per packet

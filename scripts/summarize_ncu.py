@@ -1,9 +1,11 @@
 """Summarise ncu outputs into profiles/ (tracked).
 
-    python scripts/summarize_ncu.py TAG
+    python scripts/summarize_ncu.py TAG "WORKLOAD CLASS" DEVICE_BATCH_CAP "COMMAND" [BATCHES]
 reads gpurun_out/launches_TAG.csv (gpu__time_duration.sum launch list) and
-gpurun_out/full_TAG.ncu-rep (--set full capture), writes profiles/TAG_launches.md
-and profiles/TAG_ncu_full.md.
+gpurun_out/full_TAG.ncu-rep (--set full capture), writes profiles/TAG_launches.md,
+profiles/TAG_ncu_full.md and profiles/TAG_traffic.json (per-launch DRAM bytes,
+tagged with the workload class -- bench.py's workload string without the event
+count -- and the device batch capacity, which bench.py matches before using it).
 """
 import collections
 import csv
@@ -14,6 +16,10 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag = sys.argv[1]
+wclass = sys.argv[2] if len(sys.argv) > 2 else ""
+bcap = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+command = sys.argv[4] if len(sys.argv) > 4 else ""
+nbatches = float(sys.argv[5]) if len(sys.argv) > 5 else 0.0
 out_dir = os.path.join(ROOT, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 
@@ -37,14 +43,14 @@ ours = {k: v for k, v in tot.items() if k.startswith("k_")}
 allsum = sum(ours.values())
 with open(os.path.join(out_dir, f"{tag}_launches.md"), "w") as fh:
     fh.write(f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none)\n\n")
-    fh.write("Command: `ncu --metrics gpu__time_duration.sum --clock-control none --csv "
-             "python bench.py --profile-only --events 3145728` (one step: 3 device batches of 1M events, "
-             "640x480 moving texture, filter ON, robust render). Per-launch times are cold-cache and "
-             "serialised; compare shares, not absolutes.\n\n")
+    fh.write(f"Command: `{command}`. Workload class: {wclass}; device batch capacity {bcap}. "
+             "Per-launch times are cold-cache and serialised (ncu replays each kernel alone); "
+             "compare shares, not absolutes.\n\n")
     fh.write("| kernel | launches | total us | mean us | share of our kernels |\n|---|---:|---:|---:|---:|\n")
     for k, v in sorted(ours.items(), key=lambda kv: -kv[1]):
         fh.write(f"| {k} | {cnt[k]} | {v:.1f} | {v / cnt[k]:.1f} | {v / allsum * 100:.1f}% |\n")
-    fh.write(f"\nTotal of our kernels: {allsum:.1f} us over {sum(cnt[k] for k in ours)} launches.\n")
+    fh.write(f"\nTotal of our kernels: {allsum:.1f} us over {sum(cnt[k] for k in ours)} launches"
+             + (f" ({allsum / nbatches:.1f} us per device batch over {nbatches:g} batches)" if nbatches else "") + ".\n")
 print("wrote launches summary;", len(ours), "kernels")
 
 # full capture
@@ -99,5 +105,6 @@ if os.path.exists(rep):
     import json
     with open(os.path.join(out_dir, f"{tag}_traffic.json"), "w") as fh:
         json.dump({"source": f"ncu --set full capture full_{tag}.ncu-rep (cold cache, one launch each)",
+                   "workload_class": wclass, "device_batch_cap": bcap,
                    "bytes_per_launch": {k: sum(v) / len(v) for k, v in traffic.items()}}, fh, indent=1)
     print("wrote full summary;", len(per), "kernels")
