@@ -354,6 +354,7 @@ struct fibar_engine {
     x.dbg_t = dbg_t;
     x.dbg_g = dbg_g;
     x.warm = (n_raw <= small_chunk_max && !warm_set) ? std::min(warm, 32) : warm;
+    x.fp_fused = n_raw <= small_chunk_max ? 1 : 0;
     x.halo = halo;
     x.hreg0 = halo ? hreg0 : 0;
     x.hreg1 = halo ? hreg1 : H;
@@ -466,6 +467,7 @@ int enqueue_anchors(fibar_engine *g, long long n_raw, int par, int where, cudaSt
   fibar_launch(L, "anchor", k_anchor, (int)(((long long)(T + 1) * 32 + TPB - 1) / TPB), TPB, 0, s, x);
   fibar_launch(L, "anchor_base", k_anchor_base, dim3(g->nsm / 2, NCAND), TPB, 0, s, x);
   fibar_launch(L, "anchor_scan", k_anchor_scan, NCAND + 1, 1024, 0, s, x, x.anc, NCAND);
+  if (!x.fp_fused) fibar_launch(L, "fp", k_fp, (T + TPB - 1) / TPB, TPB, 0, s, x);
   fibar_launch(L, "anchor2", k_anchor2, (int)(((long long)(T + 1) * 32 + TPB - 1) / TPB), TPB, 0, s, x);
   fibar_launch(L, "anchor_scan", k_anchor_scan, NFINE, 1024, 0, s, x, x.anc2, NFINE);
   fibar_launch(L, "predict", k_predict, 1, 1, 0, s, x);
@@ -914,7 +916,11 @@ int flush_gather(fibar_engine *g) {
   const long long n = g->dfill;
   Launcher &L = g->L;
   CK(cudaStreamWaitEvent(L.stream, g->ev_used[c], 0));   // the staging set's previous batch has read it
-  fibar_launch(L, "gather", k_gather, g->gt.n, TPB, 0, L.stream, g->gt, g->sx[c], g->sy[c], g->sp_[c]);
+  // enough CTAs per packet for ~16k events each, up to the SM count
+  long long biggest = 0;
+  for (int i = 0; i < g->gt.n; ++i) biggest = std::max(biggest, g->gt.e[i].n);
+  const int per = (int)std::max(1LL, std::min((long long)g->nsm, (biggest + 16383) / 16384));
+  fibar_launch(L, "gather", k_gather, dim3(per, g->gt.n), TPB, 0, L.stream, g->gt, g->sx[c], g->sy[c], g->sp_[c]);
   g->gt.n = 0;
   g->dfill = 0;
   g->cur ^= 1;

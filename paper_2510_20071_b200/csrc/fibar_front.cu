@@ -189,7 +189,17 @@ __global__ void __launch_bounds__(TPB) k_stage(const uint16_t *sx, const uint16_
 // destination line up, element copies otherwise.
 __global__ void __launch_bounds__(TPB) k_gather(const GatherTable tab, uint16_t *dx, uint16_t *dy, int8_t *dp) {
   pdl_wait();
-  const GatherEntry e = tab.e[blockIdx.x];
+  // packet blockIdx.y, split over gridDim.x CTAs in contiguous pieces
+  const GatherEntry ef = tab.e[blockIdx.y];
+  const long long per = (ef.n + gridDim.x - 1) / gridDim.x;
+  const long long p0 = min(ef.n, (long long)blockIdx.x * ((per + 7) & ~7LL));
+  const long long p1 = min(ef.n, p0 + ((per + 7) & ~7LL));
+  GatherEntry e = ef;
+  e.x += p0;
+  e.y += p0;
+  e.p += p0;
+  e.dst += p0;
+  e.n = p1 - p0;
   const bool vec = ((reinterpret_cast<uintptr_t>(e.x) | reinterpret_cast<uintptr_t>(e.y) |
                      reinterpret_cast<uintptr_t>(dx + e.dst) | reinterpret_cast<uintptr_t>(dy + e.dst)) & 15) == 0 &&
                    ((reinterpret_cast<uintptr_t>(e.p) | reinterpret_cast<uintptr_t>(dp + e.dst)) & 7) == 0;
@@ -685,6 +695,20 @@ __device__ void fixed_point(const Ctx &x, int c, int T, long long &Lout, long lo
   uout = unit;
 }
 
+// the fixed points of chunks 1..T, one thread each (large batches)
+__global__ void __launch_bounds__(TPB) k_fp(Ctx x) {
+  pdl_wait();
+  const int T = (int)((x.bs->B + x.chunk - 1) / x.chunk);
+  const int c = blockIdx.x * TPB + threadIdx.x + 1;
+  if (c > T) return;
+  long long L, u;
+  bool uns;
+  fixed_point(x, c, T, L, u, uns);
+  x.lc[c] = L;
+  x.lu[c] = u;
+  if (uns) x.bsn->p_geo = 1;
+}
+
 __device__ __forceinline__ long long fine_start(const Ctx &x, long long s0, long long a, long long center,
                                                 long long unit, int j) {
   long long L = center + c_fine_mul[j] * unit;
@@ -710,11 +734,16 @@ __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x) {
   // (lane 1), from the coarse counts; this chunk's goes to the window run
   long long fpL = 0, fpU = 32;
   bool uns = false;
-  if (lane < 2 && !(lane == 1 && c == 1)) fixed_point(x, c - lane, T, fpL, fpU, uns);
-  if (lane == 0) {
-    x.lc[c] = fpL;
-    x.lu[c] = fpU;
-    if (uns) x.bsn->p_geo = 1;
+  if (x.fp_fused) {   // small batches: no separate launch (k_fp computes them for large ones)
+    if (lane < 2 && !(lane == 1 && c == 1)) fixed_point(x, c - lane, T, fpL, fpU, uns);
+    if (lane == 0) {
+      x.lc[c] = fpL;
+      x.lu[c] = fpU;
+      if (uns) x.bsn->p_geo = 1;
+    }
+  } else if (lane < 2 && !(lane == 1 && c == 1)) {
+    fpL = x.lc[c - lane];
+    fpU = x.lu[c - lane];
   }
   const long long lcc = __shfl_sync(0xffffffffu, fpL, 0), lcp = c == 1 ? 0 : __shfl_sync(0xffffffffu, fpL, 1);
   const long long luc = __shfl_sync(0xffffffffu, fpU, 0), lup = c == 1 ? 32 : __shfl_sync(0xffffffffu, fpU, 1);

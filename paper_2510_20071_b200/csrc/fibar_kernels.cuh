@@ -135,6 +135,7 @@ struct Ctx {
   unsigned *hslot;           // per injected item: its in-word slot
   const unsigned long long *hin;   // this round's in-words
   int chunk, warm, debug;
+  int fp_fused;               // k_anchor2 computes the chunks' fixed points itself (small batches)
   int twarm;                  // warm-up events of a speculative long-segment piece
   unsigned blur_sleep;
   unsigned long long *dbg_t, *dbg_g;
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
 __global__ void k_batch_begin(Ctx x);
 __global__ void k_ingest_end(Ctx x);
 __global__ void k_predict(Ctx x);
+__global__ void __launch_bounds__(TPB) k_fp(Ctx x);
 __global__ void __launch_bounds__(TPB) k_stage(const uint16_t *sx, const uint16_t *sy, const int8_t *sp, long long n,
                                                uint16_t *dx, uint16_t *dy, int8_t *dp, long long *n_dev);
 __global__ void __launch_bounds__(TPB) k_gather(const GatherTable tab, uint16_t *dx, uint16_t *dy, int8_t *dp);

@@ -159,17 +159,36 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
       }
     }
   };
-  long long pos = i;
-  load(pos, pa, ba);
-  while (pos < end) {
-    const long long nx = pos + RGROUP;
-    if (nx < end) load(nx, pbuf, bbuf);
-    step(pos, pa, ba);
-    if (nx >= end) break;
-    const long long nn = nx + RGROUP;
-    if (nn < end) load(nn, pa, ba);
-    step(nx, pbuf, bbuf);
-    pos = nn;
+  if (end - i <= 4) {   // the common short segment: no group machinery
+#pragma unroll 1
+    for (long long q = i; q < end; ++q) {
+      const float p = (float)x.spol[q];
+      const unsigned bq = x.posrec[q].bidx;
+      pb = faddr(fmulr(x.alpha, pb), fmulr(x.oma, p));
+      float d = fsubr(p, pb);
+      if (x.use_gain) d = fmulr(d, g);
+      const float tt = fmulr(x.h, d);
+      lv = faddr(fmulr(x.beta, lv), tt);
+      x.t2[q] = tt;
+      *reinterpret_cast<uint2 *>(&x.posrec[q].runbase) = make_uint2(carry, __float_as_uint(lv));
+      if (bq != FIBAR_NONE) {
+        carry = bq;
+        if (q + 1 < end) x.item[bq].runpos = (unsigned)(q + 1);
+      }
+    }
+  } else {
+    long long pos = i;
+    load(pos, pa, ba);
+    while (pos < end) {
+      const long long nx = pos + RGROUP;
+      if (nx < end) load(nx, pbuf, bbuf);
+      step(pos, pa, ba);
+      if (nx >= end) break;
+      const long long nn = nx + RGROUP;
+      if (nn < end) load(nn, pa, ba);
+      step(nx, pbuf, bbuf);
+      pos = nn;
+    }
   }
   x.pbar[c] = pb;
 }
