@@ -267,6 +267,8 @@ struct fibar_engine {
   int chunk = 64, warm = 64, debug = 0;
   bool warm_set = false;   // FIBAR_WARM given: used for every batch size
   int run_smem = 0;        // FIBAR_RUN_SMEM: dynamic shared memory reserved by each k_window_run block (experiment)
+  int run_g = 8;           // FIBAR_RUN_G: lanes per chunk in the window run, small batches (0: one lane per chunk, k_window_run)
+  int run_g_large = 4;     // FIBAR_RUN_G_LARGE: the same for batches above small_chunk_max
   int vf_ctas = VF_CTAS;   // FIBAR_VF_CTAS: CTAs of the verifier's cluster (<= 16)
   // batches up to this size use 32-event speculation chunks: a small batch
   // leaves most SMs idle, so shorter serial chunk runs win over the extra
@@ -485,7 +487,16 @@ int enqueue_chain(fibar_engine *g, long long n_raw, int par, int where, cudaStre
     fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);   // (filter ON: in k_window_run)
   } else {
     const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
-    fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, (size_t)g->run_smem, s, x);
+    const int G = n_raw <= g->small_chunk_max ? g->run_g : g->run_g_large;
+    if (G == 0) {
+      fibar_launch(L, "window_run", k_window_run, (T + 127) / 128, 128, (size_t)g->run_smem, s, x);
+    } else {
+      // G lanes per chunk: 32 / G chunks per warp, four warps per block
+      const int nbk = (int)(((long long)T * G + 127) / 128);
+      if (G == 8) fibar_launch(L, "window_run", k_window_run_g8, nbk, 128, 0, s, x);
+      else if (G == 4) fibar_launch(L, "window_run", k_window_run_g4, nbk, 128, 0, s, x);
+      else fibar_launch(L, "window_run", k_window_run_g2, nbk, 128, 0, s, x);
+    }
     // an external event-record node when captured (the next batch's anchors,
     // on another stream, wait on it)
     if (ev_run) {
@@ -1139,6 +1150,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // small batches (<= small_chunk_max) warm up 32 events: the verifier
   // re-runs the extra misses cheaply (config 3: 270 -> 280 Mev/s)
   if (const char *v = getenv("FIBAR_TRACE")) g->trace = atoi(v) != 0;
+  if (const char *v = getenv("FIBAR_RUN_G")) g->run_g = atoi(v);
+  if (const char *v = getenv("FIBAR_RUN_G_LARGE")) g->run_g_large = atoi(v);
+  for (int *gg : {&g->run_g, &g->run_g_large}) *gg = *gg >= 8 ? 8 : (*gg >= 4 ? 4 : (*gg >= 2 ? 2 : 0));
   if (const char *v = getenv("FIBAR_VF_CTAS")) g->vf_ctas = std::min(16, std::max(1, atoi(v)));
   if (const char *v = getenv("FIBAR_RUN_SMEM")) {
     g->run_smem = std::max(0, atoi(v));

@@ -1047,6 +1047,210 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
   x.ch[c] = r;
 }
 
+// The same run with G lanes per chunk (32 / G chunks per warp, still in
+// lockstep).  The entries a window pops are always the next ones past its
+// start, so the group keeps the G ring entries [s, s + G) in registers: lane u
+// owns the positions = u (mod G) and holds the first one at or past s, loaded
+// as soon as the previous one was popped -- the ring load leaves the step's
+// dependency chain (it overlaps the regulator of the step that issued it), an
+// eviction of up to G entries is one compare per lane and a group reduction,
+// and the fine candidates of the start state are evaluated G at a time.  Longer
+// evictions (the collapse of a too-long start window) stream 32 entries per
+// round per group.
+template <int G>
+__device__ __forceinline__ void window_run_g(const Ctx &x) {
+  pdl_wait();
+  if (blockIdx.x == 0 && threadIdx.x == 0) open_batch(x);   // the batch's true start (after the previous verifier)
+  constexpr int CPW = 32 / G;   // chunks per warp
+  constexpr int V = 32 / G;     // ring loads in flight per lane in a long eviction
+  const long long B = x.bs->B;
+  const int T = (int)((B + x.chunk - 1) / x.chunk);
+  const int lane = threadIdx.x & 31, u = lane & (G - 1);
+  const int cw = (blockIdx.x * 4 + (threadIdx.x >> 5)) * CPW;   // the warp's first chunk
+  if (cw >= T) return;   // whole warp out of range
+  const int c = cw + lane / G;
+  const bool valid = c < T;
+  const DevState s = *x.st;
+  const long long E0 = x.bs->E0;
+  const long long s_true = s.s;             // chunk 0 starts exactly here
+  const long long s_start0 = x.bs->s_anchor;   // the anchors' start: candidate windows are clamped to it
+  const long long b = E0 + (long long)c * x.chunk;
+  const long long e = valid ? min(E0 + B, b + x.chunk) : b;
+  const long long a = valid ? chunk_warm_start(x, E0, c) : b;
+  const bool spec = valid && a != E0;
+  WState w{0, 1, 0, 0, 0};
+  // the speculative start: the fine candidates, G at a time
+  int jstar = -1;
+  long long center = 0, unit = 0;
+  if (spec) {
+    center = x.lc[c];
+    unit = x.lu[c];
+#pragma unroll 1
+    for (int j = u; j < NFINE; j += G) {
+      const long long sc = fine_start(x, s_start0, a, center, unit, j);
+      const int2 cnt = x.anc2[(long long)c * NFINE + j];
+      const long long len = a - sc;
+      if (cnt.x >= 1 && cnt.y >= 1 && regulate_fast(x, len, cnt.x, cnt.y) >= len) jstar = j;
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) jstar = max(jstar, __shfl_xor_sync(0xffffffffu, jstar, o));
+  if (valid) {
+    if (!spec) {
+      w.s = s_true;
+      w.q = s.q;
+      w.npix = s.npix;
+      w.ntiles = s.ntiles;
+      w.evctr = s.evctr;
+    } else {
+      const int g = jstar + 1 < NFINE ? jstar + 1 : NFINE - 1;
+      int2 cnt = x.anc2[(long long)c * NFINE + g];
+      w.s = fine_start(x, s_start0, a, center, unit, g);
+      // a window still growing (no eviction yet in this batch) has no fixed
+      // point near the candidates: the no-pop window [s_start, a - 1] whenever
+      // that is stable (see k_window_run)
+      const int2 c0 = x.anc0[c];
+      const long long len0 = a - s_start0;
+      if (c0.x >= 1 && c0.y >= 1 && regulate_fast(x, len0, c0.x, c0.y) >= len0) {
+        w.s = s_start0;
+        cnt = c0;
+      }
+      w.npix = cnt.x;
+      w.ntiles = cnt.y;
+      const long long len = a - w.s;
+      w.q = (cnt.x >= 1 && cnt.y >= 1) ? regulate_fast(x, len, cnt.x, cnt.y) : len;
+      if (x.debug && u == 0) {
+        long long bn = 0, bt = 0;
+        for (long long k = w.s; k < a; ++k) {
+          const uint2 rr = x.rnext[(unsigned long long)k & x.Rm];
+          bn += (unsigned long long)rr.x > (unsigned long long)(a - 1 - k);
+          bt += (unsigned long long)rr.y > (unsigned long long)(a - 1 - k);
+        }
+        if (bn != w.npix || bt != w.ntiles) atomicAdd((unsigned long long *)&x.st->dbg_bad, 1ull);
+      }
+      w.evctr = (s.evctr + (a - E0)) % x.every;
+    }
+  }
+  ChunkRec r;
+  r.st_s = w.s;
+  r.st_q = w.q;
+  unsigned wpops = 0, coop = 0;
+  const unsigned n_my = (unsigned)(e - a);
+  const unsigned n_max = __reduce_max_sync(0xffffffffu, n_my);
+  // 32-bit state relative to the batch's start window, as in k_window_run
+  const long long base = min(s_start0, s_true);
+  const unsigned sofs = (unsigned)(s_true - base);
+  const unsigned bslot = (unsigned)((unsigned long long)base & x.Rm);
+  const unsigned rm = (unsigned)x.Rm;
+  unsigned sr = (unsigned)(w.s - base);
+  const unsigned ar = (unsigned)(a - base), br = (unsigned)(b - base);
+  const unsigned e0r = (unsigned)(E0 - base);
+  unsigned q = (unsigned)w.q;
+  int np = (int)w.npix, nt = (int)w.ntiles;
+  unsigned ev = (unsigned)w.evctr;
+  const unsigned every = (unsigned)x.every;
+  unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0;
+  uint2 dnext = n_my > 0 ? x.dp[ar - e0r] : make_uint2(0, 0);
+  // this lane's ring entry: the first position = u (mod G) at or past sr
+  unsigned pu = sr + (((unsigned)u - sr) & (unsigned)(G - 1));
+  uint2 en = x.rnext[(bslot + pu) & rm];
+  for (unsigned t = 0; t < n_max; ++t) {
+    const bool act = t < n_my;
+    const unsigned jr = ar + t;
+    if (act && jr == br) {
+      r.st_s = base + sr;
+      r.st_q = q;
+    }
+    unsigned hi = sr;
+    if (act) {
+      const uint2 d = dnext;
+      if (t + 1 < n_my) dnext = x.dp[jr + 1 - e0r];
+      const unsigned js = jr - sr;
+      np += d.x > js;
+      nt += d.y > js;
+      if (js + 1 > q) hi = jr + 1 - q;
+    }
+    if (jr < br) wpops += hi - sr;
+    // the eviction [sr, hi): this lane's held entry first
+    const unsigned pu0 = pu;
+    unsigned cc = 0;   // pixels in the low half, tiles in the high half
+    if (pu < hi) {
+      const unsigned dd = jr - pu;
+      cc = (en.x > dd ? 1u : 0u) | (en.y > dd ? 0x10000u : 0u);
+      pu += G;
+    }
+#pragma unroll
+    for (int o = 1; o < G; o <<= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
+    np -= (int)(cc & 0xFFFFu);
+    nt -= (int)(cc >> 16);
+    if (__ballot_sync(0xffffffffu, pu < hi)) {
+      // more than G entries somewhere in the warp: 32 per round per group
+      int cp = 0, ct = 0;
+      const unsigned n_u = pu < hi ? (hi - pu + G - 1) / G : 0u;
+      for (unsigned i = 0; i < n_u; i += V) {
+        uint2 rr[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+          rr[v] = i + v < n_u ? x.rnext[(bslot + pu + (i + v) * G) & rm] : make_uint2(0u, 0u);
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          if (i + v >= n_u) break;
+          const unsigned dd = jr - (pu + (i + v) * G);
+          cp += rr[v].x > dd;
+          ct += rr[v].y > dd;
+        }
+      }
+      pu += n_u * G;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        cp += __shfl_xor_sync(0xffffffffu, cp, o);
+        ct += __shfl_xor_sync(0xffffffffu, ct, o);
+      }
+      np -= cp;
+      nt -= ct;
+      ++coop;
+    }
+    sr = hi;
+    if (pu != pu0) en = x.rnext[(bslot + pu) & rm];   // needed once the window start passes it
+    if (act) {
+      if (++ev >= every) {
+        ev = 0;
+        if (np >= 1 && nt >= 1) {
+          q = regulate32(x, jr - sr + 1, (unsigned)np, (unsigned)nt);
+          if (jr >= br) {
+            qlo32 = min(qlo32, q);
+            qhi32 = max(qhi32, q);
+          }
+        }
+      }
+      if (jr >= br && u == 0) {
+        x.S[jr - e0r] = sr - sofs;
+        x.Qt[jr - e0r] = q;
+      }
+    }
+  }
+  {
+    const unsigned wp = __reduce_add_sync(0xffffffffu, u == 0 ? wpops : 0u);
+    const unsigned cp = __reduce_max_sync(0xffffffffu, coop);
+    if (lane == 0) {
+      atomicAdd((unsigned long long *)&x.st->warm_pops, (unsigned long long)wp);
+      atomicAdd((unsigned long long *)&x.st->coop_iters, (unsigned long long)cp);
+    }
+  }
+  if (!valid || u != 0) return;
+  r.en_s = base + sr;
+  r.en_q = q;
+  r.en_np = np;
+  r.en_nt = nt;
+  r.en_ev = ev;
+  r.qlo = qhi32 > 0 ? (long long)qlo32 : 0x7FFFFFFFFFFFFFFFLL;
+  r.qhi = qhi32 > 0 ? (long long)qhi32 : -1;
+  x.ch[c] = r;
+}
+__global__ void __launch_bounds__(128) k_window_run_g2(Ctx x) { window_run_g<2>(x); }
+__global__ void __launch_bounds__(128) k_window_run_g4(Ctx x) { window_run_g<4>(x); }
+__global__ void __launch_bounds__(128) k_window_run_g8(Ctx x) { window_run_g<8>(x); }
+
 // Verify chunk boundaries: a chunk is exact once its speculative start state
 // equals its predecessor's end state and the predecessor is exact.  Rounds
 // re-run, in parallel, every chunk whose start disagrees with its

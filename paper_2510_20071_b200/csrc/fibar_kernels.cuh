@@ -188,6 +188,9 @@ __global__ void __launch_bounds__(TPB) k_anchor_base(Ctx x);
 __global__ void __launch_bounds__(1024) k_anchor_scan(Ctx x, int2 *anc, int nc);
 __global__ void __launch_bounds__(TPB) k_anchor2(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run(Ctx x);
+__global__ void __launch_bounds__(128) k_window_run_g2(Ctx x);
+__global__ void __launch_bounds__(128) k_window_run_g4(Ctx x);
+__global__ void __launch_bounds__(128) k_window_run_g8(Ctx x);
 __global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj_map(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x);
