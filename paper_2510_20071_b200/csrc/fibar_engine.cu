@@ -267,6 +267,7 @@ struct fibar_engine {
   int chunk = 64, warm = 64, debug = 0;
   bool warm_set = false;   // FIBAR_WARM given: used for every batch size
   int run_smem = 0;        // FIBAR_RUN_SMEM: dynamic shared memory reserved by each k_window_run block (experiment)
+  bool no_reg32x = false;  // FIBAR_REG32X=0: the 64-bit regulator fix-up everywhere (measurement)
   int run_g = 8;           // FIBAR_RUN_G: lanes per chunk in the window run, small batches (0: one lane per chunk, k_window_run)
   int run_g_large = 4;     // FIBAR_RUN_G_LARGE: the same for batches above small_chunk_max
   int vf_ctas = VF_CTAS;   // FIBAR_VF_CTAS: CTAs of the verifier's cluster (<= 16)
@@ -301,6 +302,8 @@ struct fibar_engine {
     x.num = cfg.fill_num;
     x.numA = cfg.fill_num * (long long)A;
     x.den = cfg.fill_den;
+    x.reg32x = (x.numA < (1LL << 24) && x.den < (1LL << 24) && cfg.q_max < (1LL << 22) &&
+                x.den * (cfg.q_max + 2) < (1LL << 29) && !no_reg32x) ? 1 : 0;
     x.qmin = cfg.q_min;
     x.qmax = cfg.q_max;
     x.every = cfg.regulate_every;
@@ -1150,6 +1153,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // small batches (<= small_chunk_max) warm up 32 events: the verifier
   // re-runs the extra misses cheaply (config 3: 270 -> 280 Mev/s)
   if (const char *v = getenv("FIBAR_TRACE")) g->trace = atoi(v) != 0;
+  if (const char *v = getenv("FIBAR_REG32X")) g->no_reg32x = atoi(v) == 0;
   if (const char *v = getenv("FIBAR_RUN_G")) g->run_g = atoi(v);
   if (const char *v = getenv("FIBAR_RUN_G_LARGE")) g->run_g_large = atoi(v);
   for (int *gg : {&g->run_g, &g->run_g_large}) *gg = *gg >= 8 ? 8 : (*gg >= 4 ? 4 : (*gg >= 2 ? 2 : 0));
@@ -1264,7 +1268,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->epol2[b], Bc);
     rc |= dalloc(&g->spol2[b], Bc);
   }
-  rc |= dalloc(&g->longseg, 16384);
+  rc |= dalloc(&g->longseg, MAX_LONG);
   rc |= dalloc(&g->bsd, NPAR);
   if (!rc) cudaMemset(g->bsd, 0, NPAR * sizeof(BatchState));
   for (int c = 0; c < NPAR; ++c) {

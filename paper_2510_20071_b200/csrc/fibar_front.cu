@@ -445,6 +445,43 @@ __device__ __forceinline__ unsigned regulate32(const Ctx &x, unsigned len, unsig
   return (unsigned)(q < x.qmin ? x.qmin : (q > x.qmax ? x.qmax : q));
 }
 
+// regulate32 without 64-bit arithmetic (x.reg32x: numA, den < 2^24, q_max <
+// 2^22, den * q_max < 2^29; the window invariants keep len, np, nt <= q_max + 1).
+// The float quotient carries at most 7 roundings of 2^-24 (two products in
+// the numerator, one in the denominator, __fdividef's 2 ulp), so below 2^22
+// it is within 1.75 of N / D and its truncation within 2 of the exact floor:
+// the remainder r = N - qe * D then lies in (-2D, 3D), fits 32 bits, and is
+// computed from the low words alone; two compares each way make qe the exact
+// floor.  An estimate far above the clamp returns q_max before the remainder
+// (which would wrap) is looked at.
+struct RegF {
+  float numA, den, hi;
+  unsigned numA32, den32, qmin, qmax;
+};
+__device__ __forceinline__ RegF make_regf(const Ctx &x) {
+  RegF f;
+  f.numA = (float)x.numA;
+  f.den = (float)x.den;
+  f.hi = (float)(x.qmax + 8);
+  f.numA32 = (unsigned)x.numA;
+  f.den32 = (unsigned)x.den;
+  f.qmin = (unsigned)x.qmin;
+  f.qmax = (unsigned)x.qmax;
+  return f;
+}
+__device__ __forceinline__ unsigned regulate32x(const RegF &f, unsigned len, unsigned np, unsigned nt) {
+  const float fn = __fmul_rn(__fmul_rn((float)len, (float)nt), f.numA);
+  const float fd = __fmul_rn((float)np, f.den);
+  const float qf = __fdividef(fn, fd);
+  const unsigned qe = (unsigned)qf;   // truncation (saturating)
+  const unsigned Nl = len * nt * f.numA32, Dl = np * f.den32;
+  const int r = (int)(Nl - qe * Dl), D = (int)Dl;
+  const int adj = (r >= D ? 1 : 0) + (r >= 2 * D ? 1 : 0) - (r < 0 ? 1 : 0) - (r < -D ? 1 : 0);
+  unsigned q = qe + (unsigned)adj;
+  q = qf > f.hi ? f.qmax : q;
+  return min(max(q, f.qmin), f.qmax);
+}
+
 // regulate() through the 32-bit form whenever the operands fit (always for
 // sensors up to 4.19M pixels): no double division on the candidate paths
 __device__ __forceinline__ long long regulate_fast(const Ctx &x, long long len, long long np, long long nt) {
@@ -1055,14 +1092,16 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
 // dependency chain (it overlaps the regulator of the step that issued it), an
 // eviction of up to G entries is one compare per lane and a group reduction,
 // and the fine candidates of the start state are evaluated G at a time.  Longer
-// evictions (the collapse of a too-long start window) stream 32 entries per
-// round per group.
+// evictions (the collapse of a too-long start window) stream 8 entries per
+// lane per round.  The warm-up and the chunk run as blocks of G steps: each
+// lane loads one event's links per block (the steps take them by shuffle) and
+// keeps one event's (S, Qt) to store.
 template <int G>
 __device__ __forceinline__ void window_run_g(const Ctx &x) {
   pdl_wait();
   if (blockIdx.x == 0 && threadIdx.x == 0) open_batch(x);   // the batch's true start (after the previous verifier)
   constexpr int CPW = 32 / G;   // chunks per warp
-  constexpr int V = 32 / G;     // ring loads in flight per lane in a long eviction
+  constexpr int V = 8;          // ring loads in flight per lane in a long eviction
   const long long B = x.bs->B;
   const int T = (int)((B + x.chunk - 1) / x.chunk);
   const int lane = threadIdx.x & 31, u = lane & (G - 1);
@@ -1131,51 +1170,42 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
       w.evctr = (s.evctr + (a - E0)) % x.every;
     }
   }
-  ChunkRec r;
-  r.st_s = w.s;
-  r.st_q = w.q;
-  unsigned wpops = 0, coop = 0;
-  const unsigned n_my = (unsigned)(e - a);
-  const unsigned n_max = __reduce_max_sync(0xffffffffu, n_my);
   // 32-bit state relative to the batch's start window, as in k_window_run
   const long long base = min(s_start0, s_true);
   const unsigned sofs = (unsigned)(s_true - base);
   const unsigned bslot = (unsigned)((unsigned long long)base & x.Rm);
   const unsigned rm = (unsigned)x.Rm;
   unsigned sr = (unsigned)(w.s - base);
-  const unsigned ar = (unsigned)(a - base), br = (unsigned)(b - base);
-  const unsigned e0r = (unsigned)(E0 - base);
+  const int ar = (int)(a - base), br = (int)(b - base), e0r = (int)(E0 - base);
+  const int wl = br - ar, rl = (int)(e - b);   // this chunk's warm-up and run lengths
   unsigned q = (unsigned)w.q;
   int np = (int)w.npix, nt = (int)w.ntiles;
   unsigned ev = (unsigned)w.evctr;
   const unsigned every = (unsigned)x.every;
-  unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0;
-  uint2 dnext = n_my > 0 ? x.dp[ar - e0r] : make_uint2(0, 0);
+  const bool fastreg = x.reg32x != 0;
+  const RegF rf = make_regf(x);
+  unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0, coop = 0;
+  const unsigned sr_first = sr;
   // this lane's ring entry: the first position = u (mod G) at or past sr
   unsigned pu = sr + (((unsigned)u - sr) & (unsigned)(G - 1));
   uint2 en = x.rnext[(bslot + pu) & rm];
-  for (unsigned t = 0; t < n_max; ++t) {
-    const bool act = t < n_my;
-    const unsigned jr = ar + t;
-    if (act && jr == br) {
-      r.st_s = base + sr;
-      r.st_q = q;
-    }
+  const int gb = lane & ~(G - 1);   // the group's first lane
+
+  // one event: push (d = its links), trim, re-target
+  auto step = [&](bool act, int jr, unsigned dx, unsigned dy) -> bool {
+    bool regd = false;
     unsigned hi = sr;
+    const unsigned js = (unsigned)jr - sr;
     if (act) {
-      const uint2 d = dnext;
-      if (t + 1 < n_my) dnext = x.dp[jr + 1 - e0r];
-      const unsigned js = jr - sr;
-      np += d.x > js;
-      nt += d.y > js;
-      if (js + 1 > q) hi = jr + 1 - q;
+      np += dx > js;
+      nt += dy > js;
+      if (js + 1 > q) hi = (unsigned)jr + 1 - q;
     }
-    if (jr < br) wpops += hi - sr;
     // the eviction [sr, hi): this lane's held entry first
     const unsigned pu0 = pu;
     unsigned cc = 0;   // pixels in the low half, tiles in the high half
     if (pu < hi) {
-      const unsigned dd = jr - pu;
+      const unsigned dd = (unsigned)jr - pu;
       cc = (en.x > dd ? 1u : 0u) | (en.y > dd ? 0x10000u : 0u);
       pu += G;
     }
@@ -1184,7 +1214,7 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
     np -= (int)(cc & 0xFFFFu);
     nt -= (int)(cc >> 16);
     if (__ballot_sync(0xffffffffu, pu < hi)) {
-      // more than G entries somewhere in the warp: 32 per round per group
+      // more than G entries somewhere in the warp: V per lane per round
       int cp = 0, ct = 0;
       const unsigned n_u = pu < hi ? (hi - pu + G - 1) / G : 0u;
       for (unsigned i = 0; i < n_u; i += V) {
@@ -1195,7 +1225,7 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
 #pragma unroll
         for (int v = 0; v < V; ++v) {
           if (i + v >= n_u) break;
-          const unsigned dd = jr - (pu + (i + v) * G);
+          const unsigned dd = (unsigned)jr - (pu + (i + v) * G);
           cp += rr[v].x > dd;
           ct += rr[v].y > dd;
         }
@@ -1216,17 +1246,63 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
       if (++ev >= every) {
         ev = 0;
         if (np >= 1 && nt >= 1) {
-          q = regulate32(x, jr - sr + 1, (unsigned)np, (unsigned)nt);
-          if (jr >= br) {
-            qlo32 = min(qlo32, q);
-            qhi32 = max(qhi32, q);
-          }
+          q = fastreg ? regulate32x(rf, (unsigned)jr - sr + 1, (unsigned)np, (unsigned)nt)
+                      : regulate32(x, (unsigned)jr - sr + 1, (unsigned)np, (unsigned)nt);
+          regd = true;
         }
       }
-      if (jr >= br && u == 0) {
-        x.S[jr - e0r] = sr - sofs;
-        x.Qt[jr - e0r] = q;
+    }
+    return regd;
+  };
+
+  // Warm-up, aligned so that every chunk of the warp ends it together: step t
+  // of nw * G is event br - nw * G + t, active from the chunk's warm-up start.
+  // Each lane loads the links of one event per block of G steps; the steps
+  // take them by shuffle.
+  const int wl_max = __reduce_max_sync(0xffffffffu, wl);
+  const int nw = (wl_max + G - 1) / G;
+#pragma unroll 1
+  for (int t0 = 0; t0 < nw; ++t0) {
+    const int j0 = br - (nw - t0) * G;
+    const uint2 dv = j0 + u >= ar ? x.dp[j0 + u - e0r] : make_uint2(0u, 0u);
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const unsigned dx = __shfl_sync(0xffffffffu, dv.x, gb + k);
+      const unsigned dy = __shfl_sync(0xffffffffu, dv.y, gb + k);
+      step(j0 + k >= ar, j0 + k, dx, dy);
+    }
+  }
+  ChunkRec r;
+  r.st_s = base + sr;   // state after event b - 1: the chunk's speculative start
+  r.st_q = q;
+  const unsigned wpops = sr - sr_first;
+  // The chunk itself: the window start and target after each event are kept
+  // by the lane whose index the event has in its block, and stored per block.
+  const int rl_max = __reduce_max_sync(0xffffffffu, rl);
+  const int nr = (rl_max + G - 1) / G;
+#pragma unroll 1
+  for (int t0 = 0; t0 < nr; ++t0) {
+    const int j0 = br + t0 * G;
+    const bool mine = t0 * G + u < rl;
+    const uint2 dv = mine ? x.dp[j0 + u - e0r] : make_uint2(0u, 0u);
+    unsigned sv = 0, qv = 0;
+#pragma unroll
+    for (int k = 0; k < G; ++k) {
+      const unsigned dx = __shfl_sync(0xffffffffu, dv.x, gb + k);
+      const unsigned dy = __shfl_sync(0xffffffffu, dv.y, gb + k);
+      const bool act = t0 * G + k < rl;
+      if (step(act, j0 + k, dx, dy)) {
+        qlo32 = min(qlo32, q);
+        qhi32 = max(qhi32, q);
       }
+      if (k == u) {
+        sv = sr - sofs;
+        qv = q;
+      }
+    }
+    if (mine) {
+      x.S[j0 + u - e0r] = sv;
+      x.Qt[j0 + u - e0r] = qv;
     }
   }
   {
@@ -1309,6 +1385,8 @@ __device__ int rerun_chunk_staged(const Ctx &x, WState &w, long long b, long lon
     unsigned sr = (unsigned)(w.s - s_start), q = (unsigned)w.q, ev = (unsigned)w.evctr;
     int np = (int)w.npix, nt = (int)w.ntiles;
     unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0;
+    const bool fastreg = x.reg32x != 0;
+    const RegF rf = make_regf(x);
 #pragma unroll 1
     for (unsigned jr = br; jr < er; ++jr) {
       const uint2 d = sdp[jr - br];
@@ -1330,7 +1408,8 @@ __device__ int rerun_chunk_staged(const Ctx &x, WState &w, long long b, long lon
       if (++ev >= every) {
         ev = 0;
         if (np >= 1 && nt >= 1) {
-          q = regulate32(x, jr - sr + 1, (unsigned)np, (unsigned)nt);
+          q = fastreg ? regulate32x(rf, jr - sr + 1, (unsigned)np, (unsigned)nt)
+                      : regulate32(x, jr - sr + 1, (unsigned)np, (unsigned)nt);
           qlo32 = min(qlo32, q);
           qhi32 = max(qhi32, q);
         }

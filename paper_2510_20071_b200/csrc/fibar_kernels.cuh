@@ -28,8 +28,11 @@ constexpr int IN_ITEMS = 8;
 constexpr int IN_TILE = TPB * IN_ITEMS;
 constexpr unsigned WIN_SOLO = 384;   // evictions a lane counts alone (longer: the whole warp)
 constexpr int GROUP = 8;
-constexpr int LONG_SEG = 512;    // segments longer than this go to k_temporal_long
-constexpr int MAX_LONG = 16384;
+#ifndef FIBAR_LONG_SEG
+#define FIBAR_LONG_SEG 64
+#endif
+constexpr int LONG_SEG = FIBAR_LONG_SEG;    // segments longer than this go to k_temporal_long
+constexpr int MAX_LONG = (8 << 20) / LONG_SEG;   // (a device batch holds at most 8M events)
 constexpr int LONG_TPB = 256;      // lanes per long segment (one block)
 constexpr int LONG_PIECE = 64;     // minimum events per lane before more lanes join
 constexpr int EV_PER_THREAD = 2;
@@ -92,6 +95,7 @@ struct Ctx {
   long long n_pix;
   long long num, den, qmin, qmax, every;
   long long numA;   // num * A (tile area)
+  int reg32x;       // regulate32x applies (numA, den < 2^24, q_max < 2^22, den * q_max < 2^29)
   float alpha, oma, beta, h;
   int use_gain, blur_on, spatial;
   DevState *st;

@@ -249,13 +249,48 @@ __device__ __forceinline__ void replay_piece(const Ctx &x, long long q0, long lo
 }
 
 
+// One IIR step on polarity p from shared memory; WRITE: the per-position outputs
+template <bool WRITE>
+__device__ __forceinline__ void iir_step_s(const Ctx &x, float &pb, float &lv, int pol, float g, long long q) {
+  float tt;
+  iir_step(x, pb, lv, (float)pol, g, tt);
+  if (WRITE) {
+    x.t2[q] = tt;
+    x.posrec[q].val = lv;
+  }
+}
+
+// replay the staged polarities sp[i0, i1) (global positions gq + i) from (pb, lv)
+template <bool WRITE>
+__device__ __forceinline__ void replay_smem(const Ctx &x, const int8_t *sp, int i0, int i1, float &pb, float &lv,
+                                            float g, long long gq) {
+  int i = i0;
+  for (; i < i1 && (i & 3); ++i) iir_step_s<WRITE>(x, pb, lv, sp[i], g, gq + i);
+#pragma unroll 2
+  for (; i + 4 <= i1; i += 4) {
+    const int w = *reinterpret_cast<const int *>(sp + i);
+    iir_step_s<WRITE>(x, pb, lv, (int)(int8_t)(w & 0xFF), g, gq + i);
+    iir_step_s<WRITE>(x, pb, lv, (int)(int8_t)((w >> 8) & 0xFF), g, gq + i + 1);
+    iir_step_s<WRITE>(x, pb, lv, (int)(int8_t)((w >> 16) & 0xFF), g, gq + i + 2);
+    iir_step_s<WRITE>(x, pb, lv, (int)(w >> 24), g, gq + i + 3);
+  }
+  for (; i < i1; ++i) iir_step_s<WRITE>(x, pb, lv, sp[i], g, gq + i);
+}
+
+constexpr int LT_TILE = 8192;            // events of a segment staged in shared memory at a time
+constexpr int LT_PMIN = 8;               // fewest events per lane
+constexpr long long LT_BIG = 1 << 17;    // longer segments: pieces of thousands of events straight from global memory
+
 __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
   pdl_wait();
   __shared__ float s_spb[LONG_TPB], s_slv[LONG_TPB], s_epb[LONG_TPB], s_elv[LONG_TPB];
   __shared__ unsigned s_last[LONG_TPB];
+  __shared__ __align__(16) int8_t s_pol[LT_TILE];
+  __shared__ unsigned s_bidx[LT_TILE];
+  __shared__ unsigned s_wlast[LONG_TPB / 32];
   __shared__ int s_bad;
   const unsigned n = min(x.bs->nlong, (unsigned)MAX_LONG);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (unsigned sidx = blockIdx.x; sidx < n; sidx += gridDim.x) {
     const uint2 ls = x.longseg[sidx];
     const long long st = ls.x;
@@ -273,12 +308,138 @@ __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
       }
       end = lo;
     }
+    const float g = x.use_gain ? x.gain[c] : 1.0f;
     const long long len = end - st;
+    if (len <= LT_BIG) {
+      // Tiles of the segment staged in shared memory (polarities and, filter
+      // ON, which blur each position carries).  Lane i takes the i-th piece of
+      // the tile: it starts twarm events early from zero (the float32
+      // recurrences contract, see above), or from the tile's exact start state
+      // when that is no further away, and every piece's start is checked
+      // against its left neighbour's end.
+      float pb0 = x.pbar[c], lv0 = x.l[c];
+      unsigned carry0 = x.spatial ? x.pt[c].carried : FIBAR_NONE;
+      if (x.spatial && tid == 0 && carry0 != FIBAR_NONE) x.item[carry0].runpos = (unsigned)st;
+      for (long long t0 = st; t0 < end; t0 += LT_TILE) {
+        const int tlen = (int)min((long long)LT_TILE, end - t0);
+        {
+          // staging: 16-byte loads over the aligned middle, bytes at the ends
+          const long long a0 = (t0 + 15) & ~15LL, a1 = (t0 + tlen) & ~15LL;
+          if (a0 < a1) {
+            for (long long q = a0 + 16LL * tid; q < a1; q += 16LL * LONG_TPB) {
+              const int4 v = *reinterpret_cast<const int4 *>(x.spol + q);
+              const int o = (int)(q - t0);
+              int8_t *d = s_pol + o;
+              if ((o & 15) == 0) {
+                *reinterpret_cast<int4 *>(d) = v;
+              } else {
+                const int w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int b = 0; b < 16; ++b) d[b] = (int8_t)(w[b >> 2] >> (8 * (b & 3)));
+              }
+            }
+            for (long long q = t0 + tid; q < a0; q += LONG_TPB) s_pol[q - t0] = x.spol[q];
+            for (long long q = a1 + tid; q < t0 + tlen; q += LONG_TPB) s_pol[q - t0] = x.spol[q];
+          } else {
+            for (int i = tid; i < tlen; i += LONG_TPB) s_pol[i] = x.spol[t0 + i];
+          }
+          if (x.spatial)
+            for (int i = tid; i < tlen; i += LONG_TPB) s_bidx[i] = x.posrec[t0 + i].bidx;
+        }
+        __syncthreads();
+        const int P = max(LT_PMIN, (tlen + LONG_TPB - 1) / LONG_TPB);
+        const int lanes = (tlen + P - 1) / P;
+        const bool on = tid < lanes;
+        const int q0 = on ? tid * P : tlen, q1 = on ? min(tlen, q0 + P) : tlen;
+        float pb = 0.0f, lv = 0.0f;
+        if (on) {
+          if (q0 <= x.twarm) {
+            pb = pb0;
+            lv = lv0;
+            replay_smem<false>(x, s_pol, 0, q0, pb, lv, g, t0);
+          } else {
+            replay_smem<false>(x, s_pol, q0 - x.twarm, q0, pb, lv, g, t0);
+          }
+        }
+        s_spb[tid] = pb;   // (speculative) state at the piece start
+        s_slv[tid] = lv;
+        if (x.spatial) replay_smem<true>(x, s_pol, q0, q1, pb, lv, g, t0);
+        else replay_smem<false>(x, s_pol, q0, q1, pb, lv, g, t0);
+        s_epb[tid] = pb;
+        s_elv[tid] = lv;
+        if (tid == 0) s_bad = 0;
+        __syncthreads();
+        if (on && tid > 0 && (__float_as_uint(s_spb[tid]) != __float_as_uint(s_epb[tid - 1]) ||
+                              __float_as_uint(s_slv[tid]) != __float_as_uint(s_elv[tid - 1])))
+          atomicMax(&s_bad, 1);
+        __syncthreads();
+        if (s_bad) {
+          // rare: re-run the pieces whose start was wrong, in lane order, from the exact states
+          for (int i = 1; i < lanes; ++i) {
+            if (tid == i && (__float_as_uint(s_spb[i]) != __float_as_uint(s_epb[i - 1]) ||
+                             __float_as_uint(s_slv[i]) != __float_as_uint(s_elv[i - 1]))) {
+              pb = s_epb[i - 1];
+              lv = s_elv[i - 1];
+              s_spb[i] = pb;
+              s_slv[i] = lv;
+              if (x.spatial) replay_smem<true>(x, s_pol, q0, q1, pb, lv, g, t0);
+              else replay_smem<false>(x, s_pol, q0, q1, pb, lv, g, t0);
+              s_epb[i] = pb;
+              s_elv[i] = lv;
+            }
+            __syncthreads();
+          }
+        }
+        pb0 = s_epb[lanes - 1];
+        lv0 = s_elv[lanes - 1];
+        if (x.spatial) {
+          // which blur each position builds on: the last stale event before it
+          // in the segment, or the pixel's carried blur
+          unsigned last = FIBAR_NONE;
+          for (int i = q0; i < q1; ++i)
+            if (s_bidx[i] != FIBAR_NONE) last = s_bidx[i];
+          const unsigned m = __ballot_sync(0xffffffffu, last != FIBAR_NONE);
+          if (lane == 31 - __clz(m | 1u) || (m == 0 && lane == 0)) s_wlast[wid] = m ? last : FIBAR_NONE;
+          __syncthreads();
+          unsigned carry = FIBAR_NONE;
+          const unsigned below = m & ((1u << lane) - 1u);
+          const unsigned from_lane = __shfl_sync(0xffffffffu, last, below ? 31 - __clz(below) : 0);
+          if (below) {
+            carry = from_lane;
+          } else {
+            for (int w = wid - 1; w >= 0; --w)
+              if (s_wlast[w] != FIBAR_NONE) {
+                carry = s_wlast[w];
+                break;
+              }
+            if (carry == FIBAR_NONE) carry = carry0;
+          }
+          for (int i = q0; i < q1; ++i) {
+            x.posrec[t0 + i].runbase = carry;
+            const unsigned bi = s_bidx[i];
+            if (bi != FIBAR_NONE) {
+              carry = bi;
+              if (t0 + i + 1 < end) x.item[bi].runpos = (unsigned)(t0 + i + 1);
+            }
+          }
+          for (int w = LONG_TPB / 32 - 1; w >= 0; --w)
+            if (s_wlast[w] != FIBAR_NONE) {
+              carry0 = s_wlast[w];
+              break;
+            }
+        }
+        __syncthreads();   // the tile's shared arrays are rewritten next
+      }
+      if (tid == 0) {
+        x.pbar[c] = pb0;
+        if (!x.spatial) x.l[c] = lv0;
+      }
+      continue;
+    }
     const int lanes = (int)min((long long)LONG_TPB, max(32LL, len / LONG_PIECE));
     const long long P = (len + lanes - 1) / lanes;
     const bool on = tid < lanes;
     const long long q0 = on ? min(end, st + tid * P) : end, q1 = on ? min(end, q0 + P) : end;
-    const float g = x.use_gain ? x.gain[c] : 1.0f;
     float pb = 0.0f, lv = 0.0f;
     if (tid == 0) {
       pb = x.pbar[c];
