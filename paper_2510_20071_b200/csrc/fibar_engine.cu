@@ -111,7 +111,10 @@ int ceil_log2(long long v) {
 
 // buffer sets for batches in flight (ingest of k+2 may run while k's window
 // part and k-1's blur stage run), indexed by batch % NPAR
-constexpr int NPAR = 3;
+#ifndef FIBAR_NPAR
+#define FIBAR_NPAR 5
+#endif
+constexpr int NPAR = FIBAR_NPAR;
 
 // small batches' front-end graphs are captured per size class of this many events
 constexpr long long GRAPH_CLASS = 16384;
@@ -126,6 +129,8 @@ struct GraphEntry {
   long long kernels3 = 0;
   cudaGraphExec_t exec4 = nullptr;   // kind 1: the anchors (exec2: run + verifier)
   long long kernels4 = 0;
+  cudaGraphExec_t exec5 = nullptr;   // kind 1: segments and links (exec: the sort part of the ingest)
+  long long kernels5 = 0;
   int kind = 0;              // 0: whole batch (serial schedule), 1: front end of the streamed schedule (two parts)
   int par = 0;               // kind 1: the batch parity whose buffers it uses
   int where = 0;             // kind 1: which radix-sort buffer holds the sorted keys
@@ -154,7 +159,7 @@ struct fibar_engine {
   uint2 *rnext = nullptr;
   uint16_t *raw_x = nullptr, *raw_y = nullptr;
   int8_t *raw_p = nullptr;
-  unsigned *blockcnt = nullptr;
+  unsigned *blockcnt2[NPAR] = {};   // per buffer set: two batches' sorts may be in flight (astream / astream2)
   unsigned *ekey2[NPAR] = {};
   // polarities in stream order (per batch parity: the next batch's ingest may
   // run while this one's front end reads them) and in pixel-sorted order (per
@@ -162,7 +167,7 @@ struct fibar_engine {
   // front end writes its own)
   int8_t *epol2[NPAR] = {}, *spol2[NPAR] = {};
   uint2 *longseg = nullptr;
-  unsigned *ka2[NPAR] = {}, *va2[NPAR] = {}, *kb2[NPAR] = {}, *vb2[NPAR] = {}, *hist = nullptr;
+  unsigned *ka2[NPAR] = {}, *va2[NPAR] = {}, *kb2[NPAR] = {}, *vb2[NPAR] = {}, *hist2[NPAR] = {};
   uint2 *dp2[NPAR] = {};    // per-event link distances, per batch parity
   // window starts / targets after each event and the eviction -> popping-event
   // map, per batch parity (the eviction pass of batch k runs beside the window
@@ -218,6 +223,11 @@ struct fibar_engine {
   // streamed filter-ON batches: the front end's ingest + sort (astream) and
   // window part (fstream), so batch k+1's ingest overlaps batch k's window pass
   cudaStream_t astream = nullptr, fstream = nullptr;
+  // small batches: the sort part of the ingest alternates between astream and
+  // astream2 (it reads nothing of the previous batch); segments and links,
+  // which do, follow on lstream in batch order
+  cudaStream_t astream2 = nullptr, lstream = nullptr;
+  cudaEvent_t evS[NPAR] = {};   // the set's sort part is done
   cudaEvent_t evIn = nullptr, evCp = nullptr, evA[NPAR] = {};
   // ... and the eviction pass (pstream) after the window part (evV), beside
   // the next batch's window part
@@ -255,10 +265,11 @@ struct fibar_engine {
   // one whole-batch graph (serial schedule)
   bool full_graphs = false;
   std::vector<GraphEntry> graphs;
-  uint16_t *gx = nullptr, *gy = nullptr;
-  int8_t *gp = nullptr;
+  uint16_t *gx2[NPAR] = {}, *gy2[NPAR] = {};   // fixed graph input buffers, per buffer set
+  int8_t *gp2[NPAR] = {};
   int blur_grid_serial = 148;
   cudaEvent_t evF[NPAR] = {}, evB[NPAR] = {};
+  cudaEvent_t evBuf[NPAR] = {};   // the set's blur stage is done (its buffers are free); evB also orders after a read-out
   int last_b = -1;   // parity of the newest batch with a blur stage in flight
   int last_par = -1;  // parity of the newest batch (fibar_debug_stale_items)
   bool b_used[NPAR] = {};
@@ -333,7 +344,7 @@ struct fibar_engine {
     x.raw_p = raw_p;
     x.n_raw = n_raw;
     x.n_raw_dev = nullptr;
-    x.blockcnt = blockcnt;
+    x.blockcnt = blockcnt2[par];
     x.ekey = ekey2[par];
     x.epol = epol2[par];
     x.spol = spol2[par];
@@ -427,8 +438,9 @@ int init_state(fibar_engine *g) {
 // ON) segments and links -- it reads the batch's own events and the previous
 // batch's links, never the previous window pass, so it may run ahead of it.
 // Returns where the sorted pairs are.
-int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
-                   cudaEvent_t used_ev, int par, cudaStream_t s, int &where, const long long *n_dev = nullptr) {
+int enqueue_ingest_a(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                     cudaEvent_t used_ev, int par, cudaStream_t s, int &where, const long long *n_dev = nullptr) {
+  // part A: OOB filter, compaction, pixel sort -- the batch's own events only
   Launcher &L = g->L;
   const int nb_in = (int)((n_raw + IN_TILE - 1) / IN_TILE);
   Ctx x = g->ctx(nullptr, nullptr, n_raw, par);
@@ -439,16 +451,26 @@ int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, co
   cudaStream_t s_saved = L.stream;
   L.stream = s;
   fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
-  scan_exclusive_u32(L, g->blockcnt, nb_in + 1);
+  scan_exclusive_u32(L, g->blockcnt2[par], nb_in + 1);
   fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw packet may be refilled / freed from here on
-  fibar_launch(L, "ingest_end", k_ingest_end, 1, 1, 0, s, x);
-  where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist, &g->bsd[par].B, n_raw,
+  where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist2[par], &g->bsd[par].B, n_raw,
                            g->key_bits);
+  L.stream = s_saved;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int enqueue_ingest_b(fibar_engine *g, long long n_raw, int par, int where, cudaStream_t s) {
+  // part B, in batch order: the batch's first event index, then (filter ON)
+  // segments and links, which read the previous batch's links (last-touch
+  // tables), never its window pass
+  Launcher &L = g->L;
+  cudaStream_t s_saved = L.stream;
+  L.stream = s;
+  Ctx x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+  fibar_launch(L, "ingest_end", k_ingest_end, 1, 1, 0, s, x);
   if (g->spatial) {
-    // segments and links: they read the previous batch's links (last-touch
-    // tables), never its window pass
-    x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
     const int nb = (int)((n_raw + TPB - 1) / TPB);
     fibar_launch(L, "seg_marks", k_seg_marks, nb, TPB, 0, s, x);
     fibar_launch(L, "link", k_link, nb, TPB, 0, s, x);
@@ -456,6 +478,13 @@ int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, co
   L.stream = s_saved;
   CK(cudaGetLastError());
   return 0;
+}
+
+int enqueue_ingest(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, const int8_t *rp0, long long n_raw,
+                   cudaEvent_t used_ev, int par, cudaStream_t s, int &where, const long long *n_dev = nullptr) {
+  int rc = enqueue_ingest_a(g, rx0, ry0, rp0, n_raw, used_ev, par, s, where, n_dev);
+  if (!rc) rc = enqueue_ingest_b(g, n_raw, par, where, s);
+  return rc;
 }
 
 // The window part (stream s, after the previous batch's window part): the
@@ -567,9 +596,9 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
 GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   for (auto &ge : g->graphs)
     if (ge.kind == 1 && ge.n == n_raw && ge.par == par) return &ge;
-  if (g->graphs.size() >= 16) {   // small cache: drop the oldest (freed once its launches finish)
+  if (g->graphs.size() >= 8 * NPAR) {   // small cache: drop the oldest (freed once its launches finish)
     for (cudaGraphExec_t e : {g->graphs.front().exec, g->graphs.front().exec2, g->graphs.front().exec3,
-                              g->graphs.front().exec4})
+                              g->graphs.front().exec4, g->graphs.front().exec5})
       if (e) cudaGraphExecDestroy(e);
     g->graphs.erase(g->graphs.begin());
   }
@@ -580,19 +609,20 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   ge.n = n_raw;
   ge.kind = 1;
   ge.par = par;
-  for (int part = 0; part < 4; ++part) {
+  for (int part = 0; part < 5; ++part) {
     const long long l0 = L.launches;
     cudaGraph_t graph = nullptr;
     Ctx x{};
     if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
-      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3})
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4})
         if (e) cudaGraphExecDestroy(e);
       return nullptr;
     }
     L.stream = g->capstream;
-    const int rc = part == 0   ? enqueue_ingest(g, g->gx, g->gy, g->gp, n_raw, nullptr, par, g->capstream, ge.where,
-                                                &g->bsd[par].n_raw)
+    const int rc = part == 0   ? enqueue_ingest_a(g, g->gx2[par], g->gy2[par], g->gp2[par], n_raw, nullptr, par,
+                                                  g->capstream, ge.where, &g->bsd[par].n_raw)
+                   : part == 4 ? enqueue_ingest_b(g, n_raw, par, ge.where, g->capstream)
                    : part == 1 ? enqueue_chain(g, n_raw, par, ge.where, g->capstream, x, nullptr)
                    : part == 2 ? enqueue_post(g, n_raw, par, ge.where, g->capstream)
                                : enqueue_anchors(g, n_raw, par, ge.where, g->capstream);
@@ -605,7 +635,7 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     L.launches = l0;
     if (rc || ce != cudaSuccess) {
       cudaGetLastError();
-      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3})
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4})
         if (e) cudaGraphExecDestroy(e);
       g->graphs_on = false;   // capture impossible here: stream every kernel from now on
       return nullptr;
@@ -619,9 +649,12 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     } else if (part == 2) {
       ge.exec3 = exec;
       ge.kernels3 = k;
-    } else {
+    } else if (part == 3) {
       ge.exec4 = exec;
       ge.kernels4 = k;
+    } else {
+      ge.exec5 = exec;
+      ge.kernels5 = k;
     }
   }
   g->graphs.push_back(ge);
@@ -650,20 +683,21 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   int where = 0;
   const int nb = (int)((n_raw + TPB - 1) / TPB);
   if (split) {
-    cudaStream_t sa = g->astream;
+    const bool small = g->graphs_on && !L.prof && n_raw <= g->graph_max;
+    // a small batch's sort part alternates between two streams
+    cudaStream_t sa = (small && (g->batches & 1)) ? g->astream2 : g->astream;
     CK(cudaEventRecord(g->evIn, u));
     CK(cudaStreamWaitEvent(sa, g->evIn, 0));
-    if (g->b_used[par]) CK(cudaStreamWaitEvent(sa, g->evB[par], 0));   // this parity's buffers are free
+    if (g->b_used[par]) CK(cudaStreamWaitEvent(sa, g->evBuf[par], 0));   // this parity's buffers are free (the ingest reads no brightness: it need not wait for a read-out)
     g->mark(0, sa);   // trace labels: 0/1 ingest start/end, 2/3 window part, 4/5 eviction pass, 6/7 blur stage
-    const bool small = g->graphs_on && !L.prof && n_raw <= g->graph_max;
     if (small) {
       // a small batch: each part replays one CUDA graph per (size class,
       // parity), the ingest from fixed input buffers (k_stage fills them and
       // the batch's raw count)
       const long long cls = std::min(g->graph_max, (n_raw + GRAPH_CLASS - 1) / GRAPH_CLASS * GRAPH_CLASS);
       const int nbs = (int)std::max(1LL, std::min((long long)g->nsm * 2, (n_raw / 8 + TPB - 1) / TPB));
-      fibar_launch(L, "stage", k_stage, nbs, TPB, 0, sa, rx0, ry0, rp0, (long long)n_raw, g->gx, g->gy, g->gp,
-                   &g->bsd[par].n_raw);
+      fibar_launch(L, "stage", k_stage, nbs, TPB, 0, sa, rx0, ry0, rp0, (long long)n_raw, g->gx2[par], g->gy2[par],
+                   g->gp2[par], &g->bsd[par].n_raw);
       CK(cudaEventRecord(g->evCp, sa));
       if (used_ev) CK(cudaEventRecord(used_ev, sa));
       const GraphEntry *ge = front_graph(g, cls, par);
@@ -671,8 +705,13 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       where = ge->where;
       CK(cudaGraphLaunch(ge->exec, sa));
       L.launches += ge->kernels;
-      g->mark(1, sa);
-      CK(cudaEventRecord(g->evA[par], sa));
+      CK(cudaEventRecord(g->evS[par], sa));
+      // segments and links in batch order
+      CK(cudaStreamWaitEvent(g->lstream, g->evS[par], 0));
+      CK(cudaGraphLaunch(ge->exec5, g->lstream));
+      L.launches += ge->kernels5;
+      g->mark(1, g->lstream);
+      CK(cudaEventRecord(g->evA[par], g->lstream));
       // anchors after the ingest and the previous batch's run
       cudaStream_t sn = g->nstream;
       CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
@@ -692,14 +731,20 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       L.launches += ge->kernels3;
       g->mark(5, g->pstream);
       x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
-      x.raw_x = g->gx;
-      x.raw_y = g->gy;
-      x.raw_p = g->gp;
+      x.raw_x = g->gx2[par];
+      x.raw_y = g->gy2[par];
+      x.raw_p = g->gp2[par];
     } else {
-      int rc = enqueue_ingest(g, rx0, ry0, rp0, n_raw, used_ev, par, sa, where);
+      int rc = enqueue_ingest_a(g, rx0, ry0, rp0, n_raw, used_ev, par, sa, where);
       if (rc) return rc;
       CK(cudaEventRecord(g->evCp, sa));
-      CK(cudaEventRecord(g->evA[par], sa));
+      // segments and links on lstream, where every batch's run in batch order
+      CK(cudaEventRecord(g->evS[par], sa));
+      CK(cudaStreamWaitEvent(g->lstream, g->evS[par], 0));
+      rc = enqueue_ingest_b(g, n_raw, par, where, g->lstream);
+      if (rc) return rc;
+      g->mark(1, g->lstream);
+      CK(cudaEventRecord(g->evA[par], g->lstream));
       cudaStream_t sn = g->nstream;
       CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
       L.stream = sn;
@@ -802,6 +847,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     if (!graph) {
       g->mark(7, bs);
       CK(cudaEventRecord(g->evB[par], bs));
+      CK(cudaEventRecord(g->evBuf[par], bs));
       g->b_used[par] = true;
       g->last_b = par;
     }
@@ -836,9 +882,9 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   join_blur(g);
   g->last_b = -1;
   for (bool &u : g->b_used) u = false;
-  CK(cudaMemcpyAsync(g->gx, rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(g->gy, ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
-  CK(cudaMemcpyAsync(g->gp, rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(g->gx2[0], rx0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(g->gy2[0], ry0, sizeof(uint16_t) * n_raw, cudaMemcpyDeviceToDevice, s));
+  CK(cudaMemcpyAsync(g->gp2[0], rp0, sizeof(int8_t) * n_raw, cudaMemcpyDeviceToDevice, s));
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw staging may be refilled from here on
   GraphEntry *hit = nullptr;
   for (auto &ge : g->graphs)
@@ -858,7 +904,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     int rc = 0;
     if (ce == cudaSuccess) {
       L.stream = g->capstream;
-      rc = enqueue_batch(g, g->gx, g->gy, g->gp, n_raw, nullptr, 0, true);
+      rc = enqueue_batch(g, g->gx2[0], g->gy2[0], g->gp2[0], n_raw, nullptr, 0, true);
       L.stream = s;
       ce = cudaStreamEndCapture(g->capstream, &graph);
     }
@@ -879,7 +925,7 @@ int run_batch_raw(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       // in global mode): run the same serial schedule without a graph from now on
       cudaGetLastError();
       g->graphs_on = false;
-      rc = enqueue_batch(g, g->gx, g->gy, g->gp, n_raw, nullptr, 0, true);
+      rc = enqueue_batch(g, g->gx2[0], g->gy2[0], g->gp2[0], n_raw, nullptr, 0, true);
       if (rc) return rc;
       g->batches++;
       return 0;
@@ -1257,11 +1303,14 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     cudaEventCreateWithFlags(&g->ev_used[c], cudaEventDisableTiming);
   }
   cudaStreamCreateWithFlags(&g->cstream, cudaStreamNonBlocking);
-  rc |= dalloc(&g->blockcnt, nb_in + 1);
+  const int nsets = g->spatial ? NPAR : 1;
+  for (int c = 0; c < nsets; ++c) rc |= dalloc(&g->blockcnt2[c], nb_in + 1);
   if (g->graphs_on && g->graph_max > 0) {
-    rc |= dalloc(&g->gx, g->graph_max);
-    rc |= dalloc(&g->gy, g->graph_max);
-    rc |= dalloc(&g->gp, g->graph_max);
+    for (int c = 0; c < nsets; ++c) {
+      rc |= dalloc(&g->gx2[c], g->graph_max);
+      rc |= dalloc(&g->gy2[c], g->graph_max);
+      rc |= dalloc(&g->gp2[c], g->graph_max);
+    }
   }
   for (int b = 0; b < NPAR; ++b) {
     if (b > 0 && !g->spatial) break;   // filter off: one batch at a time
@@ -1282,7 +1331,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       rc |= dalloc(&g->vb2[c], Bc);
     }
   }
-  rc |= dalloc(&g->hist, 256LL * nb_rs + 256LL * nb_rs / 4096 + 8);
+  for (int c = 0; c < (g->spatial ? NPAR : 1); ++c) rc |= dalloc(&g->hist2[c], 256LL * nb_rs + 256LL * nb_rs / 4096 + 8);
   rc |= dalloc(&g->sel, 1);
   if (!rc) cudaMemset(g->sel, 0, sizeof(SelState));
   rc |= dalloc(&g->frame, n);
@@ -1311,6 +1360,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     for (int c = 0; c < NPAR; ++c) {
       cudaEventCreateWithFlags(&g->evF[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evB[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evBuf[c], cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evS[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evA[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evV[c], cudaEventDisableTiming);
       cudaEventCreateWithFlags(&g->evN[c], cudaEventDisableTiming);
@@ -1332,6 +1383,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       cudaStreamCreateWithPriority(&g->pstream, cudaStreamNonBlocking, op);
       cudaStreamCreateWithPriority(&g->nstream, cudaStreamNonBlocking, op);
       cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&g->astream2, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&g->lstream, cudaStreamNonBlocking, lo);
     }
     rc |= dalloc(&g->last_tile, g->n_tiles);
     for (int c = 0; c < NPAR; ++c) rc |= dalloc(&g->ptt2[c], g->n_tiles);
@@ -1385,10 +1438,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
-  for (cudaStream_t st : {g->astream, g->nstream, g->fstream, g->pstream, g->bstream})
+  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->nstream, g->fstream, g->pstream, g->bstream})
     if (st) cudaStreamSynchronize(st);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->rkey, g->rnext, g->raw_x,
-                  g->raw_y, g->raw_p, g->blockcnt, g->longseg, g->hist,
+                  g->raw_y, g->raw_p, g->longseg,
                   g->bv64, g->mv64, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
@@ -1410,18 +1463,19 @@ int fibar_destroy(fibar_engine *g) {
                    g->S2[c], g->Qt2[c], g->pmap2[c], g->anc3[c], g->anc23[c], g->anc03[c], g->lc3[c], g->lu3[c]};
     for (void *p : per)
       if (p) cudaFree(p);
-    for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evA[c], g->evV[c], g->evN[c], g->evR[c]})
+    for (cudaEvent_t ev : {g->evF[c], g->evB[c], g->evBuf[c], g->evA[c], g->evV[c], g->evN[c], g->evR[c], g->evS[c]})
       if (ev) cudaEventDestroy(ev);
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
   for (auto &ge : g->graphs)
-    for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4})
+    for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4, ge.exec5})
       if (e) cudaGraphExecDestroy(e);
   if (g->capstream) cudaStreamDestroy(g->capstream);
-  for (void *q : {(void *)g->gx, (void *)g->gy, (void *)g->gp})
-    if (q) cudaFree(q);
+  for (int c = 0; c < NPAR; ++c)
+    for (void *q : {(void *)g->gx2[c], (void *)g->gy2[c], (void *)g->gp2[c], (void *)g->blockcnt2[c], (void *)g->hist2[c]})
+      if (q) cudaFree(q);
   if (g->bstream) cudaStreamDestroy(g->bstream);
-  for (cudaStream_t st : {g->astream, g->nstream, g->fstream, g->pstream})
+  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->nstream, g->fstream, g->pstream})
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t ev : {g->evIn, g->evCp})
     if (ev) cudaEventDestroy(ev);

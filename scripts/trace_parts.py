@@ -57,3 +57,11 @@ print(f"eviction     {avg(lambda k: t[k][5] - t[k][4]):.1f}   starts {avg(lambda
 print(f"blur stage   {avg(lambda k: t[k][7] - t[k][6]):.1f}   starts {avg(lambda k: t[k][6] - t[k][5]):+.1f} after the eviction pass; "
       f"{avg(lambda k: t[k][6] - t[k - 1][8]):+.1f} after the previous read-out")
 print(f"read-out     {avg(lambda k: t[k][8] - t[k][7]):.1f}")
+if os.environ.get("TRACE_ROWS"):
+    # raw rows: every mark of a few consecutive steady batches, relative to the first one's ingest start
+    k0 = ks[len(ks) // 2]
+    base = t[k0][0]
+    print("batch  " + "  ".join(f"{n:>9s}" for n in ("ing_beg", "ing_end", "win_beg", "win_end", "evi_beg", "evi_end", "blur_beg", "blur_end", "readout")))
+    for k in range(k0, k0 + 8):
+        if k in t:
+            print(f"{k:5d}  " + "  ".join(f"{t[k].get(l, float('nan')) - base:9.1f}" for l in range(9)))
