@@ -58,6 +58,12 @@ class FibarConfig(C.Structure):
     ]
 
 
+# The engine runs a batch on about a dozen CUDA streams; with the driver's
+# default of 8 hardware queues, streams that share a queue serialise falsely
+# (measured: the two ingest streams ran back to back).  Only effective when set
+# before the CUDA context is created; a C caller sets it in its own environment.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 _lib = None
 
 

@@ -166,7 +166,7 @@ struct fibar_engine {
   // parity: the temporal replay on the blur stream reads them while the next
   // front end writes its own)
   int8_t *epol2[NPAR] = {}, *spol2[NPAR] = {};
-  uint2 *longseg = nullptr;
+  uint2 *longseg2[NPAR] = {};   // long pixel segments, per buffer set (filter ON: listed by the ingest's k_link)
   unsigned *ka2[NPAR] = {}, *va2[NPAR] = {}, *kb2[NPAR] = {}, *vb2[NPAR] = {}, *hist2[NPAR] = {};
   uint2 *dp2[NPAR] = {};    // per-event link distances, per batch parity
   // window starts / targets after each event and the eviction -> popping-event
@@ -227,6 +227,16 @@ struct fibar_engine {
   // astream2 (it reads nothing of the previous batch); segments and links,
   // which do, follow on lstream in batch order
   cudaStream_t astream2 = nullptr, lstream = nullptr;
+  // asynchronous read-outs: a snapshot of l on the blur stream, the read-out
+  // itself on rstream beside the next batch's blur stage
+  cudaStream_t rstream = nullptr;
+  cudaStream_t tstream = nullptr;   // long-segment replay beside the short segments'
+  cudaEvent_t evT0 = nullptr, evT1 = nullptr;
+  float *snap[2] = {};
+  cudaEvent_t evSnap = nullptr, evRd[2] = {};
+  bool rd_used[2] = {};
+  long long n_snap = 0;
+  bool snap_on = true;   // FIBAR_SNAP=0: the read-out on the blur stream itself
   cudaEvent_t evS[NPAR] = {};   // the set's sort part is done
   cudaEvent_t evIn = nullptr, evCp = nullptr, evA[NPAR] = {};
   // ... and the eviction pass (pstream) after the window part (evV), beside
@@ -256,6 +266,7 @@ struct fibar_engine {
   }
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
+  bool green_small = false;   // FIBAR_GREEN_SMALL=1: small batches' blur in the green context too
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
   bool graphs_on = true;
   cudaStream_t capstream = nullptr;
@@ -348,7 +359,7 @@ struct fibar_engine {
     x.ekey = ekey2[par];
     x.epol = epol2[par];
     x.spol = spol2[par];
-    x.longseg = longseg;
+    x.longseg = longseg2[par];
     x.tkey = ka2[par];
     x.skey = skey;
     x.sidx = sidx;
@@ -564,7 +575,7 @@ int enqueue_post(fibar_engine *g, long long n_raw, int par, int where, cudaStrea
   Ctx x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
   const int nb = (int)((n_raw + TPB - 1) / TPB);
   fibar_launch(L, "popj_map", k_popj_map, nb, TPB, 0, s, x);
-  fibar_launch(L, "popj", k_popj, (int)((n_raw + g->n_pix + TPB) / TPB), TPB, 0, s, x);
+  fibar_launch(L, "popj", k_popj, (int)((n_raw + TPB) / TPB) + g->nsm, TPB, 0, s, x);
   fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x, 1);   // its last block closes the batch
   CK(cudaGetLastError());
   return 0;
@@ -794,8 +805,15 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
       g->mark(6, bs);
       L.stream = bs;
+      // long segments (listed by the ingest) beside the short ones, on their own stream
+      CK(cudaEventRecord(g->evT0, bs));
+      CK(cudaStreamWaitEvent(g->tstream, g->evT0, 0));
       fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, bs, x);
-      fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, bs, x);
+      L.stream = g->tstream;
+      fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, g->tstream, x);
+      CK(cudaEventRecord(g->evT1, g->tstream));
+      CK(cudaStreamWaitEvent(bs, g->evT1, 0));
+      L.stream = bs;
     } else {
       if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
       fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
@@ -808,7 +826,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       fibar_launch(L, "halo_count", k_halo_count, nbh, TPB, 0, s, x, g->hcnt, nbh);
       scan_exclusive_u32(L, g->hcnt, 4 * nbh + 1);
       fibar_launch(L, "halo_write", k_halo_write, nbh, TPB, 0, s, x, (const unsigned *)g->hcnt, nbh, g->hlist);
-      const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
+      const int nbp = (int)((n_raw + TPB) / TPB) + g->nsm;
       fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, s, x);
       g->hnb = nbh;
       g->hctx = x;
@@ -824,9 +842,9 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     }
     L.stream = bs;
     if (g->blur_on) {
-      const int nbp = (int)((n_raw + g->n_pix + TPB) / TPB);
+      const int nbp = (int)((n_raw + TPB) / TPB) + g->nsm;
       fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, bs, x);
-      if (g->gstream && !graph && n_raw > g->small_chunk_max) {
+      if (g->gstream && !graph && (n_raw > g->small_chunk_max || g->green_small)) {
         // the blur dataflow alone on its own SM partition (green context):
         // its polling no longer shares SMs with the next batch's front end
         // (large batches; a small batch's blur stage is the critical chain
@@ -1222,6 +1240,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // the second stream with the whole GPU.
   int green_sms = 24;
   if (const char *v = getenv("FIBAR_GREEN")) green_sms = atoi(v);
+  if (const char *v = getenv("FIBAR_GREEN_SMALL")) g->green_small = atoi(v) != 0;
   if (halo) green_sms = 0;
   if (green_sms > 0 && cfg->spatial_enabled && !g->serial) {
     const unsigned want = (unsigned)std::max(8, green_sms);
@@ -1317,7 +1336,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->epol2[b], Bc);
     rc |= dalloc(&g->spol2[b], Bc);
   }
-  rc |= dalloc(&g->longseg, MAX_LONG);
+  for (int c = 0; c < (g->spatial ? NPAR : 1); ++c) rc |= dalloc(&g->longseg2[c], MAX_LONG);
   rc |= dalloc(&g->bsd, NPAR);
   if (!rc) cudaMemset(g->bsd, 0, NPAR * sizeof(BatchState));
   for (int c = 0; c < NPAR; ++c) {
@@ -1385,6 +1404,16 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, lo);
       cudaStreamCreateWithPriority(&g->astream2, cudaStreamNonBlocking, lo);
       cudaStreamCreateWithPriority(&g->lstream, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&g->rstream, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&g->tstream, cudaStreamNonBlocking, hi);
+      cudaEventCreateWithFlags(&g->evT0, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evT1, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&g->evSnap, cudaEventDisableTiming);
+      for (int c = 0; c < 2; ++c) {
+        cudaEventCreateWithFlags(&g->evRd[c], cudaEventDisableTiming);
+        rc |= dalloc(&g->snap[c], n);
+      }
+      if (const char *v = getenv("FIBAR_SNAP")) g->snap_on = atoi(v) != 0;
     }
     rc |= dalloc(&g->last_tile, g->n_tiles);
     for (int c = 0; c < NPAR; ++c) rc |= dalloc(&g->ptt2[c], g->n_tiles);
@@ -1438,10 +1467,10 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
-  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->nstream, g->fstream, g->pstream, g->bstream})
+  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->nstream, g->fstream, g->pstream, g->bstream, g->rstream, g->tstream})
     if (st) cudaStreamSynchronize(st);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->rkey, g->rnext, g->raw_x,
-                  g->raw_y, g->raw_p, g->longseg,
+                  g->raw_y, g->raw_p,
                   g->bv64, g->mv64, g->ch, g->vl, g->sel, g->frame,
                   g->cnt_tmp, g->tcnt_tmp, g->q_tmp, g->dbg_t, g->dbg_g, g->hslot, g->hlist, g->hcnt};
   for (void *p : ptrs)
@@ -1472,10 +1501,15 @@ int fibar_destroy(fibar_engine *g) {
       if (e) cudaGraphExecDestroy(e);
   if (g->capstream) cudaStreamDestroy(g->capstream);
   for (int c = 0; c < NPAR; ++c)
-    for (void *q : {(void *)g->gx2[c], (void *)g->gy2[c], (void *)g->gp2[c], (void *)g->blockcnt2[c], (void *)g->hist2[c]})
+    for (void *q : {(void *)g->gx2[c], (void *)g->gy2[c], (void *)g->gp2[c], (void *)g->blockcnt2[c], (void *)g->hist2[c],
+                    (void *)g->longseg2[c]})
       if (q) cudaFree(q);
   if (g->bstream) cudaStreamDestroy(g->bstream);
-  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->nstream, g->fstream, g->pstream})
+  for (void *q : {(void *)g->snap[0], (void *)g->snap[1]})
+    if (q) cudaFree(q);
+  for (cudaEvent_t ev : {g->evSnap, g->evRd[0], g->evRd[1], g->evT0, g->evT1})
+    if (ev) cudaEventDestroy(ev);
+  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->rstream, g->tstream, g->nstream, g->fstream, g->pstream})
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t ev : {g->evIn, g->evCp})
     if (ev) cudaEventDestroy(ev);
@@ -1688,12 +1722,26 @@ int fibar_render_async(fibar_engine *g, int32_t mode, double fixed_bound, uint8_
   const bool on_blur = g->spatial && g->last_b >= 0 && !g->serial;
   // after the newest blur stage, on its stream: the next batch's front end
   // (engine stream) does not wait for the read-out, its temporal replay does
+  // -- unless the read-out works on a snapshot (rstream): then the blur
+  // stream only carries the snapshot copy
+  const bool snap = on_blur && g->snap_on && g->rstream && g->snap[0];
   cudaStream_t rs = on_blur ? g->bstream : s0;
+  const float *src = g->l;
+  if (snap) {
+    const int i = (int)(g->n_snap++ & 1);
+    if (g->rd_used[i]) CK(cudaStreamWaitEvent(g->bstream, g->evRd[i], 0));   // its previous read-out is done
+    L.stream = g->bstream;
+    fibar_launch(L, "snap", k_snap, g->nsm * 2, TPB, 0, g->bstream, (const float *)g->l, g->snap[i], g->n_pix);
+    CK(cudaEventRecord(g->evSnap, g->bstream));
+    CK(cudaStreamWaitEvent(g->rstream, g->evSnap, 0));
+    rs = g->rstream;
+    src = g->snap[i];
+  }
   L.stream = rs;
   // rendered into device memory (render_core would wait for a host frame),
   // copied to a host frame asynchronously here
   const bool dev_out = out_mem == FIBAR_MEM_DEVICE;
-  rc = render_core(L, g->l, g->n_pix, mode, fixed_bound, dev_out ? out : g->frame, FIBAR_MEM_DEVICE, nullptr, nullptr,
+  rc = render_core(L, src, g->n_pix, mode, fixed_bound, dev_out ? out : g->frame, FIBAR_MEM_DEVICE, nullptr, nullptr,
                    g->sel, g->frame, g->nsm);
   if (!rc && !dev_out) {
     cudaError_t e = cudaMemcpyAsync(out, g->frame, g->n_pix, cudaMemcpyDeviceToHost, rs);
@@ -1708,6 +1756,12 @@ int fibar_render_async(fibar_engine *g, int32_t mode, double fixed_bound, uint8_
     g->mark(8, rs);   // 8: read-out end
     cudaError_t e = cudaEventRecord(g->evB[g->last_b], rs);   // later batches order after the read-out
     if (e != cudaSuccess) rc = cuda_fail(e, "render_async event");
+    if (!rc && snap) {
+      const int i = (int)((g->n_snap - 1) & 1);
+      e = cudaEventRecord(g->evRd[i], rs);
+      if (e != cudaSuccess) rc = cuda_fail(e, "render_async event");
+      g->rd_used[i] = true;
+    }
   }
   if (!rc) {
     cudaError_t e = cudaEventRecord((cudaEvent_t)ready, rs);

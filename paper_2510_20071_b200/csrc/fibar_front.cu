@@ -353,6 +353,10 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
     const unsigned seglen = pend - (unsigned)i;
     // (atomic: the previous batch's eviction pass may be subtracting meanwhile;
     // a count not yet decremented only makes the check more conservative)
+    if (seglen > (unsigned)LONG_SEG) {   // long segment (hot pixel): listed here for k_temporal_long
+      const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
+      if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
+    }
     const unsigned wc = atomicAdd(&x.wcnt[c], seglen);
     if ((unsigned long long)wc + seglen > 65535ull) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);
     // the pixel's last-touch for the next batch (read above by this thread
@@ -1648,9 +1652,10 @@ __global__ void __launch_bounds__(TPB) k_popj(Ctx x) {
   const long long B = x.bs->B;
   const long long E0 = x.bs->E0, s_start = x.bs->s_start;
   const unsigned npop = B > 0 ? x.S[B - 1] : 0u;
-  const unsigned p = blockIdx.x * TPB + threadIdx.x;   // one thread per eviction (balanced)
+  // one thread per eviction (balanced); the grid is sized for the batch's
+  // events (about one eviction each) and strides over a collapsing window's
   unsigned nst = 0;
-  if (p < npop) {
+  for (unsigned p = blockIdx.x * TPB + threadIdx.x; p < npop; p += gridDim.x * TPB) {
     const unsigned lo = x.pmap[p];   // popping event (k_popj_map)
     const long long k = s_start + p;
     const long long j = E0 + lo;

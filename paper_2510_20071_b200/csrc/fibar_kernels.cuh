@@ -176,6 +176,7 @@ __device__ __forceinline__ float order_unkey(unsigned k) {
 }
 
 // kernels (launched by fibar_engine.cu)
+__global__ void __launch_bounds__(TPB) k_snap(const float *__restrict__ src, float *__restrict__ dst, long long n);
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks);
 __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
 __global__ void k_batch_begin(Ctx x);
@@ -212,7 +213,10 @@ __global__ void __launch_bounds__(TPB) k_halo_write(Ctx x, const unsigned *cnt, 
 __global__ void k_halo_epoch(Ctx x);
 __global__ void __launch_bounds__(TPB) k_halo_collect(Ctx x, const unsigned *hlist, long long n_in, long long n_out,
                                                       unsigned long long *out);
-__global__ void __launch_bounds__(RO_TPB, 1) k_readout(const float *__restrict__ l, long long n, SelState *sel, int mode, double fixed_bound, uint4 ranks, double g_lo, double g_hi, uint8_t *__restrict__ out, long long slice, int on_chip);
+#ifndef FIBAR_RO_MINB
+#define FIBAR_RO_MINB 2
+#endif
+__global__ void __launch_bounds__(RO_TPB, FIBAR_RO_MINB) k_readout(const float *__restrict__ l, long long n, SelState *sel, int mode, double fixed_bound, uint4 ranks, double g_lo, double g_hi, uint8_t *__restrict__ out, long long slice, int on_chip);
 __global__ void __launch_bounds__(TPB) k_evf1_decode(const uint4 *__restrict__ rec2, const uint2 *__restrict__ rec1, long long nrec, int W, int H, uint16_t *__restrict__ xo, uint16_t *__restrict__ yo, int8_t *__restrict__ po, unsigned *__restrict__ dto, unsigned long long *__restrict__ bsum, unsigned long long *__restrict__ first_bad);
 __global__ void __launch_bounds__(1024) k_evf1_block_scan(unsigned long long *bsum, int nb, unsigned long long t_base);
 __global__ void __launch_bounds__(TPB) k_evf1_times(const unsigned *__restrict__ dt, long long nrec, const unsigned long long *__restrict__ bofs, unsigned long long *__restrict__ t);

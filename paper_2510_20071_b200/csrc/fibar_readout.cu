@@ -87,7 +87,10 @@ __device__ __forceinline__ void ro_barrier(SelState *sel, unsigned gen0, unsigne
   __syncthreads();
 }
 
-__global__ void __launch_bounds__(RO_TPB, 1)
+#ifndef FIBAR_RO_MINB
+#define FIBAR_RO_MINB 2
+#endif
+__global__ void __launch_bounds__(RO_TPB, FIBAR_RO_MINB)
     k_readout(const float *__restrict__ l, long long n, SelState *sel, int mode, double fixed_bound, uint4 ranks,
               double g_lo, double g_hi, uint8_t *__restrict__ out, long long slice, int on_chip) {
   extern __shared__ __align__(16) unsigned ro_keys[];
@@ -320,6 +323,17 @@ __global__ void __launch_bounds__(RO_TPB, 1)
       o[i] = (uint8_t)ro_map(keys_here ? order_unkey(ro_keys[i]) : l[beg + i], lo, scale, deg);
   }
   RO_TS(15);
+}
+
+// A snapshot of the brightness for an asynchronous read-out (the read-out then
+// runs beside the next batch's blur stage, which rewrites l)
+__global__ void __launch_bounds__(TPB) k_snap(const float *__restrict__ src, float *__restrict__ dst, long long n) {
+  pdl_wait();
+  const long long stride = (long long)gridDim.x * TPB;
+  const long long n4 = n >> 2;
+  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n4; i += stride)
+    reinterpret_cast<float4 *>(dst)[i] = __ldcg(reinterpret_cast<const float4 *>(src) + i);
+  for (long long i = (n4 << 2) + (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += stride) dst[i] = src[i];
 }
 
 // ------------------------------------------------------------ EVF1 decode ---

@@ -117,11 +117,7 @@ __global__ void __launch_bounds__(TPB) k_temporal_runs(Ctx x) {
   const unsigned c = x.ekey[x.sidx[i]];
   const PixRec prc = x.pt[c];
   const long long end = prc.end;
-  if (end - i > LONG_SEG) {   // long segment (hot pixel): the warp-parallel kernel
-    const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
-    if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
-    return;
-  }
+  if (end - i > LONG_SEG) return;   // long segment (hot pixel): k_temporal_long (listed by k_link), beside this kernel
   unsigned carry = prc.carried;
   if (carry != FIBAR_NONE) x.item[carry].runpos = (unsigned)i;
   float pb = x.pbar[c], lv = x.l[c];
@@ -549,16 +545,22 @@ __device__ __forceinline__ void prep_item(const Ctx &x, unsigned p);
 __global__ void __launch_bounds__(TPB, PREP_MINB) k_blur_prep(Ctx x) {
   pdl_wait();
   const long long B = x.bs->B;
-  const long long q = (long long)blockIdx.x * TPB + threadIdx.x;
-  if (q < B) {
-    const unsigned bidx = x.posrec[q].bidx;
-    if (bidx != FIBAR_NONE) prep_item(x, bidx);
-    if (q == 0 || x.skey[q - 1] != x.skey[q]) {
-      const unsigned carried = x.pt[x.ekey[x.sidx[q]]].carried;
-      if (carried != FIBAR_NONE) prep_item(x, carried);
+  const long long total = B + (long long)x.bs->nco;
+  // (the grid covers the batch's events; the carried-only list, up to one
+  // entry per eviction, is strided over)
+  for (long long q = (long long)blockIdx.x * TPB + threadIdx.x; q < total; q += (long long)gridDim.x * TPB) {
+    unsigned it0 = FIBAR_NONE, it1 = FIBAR_NONE;
+    if (q < B) {
+      it0 = x.posrec[q].bidx;
+      if (q == 0 || x.skey[q - 1] != x.skey[q]) it1 = x.pt[x.ekey[x.sidx[q]]].carried;
+    } else {
+      it0 = x.colist[q - B];
     }
-  } else if (q - B < (long long)x.bs->nco) {
-    prep_item(x, x.colist[q - B]);
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+      const unsigned p = k ? it1 : it0;
+      if (p != FIBAR_NONE) prep_item(x, p);
+    }
   }
 }
 
