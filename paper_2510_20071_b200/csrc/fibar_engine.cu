@@ -266,6 +266,7 @@ struct fibar_engine {
   }
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
+  int long_grid_small = 48;   // FIBAR_LONG_GRID: k_temporal_long blocks for small batches
   bool green_small = false;   // FIBAR_GREEN_SMALL=1: small batches' blur in the green context too
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
   bool graphs_on = true;
@@ -810,7 +811,9 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaStreamWaitEvent(g->tstream, g->evT0, 0));
       fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, bs, x);
       L.stream = g->tstream;
-      fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, g->tstream, x);
+      // (a small batch has few long segments: a small grid, whose 150-register blocks need not wait for SMs)
+      fibar_launch(L, "temporal_long", k_temporal_long, n_raw <= g->small_chunk_max ? g->long_grid_small : g->nsm * 2, LONG_TPB, 0,
+                   g->tstream, x);
       CK(cudaEventRecord(g->evT1, g->tstream));
       CK(cudaStreamWaitEvent(bs, g->evT1, 0));
       L.stream = bs;
@@ -1240,6 +1243,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // the second stream with the whole GPU.
   int green_sms = 24;
   if (const char *v = getenv("FIBAR_GREEN")) green_sms = atoi(v);
+  if (const char *v = getenv("FIBAR_LONG_GRID")) g->long_grid_small = std::max(1, atoi(v));
   if (const char *v = getenv("FIBAR_GREEN_SMALL")) g->green_small = atoi(v) != 0;
   if (halo) green_sms = 0;
   if (green_sms > 0 && cfg->spatial_enabled && !g->serial) {

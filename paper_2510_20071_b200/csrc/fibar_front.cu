@@ -1483,7 +1483,7 @@ __device__ int rerun_chunk_staged(const Ctx &x, WState &w, long long b, long lon
   return merged_at != 0xFFFFFFFFu ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x) {
+__global__ void __launch_bounds__(VF_TPB, VF_TPB > 256 ? 1 : 2) k_window_verify(Ctx x) {
   pdl_wait();
   constexpr int NW = VF_TPB / 32;
   __shared__ uint2 sdp[NW][VF_DP];

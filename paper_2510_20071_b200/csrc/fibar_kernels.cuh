@@ -47,7 +47,10 @@ struct VRec {
   long long s, q, np, nt, ev;
   int c, pad;
 };
-constexpr int VF_TPB = 256;   // k_window_verify: threads per CTA (one warp per re-run)
+#ifndef FIBAR_VF_TPB
+#define FIBAR_VF_TPB 256
+#endif
+constexpr int VF_TPB = FIBAR_VF_TPB;   // k_window_verify: threads per CTA (one warp per re-run)
 constexpr int VF_CTAS = 16;   // k_window_verify: CTAs in its one cluster (non-portable size)
 
 // device packets gathered into the device staging set (non-contiguous
@@ -196,7 +199,7 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run_g2(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run_g4(Ctx x);
 __global__ void __launch_bounds__(128) k_window_run_g8(Ctx x);
-__global__ void __launch_bounds__(VF_TPB, 2) k_window_verify(Ctx x);
+__global__ void __launch_bounds__(VF_TPB, VF_TPB > 256 ? 1 : 2) k_window_verify(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj_map(Ctx x);
 __global__ void __launch_bounds__(TPB) k_popj(Ctx x);
 __global__ void __launch_bounds__(TPB) k_posinfo(Ctx x, int close);

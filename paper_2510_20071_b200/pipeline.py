@@ -30,6 +30,7 @@ import hashlib
 import logging
 import math
 import os
+import weakref
 from dataclasses import dataclass
 from fractions import Fraction
 from typing import Callable, Iterable, Iterator
@@ -735,7 +736,7 @@ def _readout_times(fps: float | None, explicit) -> tuple[Iterator[float], bool]:
     return grid(), False
 
 
-_RUN_DEPTH = 4   # read-outs in flight in run()
+_RUN_DEPTH = 8   # read-outs in flight in run() (the device pipeline holds about five batches)
 
 
 def _time_key(r, dtype):
@@ -798,10 +799,13 @@ def run(
     ring = engine.__dict__.setdefault("_run_frame_pool", []) if pipelined else []
 
     def deliver(af) -> None:
-        frame = af.frame()
+        # the frame's pixels are the pinned buffer itself (no copy); the buffer
+        # goes back to the ring once nothing refers to the array any more
+        frame = af.frame(copy=False)
+        weakref.finalize(frame.pixels, ring.append, (af.out, af.meta))
         if frame_sink is not None:
             frame_sink(af.index, frame)
-        ring.append((af.out, af.meta))
+        del frame
 
     def emit(readout) -> None:
         nonlocal frame_index
