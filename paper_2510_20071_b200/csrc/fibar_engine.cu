@@ -129,8 +129,10 @@ struct GraphEntry {
   long long kernels3 = 0;
   cudaGraphExec_t exec4 = nullptr;   // kind 1: the anchors (exec2: run + verifier)
   long long kernels4 = 0;
-  cudaGraphExec_t exec5 = nullptr;   // kind 1: segments and links (exec: the sort part of the ingest)
+  cudaGraphExec_t exec5 = nullptr;   // kind 1: segments, links and the anchors (exec: the sort part of the ingest)
   long long kernels5 = 0;
+  cudaGraphExec_t exec6 = nullptr;   // kind 1: the blur stage (replay, tap resolution, blur dataflow, final)
+  long long kernels6 = 0;
   int kind = 0;              // 0: whole batch (serial schedule), 1: front end of the streamed schedule (two parts)
   int par = 0;               // kind 1: the batch parity whose buffers it uses
   int where = 0;             // kind 1: which radix-sort buffer holds the sorted keys
@@ -267,6 +269,7 @@ struct fibar_engine {
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
   int long_grid_small = 48;   // FIBAR_LONG_GRID: k_temporal_long blocks for small batches
+  bool stage_graphs = true;   // FIBAR_STAGE_GRAPHS=0: small batches' blur stage as separate launches
   bool green_small = false;   // FIBAR_GREEN_SMALL=1: small batches' blur in the green context too
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
   bool graphs_on = true;
@@ -598,6 +601,50 @@ int enqueue_front(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   return rc;
 }
 
+// The temporal replay of the blur stage on stream bs: short segments there,
+// long ones (listed by the ingest) beside them on tstream.
+int enqueue_temporal_forked(fibar_engine *g, long long n_raw, const Ctx &x, cudaStream_t bs) {
+  Launcher &L = g->L;
+  const int nb = (int)((n_raw + TPB - 1) / TPB);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  CK(cudaStreamIsCapturing(bs, &cs));
+  CK(cudaEventRecord(g->evT0, bs));
+  CK(cudaStreamWaitEvent(g->tstream, g->evT0, 0));
+  fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, bs, x);
+  L.stream = g->tstream;
+  // (a small batch has few long segments: a small grid, whose 150-register blocks need not wait for SMs)
+  fibar_launch(L, "temporal_long", k_temporal_long, n_raw <= g->small_chunk_max ? g->long_grid_small : g->nsm * 2, LONG_TPB, 0,
+               g->tstream, x);
+  CK(cudaEventRecord(g->evT1, g->tstream));
+  CK(cudaStreamWaitEvent(bs, g->evT1, 0));
+  L.stream = bs;
+  return 0;
+}
+
+// The rest of the blur stage (no green context: small batches)
+int enqueue_blur_rest(fibar_engine *g, long long n_raw, const Ctx &x, cudaStream_t bs, bool graph) {
+  Launcher &L = g->L;
+  L.stream = bs;
+  if (g->blur_on) {
+    const int nbp = (int)((n_raw + TPB) / TPB) + g->nsm;
+    fibar_launch(L, "blur_prep", k_blur_prep, nbp, TPB, 0, bs, x);
+    fibar_launch(L, "blur", k_blur, graph ? g->blur_grid_serial : g->blur_grid, TPB, 0, bs, x);
+  }
+  fibar_launch(L, "final", k_final, g->nsm * 8, TPB, 0, bs, x);
+  return 0;
+}
+
+// the blur stage of a small batch as captured into its graph (stream: capstream)
+int capture_blur_stage(fibar_engine *g, long long n_raw, int par, int where) {
+  Ctx x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
+  x.raw_x = g->gx2[par];
+  x.raw_y = g->gy2[par];
+  x.raw_p = g->gp2[par];
+  int rc = enqueue_temporal_forked(g, n_raw, x, g->capstream);
+  if (!rc) rc = enqueue_blur_rest(g, n_raw, x, g->capstream, false);
+  return rc;
+}
+
 // The captured front end for a size class (n_raw: the class's upper bound)
 // and a parity, as two graphs: exec the ingest (reading the fixed input
 // buffers gx/gy/gp and the batch's raw count that k_stage leaves in the
@@ -610,7 +657,7 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     if (ge.kind == 1 && ge.n == n_raw && ge.par == par) return &ge;
   if (g->graphs.size() >= 8 * NPAR) {   // small cache: drop the oldest (freed once its launches finish)
     for (cudaGraphExec_t e : {g->graphs.front().exec, g->graphs.front().exec2, g->graphs.front().exec3,
-                              g->graphs.front().exec4, g->graphs.front().exec5})
+                              g->graphs.front().exec4, g->graphs.front().exec5, g->graphs.front().exec6})
       if (e) cudaGraphExecDestroy(e);
     g->graphs.erase(g->graphs.begin());
   }
@@ -621,20 +668,22 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   ge.n = n_raw;
   ge.kind = 1;
   ge.par = par;
-  for (int part = 0; part < 5; ++part) {
+  for (int part : {0, 1, 2, 4, 5}) {
     const long long l0 = L.launches;
     cudaGraph_t graph = nullptr;
     Ctx x{};
     if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
-      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4})
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4, ge.exec5, ge.exec6})
         if (e) cudaGraphExecDestroy(e);
       return nullptr;
     }
     L.stream = g->capstream;
     const int rc = part == 0   ? enqueue_ingest_a(g, g->gx2[par], g->gy2[par], g->gp2[par], n_raw, nullptr, par,
                                                   g->capstream, ge.where, &g->bsd[par].n_raw)
-                   : part == 4 ? enqueue_ingest_b(g, n_raw, par, ge.where, g->capstream)
+                   : part == 4 ? (enqueue_ingest_b(g, n_raw, par, ge.where, g->capstream) ||
+                                  enqueue_anchors(g, n_raw, par, ge.where, g->capstream))
+                   : part == 5 ? capture_blur_stage(g, n_raw, par, ge.where)
                    : part == 1 ? enqueue_chain(g, n_raw, par, ge.where, g->capstream, x, nullptr)
                    : part == 2 ? enqueue_post(g, n_raw, par, ge.where, g->capstream)
                                : enqueue_anchors(g, n_raw, par, ge.where, g->capstream);
@@ -647,7 +696,7 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     L.launches = l0;
     if (rc || ce != cudaSuccess) {
       cudaGetLastError();
-      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4})
+      for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4, ge.exec5, ge.exec6})
         if (e) cudaGraphExecDestroy(e);
       g->graphs_on = false;   // capture impossible here: stream every kernel from now on
       return nullptr;
@@ -664,9 +713,12 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     } else if (part == 3) {
       ge.exec4 = exec;
       ge.kernels4 = k;
-    } else {
+    } else if (part == 4) {
       ge.exec5 = exec;
       ge.kernels5 = k;
+    } else {
+      ge.exec6 = exec;
+      ge.kernels6 = k;
     }
   }
   g->graphs.push_back(ge);
@@ -694,6 +746,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   Ctx x{};
   int where = 0;
   const int nb = (int)((n_raw + TPB - 1) / TPB);
+  const GraphEntry *stage_graph = nullptr;   // small batches: the blur stage's graph
   if (split) {
     const bool small = g->graphs_on && !L.prof && n_raw <= g->graph_max;
     // a small batch's sort part alternates between two streams
@@ -723,14 +776,10 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaGraphLaunch(ge->exec5, g->lstream));
       L.launches += ge->kernels5;
       g->mark(1, g->lstream);
-      CK(cudaEventRecord(g->evA[par], g->lstream));
-      // anchors after the ingest and the previous batch's run
-      cudaStream_t sn = g->nstream;
-      CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
-      CK(cudaGraphLaunch(ge->exec4, sn));
-      L.launches += ge->kernels4;
-      CK(cudaEventRecord(g->evN[par], sn));
+      // (the same graph carries the anchors: they follow the previous batch's anyway)
+      CK(cudaEventRecord(g->evN[par], g->lstream));
       CK(cudaStreamWaitEvent(s, g->evN[par], 0));
+      if (g->stage_graphs && !g->green_small) stage_graph = ge;
       g->mark(2, s);
       CK(cudaGraphLaunch(ge->exec2, s));   // (records evR[par] after the run)
       L.launches += ge->kernels2;
@@ -805,18 +854,22 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaEventRecord(g->evF[par], s));
       CK(cudaStreamWaitEvent(bs, g->evF[par], 0));
       g->mark(6, bs);
+      if (stage_graph) {
+        // a small batch: the whole blur stage replays one graph
+        CK(cudaGraphLaunch(stage_graph->exec6, bs));
+        L.launches += stage_graph->kernels6;
+        L.stream = u;
+        g->mark(7, bs);
+        CK(cudaEventRecord(g->evB[par], bs));
+        CK(cudaEventRecord(g->evBuf[par], bs));
+        g->b_used[par] = true;
+        g->last_b = par;
+        CK(cudaGetLastError());
+        return 0;
+      }
       L.stream = bs;
-      // long segments (listed by the ingest) beside the short ones, on their own stream
-      CK(cudaEventRecord(g->evT0, bs));
-      CK(cudaStreamWaitEvent(g->tstream, g->evT0, 0));
-      fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, bs, x);
-      L.stream = g->tstream;
-      // (a small batch has few long segments: a small grid, whose 150-register blocks need not wait for SMs)
-      fibar_launch(L, "temporal_long", k_temporal_long, n_raw <= g->small_chunk_max ? g->long_grid_small : g->nsm * 2, LONG_TPB, 0,
-                   g->tstream, x);
-      CK(cudaEventRecord(g->evT1, g->tstream));
-      CK(cudaStreamWaitEvent(bs, g->evT1, 0));
-      L.stream = bs;
+      int rc = enqueue_temporal_forked(g, n_raw, x, bs);
+      if (rc) return rc;
     } else {
       if (!graph && g->last_b >= 0) CK(cudaStreamWaitEvent(s, g->evB[g->last_b], 0));
       fibar_launch(L, "temporal", k_temporal_runs, nb, TPB, 0, s, x);
@@ -1243,6 +1296,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // the second stream with the whole GPU.
   int green_sms = 24;
   if (const char *v = getenv("FIBAR_GREEN")) green_sms = atoi(v);
+  if (const char *v = getenv("FIBAR_STAGE_GRAPHS")) g->stage_graphs = atoi(v) != 0;
   if (const char *v = getenv("FIBAR_LONG_GRID")) g->long_grid_small = std::max(1, atoi(v));
   if (const char *v = getenv("FIBAR_GREEN_SMALL")) g->green_small = atoi(v) != 0;
   if (halo) green_sms = 0;
@@ -1501,7 +1555,7 @@ int fibar_destroy(fibar_engine *g) {
   }
   if (g->cstream) cudaStreamDestroy(g->cstream);
   for (auto &ge : g->graphs)
-    for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4, ge.exec5})
+    for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4, ge.exec5, ge.exec6})
       if (e) cudaGraphExecDestroy(e);
   if (g->capstream) cudaStreamDestroy(g->capstream);
   for (int c = 0; c < NPAR; ++c)
