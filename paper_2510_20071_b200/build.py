@@ -21,7 +21,7 @@ DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("fibar_common.cuh", "fibar
     os.path.join(HERE, "..", "include", "fibar_b200.h")]
 OUT = os.path.join(HERE, "_lib", "libfibar_b200.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-EXTRA = [f"-D{d}" for d in os.environ.get("FIBAR_DEFINES", "").split(",") if d]
+EXTRA = [f"-D{d}" for d in os.environ.get("FIBAR_DEFINES", "").split(",") if d] + os.environ.get("FIBAR_NVCC_FLAGS", "").split()
 
 
 def nvcc() -> str:

@@ -35,6 +35,7 @@
 #include <cstring>
 #include <cmath>
 #include <algorithm>
+#include <chrono>
 #include <string>
 #include <mutex>
 #include <vector>
@@ -269,6 +270,7 @@ struct fibar_engine {
   bool temporal_on_blur = true;   // FIBAR_TEMPORAL_ON_BLUR
   int gblocks = 0;
   int long_grid_small = 48;   // FIBAR_LONG_GRID: k_temporal_long blocks for small batches
+  int n_last = -1;            // the set whose anchors were enqueued last (evN)
   bool stage_graphs = true;   // FIBAR_STAGE_GRAPHS=0: small batches' blur stage as separate launches
   bool green_small = false;   // FIBAR_GREEN_SMALL=1: small batches' blur in the green context too
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
@@ -672,6 +674,7 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     const long long l0 = L.launches;
     cudaGraph_t graph = nullptr;
     Ctx x{};
+    const auto t_c0 = std::chrono::steady_clock::now();
     if (cudaStreamBeginCapture(g->capstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
       cudaGetLastError();
       for (cudaGraphExec_t e : {ge.exec, ge.exec2, ge.exec3, ge.exec4, ge.exec5, ge.exec6})
@@ -688,9 +691,16 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
                    : part == 2 ? enqueue_post(g, n_raw, par, ge.where, g->capstream)
                                : enqueue_anchors(g, n_raw, par, ge.where, g->capstream);
     L.stream = s0;
+    const auto t_c1 = std::chrono::steady_clock::now();
     cudaError_t ce = cudaStreamEndCapture(g->capstream, &graph);
     cudaGraphExec_t exec = nullptr;
     if (rc == 0 && ce == cudaSuccess) ce = cudaGraphInstantiate(&exec, graph, 0);
+    if (getenv("FIBAR_DEBUG_CAPTURE")) {
+      const auto t_c2 = std::chrono::steady_clock::now();
+      fprintf(stderr, "[fibar] capture part %d par %d n %lld: capture %.3f ms, end+instantiate %.3f ms\n", part, par, n_raw,
+              std::chrono::duration<double, std::milli>(t_c1 - t_c0).count(),
+              std::chrono::duration<double, std::milli>(t_c2 - t_c1).count());
+    }
     if (graph) cudaGraphDestroy(graph);
     const long long k = L.launches - l0;
     L.launches = l0;
@@ -773,11 +783,15 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaEventRecord(g->evS[par], sa));
       // segments and links in batch order
       CK(cudaStreamWaitEvent(g->lstream, g->evS[par], 0));
+      // the anchors read the start state the previous batch's anchors predicted
+      // (a large batch's run on nstream)
+      if (g->n_last >= 0) CK(cudaStreamWaitEvent(g->lstream, g->evN[g->n_last], 0));
       CK(cudaGraphLaunch(ge->exec5, g->lstream));
       L.launches += ge->kernels5;
       g->mark(1, g->lstream);
       // (the same graph carries the anchors: they follow the previous batch's anyway)
       CK(cudaEventRecord(g->evN[par], g->lstream));
+      g->n_last = par;
       CK(cudaStreamWaitEvent(s, g->evN[par], 0));
       if (g->stage_graphs && !g->green_small) stage_graph = ge;
       g->mark(2, s);
@@ -808,11 +822,13 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaEventRecord(g->evA[par], g->lstream));
       cudaStream_t sn = g->nstream;
       CK(cudaStreamWaitEvent(sn, g->evA[par], 0));
+      if (g->n_last >= 0) CK(cudaStreamWaitEvent(sn, g->evN[g->n_last], 0));   // (a small batch's anchors ran on lstream)
       L.stream = sn;
       rc = enqueue_anchors(g, n_raw, par, where, sn);
       L.stream = u;
       if (rc) return rc;
       CK(cudaEventRecord(g->evN[par], sn));
+      g->n_last = par;
       CK(cudaStreamWaitEvent(s, g->evN[par], 0));
       L.stream = s;
       rc = enqueue_chain(g, n_raw, par, where, s, x, nullptr);

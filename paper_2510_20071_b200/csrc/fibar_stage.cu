@@ -545,22 +545,19 @@ __device__ __forceinline__ void prep_item(const Ctx &x, unsigned p);
 __global__ void __launch_bounds__(TPB, PREP_MINB) k_blur_prep(Ctx x) {
   pdl_wait();
   const long long B = x.bs->B;
-  const long long total = B + (long long)x.bs->nco;
-  // (the grid covers the batch's events; the carried-only list, up to one
-  // entry per eviction, is strided over)
-  for (long long q = (long long)blockIdx.x * TPB + threadIdx.x; q < total; q += (long long)gridDim.x * TPB) {
-    unsigned it0 = FIBAR_NONE, it1 = FIBAR_NONE;
-    if (q < B) {
-      it0 = x.posrec[q].bidx;
-      if (q == 0 || x.skey[q - 1] != x.skey[q]) it1 = x.pt[x.ekey[x.sidx[q]]].carried;
-    } else {
-      it0 = x.colist[q - B];
+  const long long q = (long long)blockIdx.x * TPB + threadIdx.x;
+  if (q < B) {
+    const unsigned bidx = x.posrec[q].bidx;
+    if (bidx != FIBAR_NONE) prep_item(x, bidx);
+    if (q == 0 || x.skey[q - 1] != x.skey[q]) {
+      const unsigned carried = x.pt[x.ekey[x.sidx[q]]].carried;
+      if (carried != FIBAR_NONE) prep_item(x, carried);
     }
-#pragma unroll 1
-    for (int k = 0; k < 2; ++k) {
-      const unsigned p = k ? it1 : it0;
-      if (p != FIBAR_NONE) prep_item(x, p);
-    }
+  } else {
+    // the threads past the batch's events (at least nsm blocks of them) stride
+    // over the carried-only list, up to one entry per eviction
+    const long long nco = (long long)x.bs->nco, tail = (long long)gridDim.x * TPB - B;
+    for (long long k = q - B; k < nco; k += tail) prep_item(x, x.colist[k]);
   }
 }
 
