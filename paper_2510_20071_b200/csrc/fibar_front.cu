@@ -1092,8 +1092,8 @@ __global__ void __launch_bounds__(128) k_window_run(Ctx x) {
 // lockstep).  The entries a window pops are always the next ones past its
 // start, so the group keeps the G ring entries [s, s + G) in registers: lane u
 // owns the positions = u (mod G) and holds the first one at or past s, loaded
-// well before the window start reaches them -- the ring load leaves the step's
-// dependency chain, an
+// as soon as the previous one was popped (about G steps before the window start
+// reaches it) -- the ring load leaves the step's dependency chain, an
 // eviction of up to G entries is one compare per lane and a group reduction,
 // and the fine candidates of the start state are evaluated G at a time.  Longer
 // evictions (the collapse of a too-long start window) stream 8 entries per
@@ -1190,34 +1190,12 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
   const RegF rf = make_regf(x);
   unsigned qlo32 = 0xFFFFFFFFu, qhi32 = 0, coop = 0;
   const unsigned sr_first = sr;
-  // this lane's ring entries: positions = u (mod G), the first at or past sr.
-  // Four are held (pu, pu + G, pu + 2G, pu + 3G); a block of G steps consumes
-  // at most the first two (`used`), and the refill between blocks shifts the
-  // rest down and reloads behind them, so a register a load is in flight to
-  // is next read a whole block later: no step waits for the ring.  used == 3:
-  // a long eviction went past the held entries (all four reloaded).
+  // this lane's ring entry: the first position = u (mod G) at or past sr,
+  // reloaded as soon as it was popped (holding four entries per lane and
+  // refilling between blocks measured slower: more instructions per step)
   unsigned pu = sr + (((unsigned)u - sr) & (unsigned)(G - 1));
-  uint2 e0 = make_uint2(0u, 0u), e1 = e0, e2 = e0, e3 = e0;
-  int used = 3;
   auto ring = [&](unsigned pos) { return x.rnext[(bslot + pos) & rm]; };
-  auto refill = [&]() {
-    if (used == 1) {
-      e0 = e1;
-      e1 = e2;
-      e2 = e3;
-    } else if (used == 2) {
-      e0 = e2;
-      e1 = e3;
-    }
-    if (used == 3) {
-      e0 = ring(pu);
-      e1 = ring(pu + G);
-    }
-    if (used >= 2) e2 = ring(pu + 2 * G);
-    if (used >= 1) e3 = ring(pu + 3 * G);
-    used = 0;
-  };
-  refill();
+  uint2 e0 = ring(pu);
   const int gb = lane & ~(G - 1);   // the group's first lane
 
   // one event: push (d = its links), trim, re-target
@@ -1232,12 +1210,12 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
     }
     // the eviction [sr, hi): this lane's held entries first
     unsigned cc = 0;   // pixels in the low half, tiles in the high half
-    if (pu < hi && used < 2) {
-      const uint2 en = used ? e1 : e0;
+    const unsigned pu0 = pu;
+    if (pu < hi) {
+      const uint2 en = e0;
       const unsigned dd = (unsigned)jr - pu;
       cc = (en.x > dd ? 1u : 0u) | (en.y > dd ? 0x10000u : 0u);
       pu += G;
-      ++used;
     }
 #pragma unroll
     for (int o = 1; o < G; o <<= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
@@ -1261,7 +1239,6 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
         }
       }
       pu += n_u * G;
-      if (n_u) used = 3;
 #pragma unroll
       for (int o = 1; o < G; o <<= 1) {
         cp += __shfl_xor_sync(0xffffffffu, cp, o);
@@ -1272,6 +1249,7 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
       ++coop;
     }
     sr = hi;
+    if (pu != pu0) e0 = ring(pu);   // needed once the window start passes it
     if (act) {
       if (++ev >= every) {
         ev = 0;
@@ -1301,7 +1279,6 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
       const unsigned dy = __shfl_sync(0xffffffffu, dv.y, gb + k);
       step(j0 + k >= ar, j0 + k, dx, dy);
     }
-    refill();
   }
   ChunkRec r;
   r.st_s = base + sr;   // state after event b - 1: the chunk's speculative start
@@ -1335,7 +1312,6 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
       x.S[j0 + u - e0r] = sv;
       x.Qt[j0 + u - e0r] = qv;
     }
-    refill();
   }
   {
     const unsigned wp = __reduce_add_sync(0xffffffffu, u == 0 ? wpops : 0u);

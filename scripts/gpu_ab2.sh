@@ -1,5 +1,5 @@
-for i in 1 2 3; do
-timeout 600 python bench.py --config 2 --steps 5 --warmup 3 --no-cpu --no-off > gpurun_out/cfg2.json 2>gpurun_out/ab.err || tail -3 gpurun_out/ab.err
-python -c "import json; d=json.load(open('gpurun_out/cfg2.json')); print('cfg2', round(d['value'],1), round(d['e2e']['value'],1), d['window'])"
+for lib in libfibar_b200.so var_ring1.so libfibar_b200.so var_ring1.so; do
+  FIBAR_LIB=paper_2510_20071_b200/_lib/$lib timeout 600 python bench.py --config 3 --events 10000000 --steps 3 --warmup 3 --no-cpu --no-off --no-e2e > gpurun_out/ab.json 2>gpurun_out/ab.err || tail -3 gpurun_out/ab.err
+  python -c "import json; d=json.load(open('gpurun_out/ab.json')); print('cfg3 $lib', round(d['value'],1), d['kernel_ms_per_step_serialised']['window_run'])"
 done
-FIBAR_TRACE=1 python scripts/cfg2_host_probe.py 2>&1 | grep -v "^[0-9]" | tail -8
+FIBAR_LIB=paper_2510_20071_b200/_lib/var_ring1.so timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -2
