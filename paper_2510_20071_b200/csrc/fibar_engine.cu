@@ -229,7 +229,8 @@ struct fibar_engine {
   // small batches: the sort part of the ingest alternates between astream and
   // astream2 (it reads nothing of the previous batch); segments and links,
   // which do, follow on lstream in batch order
-  cudaStream_t astream2 = nullptr, lstream = nullptr;
+  cudaStream_t astream2 = nullptr, astream3 = nullptr, lstream = nullptr;
+  int sort_lanes = 2;   // FIBAR_SORT_LANES: streams a small batch's sort part rotates over (1..3)
   // asynchronous read-outs: a snapshot of l on the blur stream, the read-out
   // itself on rstream beside the next batch's blur stage
   cudaStream_t rstream = nullptr;
@@ -760,7 +761,8 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
   if (split) {
     const bool small = g->graphs_on && !L.prof && n_raw <= g->graph_max;
     // a small batch's sort part alternates between two streams
-    cudaStream_t sa = (small && (g->batches & 1)) ? g->astream2 : g->astream;
+    const int lane_i = small ? (int)(g->batches % g->sort_lanes) : 0;
+    cudaStream_t sa = lane_i == 0 ? g->astream : (lane_i == 1 ? g->astream2 : g->astream3);
     CK(cudaEventRecord(g->evIn, u));
     CK(cudaStreamWaitEvent(sa, g->evIn, 0));
     if (g->b_used[par]) CK(cudaStreamWaitEvent(sa, g->evBuf[par], 0));   // this parity's buffers are free (the ingest reads no brightness: it need not wait for a read-out)
@@ -1477,6 +1479,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       cudaStreamCreateWithPriority(&g->nstream, cudaStreamNonBlocking, op);
       cudaStreamCreateWithPriority(&g->astream, cudaStreamNonBlocking, lo);
       cudaStreamCreateWithPriority(&g->astream2, cudaStreamNonBlocking, lo);
+      cudaStreamCreateWithPriority(&g->astream3, cudaStreamNonBlocking, lo);
+      if (const char *v = getenv("FIBAR_SORT_LANES")) g->sort_lanes = std::min(3, std::max(1, atoi(v)));
       cudaStreamCreateWithPriority(&g->lstream, cudaStreamNonBlocking, lo);
       cudaStreamCreateWithPriority(&g->rstream, cudaStreamNonBlocking, lo);
       cudaStreamCreateWithPriority(&g->tstream, cudaStreamNonBlocking, hi);
@@ -1541,7 +1545,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
 
 int fibar_destroy(fibar_engine *g) {
   if (!g) return 0;
-  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->nstream, g->fstream, g->pstream, g->bstream, g->rstream, g->tstream})
+  for (cudaStream_t st : {g->astream, g->astream2, g->astream3, g->lstream, g->nstream, g->fstream, g->pstream, g->bstream, g->rstream, g->tstream})
     if (st) cudaStreamSynchronize(st);
   void *ptrs[] = {g->st, g->pbar, g->l, g->gain, g->plast, g->wcnt, g->bsd, g->last_tile, g->rkey, g->rnext, g->raw_x,
                   g->raw_y, g->raw_p,
@@ -1583,7 +1587,7 @@ int fibar_destroy(fibar_engine *g) {
     if (q) cudaFree(q);
   for (cudaEvent_t ev : {g->evSnap, g->evRd[0], g->evRd[1], g->evT0, g->evT1})
     if (ev) cudaEventDestroy(ev);
-  for (cudaStream_t st : {g->astream, g->astream2, g->lstream, g->rstream, g->tstream, g->nstream, g->fstream, g->pstream})
+  for (cudaStream_t st : {g->astream, g->astream2, g->astream3, g->lstream, g->rstream, g->tstream, g->nstream, g->fstream, g->pstream})
     if (st) cudaStreamDestroy(st);
   for (cudaEvent_t ev : {g->evIn, g->evCp})
     if (ev) cudaEventDestroy(ev);

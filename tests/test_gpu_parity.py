@@ -125,6 +125,34 @@ def test_oracle_streams(kind, w, h, n, packet, spatial):
     assert np.array_equal(fr.pixels, px) and fr.bounds == bounds and fr.degenerate == deg
 
 
+@pytest.mark.parametrize("spatial", [True, False])
+def test_dominant_pixel_segments(spatial):
+    """One pixel takes 45 % of a 400k-event batch and another 5 %: a segment
+    past the tiled replay's bound (the strided-piece path) and one of several
+    shared-memory tiles, beside texture events -- exact against the oracle."""
+    import oracle.oracle as orc
+    from paper_2510_20071_b200 import workloads
+    from paper_2510_20071_b200.core import EventArray, SensorGeometry, compute_params
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    w, h, n = 240, 180, 400_000   # (43,200 pixels: the window cannot reach the reference's u16 count cap)
+    geom = SensorGeometry(w, h)
+    ev = workloads.make("texture", geom, n, seed=23)
+    rng = np.random.default_rng(5)
+    r = rng.random(n)
+    x, y, p = ev.x.copy(), ev.y.copy(), ev.p.copy()
+    x[r < 0.45], y[r < 0.45] = 100, 77
+    x[(r >= 0.45) & (r < 0.50)], y[(r >= 0.45) & (r < 0.50)] = 7, 150
+    p[r < 0.50] = rng.choice(np.array([-1, 1], np.int8), int((r < 0.50).sum()))
+    params = compute_params(40.0, Fraction(1, 2), geom, spatial_enabled=spatial)
+    ref = orc.OracleEngine(w, h, params)
+    ref.process_array(ev.t, x, y, p)
+    eng = ReconstructionEngine(geom, params, batch_capacity=1 << 19)
+    eng.process_array(EventArray(ev.t, x, y, p))
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, "dominant pixel")
+
+
 @pytest.mark.parametrize("n,flag", [(60_000, False), (70_000, True)])
 def test_saturation_flag(n, flag):
     """one pixel with more than 65535 events in the window reaches the
