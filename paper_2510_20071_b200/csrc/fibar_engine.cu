@@ -1426,7 +1426,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
       rc |= dalloc(&g->vb2[c], Bc);
     }
   }
-  for (int c = 0; c < (g->spatial ? NPAR : 1); ++c) rc |= dalloc(&g->hist2[c], 256LL * nb_rs + 256LL * nb_rs / 4096 + 8);
+  for (int c = 0; c < (g->spatial ? NPAR : 1); ++c) rc |= dalloc(&g->hist2[c], 1024LL * nb_rs + 1024LL * nb_rs / 4096 + 8);   // (digits of up to 10 bits)
   rc |= dalloc(&g->sel, 1);
   if (!rc) cudaMemset(g->sel, 0, sizeof(SelState));
   rc |= dalloc(&g->frame, n);
