@@ -1,4 +1,5 @@
-for S in "FIBAR_SORT_LANES=2" "FIBAR_SORT_LANES=3" "FIBAR_SORT_LANES=2 FIBAR_LIB=paper_2510_20071_b200/_lib/var_npar7.so" "FIBAR_SORT_LANES=3 FIBAR_LIB=paper_2510_20071_b200/_lib/var_npar7.so"; do
-  env $S timeout 600 python bench.py --config 3 --events 10000000 --steps 3 --warmup 3 --no-cpu --no-off > gpurun_out/ab.json 2>gpurun_out/ab.err || tail -3 gpurun_out/ab.err
-  python -c "import json; d=json.load(open('gpurun_out/ab.json')); print('cfg3 $S', round(d['value'],1), round(d['e2e']['value'],1))"
-done
+mkdir -p gpurun_out
+timeout 900 python scripts/sweep_config4.py --sync --events 4000000 --max-packets 1500 --cpu-seconds 0.5 --out gpurun_out/r2d_config4_sweep_sync.json 2>&1 | grep filter | cut -c1-200
+echo "== FULL_GRAPHS=1"
+FIBAR_FULL_GRAPHS=1 timeout 900 python scripts/sweep_config4.py --sync --events 1000000 --max-packets 1000 --cpu-seconds 0.2 --out gpurun_out/tmp_sweep.json 2>&1 | grep '"on"' | cut -c1-200
+for i in 1 2; do timeout 900 python bench.py --config 1 --steps 5 --warmup 3 --no-off > gpurun_out/r2d_cfg1.json 2> gpurun_out/r2d_cfg1.err; python -c "import json; d=json.load(open('gpurun_out/r2d_cfg1.json')); print('cfg1', d['value'], d['e2e']['value'])"; done

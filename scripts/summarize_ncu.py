@@ -8,6 +8,7 @@ tagged with the workload class -- bench.py's workload string without the event
 count -- and the device batch capacity, which bench.py matches before using it).
 """
 import collections
+import re
 import csv
 import io
 import os
@@ -100,7 +101,7 @@ if os.path.exists(rep):
     for (kid, name), m in per.items():
         if kid in dram:
             rb, wb, u = dram[kid]
-            short = name.replace("k_", "", 1)
+            short = re.sub(r"_g\d+$", "", name.replace("k_", "", 1))   # (k_window_run_g8 is launched as "window_run")
             traffic.setdefault(short, []).append((rb + wb) * scale.get(u, 1.0))
     import json
     with open(os.path.join(out_dir, f"{tag}_traffic.json"), "w") as fh:
