@@ -262,6 +262,46 @@ def test_launch_modes_agree(monkeypatch):
         eng.close()
 
 
+@pytest.mark.parametrize("env", [
+    {"FIBAR_RUN_G": "0", "FIBAR_RUN_G_LARGE": "0"},          # one lane per chunk (k_window_run)
+    {"FIBAR_RUN_G": "4", "FIBAR_RUN_G_LARGE": "8"},
+    {"FIBAR_RUN_G": "2", "FIBAR_RUN_G_LARGE": "2", "FIBAR_REG32X": "0"},
+    {"FIBAR_SORT_LANES": "1", "FIBAR_STAGE_GRAPHS": "0", "FIBAR_SNAP": "0"},
+    {"FIBAR_SORT_LANES": "3", "FIBAR_GREEN_SMALL": "1", "FIBAR_LONG_GRID": "3"},
+    {"FIBAR_GRAPHS": "0"},
+])
+def test_schedule_knobs_agree(monkeypatch, env):
+    """The window run's lanes per chunk, the 32-bit regulator, the sort
+    streams, the blur-stage graph, the read-out snapshot and the rest of
+    DESIGN section 9 never change a result: small batches (graphs) and large
+    ones mixed, a read-out after every packet, frames and final state exact."""
+    from paper_2510_20071_b200.pipeline import ReconstructionEngine
+    import oracle.oracle as orc
+    from paper_2510_20071_b200 import workloads
+    from paper_2510_20071_b200.core import SensorGeometry, compute_params
+    geom = SensorGeometry(320, 240)
+    ev = workloads.make("texture_noise_hot", geom, 700_000, seed=41)
+    params = compute_params(40.0, Fraction(1, 2), geom)
+    cuts = [0, 30_000, 60_000, 400_000, 430_000, 431_000, 700_000]   # small, large (two device batches), small, tiny, large
+    ref = orc.OracleEngine(geom.width, geom.height, params)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    eng = ReconstructionEngine(geom, params, batch_capacity=1 << 18)
+    pending = []
+    for a, b in zip(cuts[:-1], cuts[1:]):
+        blk = ev.slice(a, b)
+        ref.process_array(blk.t, blk.x, blk.y, blk.p)
+        eng.process_array(blk)
+        pending.append((eng.render_async("robust"), ref.render("robust")))
+    for af, (px, bounds, deg) in pending:
+        fr = af.frame()
+        assert np.array_equal(fr.pixels, px) and fr.bounds == bounds and fr.degenerate == deg, env
+    want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
+                qx=ref.qx, qy=ref.qy, qs=ref.qs)
+    assert_state(eng, want, str(env))
+    eng.close()
+
+
 @pytest.mark.parametrize("kind,w,h,n,packet,kw", [
     # hot pixels at config-3 geometry: long segments, several 1M-event batches
     ("texture_noise_hot", 1280, 720, 3_000_000, 100_000, dict(bcap=1 << 20)),
