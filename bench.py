@@ -111,7 +111,7 @@ def workload(args, rank, config=None, events=None, packet=None, spatial=None, re
 class ClockSampler:
     """nvidia-smi-equivalent clock / throttle sampling via NVML during the timed region."""
 
-    def __init__(self, index=0, period=0.05):
+    def __init__(self, index=0, period=float(os.environ.get("BENCH_CLOCK_PERIOD", "0.05"))):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self.period = period
         self._stop = threading.Event()
@@ -142,7 +142,7 @@ class ClockSampler:
                         self.reasons.add(k)
             except Exception:
                 pass
-            time.sleep(self.period)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         if self.nv:

@@ -1306,13 +1306,15 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   }
   if (const char *v = getenv("FIBAR_DEBUG_WINDOW")) g->debug = atoi(v);
   if (const char *v = getenv("FIBAR_SERIAL")) g->serial = atoi(v) != 0;
-  // The blur dataflow kernel runs in a CUDA green context of 24 SMs (5
+  // The blur dataflow kernel runs in a CUDA green context of 48 SMs (5
   // blocks each, all resident): its polling lanes stop sharing SMs with the
-  // next batch's front end (config 2: 9.3 -> 9.0 ms / 10M with 16 SMs, 8.68 ->
-  // 8.50 ms with 24 SMs x 5 blocks, r1h).  FIBAR_GREEN=n sets the SM
+  // next batch's front end.  With the round-2 front end the blur stage paces a
+  // large batch, and 48 SMs beat 24 (config 2: 1091 -> 1176 Mev/s, config 5:
+  // 1128 -> 1232; 40: 1161 / 1214, 56: 1194 / 1244, 64: 1045 / -).
+  // FIBAR_GREEN=n sets the SM
   // count, 0 turns it off; without green-context support the blur stays on
   // the second stream with the whole GPU.
-  int green_sms = 24;
+  int green_sms = 48;
   if (const char *v = getenv("FIBAR_GREEN")) green_sms = atoi(v);
   if (const char *v = getenv("FIBAR_STAGE_GRAPHS")) g->stage_graphs = atoi(v) != 0;
   if (const char *v = getenv("FIBAR_LONG_GRID")) g->long_grid_small = std::max(1, atoi(v));
