@@ -1277,7 +1277,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // batches (measured, Mev/s: 1280x720 with one read-out 816 / 945 / 986 at
   // 1M / 2M / 3.7M; 2560x1440 757 / 1062 / 1107 / 1090 at 1M / 4M / 6M / 8M;
   // 640x480 1122 / 1213 / 1210 / 1197 at 768k / 1M / 1.2M / 1.5M).
-  const long long bauto = std::min(6LL << 20, std::max(1LL << 20, (4 * n + 65535) / 65536 * 65536));
+  // default device batch: 2 events per pixel (the blur stage paces large batches, and its DAG
+  // deepens with the batch: 640x480 1178 -> 1222 Mev/s, 1280x720 1222 -> 1283 against 4 per pixel)
+  const long long bauto = std::min(6LL << 20, std::max(1LL << 19, (2 * n + 65535) / 65536 * 65536));
   g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : bauto;
   if (g->Bcap > (1LL << 28)) g->Bcap = 1LL << 28;
   if (g->Bcap < 1024) g->Bcap = std::max(g->Bcap, 16LL);
