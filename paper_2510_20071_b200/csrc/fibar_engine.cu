@@ -272,6 +272,7 @@ struct fibar_engine {
   int gblocks = 0;
   int long_grid_small = 48;   // FIBAR_LONG_GRID: k_temporal_long blocks for small batches
   int n_last = -1;            // the set whose anchors were enqueued last (evN)
+  bool anchors_split = false;   // FIBAR_ANCHOR_STREAM=1: small batches' anchors as their own graph on nstream
   bool stage_graphs = true;   // FIBAR_STAGE_GRAPHS=0: small batches' blur stage as separate launches
   bool green_small = false;   // FIBAR_GREEN_SMALL=1: small batches' blur in the green context too
   // small batches: one CUDA graph per batch size, fed from fixed input buffers
@@ -671,7 +672,8 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
   ge.n = n_raw;
   ge.kind = 1;
   ge.par = par;
-  for (int part : {0, 1, 2, 4, 5}) {
+  for (int part : {0, 1, 2, 3, 4, 5}) {
+    if (part == 3 && !g->anchors_split) continue;   // (the anchors ride in the links' graph)
     const long long l0 = L.launches;
     cudaGraph_t graph = nullptr;
     Ctx x{};
@@ -686,7 +688,7 @@ GraphEntry *front_graph(fibar_engine *g, long long n_raw, int par) {
     const int rc = part == 0   ? enqueue_ingest_a(g, g->gx2[par], g->gy2[par], g->gp2[par], n_raw, nullptr, par,
                                                   g->capstream, ge.where, &g->bsd[par].n_raw)
                    : part == 4 ? (enqueue_ingest_b(g, n_raw, par, ge.where, g->capstream) ||
-                                  enqueue_anchors(g, n_raw, par, ge.where, g->capstream))
+                                  (g->anchors_split ? 0 : enqueue_anchors(g, n_raw, par, ge.where, g->capstream)))
                    : part == 5 ? capture_blur_stage(g, n_raw, par, ge.where)
                    : part == 1 ? enqueue_chain(g, n_raw, par, ge.where, g->capstream, x, nullptr)
                    : part == 2 ? enqueue_post(g, n_raw, par, ge.where, g->capstream)
@@ -787,12 +789,22 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       CK(cudaStreamWaitEvent(g->lstream, g->evS[par], 0));
       // the anchors read the start state the previous batch's anchors predicted
       // (a large batch's run on nstream)
-      if (g->n_last >= 0) CK(cudaStreamWaitEvent(g->lstream, g->evN[g->n_last], 0));
+      if (!g->anchors_split && g->n_last >= 0) CK(cudaStreamWaitEvent(g->lstream, g->evN[g->n_last], 0));
       CK(cudaGraphLaunch(ge->exec5, g->lstream));
       L.launches += ge->kernels5;
       g->mark(1, g->lstream);
-      // (the same graph carries the anchors: they follow the previous batch's anyway)
-      CK(cudaEventRecord(g->evN[par], g->lstream));
+      if (g->anchors_split) {
+        // the anchors on their own stream: the links of the next batch need not wait for them
+        CK(cudaEventRecord(g->evA[par], g->lstream));
+        CK(cudaStreamWaitEvent(g->nstream, g->evA[par], 0));
+        if (g->n_last >= 0) CK(cudaStreamWaitEvent(g->nstream, g->evN[g->n_last], 0));
+        CK(cudaGraphLaunch(ge->exec4, g->nstream));
+        L.launches += ge->kernels4;
+        CK(cudaEventRecord(g->evN[par], g->nstream));
+      } else {
+        // (the same graph carries the anchors: they follow the previous batch's anyway)
+        CK(cudaEventRecord(g->evN[par], g->lstream));
+      }
       g->n_last = par;
       CK(cudaStreamWaitEvent(s, g->evN[par], 0));
       if (g->stage_graphs && !g->green_small) stage_graph = ge;
@@ -1318,6 +1330,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // the second stream with the whole GPU.
   int green_sms = 48;
   if (const char *v = getenv("FIBAR_GREEN")) green_sms = atoi(v);
+  if (const char *v = getenv("FIBAR_ANCHOR_STREAM")) g->anchors_split = atoi(v) != 0;
   if (const char *v = getenv("FIBAR_STAGE_GRAPHS")) g->stage_graphs = atoi(v) != 0;
   if (const char *v = getenv("FIBAR_LONG_GRID")) g->long_grid_small = std::max(1, atoi(v));
   if (const char *v = getenv("FIBAR_GREEN_SMALL")) g->green_small = atoi(v) != 0;
