@@ -3,7 +3,7 @@
 # --set full capture of the step's top kernels on a config-3 prefix, the other
 # configs' lines, the config-4 sweep and the stream-part timeline.
 # usage: bash scripts/gpu_round3.sh TAG
-TAG=${1:-r2c}
+TAG=${1:-r2e}
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv
 timeout 900 python -m pytest tests -q -m gpu 2>&1 | tail -2
@@ -23,3 +23,4 @@ timeout 1500 python bench.py --config 5 --events 30000000 --steps 3 --warmup 3 -
 timeout 900 python scripts/sweep_config4.py --out gpurun_out/${TAG}_config4_sweep.json 2>&1 | tail -10
 TRACE_ROWS=1 timeout 300 python scripts/trace_parts.py 6000000 > gpurun_out/${TAG}_trace_parts.txt 2>&1
 cat gpurun_out/${TAG}_trace_parts.txt
+timeout 900 python scripts/sweep_config4.py --sync --events 4000000 --max-packets 1500 --cpu-seconds 0.5 --out gpurun_out/${TAG}_config4_sweep_sync.json 2>&1 | tail -8 | cut -c1-160
