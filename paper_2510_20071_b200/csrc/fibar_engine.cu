@@ -368,6 +368,7 @@ struct fibar_engine {
     x.epol = epol2[par];
     x.spol = spol2[par];
     x.longseg = longseg2[par];
+    x.max_long = (unsigned)(Bcap / LONG_SEG + 1);
     x.tkey = ka2[par];
     x.skey = skey;
     x.sidx = sidx;
@@ -1291,7 +1292,9 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   // 640x480 1122 / 1213 / 1210 / 1197 at 768k / 1M / 1.2M / 1.5M).
   // default device batch: 2 events per pixel (the blur stage paces large batches, and its DAG
   // deepens with the batch: 640x480 1178 -> 1222 Mev/s, 1280x720 1222 -> 1283 against 4 per pixel)
-  const long long bauto = std::min(6LL << 20, std::max(1LL << 19, (2 * n + 65535) / 65536 * 65536));
+  // (filter OFF has no blur DAG: 4 per pixel, at least 1M)
+  const long long bauto = cfg->spatial_enabled ? std::min(6LL << 20, std::max(1LL << 19, (2 * n + 65535) / 65536 * 65536))
+                                              : std::min(6LL << 20, std::max(1LL << 20, (4 * n + 65535) / 65536 * 65536));
   g->Bcap = cfg->batch_capacity > 0 ? cfg->batch_capacity : bauto;
   if (g->Bcap > (1LL << 28)) g->Bcap = 1LL << 28;
   if (g->Bcap < 1024) g->Bcap = std::max(g->Bcap, 16LL);
@@ -1429,7 +1432,7 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
     rc |= dalloc(&g->epol2[b], Bc);
     rc |= dalloc(&g->spol2[b], Bc);
   }
-  for (int c = 0; c < (g->spatial ? NPAR : 1); ++c) rc |= dalloc(&g->longseg2[c], MAX_LONG);
+  for (int c = 0; c < (g->spatial ? NPAR : 1); ++c) rc |= dalloc(&g->longseg2[c], g->Bcap / LONG_SEG + 1);
   rc |= dalloc(&g->bsd, NPAR);
   if (!rc) cudaMemset(g->bsd, 0, NPAR * sizeof(BatchState));
   for (int c = 0; c < NPAR; ++c) {

@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(TPB) k_link(Ctx x) {
     // a count not yet decremented only makes the check more conservative)
     if (seglen > (unsigned)LONG_SEG) {   // long segment (hot pixel): listed here for k_temporal_long
       const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
-      if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
+      if (slot < x.max_long) x.longseg[slot] = make_uint2((unsigned)i, c);
     }
     const unsigned wc = atomicAdd(&x.wcnt[c], seglen);
     if ((unsigned long long)wc + seglen > 65535ull) atomicAdd((unsigned long long *)&x.st->saturated, 1ull);

@@ -32,7 +32,6 @@ constexpr int GROUP = 8;
 #define FIBAR_LONG_SEG 64
 #endif
 constexpr int LONG_SEG = FIBAR_LONG_SEG;    // segments longer than this go to k_temporal_long
-constexpr int MAX_LONG = (8 << 20) / LONG_SEG;   // (a device batch holds at most 8M events)
 constexpr int LONG_TPB = 256;      // lanes per long segment (one block)
 constexpr int LONG_PIECE = 64;     // minimum events per lane before more lanes join
 constexpr int EV_PER_THREAD = 2;
@@ -122,6 +121,7 @@ struct Ctx {
   unsigned *ekey;
   int8_t *epol, *spol;
   uint2 *longseg;
+  unsigned max_long;              // entries of longseg: batch capacity / LONG_SEG + 1 (every long segment fits)
   unsigned *tkey;                 // unsorted tile-major keys (sort input)
   const unsigned *skey, *sidx;    // sorted keys / batch-local event index
   uint2 *dp;

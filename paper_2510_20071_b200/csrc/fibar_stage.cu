@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(TPB) k_temporal(Ctx x) {
   const long long end = x.spatial ? (long long)x.pt[c].end : -1;
   if (i + LONG_SEG < B && x.skey[i + LONG_SEG] == key) {   // long segment: the warp-parallel kernel
     const unsigned slot = atomicAdd(&x.bs->nlong, 1u);
-    if (slot < MAX_LONG) x.longseg[slot] = make_uint2((unsigned)i, c);
+    if (slot < x.max_long) x.longseg[slot] = make_uint2((unsigned)i, c);
     return;
   }
   float pb = x.pbar[c], lv = x.l[c];
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(LONG_TPB) k_temporal_long(Ctx x) {
   __shared__ unsigned s_bidx[LT_TILE];
   __shared__ unsigned s_wlast[LONG_TPB / 32];
   __shared__ int s_bad;
-  const unsigned n = min(x.bs->nlong, (unsigned)MAX_LONG);
+  const unsigned n = min(x.bs->nlong, x.max_long);
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   for (unsigned sidx = blockIdx.x; sidx < n; sidx += gridDim.x) {
     const uint2 ls = x.longseg[sidx];
