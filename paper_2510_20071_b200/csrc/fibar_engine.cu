@@ -12,7 +12,8 @@
 //                                            same-tile event; per ring slot: distance to next
 //   window     k_anchor / k_anchor_scan /    the reference's FIFO window (_kernels.py:132-205)
 //              k_fp / k_anchor2 /            reproduced exactly by chunked speculation +
-//              k_window_run / k_window_verify verification
+//              k_window_run_g8 /             verification
+//              k_window_verify
 //   stale      k_popj                        eviction event of every popped entry; stale iff
 //                                            the pixel has no later event before its eviction
 //   temporal   k_posinfo / k_temporal_runs / per-pixel in-order replay of the two-stage IIR
@@ -25,8 +26,9 @@
 //   read-out   k_readout                     exact percentile select + float64 map in one
 //                                            cooperative kernel (pipeline.py:247-269)
 //
-// Filter ON, the blur stage of batch k runs on a second stream while batch k+1's
-// front end runs; small batches replay a captured CUDA graph
+// Filter ON, a batch's parts run on the engine's own streams -- sort, links +
+// anchors, window, eviction, blur stage, read-out -- with about five batches in
+// flight; small batches replay one captured CUDA graph per part
 // (4.6); consecutive kernels use programmatic dependent launch (pdl_wait()).
 // Float32 arithmetic uses __fmul_rn/__fadd_rn (never contracted to FMA) so the
 // result is bit-identical to the reference's strict-IEEE numba kernels.
@@ -1285,11 +1287,8 @@ int fibar_create(const fibar_config *cfg, void *stream, fibar_engine **out) {
   g->spatial = cfg->spatial_enabled != 0;
   g->blur_on = cfg->blur_enabled != 0;
   g->use_gain = cfg->gain != nullptr;
-  // default device batch: 4 events per pixel (a multiple of 64k), between 1M
-  // and 6M events.  Large sensors have long windows and gain from long
-  // batches (measured, Mev/s: 1280x720 with one read-out 816 / 945 / 986 at
-  // 1M / 2M / 3.7M; 2560x1440 757 / 1062 / 1107 / 1090 at 1M / 4M / 6M / 8M;
-  // 640x480 1122 / 1213 / 1210 / 1197 at 768k / 1M / 1.2M / 1.5M).
+  // (round 1, 4 events per pixel, Mev/s: 1280x720 with one read-out 816 / 945 / 986 at 1M / 2M /
+  // 3.7M; 640x480 1122 / 1213 / 1210 / 1197 at 768k / 1M / 1.2M / 1.5M -- the front end paced a batch then)
   // default device batch: 2 events per pixel (the blur stage paces large batches, and its DAG
   // deepens with the batch: 640x480 1178 -> 1222 Mev/s, 1280x720 1222 -> 1283 against 4 per pixel)
   // (filter OFF has no blur DAG: 4 per pixel, at least 1M)
