@@ -1217,6 +1217,7 @@ __device__ __forceinline__ void window_run_g(const Ctx &x) {
       cc = (en.x > dd ? 1u : 0u) | (en.y > dd ? 0x10000u : 0u);
       pu += G;
     }
+    // (butterfly: one redux.sync per group with sub-warp masks measured slower, run 43 -> 61 us)
 #pragma unroll
     for (int o = 1; o < G; o <<= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
     np -= (int)(cc & 0xFFFFu);
