@@ -736,6 +736,7 @@ def _readout_times(fps: float | None, explicit) -> tuple[Iterator[float], bool]:
     return grid(), False
 
 
+_RUN_ZERO_COPY_MAX = 32   # frames handed out as views of pinned buffers at a time
 _RUN_DEPTH = 8   # read-outs in flight in run() (the device pipeline holds about five batches)
 
 
@@ -798,11 +799,24 @@ def run(
     # pinned frame buffers, kept on the engine across run() calls
     ring = engine.__dict__.setdefault("_run_frame_pool", []) if pipelined else []
 
+    lent = engine.__dict__.setdefault("_run_frames_lent", [0]) if pipelined else [0]
+
+    def give_back(buf) -> None:
+        ring.append(buf)
+        lent[0] -= 1
+
     def deliver(af) -> None:
         # the frame's pixels are the pinned buffer itself (no copy); the buffer
-        # goes back to the ring once nothing refers to the array any more
-        frame = af.frame(copy=False)
-        weakref.finalize(frame.pixels, ring.append, (af.out, af.meta))
+        # goes back to the ring once nothing refers to the array any more.  A
+        # sink that keeps its frames gets copies from the 33rd on, so the
+        # pinned memory lent out stays bounded.
+        if lent[0] < _RUN_ZERO_COPY_MAX:
+            frame = af.frame(copy=False)
+            lent[0] += 1
+            weakref.finalize(frame.pixels, give_back, (af.out, af.meta))
+        else:
+            frame = af.frame()
+            ring.append((af.out, af.meta))
         if frame_sink is not None:
             frame_sink(af.index, frame)
         del frame
