@@ -1,4 +1,8 @@
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
-python scripts/e2e_profile.py 2>&1 | grep "run()"
-timeout 600 python bench.py --config 3 --events 10000000 --steps 3 --warmup 3 --no-cpu --no-off > gpurun_out/ab.json 2>gpurun_out/ab.err || tail -3 gpurun_out/ab.err
-python -c "import json; d=json.load(open('gpurun_out/ab.json')); print('cfg3', round(d['value'],1), round(d['e2e']['value'],1), d['roofline']['traffic'], d['roofline']['traffic_ratio'])"
+mkdir -p gpurun_out
+timeout 1500 python bench.py > gpurun_out/r2f_bench.json 2> gpurun_out/r2f_bench.err; echo "bench rc=$?"
+timeout 900 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/r2f_bench_reference.json 2> gpurun_out/r2f_ref.err; echo "ref rc=$?"
+python -c "
+import json
+d=json.load(open('gpurun_out/r2f_bench.json')); r=json.load(open('gpurun_out/r2f_bench_reference.json'))
+print(d['value'], d['e2e']['value'], d['parity']['frames'], d['parity']['state'], d['roofline']['kernel'], d['roofline']['frac'], d['roofline']['traffic_ratio'], r['value'])
+print({k: round(v['value']) for k, v in d['filter_off'].items()}, d['clocks'])"
