@@ -152,6 +152,15 @@ int fibar_read_state(fibar_engine *eng, float *p_bar, float *l, uint16_t *active
  * exceeds cap.  Filter ON only (else *n_out = 0). */
 int fibar_debug_stale_items(fibar_engine *eng, int64_t *event_idx, uint32_t *pixel, int64_t cap, int64_t *n_out);
 
+/* Parity surface for the window regulator: the 32-bit form the window kernels
+ * use (float quotient + exact remainder fix-up) beside the reference's integer
+ * formula q = clamp(len * n_tiles * A * num // (den * n_pix), q_min, q_max)
+ * (_kernels.py:195-201) in exact 64-bit arithmetic, for n host triples
+ * (len, n_pix_active, n_tiles_active), n_pix_active >= 1.  Fails unless the
+ * 32-bit form applies (num * A, den < 2^24, q_max < 2^22, den * q_max < 2^29). */
+int fibar_debug_regulate(int64_t num, int64_t den, int32_t tile_area, int64_t q_min, int64_t q_max, const uint32_t *len,
+                         const uint32_t *np, const uint32_t *nt, int64_t n, uint32_t *out_fast, uint32_t *out_exact);
+
 /* Measurement: with FIBAR_TRACE=1 set at creation, timing events are recorded
  * at the stream-part boundaries of every streamed batch (labels 0/1 ingest
  * start/end, 2/3 window part, 4/5 eviction pass, 6/7 blur stage, 8 read-out

@@ -27,6 +27,7 @@ EXPORTED = (
     "fibar_brightness_ptr", "fibar_last_error", "fibar_profile", "fibar_profile_read", "fibar_pending", "fibar_debug_times", "fibar_debug_prep", "fibar_debug_readout_times", "fibar_render_grid", "fibar_copy_brightness", "fibar_decode_evf1",
     "fibar_count_events", "fibar_pixel_trace", "fibar_pixel_trace_iir",
     "fibar_halo_batch", "fibar_halo_round", "fibar_halo_finish", "fibar_render_async", "fibar_debug_stale_items", "fibar_debug_trace",
+    "fibar_debug_regulate",
 )
 
 
@@ -108,6 +109,7 @@ def load(path: str | None = None):
         "fibar_halo_finish": ([P], C.c_int),
         "fibar_render_async": ([P, i32, f64, P, i32, P, P], C.c_int),
         "fibar_debug_stale_items": ([P, P, P, i64, P], C.c_int),
+        "fibar_debug_regulate": ([i64, i64, i32, i64, i64, P, P, P, i64, P, P], C.c_int),
         "fibar_debug_trace": ([P, i64, P, P, P, P], C.c_int),
     }
     for name, (args, res) in sig.items():

@@ -1959,6 +1959,37 @@ int fibar_debug_stale_items(fibar_engine *g, int64_t *event_idx, uint32_t *pixel
   return k > cap ? fail(FIBAR_E_CONFIG, "stale item buffer too small") : 0;
 }
 
+int fibar_debug_regulate(int64_t num, int64_t den, int32_t tile_area, int64_t q_min, int64_t q_max, const uint32_t *len,
+                         const uint32_t *np, const uint32_t *nt, int64_t n, uint32_t *out_fast, uint32_t *out_exact) {
+  if (n <= 0) return 0;
+  const long long numA = num * (long long)tile_area;
+  if (!(numA > 0 && numA < (1LL << 24) && den > 0 && den < (1LL << 24) && q_min >= 1 && q_min <= q_max && q_max < (1LL << 22) &&
+        den * (q_max + 2) < (1LL << 29)))
+    return fail(FIBAR_E_CONFIG, "regulate32x does not apply to these parameters");
+  Ctx x{};
+  x.num = num;
+  x.den = den;
+  x.A = tile_area;
+  x.numA = numA;
+  x.qmin = q_min;
+  x.qmax = q_max;
+  unsigned *d = nullptr;
+  CK(cudaMalloc(&d, sizeof(unsigned) * 5 * n));
+  cudaError_t e = cudaMemcpy(d, len, sizeof(unsigned) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + n, np, sizeof(unsigned) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + 2 * n, nt, sizeof(unsigned) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) {
+    k_debug_regulate<<<(int)std::min<long long>(1184, (n + TPB - 1) / TPB), TPB>>>(x, d, d + n, d + 2 * n, (long long)n, d + 3 * n,
+                                                                                  d + 4 * n);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(out_fast, d + 3 * n, sizeof(unsigned) * n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(out_exact, d + 4 * n, sizeof(unsigned) * n, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return cuda_fail(e, "fibar_debug_regulate");
+  return 0;
+}
+
 int fibar_debug_trace(fibar_engine *g, int64_t cap, int64_t *batch, int32_t *label, double *ms, int64_t *n_out) {
   if (!g || !n_out) return fail(FIBAR_E_CONFIG, "null argument");
   CK(cudaDeviceSynchronize());

@@ -494,6 +494,22 @@ __device__ __forceinline__ long long regulate_fast(const Ctx &x, long long len, 
   return regulate(x, len, np, nt);
 }
 
+// parity surface for the regulator: regulate32x beside the exact 64-bit floor
+// for arbitrary (len, np, nt) -- fibar_debug_regulate
+__global__ void __launch_bounds__(TPB) k_debug_regulate(Ctx x, const unsigned *len, const unsigned *np, const unsigned *nt,
+                                                        long long n, unsigned *out_fast, unsigned *out_exact) {
+  const RegF rf = make_regf(x);
+  for (long long i = (long long)blockIdx.x * TPB + threadIdx.x; i < n; i += (long long)gridDim.x * TPB) {
+    out_fast[i] = regulate32x(rf, len[i], np[i], nt[i]);
+    // the reference's integer formula (_kernels.py:195-201) in exact 64-bit arithmetic
+    const unsigned long long N = (unsigned long long)len[i] * nt[i] * (unsigned long long)x.numA;
+    const unsigned long long D = (unsigned long long)x.den * np[i];
+    const unsigned long long q = N / D;
+    out_exact[i] = (unsigned)(q < (unsigned long long)x.qmin ? (unsigned long long)x.qmin
+                                                             : (q > (unsigned long long)x.qmax ? (unsigned long long)x.qmax : q));
+  }
+}
+
 // The reference's per-event queue bookkeeping (_kernels.py:132-205) restated on
 // the suffix window [s, j]: the push of event j activates its pixel / tile iff
 // its previous same-pixel / same-tile event lies before s; the trim pops

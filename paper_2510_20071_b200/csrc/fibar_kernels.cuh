@@ -180,6 +180,8 @@ __device__ __forceinline__ float order_unkey(unsigned k) {
 
 // kernels (launched by fibar_engine.cu)
 __global__ void __launch_bounds__(TPB) k_snap(const float *__restrict__ src, float *__restrict__ dst, long long n);
+__global__ void __launch_bounds__(TPB) k_debug_regulate(Ctx x, const unsigned *len, const unsigned *np, const unsigned *nt,
+                                                        long long n, unsigned *out_fast, unsigned *out_exact);
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks);
 __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
 __global__ void k_batch_begin(Ctx x);

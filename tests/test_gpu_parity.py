@@ -445,3 +445,48 @@ def test_many_batch_sizes_cycle_the_graph_cache():
     want = dict(p_bar=ref.p_bar, l=ref.l, active_count=ref.active_count, tile_count=ref.tile_count,
                 qx=ref.qx, qy=ref.qy, qs=ref.qs)
     assert_state(eng, want, "graph cache cycling")
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("num,den,area,q_min,q_max", [
+    (1, 2, 4, 256, 921_600),        # config 3 (fill 1/2, 2x2 tiles)
+    (2, 3, 9, 64, 307_200),         # fill 2/3, tile side 3
+    (1, 2, 4, 1, (1 << 22) - 1),    # the largest q_max the 32-bit form takes
+    (7, 127, 25, 16, 4_000_000),    # odd ratio, den * q_max just under 2^29
+    (1_000_003, 3, 16, 1, 100_000),  # num * A close to 2^24: quotients far above the clamp
+])
+def test_regulator_32bit_form_is_the_exact_floor(num, den, area, q_min, q_max):
+    """regulate32x (float quotient + 32-bit remainder fix-up, the form the window
+    kernels step with) equals the reference's integer formula
+    (_kernels.py:195-201) on random triples and on triples built around exact
+    multiples N = k D, where a float quotient alone would be off by one."""
+    import ctypes as C
+    from paper_2510_20071_b200 import _native
+    lib = _native.load()
+    rng = np.random.default_rng(num * 31 + den)
+    n = 2_000_000
+    # random windows: len <= q_max + 1, 1 <= nt <= np <= len, over all magnitudes
+    mag = rng.integers(0, 23, n)
+    ln = np.minimum(q_max + 1, 1 + (rng.random(n) * (2.0 ** mag)).astype(np.int64)).astype(np.int64)
+    npx = 1 + (rng.random(n) * ln).astype(np.int64)
+    npx = np.minimum(npx, ln)
+    ntl = 1 + (rng.random(n) * npx).astype(np.int64)
+    ntl = np.minimum(ntl, npx)
+    # adversarial third: choose len so that len * nt * numA is k * (den * np) + {-1, 0, +1} when possible
+    m = n // 3
+    numA = num * area
+    D = den * npx[:m]
+    k = 1 + (rng.random(m) * min(q_max + 4, 1 << 22)).astype(np.int64)
+    target = k * D + rng.integers(-1, 2, m)
+    ln_adv = np.clip(np.rint(target / (ntl[:m] * numA)).astype(np.int64), np.maximum(npx[:m], 1), q_max + 1)
+    ln[:m] = ln_adv
+    want = np.clip((ln * numA * ntl) // (den * npx), q_min, q_max).astype(np.uint32)
+    a, b, c = (np.ascontiguousarray(v, np.uint32) for v in (ln, npx, ntl))
+    fast = np.empty(n, np.uint32)
+    exact = np.empty(n, np.uint32)
+    rc = lib.fibar_debug_regulate(num, den, area, q_min, q_max, a.ctypes.data, b.ctypes.data, c.ctypes.data, n,
+                                  fast.ctypes.data, exact.ctypes.data)
+    _native.check(rc, "fibar_debug_regulate")
+    assert np.array_equal(exact, want)          # the device's 64-bit reference agrees with numpy
+    bad = np.nonzero(fast != want)[0]
+    assert bad.size == 0, (bad[:5], ln[bad[:5]], npx[bad[:5]], ntl[bad[:5]], fast[bad[:5]], want[bad[:5]])
