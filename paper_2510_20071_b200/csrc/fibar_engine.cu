@@ -491,8 +491,8 @@ int enqueue_ingest_b(fibar_engine *g, long long n_raw, int par, int where, cudaS
   cudaStream_t s_saved = L.stream;
   L.stream = s;
   Ctx x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
-  fibar_launch(L, "ingest_end", k_ingest_end, 1, 1, 0, s, x);
   if (g->spatial) {
+    fibar_launch(L, "ingest_end", k_ingest_end, 1, 1, 0, s, x);
     const int nb = (int)((n_raw + TPB - 1) / TPB);
     fibar_launch(L, "seg_marks", k_seg_marks, nb, TPB, 0, s, x);
     fibar_launch(L, "link", k_link, nb, TPB, 0, s, x);
@@ -538,7 +538,7 @@ int enqueue_chain(fibar_engine *g, long long n_raw, int par, int where, cudaStre
   Launcher &L = g->L;
   x = g->ctx(where ? g->kb2[par] : g->ka2[par], where ? g->vb2[par] : g->va2[par], n_raw, par);
   if (!g->spatial) {
-    fibar_launch(L, "batch_begin", k_batch_begin, 1, 1, 0, s, x);   // (filter ON: in k_window_run)
+    // (the batch is opened by k_compact; filter ON: by k_window_run)
   } else {
     const int T = (int)((n_raw + x.chunk - 1) / x.chunk);
     const int G = n_raw <= g->small_chunk_max ? g->run_g : g->run_g_large;
@@ -962,7 +962,7 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
     fibar_launch(L, "posinfo", k_posinfo, nb, TPB, 0, s, x, 0);
     fibar_launch(L, "temporal", k_temporal, nb, TPB, 0, s, x);
     fibar_launch(L, "temporal_long", k_temporal_long, g->nsm * 2, LONG_TPB, 0, s, x);
-    fibar_launch(L, "batch_end", k_batch_end, 1, 1, 0, s, x);
+    // (the event count was added by k_compact)
   }
   L.stream = u;
   CK(cudaGetLastError());

@@ -98,6 +98,8 @@ __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
   }
 }
 
+__device__ __forceinline__ void open_batch(const Ctx &x);
+
 __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   pdl_wait();
   __shared__ unsigned wsum[TPB / 32];
@@ -154,6 +156,16 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     b->qlo = 0x7FFFFFFFFFFFFFFFLL;
     b->qhi = -1;
     b->nclosed = 0;
+    if (!x.spatial) {
+      // filter OFF runs on one stream, batch after batch: the batch's first
+      // event index, its opening and its event count need no kernels of their
+      // own (filter ON: k_ingest_end in batch order, k_window_run, k_posinfo)
+      DevState *s = x.st;
+      b->E0 = s->Ein;
+      s->Ein += b->B;
+      open_batch(x);
+      s->E += b->B;
+    }
   }
 }
 

@@ -1,8 +1,5 @@
-mkdir -p gpurun_out
-timeout 1500 python bench.py > gpurun_out/r2f_bench.json 2> gpurun_out/r2f_bench.err; echo "bench rc=$?"
-timeout 900 python bench.py --impl reference --steps 1 --warmup 1 > gpurun_out/r2f_bench_reference.json 2> gpurun_out/r2f_ref.err; echo "ref rc=$?"
-python -c "
-import json
-d=json.load(open('gpurun_out/r2f_bench.json')); r=json.load(open('gpurun_out/r2f_bench_reference.json'))
-print(d['value'], d['e2e']['value'], d['parity']['frames'], d['parity']['state'], d['roofline']['kernel'], d['roofline']['frac'], d['roofline']['traffic_ratio'], r['value'])
-print({k: round(v['value']) for k, v in d['filter_off'].items()}, d['clocks'])"
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+for i in 1 2; do timeout 900 python bench.py --config 1 --steps 5 --warmup 3 --no-off > gpurun_out/r2e_cfg1.json 2> gpurun_out/r2e_cfg1.err; python -c "import json; d=json.load(open('gpurun_out/r2e_cfg1.json')); print('cfg1', round(d['value'],1), round(d['e2e']['value'],1), d['parity']['state'], d['gpu_launches'])"; done
+timeout 900 python scripts/sweep_config4.py --sync --events 4000000 --max-packets 1500 --cpu-seconds 0.3 --out gpurun_out/tmp_sync.json 2>&1 | grep '"off"' | cut -c1-170
+timeout 900 python scripts/sweep_config4.py --events 20000000 --cpu-seconds 0.3 --out gpurun_out/tmp_async.json 2>&1 | grep '"off"' | cut -c1-170
