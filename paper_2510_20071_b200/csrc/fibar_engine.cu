@@ -776,7 +776,9 @@ int enqueue_batch(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, con
       // a small batch: each part replays one CUDA graph per (size class,
       // parity), the ingest from fixed input buffers (k_stage fills them and
       // the batch's raw count)
-      const long long cls = std::min(g->graph_max, (n_raw + GRAPH_CLASS - 1) / GRAPH_CLASS * GRAPH_CLASS);
+      // (a class of its own for packets of up to one sort tile: sorted on chip by one CTA)
+      const long long cls = n_raw <= 2048 ? std::min(g->graph_max, 2048LL)
+                                          : std::min(g->graph_max, (n_raw + GRAPH_CLASS - 1) / GRAPH_CLASS * GRAPH_CLASS);
       const int nbs = (int)std::max(1LL, std::min((long long)g->nsm * 2, (n_raw / 8 + TPB - 1) / TPB));
       fibar_launch(L, "stage", k_stage, nbs, TPB, 0, sa, rx0, ry0, rp0, (long long)n_raw, g->gx2[par], g->gy2[par],
                    g->gp2[par], &g->bsd[par].n_raw);

@@ -232,6 +232,92 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const unsigned *__res
   }
 }
 
+// A tiny batch (up to one tile of 2048 pairs) sorted by one CTA in shared
+// memory: the same stable LSD passes (8-bit digits, match_any ranks in a warp,
+// per-warp counters, warps in item order) without leaving the chip -- one
+// launch instead of three per pass.  Keys in, (keys, original index) out.
+__global__ void __launch_bounds__(RS_THREADS) k_sort_tiny(const unsigned *__restrict__ kin, unsigned *__restrict__ kout,
+                                                          unsigned *__restrict__ vout,
+                                                          const long long *__restrict__ n_dev, int bits) {
+  pdl_wait();
+  __shared__ unsigned sk[2][RS_TILE], sv[2][RS_TILE];
+  __shared__ unsigned wcnt[RS_WARPS][256];
+  __shared__ unsigned wtot[RS_WARPS];
+  const int n = (int)min((long long)RS_TILE, *n_dev);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < n; i += RS_THREADS) {
+    sk[0][i] = kin[i];
+    sv[0][i] = (unsigned)i;
+  }
+  int cur = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  const int base = wid * (RS_ITEMS * 32);
+  for (int shift = 0; shift < bits; shift += 8) {
+    for (int i = threadIdx.x; i < RS_WARPS * 256; i += RS_THREADS) (&wcnt[0][0])[i] = 0;
+    __syncthreads();
+    unsigned key[RS_ITEMS], val[RS_ITEMS], loc[RS_ITEMS];
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+      const int i = base + r * 32 + lane;
+      const bool valid = i < n;
+      const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+      key[r] = valid ? sk[cur][i] : 0u;
+      val[r] = valid ? sv[cur][i] : 0u;
+      const unsigned d = (key[r] >> shift) & 255u;
+      if (valid) {
+        const unsigned peers = __match_any_sync(vmask, d);
+        const unsigned before = wcnt[wid][d];
+        loc[r] = before + __popc(peers & lt);
+        __syncwarp(vmask);
+        if ((peers & lt) == 0) wcnt[wid][d] = before + __popc(peers);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    {
+      // digit d = threadIdx.x: exclusive prefix over (digit, warp)
+      const int d = threadIdx.x;
+      unsigned tot = 0;
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) tot += wcnt[w][d];
+      unsigned incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (lane == 31) wtot[wid] = incl;
+      __syncthreads();
+      unsigned run = incl - tot;
+      for (int w = 0; w < wid; ++w) run += wtot[w];
+#pragma unroll
+      for (int w = 0; w < RS_WARPS; ++w) {
+        const unsigned t = wcnt[w][d];
+        wcnt[w][d] = run;
+        run += t;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < RS_ITEMS; ++r) {
+      const int i = base + r * 32 + lane;
+      if (i < n) {
+        const unsigned d = (key[r] >> shift) & 255u;
+        const unsigned pos = wcnt[wid][d] + loc[r];
+        sk[cur ^ 1][pos] = key[r];
+        sv[cur ^ 1][pos] = val[r];
+      }
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += RS_THREADS) {
+    kout[i] = sk[cur][i];
+    vout[i] = sv[cur][i];
+  }
+}
+
 // Sort (keys, index) for n_dev (<= n_max) items; `bits` significant key bits.
 // Pass 0 reads k_a with implicit identity payload; passes alternate between
 // the (a) and (b) buffers.  Returns 0 if the result is in (k_a, v_a), 1 if in
@@ -239,6 +325,10 @@ __global__ void __launch_bounds__(RS_THREADS) k_rs_scatter(const unsigned *__res
 int radix_sort_pairs(Launcher &L, unsigned *k_a, unsigned *v_a, unsigned *k_b, unsigned *v_b, unsigned *hist,
                      const long long *n_dev, long long n_max, int bits) {
   const int nblocks = (int)((n_max + RS_TILE - 1) / RS_TILE);
+  if (n_max > 0 && n_max <= RS_TILE) {   // one tile: sorted on chip by one CTA, result in (k_b, v_b)
+    fibar_launch(L, "sort_tiny", k_sort_tiny, 1, RS_THREADS, 0, L.stream, (const unsigned *)k_a, k_b, v_b, n_dev, bits);
+    return 1;
+  }
   // the fewest passes with digits of at most RS_MAX_BITS bits, the digits as narrow as that allows
   const int passes = bits <= 0 ? 1 : (bits + RS_MAX_BITS - 1) / RS_MAX_BITS;
   const int dbits = bits <= 0 ? 1 : (bits + passes - 1) / passes;
