@@ -472,9 +472,14 @@ int enqueue_ingest_a(fibar_engine *g, const uint16_t *rx0, const uint16_t *ry0, 
   x.n_raw_dev = n_dev;   // n_raw is then the size class's upper bound
   cudaStream_t s_saved = L.stream;
   L.stream = s;
-  fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
-  scan_exclusive_u32(L, g->blockcnt2[par], nb_in + 1);
-  fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in);
+  if (nb_in == 1) {
+    // one tile: the block counts, scans and compacts by itself
+    fibar_launch(L, "compact", k_compact, 1, TPB, 0, s, x, 1, 1);
+  } else {
+    fibar_launch(L, "count_inb", k_count_inb, nb_in, TPB, 0, s, x, nb_in);
+    scan_exclusive_u32(L, g->blockcnt2[par], nb_in + 1);
+    fibar_launch(L, "compact", k_compact, nb_in, TPB, 0, s, x, nb_in, 0);
+  }
   if (used_ev) CK(cudaEventRecord(used_ev, s));   // the raw packet may be refilled / freed from here on
   where = radix_sort_pairs(L, g->ka2[par], g->va2[par], g->kb2[par], g->vb2[par], g->hist2[par], &g->bsd[par].B, n_raw,
                            g->key_bits);

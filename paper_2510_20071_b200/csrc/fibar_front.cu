@@ -100,7 +100,10 @@ __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks) {
 
 __device__ __forceinline__ void open_batch(const Ctx &x);
 
-__global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
+// fused != 0 (one block only): the packet fits one tile, so the block also
+// counts the out-of-bounds events and takes its total from its own scan --
+// no k_count_inb, no scan kernel
+__global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks, int fused) {
   pdl_wait();
   __shared__ unsigned wsum[TPB / 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -112,9 +115,16 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   int ps[IN_ITEMS];
   load_in(x, n_raw, base, xs, ys, ps, true);
 #pragma unroll
+  unsigned oob = 0;
   for (int r = 0; r < IN_ITEMS; ++r) {
-    keep[r] = base + r < n_raw && on_sensor(x, xs[r], ys[r]) && in_band(x, ys[r]);
+    const bool ok = base + r < n_raw && on_sensor(x, xs[r], ys[r]);
+    oob += (fused && base + r < n_raw && !ok) ? 1u : 0u;
+    keep[r] = ok && in_band(x, ys[r]);
     cnt += keep[r];
+  }
+  if (fused) {
+    oob = __reduce_add_sync(0xffffffffu, oob);
+    if (lane == 0 && oob) atomicAdd((unsigned long long *)&x.st->oob, (unsigned long long)oob);
   }
   unsigned incl = cnt;
 #pragma unroll
@@ -126,7 +136,7 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
   __syncthreads();
   unsigned wofs = 0;
   for (int w = 0; w < wid; ++w) wofs += wsum[w];
-  unsigned pos = x.blockcnt[blockIdx.x] + wofs + incl - cnt;
+  unsigned pos = (fused ? 0u : x.blockcnt[blockIdx.x]) + wofs + incl - cnt;
 #pragma unroll
   for (int r = 0; r < IN_ITEMS; ++r) {
     if (!keep[r]) continue;
@@ -144,7 +154,10 @@ __global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks) {
     // epoch) is set by k_batch_begin, so ingest may run ahead of the previous
     // batch's window pass
     BatchState *b = x.bs;
-    b->B = x.blockcnt[nblocks];
+    unsigned total = 0;
+    if (fused)
+      for (int w = 0; w < TPB / 32; ++w) total += wsum[w];
+    b->B = fused ? total : x.blockcnt[nblocks];
     b->npop = 0;
     b->stale_batch = 0;
     b->ticket = 0;

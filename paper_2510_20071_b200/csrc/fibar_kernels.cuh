@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(TPB) k_snap(const float *__restrict__ src, flo
 __global__ void __launch_bounds__(TPB) k_debug_regulate(Ctx x, const unsigned *len, const unsigned *np, const unsigned *nt,
                                                         long long n, unsigned *out_fast, unsigned *out_exact);
 __global__ void __launch_bounds__(TPB) k_count_inb(Ctx x, int nblocks);
-__global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks);
+__global__ void __launch_bounds__(TPB) k_compact(Ctx x, int nblocks, int fused);
 __global__ void k_batch_begin(Ctx x);
 __global__ void k_ingest_end(Ctx x);
 __global__ void k_predict(Ctx x);

@@ -1,5 +1,4 @@
-for i in 1 2 3; do
-timeout 600 python bench.py --config 3 --events 10000000 --steps 3 --warmup 3 --no-cpu --no-off > gpurun_out/ab.json 2>gpurun_out/ab.err || tail -3 gpurun_out/ab.err
-python -c "import json; d=json.load(open('gpurun_out/ab.json')); print('cfg3', round(d['value'],1), round(d['e2e']['value'],1))"
-done
-python scripts/e2e_profile.py 2>&1 | grep "run()"
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -1
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python scripts/sweep_config4.py --sync --events 4000000 --max-packets 1500 --cpu-seconds 0.3 --out gpurun_out/r2e_config4_sweep_sync.json 2>&1 | grep '"packet": 1000,' | cut -c1-170
+timeout 900 python scripts/sweep_config4.py --events 20000000 --out gpurun_out/r2e_config4_sweep.json 2>&1 | grep '"packet": 1000,' | cut -c1-170
