@@ -411,7 +411,7 @@ def run_ours(args, rank, world, dist):
 
     e2e = None
     if not args.no_e2e:
-        t_h = timed(step_host, max(1, args.steps), 1)
+        t_h = timed(step_host, max(1, args.steps), max(1, min(args.warmup, 2)))
         e2e = {"value": n * world * max(1, args.steps) / t_h / 1e6, "unit": UNIT,
                "h2d_bytes_per_step": int(5 * n),
                "d2h_bytes_per_step": int((geom.n_pix + 16) * nfr),
