@@ -514,8 +514,13 @@ __device__ __forceinline__ unsigned regulate32x(const RegF &f, unsigned len, uns
 // regulate() through the 32-bit form whenever the operands fit (always for
 // sensors up to 4.19M pixels): no double division on the candidate paths
 __device__ __forceinline__ long long regulate_fast(const Ctx &x, long long len, long long np, long long nt) {
-  if (len < (1LL << 32) && np < (1LL << 32) && nt < (1LL << 32))
+  if (len < (1LL << 32) && np < (1LL << 32) && nt < (1LL << 32)) {
+    // (a window of at most q_max + 1 entries with nt <= np <= len -- every candidate window,
+    // prediction and speculative start: no 64-bit arithmetic)
+    if (x.reg32x && len <= x.qmax + 1 && np <= len && nt <= np && np >= 1)
+      return (long long)regulate32x(make_regf(x), (unsigned)len, (unsigned)np, (unsigned)nt);
     return (long long)regulate32(x, (unsigned)len, (unsigned)np, (unsigned)nt);
+  }
   return regulate(x, len, np, nt);
 }
 
